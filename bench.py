@@ -1,0 +1,347 @@
+#!/usr/bin/env python
+"""Benchmark of the sparse-DNN inference hot path (BASELINE.json metric:
+edges/sec = inputs x sum_l nnz(W_l) / time, 65536-neuron x 1920-layer net).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4]
+    python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
+    python bench.py --impl reference          # the CPU oracle, timed on host cores
+
+A step is one whole inference (all hot-path rows a2-a6): densify the input
+CSR, run every layer (one captured CUDA Graph), read out the categories and,
+for N > 1, all-gather the category bitmasks over NCCL.  Inputs are resident in
+HBM when the timed region starts (`value`); `e2e` repeats the measurement
+through the host-buffer call sdnn_infer (H2D of Y0 + D2H of the categories
+inside the timed region).  Multi-GPU is weak scaling: every rank infers its
+own 60,000-input batch against a replica of the weights.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (neurons, layers, inputs) -- BASELINE.json "configs"
+    "c1": (1024, 120, 1000),
+    "c2": (4096, 480, 60000),
+    "c3": (16384, 1920, 60000),
+    "c4": (65536, 1920, 60000),
+}
+METRIC = "edges/sec (inputs×nnz/time) for 65536-neuron×1920-layer net at 1/2/4/8 B200"
+UNIT = "edges/s"
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 3 + i and s[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def make_inputs(n, B, rank):
+    import sdnngen as g
+    seed = g.input_seed(n) if rank == 0 else g.input_seed(n) ^ (0x9E37 * rank)
+    return g.ms_inputs(n, B, seed=seed)
+
+
+# ---------------------------------------------------------------- reference arm
+
+def run_reference(args):
+    """The CPU oracle as it stands, on the GPU arm's workload: each step infers a
+    bounded sample of the 60,000 inputs through all layers; edges/s counts
+    sample_rows x sum nnz per oracle-second (generation of the layers excluded)."""
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import oracle
+    import sdnngen as g
+    n, L, B = CONFIGS[args.config]
+    spec = g.rn_spec(n, L)
+    rp, idx = make_inputs(n, B, 0)
+    cores = oracle.default_threads()
+    rows_per_step = args.ref_rows or max(1, cores)
+    r = np.random.default_rng(1234)
+    nsteps = args.warmup + args.steps
+    samples = [np.sort(r.choice(B, rows_per_step, replace=False)) for _ in range(nsteps)]
+    objs = []
+    for rows in samples:
+        srp, sidx, _ = oracle.subset_rows(rp, idx, None, rows)
+        objs.append(oracle.Oracle(n, srp, sidx, None))
+    total_nnz = 0
+    for l in range(L):
+        lay = g.gen_layer(spec, l, fmt="csr")
+        total_nnz += lay.colidx.size
+        for o in objs:
+            o.apply(lay, nthreads=cores)
+    secs = [o.layer_seconds for o in objs[args.warmup:]]
+    t = sum(secs) / len(secs)
+    value = rows_per_step * total_nnz / t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": f"rn{n}x{L}-ms", "neurons": n, "layers": L,
+                   "inputs_sampled_per_step": rows_per_step, "inputs_full": B},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": f"{rows_per_step} random rows of the {B}-input batch per step, "
+                                   f"all {L} layers (oracle/sdnn_oracle.c, {cores} threads)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(n, L, spec, rp, idx, rows):
+    """Bounded oracle sample timed on host cores (rank 0, N = 1 only)."""
+    import oracle
+    cores = oracle.default_threads()
+    t0 = time.time()
+    _, _, _, secs = oracle.infer_spec_rows(spec, rp, idx, None, rows, nthreads=cores)
+    total_nnz = 32 * n * L
+    return {"value": rows.size * total_nnz / secs, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{rows.size} random rows of the 60000-input batch, all {L} layers "
+                      f"({secs:.1f} s oracle time, {time.time() - t0:.1f} s incl. layer generation)"}
+
+
+# ---------------------------------------------------------------- GPU arm
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2004_10908_b200 as sd
+    import sdnngen as g
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    n, L, B = CONFIGS[args.config]
+    if args.scaling == "strong" and ws > 1:
+        B_rank = (B + ws - 1) // ws
+    else:
+        B_rank = B
+    spec = g.rn_spec(n, L)
+    t0 = time.time()
+    net = sd.Net.from_spec(spec, fmt="ell", threads=args.load_threads, device=local,
+                           flags=sd.SDNN_F_PROFILE)
+    t_load = time.time() - t0
+    rp, idx = make_inputs(n, B, rank)
+    if args.scaling == "strong" and ws > 1:
+        import oracle as _o  # noqa: F401  (not used: subset by slicing below)
+    if B_rank != B:
+        lo, hi = rank * B_rank, min(B, (rank + 1) * B_rank)
+        base = rp[lo]
+        idx = idx[rp[lo]:rp[hi]].copy()
+        rp = (rp[lo:hi + 1] - base).copy()
+    batch = rp.size - 1
+    rp_t = torch.from_numpy(rp).to(dev)
+    idx_t = torch.from_numpy(idx).to(dev)
+    words = (batch + 31) // 32
+    alive = torch.empty(words, dtype=torch.int32, device=dev)
+    gathered = torch.empty(words * ws, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        net.infer_torch(rp_t, idx_t, None, alive_t=alive, stream=stream)
+        if ws > 1:
+            dist.all_gather_into_tensor(gathered, alive)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    if ws > 1:
+        dist.barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize(dev)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize(dev)
+    if ws > 1:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    st = net.stats()
+    layer_ms = net.layer_times()                     # per-layer kernel durations, last step
+    if ws > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    total_nnz = st["total_nnz"]
+    edges_rank = batch * total_nnz
+    value = edges_rank * ws / (ms * 1e-3) if args.scaling != "strong" else B * total_nnz / (ms * 1e-3)
+
+    # ---- roofline of the dominant kernel (the layer kernel) --------------------
+    live = st["live_rows"]
+    kept0 = st["kept_rows"]
+    live_in = [kept0] + live[:-1]                    # rows each layer processes (algorithmic)
+    alg_bytes = sum(8.0 * n * r for r in live_in)   # read + write 4 B per live row-neuron per layer
+    kern_s = sum(layer_ms) * 1e-3
+    pk = peaks()
+    peak = pk["hbm_gbs"] if pk else 6650.0
+    achieved = alg_bytes / kern_s / 1e9 if kern_s > 0 else None
+    traffic = None
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "layer_traffic.json")))
+        if prof.get("config") == args.config:
+            traffic = prof.get("dram_bytes_per_live_row_neuron")
+            traffic = None if traffic is None else traffic * alg_bytes / 8.0 / L
+    except Exception:
+        pass
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+            "kernel": "k_layer_uniform (per-layer launch, avg over the last step's "
+                      f"{L} launches)",
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if pk else "fallback 6.65 TB/s",
+            "kernel_share_of_step": kern_s / (ms * 1e-3),
+            "alg_bytes_per_launch": alg_bytes / L}
+
+    # ---- e2e through the public host-buffer call --------------------------------
+    e2e = None
+    if not args.no_e2e:
+        rp_h = torch.from_numpy(rp).pin_memory().numpy()
+        idx_h = torch.from_numpy(idx).pin_memory().numpy()
+        for _ in range(1):
+            cats, _ = net.infer(rp_h, idx_h, None)
+        times = []
+        for _ in range(args.e2e_steps):
+            if ws > 1:
+                dist.barrier()
+            t1 = time.perf_counter()
+            cats, _ = net.infer(rp_h, idx_h, None)
+            times.append(time.perf_counter() - t1)
+        te = float(np.mean(times))
+        if ws > 1:
+            t = torch.tensor([te], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            te = float(t.item())
+        e2e = {"value": edges_rank * ws / te, "unit": UNIT,
+               "h2d_bytes_per_step": int(rp_h.nbytes + idx_h.nbytes),
+               "d2h_bytes_per_step": int(4 + 4 * cats.size), "ms_per_step": te * 1e3,
+               "call": "sdnn_infer (host CSR in, host categories out)"}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        r = np.random.default_rng(99)
+        rows = np.sort(r.choice(batch, args.cpu_rows, replace=False))
+        cpu = cpu_baseline(n, L, spec, rp, idx, rows)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak" if args.scaling != "strong" else "strong", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"rn{n}x{L}-ms{B}", "neurons": n, "layers": L,
+                       "nnz_per_column": 32, "inputs_per_gpu": batch,
+                       "global_batch": batch * ws if args.scaling != "strong" else B,
+                       "network": "RadiX-Net-shaped (sdnngen.rn_spec), w=1/16, b=%g" % spec.bias,
+                       "inputs": "binary MNIST-shaped strokes (sdnngen.ms_inputs)",
+                       "parallelism": f"dp{ws}" if ws > 1 else "single",
+                       "l2": "inputs larger than L2 (Y = %.1f GB per GPU)" % (4.0 * n * batch / 1e9)},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(st["launches_per_infer"] * args.steps),
+            "clocks": clk.summary(),
+            "live_edges_per_s": st["live_edges"] * ws / (ms * 1e-3),
+            "survivors": {"kept_after_densify": kept0, "after_layer": {str(i): live[i] for i in
+                          sorted(set([0, 1, 2, 4, 8, 16, 32, 64, L // 2, L - 1])) if i < L},
+                          "categories": int(live[-1]) if live else None,
+                          "category_fraction": (live[-1] / batch) if live and batch else None},
+            "load_seconds": t_load,
+        }
+        print(json.dumps(line), flush=True)
+    net.close()
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="sdnn", choices=["sdnn", "reference"])
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-rows", type=int, default=16)
+    ap.add_argument("--ref-rows", type=int, default=0)
+    ap.add_argument("--load-threads", type=int, default=8)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "sdnn":
+        print("warning: the contract asks for >= 3 warm-up steps", file=sys.stderr)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

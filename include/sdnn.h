@@ -1,0 +1,196 @@
+/*
+ * sdnn.h -- C ABI of the B200-native sparse-DNN inference hot path.
+ *
+ * The operation (one call of sdnn_infer / sdnn_infer_device):
+ *
+ *   Y_0          = the input matrix (B rows x N neurons), given as CSR
+ *   Y_{l+1}      = min(max(Y_l . W_l + b_l, 0), YMAX)      l = 0 .. L-1
+ *   categories   = { i : exists j, Y_L[i][j] > 0 }          ascending, 0-based
+ *
+ *   - layer formula, YMAX = 32, "which rows remain nonzero", the function names
+ *     sdnn_create / sdnn_infer / sdnn_destroy: BASELINE.json north_star;
+ *   - dataset parts (input matrix, L sparse layers, bias values, truth
+ *     categories): PAPER.md:2557-2559 (Sec. 7.4, Large Sparse Neural Network
+ *     Inference); the golden check of categories: PAPER.md:2570;
+ *   - raw caller-owned pointers, no data abstraction: the design stance of
+ *     PAPER.md:646-660 (Sec. 4.5).
+ *
+ * Arithmetic (readings A5/A6, identical to the oracle's): every
+ * output is the fp32 chain  acc = +0; acc = fmaf(Y[i][k_t], w_t, acc)  over the
+ * column's stored sources k_t in ASCENDING k, then z = acc + b_j (one fp32
+ * add), then y = z > 0 ? fminf(z, YMAX) : +0.  Results are therefore
+ * bit-identical to the CPU oracle (oracle/), not merely within tolerance.
+ *
+ * Conventions for every function:
+ *   - return SDNN_OK (0) or a negative sdnn_status; on error the outputs are
+ *     unspecified and sdnn_last_error() returns a thread-local message;
+ *   - SDNN_E_CUDA is sticky: the handle must be destroyed;
+ *   - a handle is not re-entrant: do not call two functions on the same handle
+ *     concurrently (sdnn_set_layer on DIFFERENT layers is the one exception);
+ *   - the caller owns every buffer it passes; the library keeps no caller
+ *     pointer after a call returns (sdnn_infer_device: until the stream reaches
+ *     the end of the enqueued work).
+ */
+#ifndef SDNN_H
+#define SDNN_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SDNN_ABI_VERSION 1
+
+typedef struct sdnn_net sdnn_net;
+typedef int32_t sdnn_status;
+
+enum {
+  SDNN_OK = 0,
+  SDNN_E_ARG = -1,          /* NULL pointer, size out of range, bad option        */
+  SDNN_E_FORMAT = -2,       /* malformed CSR/ELL, duplicate entry, non-finite     */
+  SDNN_E_UNSUPPORTED = -3,  /* valid but outside this build (e.g. N > 2^30)      */
+  SDNN_E_NOMEM = -4,        /* host or device allocation failed                  */
+  SDNN_E_CUDA = -5,         /* CUDA runtime error (sticky)                       */
+  SDNN_E_STATE = -6         /* call out of order (e.g. infer before all layers)  */
+};
+
+/* Weight formats of one layer W_l (an N x N sparse matrix; W_l[k][j] connects
+ * input neuron k to output neuron j, i.e. Y_{l+1} = Y_l . W_l). */
+enum {
+  SDNN_W_CSR = 0,    /* rows = input neurons k: rowptr[N+1], idx[nnz] = output j */
+  SDNN_W_ELLCOL = 1  /* per OUTPUT j, ell_k slots: idx[j*ell_k + t] = source k or -1
+                        (padding, any position); slot order is irrelevant          */
+};
+
+typedef struct sdnn_layer {
+  int32_t format;          /* SDNN_W_CSR or SDNN_W_ELLCOL                                 */
+  int32_t ell_k;           /* ELLCOL: slots per output (>= 0); CSR: ignored               */
+  const int64_t *rowptr;   /* CSR: [N+1], rowptr[0] = 0, non-decreasing; ELLCOL: NULL    */
+  const int32_t *idx;      /* CSR: [rowptr[N]] output ids; ELLCOL: [N*ell_k] source ids  */
+  const float *val;        /* same length as idx, or NULL: every stored value is
+                              uniform_value (the challenge style, w = 1/16)              */
+  float uniform_value;     /* used iff val == NULL                                        */
+} sdnn_layer;
+
+/* Option flags */
+enum {
+  SDNN_F_NO_COMPACT = 1u << 0,   /* never drop dead rows (always also implied when some
+                                    bias > 0, because then a dead row can revive)        */
+  SDNN_F_NO_GROUPS = 1u << 1,    /* do not merge columns with identical source lists
+                                    (forces the one-column-per-group gather path)        */
+  SDNN_F_NO_GRAPH = 1u << 2,     /* launch the layer chain as a plain stream loop
+                                    instead of one captured CUDA Graph (f1 study)        */
+  SDNN_F_NO_RESIDENT = 1u << 3,  /* disable the SMEM-resident multi-layer kernel        */
+  SDNN_F_TRUST_INPUT = 1u << 4,  /* sdnn_infer: skip host validation of Y0              */
+  SDNN_F_PROFILE = 1u << 5       /* record a CUDA event pair around every layer kernel
+                                    (read back with sdnn_layer_times)                    */
+};
+
+typedef struct sdnn_opts {
+  int32_t device;   /* CUDA device ordinal; -1 = the calling thread's current device  */
+  uint32_t flags;   /* SDNN_F_*                                                        */
+  float ymax;       /* clip value YMAX (> 0, finite); north_star: 32                   */
+  void *stream;     /* cudaStream_t for sdnn_infer (NULL = a stream owned by the net) */
+} sdnn_opts;        /* passing opts = NULL means {-1, 0, 32.0f, NULL}                  */
+
+/* Create a network handle and load all L layers.
+ *   neurons  N, 1 <= N <= 65536 on this build (u16 source indices); larger N
+ *            returns SDNN_E_UNSUPPORTED;
+ *   layers   L >= 0;
+ *   W        [layers] layer descriptors (may be NULL iff layers == 0);
+ *   bias     [layers * neurons] fp32, layer-major (b_l = bias + l*neurons);
+ *   out      receives the handle (set to NULL on error).
+ * Validates every layer (index range, monotone rowptr, no duplicate (k,j),
+ * finite values), packs it into the device layout and
+ * uploads it; weights stay resident in HBM for the life of the handle. */
+sdnn_status sdnn_create(int32_t neurons, int32_t layers, const sdnn_layer *W,
+                        const float *bias, const sdnn_opts *opts, sdnn_net **out);
+
+/* Streamed creation for networks too large to stage on the host at once
+ * (65536 x 1920 is 4.0e9 nonzeros): create the handle, then call
+ * sdnn_set_layer for every l in [0, layers) (any order; distinct layers may be
+ * set from different host threads concurrently).  sdnn_infer* returns
+ * SDNN_E_STATE until every layer has been set. */
+sdnn_status sdnn_create_empty(int32_t neurons, int32_t layers, const sdnn_opts *opts,
+                              sdnn_net **out);
+sdnn_status sdnn_set_layer(sdnn_net *net, int32_t l, const sdnn_layer *W_l,
+                           const float *bias_l /* [neurons] */);
+
+/* Synchronous inference from HOST buffers (the end-to-end call).
+ *   y0_rowptr   [batch+1] int64, y0_rowptr[0] = 0, non-decreasing;
+ *   y0_idx      [y0_rowptr[batch]] int32 neuron ids in [0, N), no duplicate per row;
+ *   y0_val      same length, finite, or NULL meaning every stored value is 1.0f
+ *               (binary challenge-style input);
+ *   batch       B >= 0;
+ *   categories  [batch] capacity; receives the ascending 0-based category ids;
+ *   n_categories receives their count;
+ *   y_out       NULL, or [batch * neurons] fp32 row-major: receives Y_L.
+ * Host->device copy of Y0, the whole layer chain and the device->host copy of
+ * the categories all happen inside this call; the device work runs on
+ * opts->stream (or the handle's stream) and is complete on return. */
+sdnn_status sdnn_infer(sdnn_net *net, const int64_t *y0_rowptr, const int32_t *y0_idx,
+                       const float *y0_val, int64_t batch, int32_t *categories,
+                       int64_t *n_categories, float *y_out);
+
+/* Asynchronous inference from DEVICE buffers on `stream` (cudaStream_t; NULL =
+ * legacy default stream).  Same Y0 layout as sdnn_infer, all pointers device
+ * pointers; Y0 is NOT validated here.
+ *   d_alive   [ceil(batch/32)] uint32 device bitmask: bit (i%32) of word i/32 is
+ *             set iff row i is a category (all other bits are cleared);
+ *   d_y_out   NULL or [batch * neurons] fp32 device, row-major Y_L.
+ * This is the entry point of the torch / NCCL multi-GPU driver: pointers come
+ * from tensor.data_ptr(), the stream from torch.cuda.current_stream(). */
+sdnn_status sdnn_infer_device(sdnn_net *net, const int64_t *d_rowptr, const int32_t *d_idx,
+                              const float *d_val, int64_t batch, uint32_t *d_alive,
+                              float *d_y_out, void *stream);
+
+/* Statistics of the handle and of its last completed inference. */
+typedef struct sdnn_stats {
+  int32_t struct_size;        /* caller sets sizeof(sdnn_stats) (versioning)            */
+  int32_t neurons, layers;
+  int32_t path;               /* 0 = per-layer streaming kernels, 1 = SMEM-resident     */
+  int32_t grouped_layers;     /* layers packed with >1 column per source-list group    */
+  int32_t max_group;          /* largest group size (columns sharing a source list)    */
+  int32_t max_k;              /* largest column nnz over all layers                    */
+  int32_t compaction;         /* 1 if dead-row compaction is enabled                   */
+  int64_t packed_weight_bytes;/* device bytes of packed W and bias                     */
+  int64_t total_nnz;          /* sum over layers of stored nonzeros                    */
+  int64_t last_batch;
+  int64_t last_n_categories;
+  int64_t launches_per_infer; /* kernels (graph nodes) one inference launches          */
+  int64_t live_edges;         /* sum_l (rows nonzero before layer l) * nnz_l, last call */
+  int64_t kept_rows;          /* rows entering layer 0 (empty rows dropped when exact)   */
+} sdnn_stats;
+
+/* live_rows: NULL or [layers] receives the number of rows still nonzero after
+ * each layer of the last inference (the survivor profile). */
+sdnn_status sdnn_stats_get(const sdnn_net *net, sdnn_stats *out, int64_t *live_rows);
+
+/* SDNN_F_PROFILE only: device duration (ms) of every layer kernel of the last
+ * inference, from CUDA events recorded on the launching stream around it.
+ * ms: [layers].  Synchronises the handle's work. */
+sdnn_status sdnn_layer_times(const sdnn_net *net, float *ms);
+
+/* Host-only validation + packing of one layer (no device needed): the same
+ * checks and grouping sdnn_set_layer performs, reported in `info`. */
+typedef struct sdnn_layer_info {
+  int32_t ngroups;   /* groups of columns with identical ascending source lists */
+  int32_t kmax;      /* largest column nnz                                      */
+  int32_t gmax;      /* largest group                                           */
+  int32_t uniform;   /* 1 if every stored value is bit-identical                */
+  int32_t regular;   /* 1 if every group has kmax sources and gmax members      */
+  int32_t bias_nonpositive;
+  int64_t nnz;
+} sdnn_layer_info;
+sdnn_status sdnn_validate_layer(int32_t neurons, const sdnn_layer *W_l, const float *bias_l,
+                                uint32_t flags, sdnn_layer_info *info);
+
+void sdnn_destroy(sdnn_net *net);          /* NULL-safe; frees all device memory       */
+const char *sdnn_last_error(void);         /* thread-local, never NULL                 */
+int32_t sdnn_abi_version(void);            /* == SDNN_ABI_VERSION                      */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SDNN_H */

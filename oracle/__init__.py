@@ -139,3 +139,22 @@ def subset_rows(rowptr, idx, val, rows):
     take = np.concatenate([np.arange(s, e) for s, e in zip(starts, ends)]) if rows.size else np.zeros(0, np.int64)
     take = take.astype(np.int64)
     return sub_ptr, idx[take], (None if val is None else val[take])
+
+
+def infer_spec_rows(spec, rowptr, idx, val=None, rows=None, ymax: float = 32.0,
+                    nthreads: Optional[int] = None, profile: bool = False):
+    """Oracle on a subset of rows of a generated network (sdnngen spec),
+    generating one CSR layer at a time (bounded host memory at 65536 x 1920).
+    Row independence (invariant I4) makes the subset exact.  Returns
+    (categories, Y_L, live profile, oracle seconds excluding generation)."""
+    import sdnngen
+    if rows is not None:
+        rowptr, idx, val = subset_rows(rowptr, idx, val, rows)
+    o = Oracle(spec.n, rowptr, idx, val)
+    prof = [] if profile else None
+    for l in range(spec.L):
+        lay = sdnngen.gen_layer(spec, l, fmt="csr")
+        o.apply(lay, ymax=ymax, nthreads=nthreads)
+        if profile:
+            prof.append(o.live_rows())
+    return o.categories(), o.Y, prof, o.layer_seconds

@@ -1,0 +1,313 @@
+"""B200-native sparse-DNN inference (arXiv 2004.10908, Sec. 7.4 hot path).
+
+Thin Python binding of the C ABI in ``include/sdnn.h`` (argument marshalling
+only -- every step of the path runs in the CUDA kernels of ``libsdnn.so``):
+
+    sdnn_create / sdnn_create_empty / sdnn_set_layer   load W_l, b_l (resident in HBM)
+    sdnn_infer          host CSR Y0 -> ascending category ids (end-to-end call)
+    sdnn_infer_device   device CSR Y0 -> device category bitmask (torch / NCCL path)
+    sdnn_stats_get      survivor profile, launch count, packed bytes
+    sdnn_destroy
+
+There is no CPU fallback: importing this package without the built
+``libsdnn.so`` raises, and every call needs a CUDA device.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from concurrent.futures import ThreadPoolExecutor
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsdnn.so")
+
+SDNN_OK, SDNN_E_ARG, SDNN_E_FORMAT, SDNN_E_UNSUPPORTED = 0, -1, -2, -3
+SDNN_E_NOMEM, SDNN_E_CUDA, SDNN_E_STATE = -4, -5, -6
+SDNN_W_CSR, SDNN_W_ELLCOL = 0, 1
+SDNN_F_NO_COMPACT, SDNN_F_NO_GROUPS, SDNN_F_NO_GRAPH = 1, 2, 4
+SDNN_F_NO_RESIDENT, SDNN_F_TRUST_INPUT, SDNN_F_PROFILE = 8, 16, 32
+
+EXPORTS = ["sdnn_create", "sdnn_create_empty", "sdnn_set_layer", "sdnn_infer",
+           "sdnn_infer_device", "sdnn_stats_get", "sdnn_validate_layer", "sdnn_destroy",
+           "sdnn_last_error", "sdnn_abi_version", "sdnn_layer_times"]
+
+
+class SdnnError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"sdnn status {status}: {msg}")
+        self.status = status
+
+
+class sdnn_layer(ctypes.Structure):
+    _fields_ = [("format", ctypes.c_int32), ("ell_k", ctypes.c_int32),
+                ("rowptr", ctypes.c_void_p), ("idx", ctypes.c_void_p),
+                ("val", ctypes.c_void_p), ("uniform_value", ctypes.c_float)]
+
+
+class sdnn_opts(ctypes.Structure):
+    _fields_ = [("device", ctypes.c_int32), ("flags", ctypes.c_uint32),
+                ("ymax", ctypes.c_float), ("stream", ctypes.c_void_p)]
+
+
+class sdnn_layer_info(ctypes.Structure):
+    _fields_ = [("ngroups", ctypes.c_int32), ("kmax", ctypes.c_int32), ("gmax", ctypes.c_int32),
+                ("uniform", ctypes.c_int32), ("regular", ctypes.c_int32),
+                ("bias_nonpositive", ctypes.c_int32), ("nnz", ctypes.c_int64)]
+
+
+class sdnn_stats(ctypes.Structure):
+    _fields_ = [("struct_size", ctypes.c_int32), ("neurons", ctypes.c_int32),
+                ("layers", ctypes.c_int32), ("path", ctypes.c_int32),
+                ("grouped_layers", ctypes.c_int32), ("max_group", ctypes.c_int32),
+                ("max_k", ctypes.c_int32), ("compaction", ctypes.c_int32),
+                ("packed_weight_bytes", ctypes.c_int64), ("total_nnz", ctypes.c_int64),
+                ("last_batch", ctypes.c_int64), ("last_n_categories", ctypes.c_int64),
+                ("launches_per_infer", ctypes.c_int64), ("live_edges", ctypes.c_int64),
+                ("kept_rows", ctypes.c_int64)]
+
+
+_LIB = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libsdnn.so (fails loudly when it has not been built)."""
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2004_10908_b200.build` "
+                              "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        V, I32, I64, U32 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32
+        P = ctypes.POINTER
+        L.sdnn_create.argtypes = [I32, I32, P(sdnn_layer), V, P(sdnn_opts), P(V)]
+        L.sdnn_create_empty.argtypes = [I32, I32, P(sdnn_opts), P(V)]
+        L.sdnn_set_layer.argtypes = [V, I32, P(sdnn_layer), V]
+        L.sdnn_infer.argtypes = [V, V, V, V, I64, V, P(I64), V]
+        L.sdnn_infer_device.argtypes = [V, V, V, V, I64, V, V, V]
+        L.sdnn_stats_get.argtypes = [V, P(sdnn_stats), V]
+        L.sdnn_validate_layer.argtypes = [I32, P(sdnn_layer), V, U32, P(sdnn_layer_info)]
+        L.sdnn_layer_times.argtypes = [V, V]
+        L.sdnn_destroy.argtypes = [V]
+        L.sdnn_destroy.restype = None
+        L.sdnn_last_error.argtypes = []
+        L.sdnn_last_error.restype = ctypes.c_char_p
+        L.sdnn_abi_version.restype = I32
+        for name in ["sdnn_create", "sdnn_create_empty", "sdnn_set_layer", "sdnn_infer",
+                     "sdnn_infer_device", "sdnn_stats_get", "sdnn_validate_layer",
+                     "sdnn_layer_times"]:
+            getattr(L, name).restype = I32
+        _LIB = L
+    return _LIB
+
+
+def _check(status: int):
+    if status != SDNN_OK:
+        raise SdnnError(status, lib().sdnn_last_error().decode(errors="replace"))
+
+
+def _p(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data
+
+
+def _opts(device=-1, flags=0, ymax=32.0, stream=None):
+    return sdnn_opts(int(device), int(flags), float(ymax), stream)
+
+
+def make_layer(layer, fmt: str = "csr"):
+    """sdnn_layer (plus the arrays it points to) from an object with rowptr,
+    colidx, val, ell, ell_val, uniform (sdnngen.Layer) or a dict."""
+    get = (lambda k: layer[k]) if isinstance(layer, dict) else (lambda k: getattr(layer, k))
+    if fmt == "csr":
+        rowptr = np.ascontiguousarray(get("rowptr"), np.int64)
+        idx = np.ascontiguousarray(get("colidx"), np.int32)
+        val = get("val")
+        val = None if val is None else np.ascontiguousarray(val, np.float32)
+        keep = (rowptr, idx, val)
+        s = sdnn_layer(SDNN_W_CSR, 0, _p(rowptr), _p(idx), _p(val), float(get("uniform")))
+    elif fmt == "ell":
+        ell = np.ascontiguousarray(get("ell"), np.int32)
+        val = get("ell_val")
+        val = None if val is None else np.ascontiguousarray(val, np.float32)
+        keep = (ell, val)
+        s = sdnn_layer(SDNN_W_ELLCOL, int(ell.shape[1]), None, _p(ell), _p(val),
+                       float(get("uniform")))
+    else:
+        raise ValueError(fmt)
+    return s, keep
+
+
+# ----------------------------------------------------------------- raw calls
+
+def sdnn_create(neurons: int, layers: Sequence, bias: np.ndarray, fmt: str = "csr",
+                device: int = -1, flags: int = 0, ymax: float = 32.0):
+    L = len(layers)
+    descs = (sdnn_layer * max(L, 1))()
+    keep = []
+    for l, lay in enumerate(layers):
+        descs[l], k = make_layer(lay, fmt)
+        keep.append(k)
+    bias = np.ascontiguousarray(bias, np.float32).reshape(-1)
+    h = ctypes.c_void_p()
+    o = _opts(device, flags, ymax)
+    _check(lib().sdnn_create(neurons, L, descs, _p(bias), ctypes.byref(o), ctypes.byref(h)))
+    return h
+
+
+def sdnn_create_empty(neurons: int, layers: int, device: int = -1, flags: int = 0,
+                      ymax: float = 32.0):
+    h = ctypes.c_void_p()
+    o = _opts(device, flags, ymax)
+    _check(lib().sdnn_create_empty(neurons, layers, ctypes.byref(o), ctypes.byref(h)))
+    return h
+
+
+def sdnn_set_layer(handle, l: int, layer, bias_l: np.ndarray, fmt: str = "csr"):
+    desc, keep = make_layer(layer, fmt)
+    bias_l = np.ascontiguousarray(bias_l, np.float32)
+    _check(lib().sdnn_set_layer(handle, int(l), ctypes.byref(desc), _p(bias_l)))
+    del keep
+
+
+def sdnn_infer(handle, rowptr: np.ndarray, idx: np.ndarray, val: Optional[np.ndarray],
+               neurons: int = 0, want_y: bool = False):
+    """Host-buffer inference.  Returns (categories int32[ncat], Y_L or None)."""
+    rowptr = np.ascontiguousarray(rowptr, np.int64)
+    idx = np.ascontiguousarray(idx, np.int32)
+    val = None if val is None else np.ascontiguousarray(val, np.float32)
+    batch = rowptr.size - 1
+    cats = np.empty(max(batch, 1), np.int32)
+    n = ctypes.c_int64()
+    y = np.empty((batch, neurons), np.float32) if want_y else None
+    _check(lib().sdnn_infer(handle, _p(rowptr), _p(idx), _p(val), batch, _p(cats),
+                            ctypes.byref(n), _p(y)))
+    return cats[:n.value].copy(), y
+
+
+def sdnn_infer_device(handle, d_rowptr: int, d_idx: int, d_val: Optional[int], batch: int,
+                      d_alive: Optional[int], d_y_out: Optional[int] = None, stream: int = 0):
+    _check(lib().sdnn_infer_device(handle, d_rowptr, d_idx, d_val, int(batch), d_alive,
+                                   d_y_out, stream or None))
+
+
+def sdnn_stats_get(handle, layers: int = 0):
+    s = sdnn_stats()
+    s.struct_size = ctypes.sizeof(sdnn_stats)
+    live = np.zeros(max(layers, 1), np.int64)
+    _check(lib().sdnn_stats_get(handle, ctypes.byref(s), _p(live)))
+    out = {f: getattr(s, f) for f, _ in sdnn_stats._fields_}
+    out["live_rows"] = live[:layers].tolist()
+    return out
+
+
+def sdnn_validate_layer(neurons: int, layer, bias_l, fmt: str = "csr", flags: int = 0):
+    """Host-only validation + grouping of one layer (no device needed)."""
+    desc, keep = make_layer(layer, fmt)
+    bias_l = np.ascontiguousarray(bias_l, np.float32)
+    info = sdnn_layer_info()
+    _check(lib().sdnn_validate_layer(int(neurons), ctypes.byref(desc), _p(bias_l), int(flags),
+                                     ctypes.byref(info)))
+    del keep
+    return {f: getattr(info, f) for f, _ in sdnn_layer_info._fields_}
+
+
+def sdnn_destroy(handle):
+    if handle:
+        lib().sdnn_destroy(handle)
+
+
+# ------------------------------------------------------------- convenience
+
+class Net:
+    """Owning wrapper around an sdnn_net handle."""
+
+    def __init__(self, neurons: int, layers: int, flags: int = 0, ymax: float = 32.0,
+                 device: int = -1):
+        self.n, self.L = int(neurons), int(layers)
+        self.h = sdnn_create_empty(self.n, self.L, device=device, flags=flags, ymax=ymax)
+
+    @classmethod
+    def from_layers(cls, neurons: int, layers: Sequence, fmt: str = "csr", **kw):
+        net = cls.__new__(cls)
+        net.n, net.L = int(neurons), len(layers)
+        bias = np.concatenate([np.asarray(l.bias if not isinstance(l, dict) else l["bias"],
+                                          np.float32) for l in layers]) if layers else np.zeros(0, np.float32)
+        net.h = sdnn_create(neurons, layers, bias, fmt=fmt, **kw)
+        return net
+
+    @classmethod
+    def from_spec(cls, spec, fmt: str = "ell", threads: int = 8, **kw):
+        """Generate (sdnngen) and load every layer, `threads` layers at a time
+        (ctypes releases the GIL while a layer is packed and uploaded)."""
+        import sdnngen
+        net = cls(spec.n, spec.L, **kw)
+
+        def one(l):
+            lay = sdnngen.gen_layer(spec, l, fmt=fmt)
+            sdnn_set_layer(net.h, l, lay, lay.bias, fmt=fmt)
+
+        if threads <= 1:
+            for l in range(spec.L):
+                one(l)
+        else:
+            with ThreadPoolExecutor(threads) as ex:
+                list(ex.map(one, range(spec.L)))
+        return net
+
+    def set_layer(self, l, layer, bias, fmt="csr"):
+        sdnn_set_layer(self.h, l, layer, bias, fmt)
+
+    def infer(self, rowptr, idx, val=None, want_y=False):
+        return sdnn_infer(self.h, rowptr, idx, val, self.n, want_y)
+
+    def infer_device(self, d_rowptr, d_idx, d_val, batch, d_alive, d_y_out=None, stream=0):
+        sdnn_infer_device(self.h, d_rowptr, d_idx, d_val, batch, d_alive, d_y_out, stream)
+
+    def infer_torch(self, rowptr_t, idx_t, val_t=None, alive_t=None, y_t=None, stream=None):
+        """Device inference on torch CUDA tensors (plumbing only).  Returns the
+        int32 bitmask tensor of ceil(B/32) words (bit i%32 of word i//32 = row i)."""
+        import torch
+        batch = rowptr_t.numel() - 1
+        if alive_t is None:
+            alive_t = torch.empty((batch + 31) // 32, dtype=torch.int32, device=rowptr_t.device)
+        s = stream if stream is not None else torch.cuda.current_stream(rowptr_t.device)
+        sdnn_infer_device(self.h, rowptr_t.data_ptr(), idx_t.data_ptr(),
+                          None if val_t is None else val_t.data_ptr(), batch,
+                          alive_t.data_ptr() if alive_t.numel() else None,
+                          None if y_t is None else y_t.data_ptr(), s.cuda_stream)
+        return alive_t
+
+    def stats(self):
+        return sdnn_stats_get(self.h, self.L)
+
+    def layer_times(self):
+        """Per-layer kernel durations (ms) of the last inference (SDNN_F_PROFILE)."""
+        ms = np.zeros(max(self.L, 1), np.float32)
+        _check(lib().sdnn_layer_times(self.h, _p(ms)))
+        return ms[:self.L].tolist()
+
+    def close(self):
+        if getattr(self, "h", None):
+            sdnn_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+def bitmask_to_ids(words: np.ndarray, batch: int) -> np.ndarray:
+    """Decode a category bitmask (uint32/int32 words) into ascending row ids."""
+    w = np.asarray(words).view(np.uint32)
+    bits = np.unpackbits(w.view(np.uint8), bitorder="little")[:batch]
+    return np.flatnonzero(bits).astype(np.int32)

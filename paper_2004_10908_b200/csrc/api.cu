@@ -1,0 +1,694 @@
+// api.cu -- the C ABI of include/sdnn.h: handle lifetime, streamed layer
+// loading into resident HBM, workspace management, the whole-network launch
+// (one captured CUDA Graph of the layer chain, "a cudaFlow maps
+// to a CUDA graph that can be executed using a single CPU call"), and the
+// host-buffer end-to-end call.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/sdnn.h"
+#include "sdnn_internal.h"
+
+using namespace sdnn;
+
+namespace {
+
+thread_local std::string g_err = "";
+
+sdnn_status fail(sdnn_status s, const std::string &m) {
+  g_err = m;
+  return s;
+}
+
+// bump allocator over large cudaMalloc chunks (layers are loaded once, freed
+// together at destroy)
+struct Arena {
+  std::vector<void *> chunks;
+  char *cur = nullptr;
+  size_t left = 0;
+  size_t total = 0;
+  std::mutex mu;
+  static constexpr size_t kChunk = size_t(256) << 20;
+  cudaError_t alloc(size_t bytes, void **out) {
+    std::lock_guard<std::mutex> g(mu);
+    bytes = (bytes + 255) & ~size_t(255);
+    if (bytes > left) {
+      const size_t sz = std::max(bytes, kChunk);
+      void *p = nullptr;
+      cudaError_t e = cudaMalloc(&p, sz);
+      if (e != cudaSuccess) return e;
+      chunks.push_back(p);
+      cur = (char *)p;
+      left = sz;
+    }
+    *out = cur;
+    cur += bytes;
+    left -= bytes;
+    total += bytes;
+    return cudaSuccess;
+  }
+  void release() {
+    for (void *p : chunks) cudaFree(p);
+    chunks.clear();
+    cur = nullptr;
+    left = 0;
+  }
+};
+
+}  // namespace
+
+struct sdnn_net {
+  int32_t n = 0, L = 0;
+  sdnn_opts opts{-1, 0u, 32.f, nullptr};
+  int device = 0;
+  cudaStream_t own = nullptr;
+  Arena arena;
+  std::vector<DevLayer> dl;
+  std::vector<uint8_t> set;        // layer loaded?
+  std::vector<uint8_t> bias_nonpos;
+  std::vector<int64_t> nnz;
+  std::atomic<int> nset{0};
+  int32_t grouped_layers = 0, max_group = 0, max_k = 0;
+  std::mutex stat_mu;
+  bool sticky = false;
+  LaunchCfg cfg;
+  // workspace
+  Workspace ws;
+  int64_t ws_cap = -1;             // stride the workspace was sized for
+  // captured layer chain
+  cudaGraphExec_t chain = nullptr;
+  bool chain_compact = false;
+  int64_t chain_launches = 0;
+  // device staging of Y0 for the host call
+  int64_t *d_rowptr = nullptr;
+  int32_t *d_idx = nullptr;
+  float *d_val = nullptr;
+  int64_t cap_rows = -1, cap_nnz = -1, cap_val = -1;
+  // pinned host staging
+  void *h_stage = nullptr;
+  size_t h_stage_cap = 0;
+  int32_t *h_cats = nullptr;
+  int64_t h_cats_cap = 0;
+  // per-layer timing events (SDNN_F_PROFILE)
+  std::vector<cudaEvent_t> ev_before, ev_after;
+  bool profiled = false;
+  // stats
+  int64_t last_batch = 0, last_ncat = 0, launches = 0;
+  std::vector<int32_t> last_live;
+};
+
+namespace {
+
+#define CK(call)                                                                 \
+  do {                                                                           \
+    cudaError_t _e = (call);                                                     \
+    if (_e != cudaSuccess) {                                                     \
+      net->sticky = true;                                                        \
+      return fail(SDNN_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(_e)); \
+    }                                                                            \
+  } while (0)
+
+bool compact_enabled(const sdnn_net *net) {
+  if (net->opts.flags & SDNN_F_NO_COMPACT) return false;
+  if (net->L < 1) return false;
+  for (int l = 0; l < net->L; ++l)
+    if (!net->bias_nonpos[l]) return false;     // a dead row could revive (reading A2/I2)
+  return true;
+}
+
+sdnn_status check_opts(const sdnn_opts *o, sdnn_opts &out) {
+  out = sdnn_opts{-1, 0u, 32.f, nullptr};
+  if (o) out = *o;
+  if (!(out.ymax > 0.f) || !std::isfinite(out.ymax)) return fail(SDNN_E_ARG, "ymax must be finite and > 0");
+  return SDNN_OK;
+}
+
+sdnn_status set_device(sdnn_net *net) {
+  if (net->sticky) return fail(SDNN_E_CUDA, "handle is in a failed CUDA state; destroy it");
+  CK(cudaSetDevice(net->device));
+  return SDNN_OK;
+}
+
+void free_ws(sdnn_net *net) {
+  Workspace &w = net->ws;
+  for (int i = 0; i < 2; ++i) {
+    cudaFree(w.Y[i]);
+    cudaFree(w.rid[i]);
+    cudaFree(w.alive[i]);
+    w.Y[i] = nullptr;
+    w.rid[i] = nullptr;
+    w.alive[i] = nullptr;
+  }
+  cudaFree(w.inmask);
+  cudaFree(w.wpre);
+  cudaFree(w.st);
+  cudaFree(w.live);
+  cudaFree(w.cats);
+  cudaFree(w.ncat);
+  w = Workspace();
+  if (net->chain) cudaGraphExecDestroy(net->chain);
+  net->chain = nullptr;
+  net->ws_cap = -1;
+}
+
+sdnn_status ensure_ws(sdnn_net *net, int64_t batch) {
+  const int64_t stride = std::max<int64_t>(128, (batch + 127) / 128 * 128);
+  if (net->ws_cap >= stride) return SDNN_OK;
+  free_ws(net);
+  if ((int64_t)net->n * stride > (int64_t(1) << 36)) return fail(SDNN_E_UNSUPPORTED, "batch too large");
+  Workspace &w = net->ws;
+  w.stride = stride;
+  w.words = stride / 32;
+  const size_t ybytes = sizeof(float) * (size_t)net->n * (size_t)stride;
+  for (int i = 0; i < 2; ++i) {
+    if (cudaMalloc(&w.Y[i], ybytes) != cudaSuccess) {
+      cudaGetLastError();
+      free_ws(net);
+      return fail(SDNN_E_NOMEM, "cannot allocate activation buffers (" + std::to_string(2 * ybytes) + " B)");
+    }
+    CK(cudaMalloc(&w.rid[i], sizeof(int32_t) * stride));
+    CK(cudaMalloc(&w.alive[i], sizeof(uint32_t) * w.words));
+  }
+  CK(cudaMemset(w.Y[1], 0, ybytes));
+  CK(cudaMalloc(&w.inmask, sizeof(uint32_t) * w.words));
+  CK(cudaMalloc(&w.wpre, sizeof(int32_t) * (w.words + 1)));
+  CK(cudaMalloc(&w.st, sizeof(LayerState) * (net->L + 1)));
+  CK(cudaMalloc(&w.live, sizeof(int32_t) * std::max(1, net->L)));
+  CK(cudaMalloc(&w.cats, sizeof(int32_t) * stride));
+  CK(cudaMalloc(&w.ncat, sizeof(int32_t)));
+  net->ws_cap = stride;
+  return SDNN_OK;
+}
+
+void enqueue_chain(sdnn_net *net, bool compact, cudaStream_t s, int64_t *launches) {
+  const float ymax = net->opts.ymax;
+  const bool prof = (net->opts.flags & SDNN_F_PROFILE) && (int)net->ev_before.size() == net->L;
+  int64_t c = 0;
+  for (int32_t l = 0; l < net->L; ++l) {
+    if (prof) cudaEventRecordWithFlags(net->ev_before[l], s, cudaEventRecordExternal);
+    launch_layer(net->cfg, net->ws, net->dl[l], l, ymax, net->n, s);
+    if (prof) cudaEventRecordWithFlags(net->ev_after[l], s, cudaEventRecordExternal);
+    ++c;
+    if (l + 1 < net->L) {
+      launch_scan(net->ws, l, compact, net->n, s);
+      launch_compact_copy(net->cfg, net->ws, l, net->n, s);
+      c += 2;
+    }
+  }
+  if (launches) *launches = c;
+}
+
+sdnn_status run_chain(sdnn_net *net, bool compact, cudaStream_t s) {
+  if (net->L == 0) return SDNN_OK;
+  if (net->opts.flags & SDNN_F_NO_GRAPH) {
+    enqueue_chain(net, compact, s, &net->chain_launches);
+    CK(cudaGetLastError());
+    return SDNN_OK;
+  }
+  if (!net->chain || net->chain_compact != compact) {
+    if (net->chain) cudaGraphExecDestroy(net->chain);
+    net->chain = nullptr;
+    cudaStream_t cs;
+    CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    cudaGraph_t graph;
+    CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    enqueue_chain(net, compact, cs, &net->chain_launches);
+    cudaError_t e = cudaStreamEndCapture(cs, &graph);
+    cudaStreamDestroy(cs);
+    CK(e);
+    e = cudaGraphInstantiate(&net->chain, graph, 0);
+    cudaGraphDestroy(graph);
+    CK(e);
+    net->chain_compact = compact;
+  }
+  CK(cudaGraphLaunch(net->chain, s));
+  return SDNN_OK;
+}
+
+// Everything of one inference after Y0 is on the device.
+sdnn_status infer_device_impl(sdnn_net *net, const int64_t *d_rowptr, const int32_t *d_idx,
+                              const float *d_val, int64_t batch, uint32_t *d_alive,
+                              float *d_yout, cudaStream_t s) {
+  if (net->nset.load() != net->L) return fail(SDNN_E_STATE, "not every layer has been set");
+  sdnn_status st = ensure_ws(net, batch);
+  if (st) return st;
+  const bool compact = compact_enabled(net);
+  launch_densify(net->cfg, net->ws, net->n, batch, d_rowptr, d_idx, d_val, compact, s);
+  int64_t launches = 4;
+  if (net->L == 0) {
+    launch_zero_layers_alive(net->ws, batch, d_rowptr, d_val, s);
+    launches += 1;
+  } else {
+    st = run_chain(net, compact, s);
+    if (st) return st;
+    launches += net->chain_launches;
+  }
+  const int32_t last = net->L == 0 ? 0 : net->L - 1;
+  launch_readout(net->ws, last, net->L > 0, d_alive, batch, s);
+  launches += 1 + (d_alive ? 1 : 0);
+  if (d_yout) {
+    launch_yout(net->ws, net->L == 0 ? -1 : last, net->n, batch, d_yout, s);
+    launches += 2;
+  }
+  CK(cudaGetLastError());
+  net->last_batch = batch;
+  net->launches = launches;
+  net->profiled = (net->opts.flags & SDNN_F_PROFILE) && net->L > 0;
+  return SDNN_OK;
+}
+
+int nthreads_default() {
+  unsigned h = std::thread::hardware_concurrency();
+  return (int)std::max(1u, std::min(h, 32u));
+}
+
+template <class F>
+void parallel_for(int64_t n, int nt, F f) {
+  if (nt <= 1 || n < 4096) {
+    f(0, n);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (int t = 0; t < nt; ++t) {
+    const int64_t a = n * t / nt, b = n * (t + 1) / nt;
+    th.emplace_back([=] { f(a, b); });
+  }
+  for (auto &x : th) x.join();
+}
+
+// Host validation of Y0 (sdnn_infer only): monotone rowptr, index range,
+// no duplicate per row, finite values.
+sdnn_status validate_y0(int32_t n, const int64_t *rowptr, const int32_t *idx, const float *val,
+                        int64_t batch) {
+  if (rowptr[0] != 0) return fail(SDNN_E_FORMAT, "y0_rowptr[0] != 0");
+  for (int64_t i = 0; i < batch; ++i)
+    if (rowptr[i + 1] < rowptr[i]) return fail(SDNN_E_FORMAT, "y0_rowptr not non-decreasing");
+  std::atomic<int64_t> bad{-1};
+  std::atomic<int> kind{0};
+  const int nt = nthreads_default();
+  parallel_for(batch, nt, [&](int64_t a, int64_t b) {
+    std::vector<int64_t> mark(n, -1);
+    for (int64_t i = a; i < b && bad.load() < 0; ++i)
+      for (int64_t e = rowptr[i]; e < rowptr[i + 1]; ++e) {
+        const int32_t k = idx[e];
+        if (k < 0 || k >= n) { bad = i; kind = 1; break; }
+        if (mark[k] == i) { bad = i; kind = 2; break; }
+        mark[k] = i;
+        if (val && !std::isfinite(val[e])) { bad = i; kind = 3; break; }
+      }
+  });
+  if (bad.load() >= 0) {
+    const char *what[] = {"", "index out of range", "duplicate index", "non-finite value"};
+    return fail(SDNN_E_FORMAT, std::string("Y0 row ") + std::to_string(bad.load()) + ": " + what[kind.load()]);
+  }
+  return SDNN_OK;
+}
+
+void *grow_pinned(sdnn_net *net, size_t bytes) {
+  if (bytes <= net->h_stage_cap) return net->h_stage;
+  if (net->h_stage) cudaFreeHost(net->h_stage);
+  net->h_stage = nullptr;
+  net->h_stage_cap = 0;
+  const size_t cap = std::max(bytes, net->h_stage_cap * 3 / 2);
+  if (cudaHostAlloc(&net->h_stage, cap, cudaHostAllocDefault) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  net->h_stage_cap = cap;
+  return net->h_stage;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+int32_t sdnn_abi_version(void) { return SDNN_ABI_VERSION; }
+
+const char *sdnn_last_error(void) { return g_err.c_str(); }
+
+sdnn_status sdnn_create_empty(int32_t neurons, int32_t layers, const sdnn_opts *opts,
+                              sdnn_net **out) {
+  if (!out) return fail(SDNN_E_ARG, "out is NULL");
+  *out = nullptr;
+  if (neurons < 1) return fail(SDNN_E_ARG, "neurons < 1");
+  if (neurons > 65536) return fail(SDNN_E_UNSUPPORTED, "neurons > 65536 (u16 source indices)");
+  if (layers < 0) return fail(SDNN_E_ARG, "layers < 0");
+  sdnn_opts o;
+  sdnn_status st = check_opts(opts, o);
+  if (st) return st;
+  int dev = o.device;
+  if (dev < 0) {
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(SDNN_E_CUDA, "no CUDA device");
+    }
+  }
+  if (cudaSetDevice(dev) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(SDNN_E_CUDA, "cannot select CUDA device " + std::to_string(dev));
+  }
+  sdnn_net *net = new (std::nothrow) sdnn_net();
+  if (!net) return fail(SDNN_E_NOMEM, "host allocation failed");
+  net->n = neurons;
+  net->L = layers;
+  net->opts = o;
+  net->device = dev;
+  net->dl.resize(layers);
+  net->set.assign(layers, 0);
+  net->bias_nonpos.assign(layers, 1);
+  net->nnz.assign(layers, 0);
+  net->last_live.assign(std::max(layers, 1), 0);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  net->cfg.sms = sms;
+  net->cfg.layer_blocks = sms * 2;   // 2 resident 256-thread CTAs per SM (128 regs)
+  net->cfg.copy_blocks = sms * 4;
+  if (cudaStreamCreateWithFlags(&net->own, cudaStreamNonBlocking) != cudaSuccess) {
+    cudaGetLastError();
+    delete net;
+    return fail(SDNN_E_CUDA, "cudaStreamCreate failed");
+  }
+  if (o.flags & SDNN_F_PROFILE) {
+    net->ev_before.resize(layers);
+    net->ev_after.resize(layers);
+    for (int l = 0; l < layers; ++l)
+      if (cudaEventCreate(&net->ev_before[l]) != cudaSuccess ||
+          cudaEventCreate(&net->ev_after[l]) != cudaSuccess) {
+        cudaGetLastError();
+        sdnn_destroy(net);
+        return fail(SDNN_E_CUDA, "cudaEventCreate failed");
+      }
+  }
+  *out = net;
+  return SDNN_OK;
+}
+
+sdnn_status sdnn_set_layer(sdnn_net *net, int32_t l, const sdnn_layer *W, const float *bias_l) {
+  if (!net || !W || !bias_l) return fail(SDNN_E_ARG, "NULL argument");
+  if (l < 0 || l >= net->L) return fail(SDNN_E_ARG, "layer index out of range");
+  sdnn_status st = set_device(net);
+  if (st) return st;
+  LayerIn in{W->format, W->ell_k, W->rowptr, W->idx, W->val, W->uniform_value};
+  PackedLayer p;
+  std::string msg;
+  const int rc = pack_layer(net->n, in, bias_l, !(net->opts.flags & SDNN_F_NO_GROUPS), p, msg);
+  if (rc) return fail(rc, "layer " + std::to_string(l) + ": " + msg);
+  // upload: one arena block per layer
+  const size_t G = p.ngroups;
+  const size_t b_src = sizeof(uint16_t) * p.src.size(), b_col = sizeof(int32_t) * p.col.size();
+  const size_t b_gk = sizeof(int32_t) * G, b_val = sizeof(float) * p.val.size();
+  const size_t b_bias = sizeof(float) * net->n;
+  auto up = [&](const void *h, size_t bytes, void **d) -> sdnn_status {
+    if (bytes == 0) { *d = nullptr; return SDNN_OK; }
+    cudaError_t e = net->arena.alloc(bytes, d);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(SDNN_E_NOMEM, "device allocation for layer " + std::to_string(l) + " failed");
+    }
+    CK(cudaMemcpy(*d, h, bytes, cudaMemcpyHostToDevice));
+    return SDNN_OK;
+  };
+  DevLayer d{};
+  void *ps = nullptr, *pc = nullptr, *pk = nullptr, *pg = nullptr, *pv = nullptr, *pb = nullptr;
+  if ((st = up(p.src.data(), b_src, &ps)) || (st = up(p.col.data(), b_col, &pc)) ||
+      (st = up(p.gk.data(), b_gk, &pk)) || (st = up(p.gg.data(), b_gk, &pg)) ||
+      (st = up(p.val.data(), b_val, &pv)) || (st = up(p.bias.data(), b_bias, &pb)))
+    return st;
+  d.src = (const uint16_t *)ps;
+  d.col = (const int32_t *)pc;
+  d.gk = (const int32_t *)pk;
+  d.gg = (const int32_t *)pg;
+  d.val = p.uniform ? nullptr : (const float *)pv;
+  d.bias = (const float *)pb;
+  d.ngroups = p.ngroups;
+  d.kmax = p.kmax;
+  d.gmax = p.gmax;
+  d.wu = p.wu;
+  d.uniform = p.uniform ? 1 : 0;
+  d.regular = p.regular ? 1 : 0;
+  d.nnz = p.nnz;
+  {
+    std::lock_guard<std::mutex> g(net->stat_mu);
+    const bool was = net->set[l];
+    net->dl[l] = d;
+    net->bias_nonpos[l] = p.bias_nonpos ? 1 : 0;
+    net->nnz[l] = p.nnz;
+    if (p.gmax > 1) net->grouped_layers += was ? 0 : 1;
+    net->max_group = std::max(net->max_group, p.gmax);
+    net->max_k = std::max(net->max_k, p.kmax);
+    if (!was) {
+      net->set[l] = 1;
+      net->nset.fetch_add(1);
+    }
+    if (net->chain) {                     // layer pointers changed: recapture
+      cudaGraphExecDestroy(net->chain);
+      net->chain = nullptr;
+    }
+  }
+  return SDNN_OK;
+}
+
+sdnn_status sdnn_create(int32_t neurons, int32_t layers, const sdnn_layer *W, const float *bias,
+                        const sdnn_opts *opts, sdnn_net **out) {
+  if (!out) return fail(SDNN_E_ARG, "out is NULL");
+  *out = nullptr;
+  if (layers > 0 && (!W || !bias)) return fail(SDNN_E_ARG, "W or bias is NULL");
+  sdnn_net *net = nullptr;
+  sdnn_status st = sdnn_create_empty(neurons, layers, opts, &net);
+  if (st) return st;
+  // pack layers in parallel (create-time, not in the timed region)
+  const int nt = std::min(nthreads_default(), std::max(1, layers));
+  std::vector<sdnn_status> rcs(nt, SDNN_OK);
+  std::vector<std::string> errs(nt);
+  std::vector<std::thread> th;
+  std::atomic<int> next{0};
+  for (int t = 0; t < nt; ++t)
+    th.emplace_back([&, t] {
+      cudaSetDevice(net->device);
+      for (int l = next++; l < layers; l = next++) {
+        const sdnn_status r = sdnn_set_layer(net, l, &W[l], bias + (int64_t)l * neurons);
+        if (r && !rcs[t]) {
+          rcs[t] = r;
+          errs[t] = sdnn_last_error();
+        }
+      }
+    });
+  for (auto &x : th) x.join();
+  for (int t = 0; t < nt; ++t)
+    if (rcs[t]) {
+      sdnn_destroy(net);
+      return fail(rcs[t], errs[t]);
+    }
+  *out = net;
+  return SDNN_OK;
+}
+
+sdnn_status sdnn_infer_device(sdnn_net *net, const int64_t *d_rowptr, const int32_t *d_idx,
+                              const float *d_val, int64_t batch, uint32_t *d_alive,
+                              float *d_y_out, void *stream) {
+  if (!net) return fail(SDNN_E_ARG, "net is NULL");
+  if (batch < 0) return fail(SDNN_E_ARG, "batch < 0");
+  if (batch > (int64_t(1) << 30)) return fail(SDNN_E_UNSUPPORTED, "batch > 2^30");
+  if (!d_rowptr) return fail(SDNN_E_ARG, "d_rowptr is NULL");
+  sdnn_status st = set_device(net);
+  if (st) return st;
+  return infer_device_impl(net, d_rowptr, d_idx, d_val, batch, d_alive, d_y_out,
+                           (cudaStream_t)stream);
+}
+
+sdnn_status sdnn_infer(sdnn_net *net, const int64_t *y0_rowptr, const int32_t *y0_idx,
+                       const float *y0_val, int64_t batch, int32_t *categories,
+                       int64_t *n_categories, float *y_out) {
+  if (!net || !y0_rowptr || !n_categories) return fail(SDNN_E_ARG, "NULL argument");
+  if (batch < 0) return fail(SDNN_E_ARG, "batch < 0");
+  if (batch > (int64_t(1) << 30)) return fail(SDNN_E_UNSUPPORTED, "batch > 2^30");
+  if (batch > 0 && !categories) return fail(SDNN_E_ARG, "categories is NULL");
+  sdnn_status st = set_device(net);
+  if (st) return st;
+  const int64_t nnz = y0_rowptr[batch];
+  if (nnz > 0 && !y0_idx) return fail(SDNN_E_ARG, "y0_idx is NULL");
+  if (!(net->opts.flags & SDNN_F_TRUST_INPUT)) {
+    st = validate_y0(net->n, y0_rowptr, y0_idx, y0_val, batch);
+    if (st) return st;
+  }
+  cudaStream_t s = net->opts.stream ? (cudaStream_t)net->opts.stream : net->own;
+  // device input buffers (grow-only)
+  if (batch + 1 > net->cap_rows) {
+    cudaFree(net->d_rowptr);
+    net->d_rowptr = nullptr;
+    CK(cudaMalloc(&net->d_rowptr, sizeof(int64_t) * (batch + 1)));
+    net->cap_rows = batch + 1;
+  }
+  if (nnz > net->cap_nnz) {
+    cudaFree(net->d_idx);
+    net->d_idx = nullptr;
+    CK(cudaMalloc(&net->d_idx, sizeof(int32_t) * std::max<int64_t>(nnz, 1)));
+    net->cap_nnz = nnz;
+  }
+  if (y0_val && nnz > net->cap_val) {
+    cudaFree(net->d_val);
+    net->d_val = nullptr;
+    CK(cudaMalloc(&net->d_val, sizeof(float) * std::max<int64_t>(nnz, 1)));
+    net->cap_val = nnz;
+  }
+  // host -> pinned staging -> device, chunked so the memcpy of chunk c+1
+  // overlaps the DMA of chunk c
+  {
+    struct Part { const void *h; void *d; size_t bytes; };
+    Part parts[3] = {{y0_rowptr, net->d_rowptr, sizeof(int64_t) * (size_t)(batch + 1)},
+                     {y0_idx, net->d_idx, sizeof(int32_t) * (size_t)nnz},
+                     {y0_val, net->d_val, y0_val ? sizeof(float) * (size_t)nnz : 0}};
+    const size_t kChunk = size_t(64) << 20;
+    char *stage = (char *)grow_pinned(net, 2 * kChunk);
+    if (!stage) return fail(SDNN_E_NOMEM, "pinned staging allocation failed");
+    cudaEvent_t ev[2];
+    CK(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+    bool used[2] = {false, false};
+    int slot = 0;
+    for (const Part &p : parts) {
+      if (p.bytes == 0) continue;
+      cudaPointerAttributes pa;
+      if (cudaPointerGetAttributes(&pa, p.h) == cudaSuccess && pa.type == cudaMemoryTypeHost) {
+        // caller's buffer is page-locked: DMA straight from it
+        CK(cudaMemcpyAsync(p.d, p.h, p.bytes, cudaMemcpyHostToDevice, s));
+        continue;
+      }
+      cudaGetLastError();
+      for (size_t off = 0; off < p.bytes; off += kChunk) {
+        const size_t b = std::min(kChunk, p.bytes - off);
+        if (used[slot]) CK(cudaEventSynchronize(ev[slot]));
+        std::memcpy(stage + slot * kChunk, (const char *)p.h + off, b);
+        CK(cudaMemcpyAsync((char *)p.d + off, stage + slot * kChunk, b, cudaMemcpyHostToDevice, s));
+        CK(cudaEventRecord(ev[slot], s));
+        used[slot] = true;
+        slot ^= 1;
+      }
+    }
+    cudaEventDestroy(ev[0]);
+    cudaEventDestroy(ev[1]);
+  }
+  st = infer_device_impl(net, net->d_rowptr, net->d_idx, y0_val ? net->d_val : nullptr, batch,
+                         nullptr, nullptr, s);
+  if (st) return st;
+  float *d_yout = nullptr;
+  if (y_out && batch > 0) {
+    CK(cudaMalloc(&d_yout, sizeof(float) * (size_t)net->n * (size_t)batch));
+    launch_yout(net->ws, net->L == 0 ? -1 : net->L - 1, net->n, batch, d_yout, s);
+  }
+  int32_t ncat = 0;
+  CK(cudaMemcpyAsync(&ncat, net->ws.ncat, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (ncat > 0) CK(cudaMemcpy(categories, net->ws.cats, sizeof(int32_t) * ncat, cudaMemcpyDeviceToHost));
+  if (d_yout) {
+    CK(cudaMemcpy(y_out, d_yout, sizeof(float) * (size_t)net->n * (size_t)batch, cudaMemcpyDeviceToHost));
+    cudaFree(d_yout);
+  }
+  *n_categories = ncat;
+  net->last_ncat = ncat;
+  return SDNN_OK;
+}
+
+sdnn_status sdnn_validate_layer(int32_t neurons, const sdnn_layer *W, const float *bias_l,
+                                uint32_t flags, sdnn_layer_info *info) {
+  if (!W || !bias_l) return fail(SDNN_E_ARG, "NULL argument");
+  if (neurons < 1) return fail(SDNN_E_ARG, "neurons < 1");
+  if (neurons > 65536) return fail(SDNN_E_UNSUPPORTED, "neurons > 65536 (u16 source indices)");
+  LayerIn in{W->format, W->ell_k, W->rowptr, W->idx, W->val, W->uniform_value};
+  PackedLayer p;
+  std::string msg;
+  const int rc = pack_layer(neurons, in, bias_l, !(flags & SDNN_F_NO_GROUPS), p, msg);
+  if (rc) return fail(rc, msg);
+  if (info) {
+    info->ngroups = p.ngroups;
+    info->kmax = p.kmax;
+    info->gmax = p.gmax;
+    info->uniform = p.uniform ? 1 : 0;
+    info->regular = p.regular ? 1 : 0;
+    info->bias_nonpositive = p.bias_nonpos ? 1 : 0;
+    info->nnz = p.nnz;
+  }
+  return SDNN_OK;
+}
+
+sdnn_status sdnn_layer_times(const sdnn_net *cnet, float *ms) {
+  sdnn_net *net = const_cast<sdnn_net *>(cnet);
+  if (!net || !ms) return fail(SDNN_E_ARG, "NULL argument");
+  if (!(net->opts.flags & SDNN_F_PROFILE)) return fail(SDNN_E_STATE, "handle not created with SDNN_F_PROFILE");
+  if (!net->profiled) return fail(SDNN_E_STATE, "no profiled inference yet");
+  sdnn_status st = set_device(net);
+  if (st) return st;
+  for (int l = 0; l < net->L; ++l) {
+    CK(cudaEventSynchronize(net->ev_after[l]));
+    CK(cudaEventElapsedTime(&ms[l], net->ev_before[l], net->ev_after[l]));
+  }
+  return SDNN_OK;
+}
+
+sdnn_status sdnn_stats_get(const sdnn_net *cnet, sdnn_stats *out, int64_t *live_rows) {
+  sdnn_net *net = const_cast<sdnn_net *>(cnet);
+  if (!net || !out) return fail(SDNN_E_ARG, "NULL argument");
+  if (out->struct_size < (int32_t)sizeof(sdnn_stats)) return fail(SDNN_E_ARG, "struct_size too small");
+  sdnn_stats s{};
+  s.struct_size = sizeof(sdnn_stats);
+  s.neurons = net->n;
+  s.layers = net->L;
+  s.path = 0;
+  s.grouped_layers = net->grouped_layers;
+  s.max_group = net->max_group;
+  s.max_k = net->max_k;
+  s.compaction = compact_enabled(net) ? 1 : 0;
+  s.packed_weight_bytes = (int64_t)net->arena.total;
+  for (int l = 0; l < net->L; ++l) s.total_nnz += net->nnz[l];
+  s.last_batch = net->last_batch;
+  s.last_n_categories = net->last_ncat;
+  s.launches_per_infer = net->launches;
+  if (net->L > 0 && net->ws.live && net->last_batch > 0) {
+    sdnn_status st = set_device(net);
+    if (st) return st;
+    std::vector<int32_t> live(net->L);
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(live.data(), net->ws.live, sizeof(int32_t) * net->L, cudaMemcpyDeviceToHost));
+    if (live_rows)
+      for (int l = 0; l < net->L; ++l) live_rows[l] = live[l];
+    // live edges: layer l processes the rows alive after layer l-1 (all kept rows for l = 0)
+    int32_t kept0 = 0;
+    LayerState s0;
+    CK(cudaMemcpy(&s0, net->ws.st, sizeof(LayerState), cudaMemcpyDeviceToHost));
+    kept0 = s0.width;
+    s.kept_rows = kept0;
+    for (int l = 0; l < net->L; ++l)
+      s.live_edges += (int64_t)(l == 0 ? kept0 : live[l - 1]) * net->nnz[l];
+  }
+  *out = s;
+  return SDNN_OK;
+}
+
+void sdnn_destroy(sdnn_net *net) {
+  if (!net) return;
+  cudaSetDevice(net->device);
+  cudaDeviceSynchronize();
+  free_ws(net);
+  net->arena.release();
+  cudaFree(net->d_rowptr);
+  cudaFree(net->d_idx);
+  cudaFree(net->d_val);
+  if (net->h_stage) cudaFreeHost(net->h_stage);
+  if (net->own) cudaStreamDestroy(net->own);
+  for (auto e : net->ev_before) if (e) cudaEventDestroy(e);
+  for (auto e : net->ev_after) if (e) cudaEventDestroy(e);
+  cudaGetLastError();
+  delete net;
+}
+
+}  // extern "C"

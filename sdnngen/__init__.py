@@ -204,14 +204,31 @@ def _csr_from_ell(n: int, ell: np.ndarray, ell_val: Optional[np.ndarray]):
     return rowptr, colidx, val
 
 
-def gen_layer(spec: NetSpec, l: int) -> Layer:
+def _rn_lists(n: int, l: int, outer: np.ndarray, inner: np.ndarray) -> np.ndarray:
+    lib = _helper()
+    if lib is None:
+        return outer[_rn_sets(n, l, inner)].astype(np.int32)
+    out = np.empty((n, 32), np.int32)
+    outer = np.ascontiguousarray(outer, np.int64)
+    inner = np.ascontiguousarray(inner, np.int64)
+    lib.rn_lists(n, rn_field(n, l), _p(outer), _p(inner), _p(out))
+    return out
+
+
+def gen_layer(spec: NetSpec, l: int, fmt: str = "both") -> Layer:
+    """Layer l of the network.  fmt: "both" (CSR + ELL), "csr" or "ell" (the
+    other format's fields are left empty where producing them costs time)."""
     n = spec.n
+    want_csr, want_ell = fmt in ("both", "csr"), fmt in ("both", "ell")
+    empty_i64, empty_i32 = np.zeros(0, np.int64), np.zeros((0, 32), np.int32)
     if spec.kind == "rn":
         pin, pout = _perm(spec, l), _perm(spec, l + 1)
-        inv_in, inv_out = _inv(pin), _inv(pout)
-        c = np.arange(n, dtype=np.int64)
-        ell = pin[_rn_sets(n, l, inv_out[c])].astype(np.int32)        # sources of output c
-        rowptr, colidx = _csr_from_out_lists(n, pout[_rn_sets(n, l, inv_in[c])])
+        ell = _rn_lists(n, l, pin, _inv(pout)) if want_ell else empty_i32
+        if want_csr:
+            rowptr = np.arange(0, (n + 1) * 32, 32, dtype=np.int64)
+            colidx = _rn_lists(n, l, pout, _inv(pin)).reshape(-1)
+        else:
+            rowptr, colidx = empty_i64, np.zeros(0, np.int32)
         val = ell_val = None
     elif spec.kind == "ka":
         pin, pout = _perm(spec, l), _perm(spec, l + 1)
@@ -251,8 +268,10 @@ def gen_layer(spec: NetSpec, l: int) -> Layer:
         raise ValueError(spec.kind)
     if spec.kind != "irr" and spec.wdist == "random":
         r = _rng(spec.seed, 5, l)
+        if ell.size == 0:
+            raise ValueError("random weights need the ELL structure (fmt='both' or 'ell')")
         ell_val = r.uniform(-0.05, 0.15, size=ell.shape).astype(np.float32)
-        _, _, val = _csr_from_ell(n, ell, ell_val)
+        rowptr, colidx, val = _csr_from_ell(n, ell, ell_val)
     if spec.kind == "irr":
         lo, hi = spec.extra["bias_range"]
         bias = _rng(spec.seed, 6, l).uniform(lo, hi, size=n).astype(np.float32)
@@ -293,6 +312,7 @@ def _helper():
         V, I64, I32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32
         lib.ms_count.argtypes = [I64, V, I32, I32, V, V, V, V]
         lib.ms_fill.argtypes = [I64, V, I32, I32, V, V, V, V, V]
+        lib.rn_lists.argtypes = [I64, I32, V, V, V]
         _HELPER = lib
     except Exception:                       # pragma: no cover - gcc missing
         _HELPER = False

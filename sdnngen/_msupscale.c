@@ -43,3 +43,16 @@ void ms_fill(int64_t B, const uint8_t *img, int32_t h, int32_t w,
         }
     }
 }
+
+/* RadiX-Net butterfly lists: out[c*32 + v] = outer[(inner[c] & ~(31<<p)) | (v<<p)].
+ * With outer = pi_l, inner = pi_{l+1}^-1 this is the source list of output c
+ * (ELLCOL); with outer = pi_{l+1}, inner = pi_l^-1 the output list of input c
+ * (CSR row c).  Index bookkeeping only. */
+void rn_lists(int64_t n, int32_t p, const int64_t *outer, const int64_t *inner, int32_t *out) {
+    const int64_t mask = ~((int64_t)31 << p);
+    for (int64_t c = 0; c < n; ++c) {
+        const int64_t base = inner[c] & mask;
+        int32_t *o = out + c * 32;
+        for (int64_t v = 0; v < 32; ++v) o[v] = (int32_t)outer[base | (v << p)];
+    }
+}

@@ -1,0 +1,149 @@
+"""CPU-side checks of the C-ABI boundary: the library builds, loads and exports
+every symbol include/sdnn.h declares; host validation and grouping (no device
+needed); the product path never imports the oracle and fails loudly without a
+device."""
+import ast
+import os
+import re
+
+import numpy as np
+import pytest
+
+import sdnngen as g
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def sd():
+    from paper_2004_10908_b200 import build
+    build.build()
+    import paper_2004_10908_b200 as sd
+    sd.lib()
+    return sd
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "sdnn.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(sdnn_[a-z_]+)\s*\(", src)))
+
+
+def test_exports_every_declared_symbol(sd):
+    declared = header_functions()
+    assert len(declared) >= 9
+    L = sd.lib()
+    for name in declared:
+        assert hasattr(L, name), name
+    assert sorted(sd.EXPORTS) == declared
+    assert L.sdnn_abi_version() == 1
+
+
+def test_destroy_null_is_safe(sd):
+    sd.lib().sdnn_destroy(None)
+
+
+def _csr(n, edges, vals=None):
+    rowptr = np.zeros(n + 1, np.int64)
+    edges = sorted(edges)
+    for k, j in edges:
+        rowptr[k + 1] += 1
+    rowptr = np.cumsum(rowptr).astype(np.int64)
+    colidx = np.array([j for k, j in edges], np.int32)
+    return dict(rowptr=rowptr, colidx=colidx, val=vals, uniform=0.0625)
+
+
+def test_validate_errors(sd):
+    n = 4
+    b = np.zeros(n, np.float32)
+    ok = _csr(n, [(0, 1), (1, 1), (3, 2)])
+    info = sd.sdnn_validate_layer(n, ok, b)
+    assert info["nnz"] == 3 and info["uniform"] == 1 and info["kmax"] == 2
+    bad_range = dict(ok, colidx=np.array([1, 1, 7], np.int32))
+    with pytest.raises(sd.SdnnError) as e:
+        sd.sdnn_validate_layer(n, bad_range, b)
+    assert e.value.status == sd.SDNN_E_FORMAT
+    dup = _csr(n, [(0, 1), (0, 2)])
+    dup["colidx"] = np.array([1, 1], np.int32)
+    with pytest.raises(sd.SdnnError) as e:
+        sd.sdnn_validate_layer(n, dup, b)
+    assert e.value.status == sd.SDNN_E_FORMAT and "duplicate" in str(e.value)
+    nonmono = dict(ok, rowptr=np.array([0, 2, 1, 3, 3], np.int64))
+    with pytest.raises(sd.SdnnError):
+        sd.sdnn_validate_layer(n, nonmono, b)
+    nan_w = dict(ok, val=np.array([1, np.nan, 1], np.float32))
+    with pytest.raises(sd.SdnnError):
+        sd.sdnn_validate_layer(n, nan_w, b)
+    with pytest.raises(sd.SdnnError):
+        sd.sdnn_validate_layer(n, ok, np.array([0, np.inf, 0, 0], np.float32))
+    with pytest.raises(sd.SdnnError) as e:
+        sd.sdnn_validate_layer(70000, ok, np.zeros(70000, np.float32))
+    assert e.value.status == sd.SDNN_E_UNSUPPORTED
+    info = sd.sdnn_validate_layer(n, ok, np.array([0, 0.5, 0, 0], np.float32))
+    assert info["bias_nonpositive"] == 0
+
+
+def test_validate_ellcol(sd):
+    n = 4
+    ell = np.array([[1, -1], [-1, -1], [3, 0], [2, 1]], np.int32)
+    info = sd.sdnn_validate_layer(n, dict(ell=ell, ell_val=None, uniform=0.5), np.zeros(n, np.float32),
+                                  fmt="ell")
+    assert info["nnz"] == 5 and info["kmax"] == 2
+    bad = np.array([[1, 1], [-1, -1], [3, 0], [2, 1]], np.int32)
+    with pytest.raises(sd.SdnnError):
+        sd.sdnn_validate_layer(n, dict(ell=bad, ell_val=None, uniform=0.5),
+                               np.zeros(n, np.float32), fmt="ell")
+    oob = np.array([[9, -1], [-1, -1], [3, 0], [2, 1]], np.int32)
+    with pytest.raises(sd.SdnnError):
+        sd.sdnn_validate_layer(n, dict(ell=oob, ell_val=None, uniform=0.5),
+                               np.zeros(n, np.float32), fmt="ell")
+
+
+@pytest.mark.parametrize("fmt", ["csr", "ell"])
+def test_grouping_rn_rr(sd, fmt):
+    n = 1024
+    lay = g.gen_layer(g.rn_spec(n, 3), 1)
+    info = sd.sdnn_validate_layer(n, lay, lay.bias, fmt=fmt)
+    assert (info["ngroups"], info["gmax"], info["kmax"], info["regular"], info["uniform"]) == \
+        (n // 32, 32, 32, 1, 1)
+    info = sd.sdnn_validate_layer(n, lay, lay.bias, fmt=fmt, flags=sd.SDNN_F_NO_GROUPS)
+    assert (info["ngroups"], info["gmax"]) == (n, 1)
+    lay = g.gen_layer(g.rr_spec(n, 3), 1)
+    info = sd.sdnn_validate_layer(n, lay, lay.bias, fmt=fmt)
+    assert (info["ngroups"], info["gmax"], info["kmax"]) == (n, 1, 32)
+
+
+def test_irregular_layer_info(sd):
+    spec = g.random_spec(200, 1, seed=3, kmin=0, kmax=40)
+    lay = g.gen_layer(spec, 0)
+    info = sd.sdnn_validate_layer(200, lay, lay.bias)
+    assert info["uniform"] == 0 and info["regular"] == 0 and info["kmax"] == 40
+    assert info["nnz"] == lay.colidx.size
+
+
+def test_no_device_fails_loudly(sd):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("has a GPU")
+    with pytest.raises(sd.SdnnError) as e:
+        sd.Net(64, 1)
+    assert e.value.status == sd.SDNN_E_CUDA
+
+
+def test_product_path_never_touches_oracle():
+    """The product package must not import, link or execute anything under
+    oracle/ (only tests, smoke and bench's cpu_baseline may)."""
+    pkg = os.path.join(ROOT, "paper_2004_10908_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            p = os.path.join(dirpath, f)
+            if f.endswith(".py"):
+                tree = ast.parse(open(p).read())
+                for node in ast.walk(tree):
+                    if isinstance(node, ast.Import):
+                        assert all(not a.name.startswith("oracle") for a in node.names), p
+                    if isinstance(node, ast.ImportFrom):
+                        assert not (node.module or "").startswith("oracle"), p
+            if f.endswith((".cu", ".cpp", ".h", ".py")):
+                txt = open(p).read()
+                assert "sdnn_oracle" not in txt and "liboracle" not in txt, p

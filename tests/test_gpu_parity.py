@@ -1,0 +1,232 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element
+by element on the same seeded inputs.  The bar (BASELINE.json north_star):
+categories bit-exact; activations within 1e-5 rel / 1e-6 abs -- this build is
+held to the stricter bit-exact standard for activations too, because both
+sides evaluate the same canonical fp32 chain (A5)."""
+import numpy as np
+import pytest
+
+import oracle
+import sdnngen as g
+
+pytestmark = pytest.mark.gpu
+
+RTOL, ATOL = 1e-5, 1e-6            # north_star tolerance (asserted in addition to bit-exactness)
+
+
+@pytest.fixture(scope="module")
+def sd():
+    from paper_2004_10908_b200 import build
+    build.build()
+    import paper_2004_10908_b200 as sd
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    return sd
+
+
+def assert_parity(cats_gpu, Y_gpu, cats_or, Y_or):
+    assert np.array_equal(cats_gpu, np.flatnonzero(cats_or).astype(np.int32))
+    if Y_gpu is not None:
+        np.testing.assert_allclose(Y_gpu, Y_or, rtol=RTOL, atol=ATOL)
+        assert np.array_equal(Y_gpu.view(np.uint32), Y_or.view(np.uint32))
+
+
+def run_gpu(sd, n, layers, rp, idx, val, fmt="csr", flags=0, ymax=32.0, want_y=True):
+    with sd.Net.from_layers(n, layers, fmt=fmt, flags=flags, ymax=ymax) as net:
+        cats, Y = net.infer(rp, idx, val, want_y=want_y)
+        st = net.stats()
+    return cats, Y, st
+
+
+FLAGS = [0, 1, 2, 4]   # default, NO_COMPACT, NO_GROUPS, NO_GRAPH
+
+
+@pytest.mark.parametrize("name", ["H1", "H2", "H3", "H3_ymax2", "H4", "H5"])
+@pytest.mark.parametrize("flags", FLAGS)
+def test_hand_nets(sd, hand_nets, name, flags):
+    net = hand_nets[name]
+    layers = [dict(l, uniform=0.0) for l in net.layers]
+    cats, Y, _ = run_gpu(sd, net.n, layers, net.y0_rowptr, net.y0_idx, net.y0_val,
+                         flags=flags, ymax=net.ymax)
+    assert cats.tolist() == net.expected_categories
+    assert np.array_equal(Y.view(np.uint32), net.expected_Y.view(np.uint32))
+
+
+@pytest.fixture(scope="module")
+def c1():
+    """configs[0]: 1024 neurons x 120 layers, 32 nnz/column, 1000 binary inputs."""
+    spec = g.rn_spec(1024, 120)
+    layers = list(g.iter_layers(spec))
+    rp, idx = g.ms_inputs(1024, 1000)
+    cats, Y, prof = oracle.infer(1024, layers, rp, idx, None, profile=True)
+    return spec, layers, rp, idx, cats, Y, prof
+
+
+@pytest.mark.parametrize("fmt", ["csr", "ell"])
+@pytest.mark.parametrize("flags", FLAGS)
+def test_c1_full(sd, c1, fmt, flags):
+    spec, layers, rp, idx, cats, Y, prof = c1
+    cg, Yg, st = run_gpu(sd, 1024, layers, rp, idx, None, fmt=fmt, flags=flags)
+    assert_parity(cg, Yg, cats, Y)
+    assert st["live_rows"] == prof
+    assert 0 < cats.sum() < cats.size
+
+
+def test_ka_known_answer(sd):
+    from test_oracle_pins import ka_expected
+    spec = g.ka_spec(1024, 24)
+    layers = list(g.iter_layers(spec))
+    rp, idx, cnt = g.ka_inputs(1024, 2000, seed=21)
+    cg, Yg, _ = run_gpu(sd, 1024, layers, rp, idx, None, fmt="ell")
+    Yx = ka_expected(spec, cnt)
+    assert np.array_equal(Yg.view(np.uint32), Yx.view(np.uint32))
+    assert np.array_equal(cg, np.flatnonzero((Yx > 0).any(1)))
+
+
+def test_rr_general_gather(sd):
+    n, L = 2048, 20
+    spec = g.rr_spec(n, L)
+    layers = list(g.iter_layers(spec))
+    rp, idx, val = g.random_inputs(n, 700, seed=4, density=0.3, lo=0.0, hi=3.0)
+    cats, Y, _ = oracle.infer(n, layers, rp, idx, val)
+    cg, Yg, st = run_gpu(sd, n, layers, rp, idx, val)
+    assert st["max_group"] == 1
+    assert_parity(cg, Yg, cats, Y)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_irregular_random_weights(sd, seed):
+    """Per-slot weights (general kernel), K up to 40 (>32 path), empty columns,
+    width not a multiple of 32, negative inputs, some positive biases (so
+    compaction must switch itself off)."""
+    n, L = 300, 5
+    spec = g.random_spec(n, L, seed=40 + seed, kmin=0, kmax=40, bias=(-0.3, 0.05))
+    layers = list(g.iter_layers(spec))
+    rp, idx, val = g.random_inputs(n, 333, seed=50 + seed)
+    cats, Y, _ = oracle.infer(n, layers, rp, idx, val)
+    for flags in (0, 2):
+        cg, Yg, st = run_gpu(sd, n, layers, rp, idx, val, flags=flags)
+        assert st["compaction"] == 0
+        assert_parity(cg, Yg, cats, Y)
+
+
+def test_rn_random_weights_grouped(sd):
+    """Groups of 32 with per-slot weights: one source load, 32 chains."""
+    n, L = 1024, 12
+    spec = g.rn_spec(n, L, wdist="random", bias=-0.2)
+    layers = list(g.iter_layers(spec))
+    rp, idx, val = g.random_inputs(n, 500, seed=8, density=0.3, lo=0.0, hi=2.0)
+    cats, Y, _ = oracle.infer(n, layers, rp, idx, val)
+    for fmt in ("csr", "ell"):
+        cg, Yg, st = run_gpu(sd, n, layers, rp, idx, val, fmt=fmt)
+        assert st["max_group"] == 32
+        assert_parity(cg, Yg, cats, Y)
+
+
+@pytest.mark.parametrize("B", [1, 31, 33, 127, 129, 1000, 4097])
+def test_ragged_batches(sd, B):
+    n, L = 1024, 16
+    spec = g.rn_spec(n, L)
+    layers = list(g.iter_layers(spec))
+    rp, idx = g.ms_inputs(n, B, seed=77)
+    cats, Y, _ = oracle.infer(n, layers, rp, idx, None)
+    cg, Yg, _ = run_gpu(sd, n, layers, rp, idx, None, fmt="ell")
+    assert_parity(cg, Yg, cats, Y)
+
+
+def test_edge_cases(sd):
+    n = 64
+    spec = g.rn_spec(n, 3)
+    layers = list(g.iter_layers(spec))
+    # empty batch
+    cg, Yg, _ = run_gpu(sd, n, layers, np.zeros(1, np.int64), np.zeros(0, np.int32), None)
+    assert cg.size == 0 and Yg.shape == (0, n)
+    # all rows empty -> nothing survives, everything compacted away after densify
+    rp = np.zeros(40, np.int64)
+    cg, Yg, st = run_gpu(sd, n, layers, rp, np.zeros(0, np.int32), None)
+    assert cg.size == 0 and not Yg.any()
+    # zero layers: categories = rows with a positive entry
+    rp = np.array([0, 2, 2, 3, 4], np.int64)
+    idx = np.array([1, 3, 0, 5], np.int32)
+    val = np.array([0.5, -1.0, -2.0, 3.0], np.float32)
+    with sd.Net(n, 0) as net:
+        cg, Yg = net.infer(rp, idx, val, want_y=True)
+    assert cg.tolist() == [0, 3]
+    assert np.array_equal(Yg, g.dense_from_csr(rp, idx, val, n))
+    # invalid Y0 is rejected by the host call
+    with sd.Net.from_layers(n, layers) as net:
+        with pytest.raises(sd.SdnnError):
+            net.infer(np.array([0, 2], np.int64), np.array([3, 3], np.int32), None)
+        with pytest.raises(sd.SdnnError):
+            net.infer(np.array([0, 1], np.int64), np.array([n], np.int32), None)
+    # inference before all layers are set
+    net = sd.Net(n, 2)
+    with pytest.raises(sd.SdnnError) as e:
+        net.infer(np.array([0, 1], np.int64), np.array([3], np.int32), None)
+    assert e.value.status == sd.SDNN_E_STATE
+    net.close()
+
+
+def test_device_api_torch(sd, c1):
+    import torch
+    spec, layers, rp, idx, cats, Y, prof = c1
+    with sd.Net.from_layers(1024, layers, fmt="ell") as net:
+        dev = torch.device("cuda:0")
+        rp_t = torch.from_numpy(rp).to(dev)
+        idx_t = torch.from_numpy(idx).to(dev)
+        y_t = torch.empty((rp.size - 1, 1024), dtype=torch.float32, device=dev)
+        alive = net.infer_torch(rp_t, idx_t, None, y_t=y_t)
+        torch.cuda.synchronize()
+        ids = sd.bitmask_to_ids(alive.cpu().numpy(), rp.size - 1)
+        assert np.array_equal(ids, np.flatnonzero(cats))
+        assert np.array_equal(y_t.cpu().numpy().view(np.uint32), Y.view(np.uint32))
+        # on a side stream, twice (determinism, reuse of the captured graph)
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            a2 = net.infer_torch(rp_t, idx_t, None)
+            a3 = net.infer_torch(rp_t, idx_t, None, alive_t=torch.empty_like(a2))
+        s.synchronize()
+        assert torch.equal(a2, alive) and torch.equal(a3, alive)
+
+
+def test_row_independence_on_gpu(sd, c1):
+    spec, layers, rp, idx, cats, Y, prof = c1
+    rows = np.random.default_rng(5).choice(rp.size - 1, 123, replace=False)
+    srp, sidx, _ = oracle.subset_rows(rp, idx, None, rows)
+    cg, Yg, _ = run_gpu(sd, 1024, layers, srp, sidx, None)
+    assert np.array_equal(cg, np.flatnonzero(cats[rows]))
+    assert np.array_equal(Yg.view(np.uint32), Y[rows].view(np.uint32))
+
+
+# ---------------------------------------------------------------------------
+# BASELINE.json's full sizes, in the launch configuration bench.py times: the
+# full 60000-input batch on the GPU, checked on sampled rows the oracle
+# computes one by one (row independence, I4), sentinel rows included.
+# ---------------------------------------------------------------------------
+def _full_size(sd, n, L, nsample):
+    spec = g.rn_spec(n, L)
+    rp, idx = g.ms_inputs(n, 60000)
+    with sd.Net.from_spec(spec, fmt="ell", threads=8) as net:
+        cats, _ = net.infer(rp, idx, None)
+        st = net.stats()
+    r = np.random.default_rng(n)
+    rows = np.unique(np.concatenate([r.choice(60000, nsample, replace=False),
+                                     [998, 999, 1998, 1999, 59998, 59999]]))
+    oc, _, _, _ = oracle.infer_spec_rows(spec, rp, idx, None, rows)
+    got = np.isin(rows, cats)
+    assert np.array_equal(got, oc), rows[got != oc]
+    assert got[np.isin(rows, [999, 1999, 59999])].all()           # all-ones sentinels
+    assert not got[np.isin(rows, [998, 1998, 59998])].any()       # empty sentinels
+    # survivor profile sanity: non-increasing, final == number of categories
+    live = st["live_rows"]
+    assert all(a >= b for a, b in zip(live, live[1:])) and live[-1] == cats.size
+    return cats, st
+
+
+def test_full_size_c2(sd):
+    _full_size(sd, 4096, 480, 200)
+
+
+@pytest.mark.slow
+def test_full_size_c4(sd):
+    _full_size(sd, 65536, 1920, 24)
