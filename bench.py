@@ -320,6 +320,24 @@ def run_gpu(args):
         dist.destroy_process_group()
 
 
+def run_oneshot(args):
+    """Minimal driver for ncu: no e2e, no oracle, no collectives."""
+    import torch
+
+    import paper_2004_10908_b200 as sd
+    import sdnngen as g
+    n, L, B = CONFIGS[args.config]
+    net = sd.Net.from_spec(g.rn_spec(n, L), fmt="ell", threads=args.load_threads, device=0)
+    rp, idx = make_inputs(n, B, 0)
+    rp_t, idx_t = torch.from_numpy(rp).cuda(), torch.from_numpy(idx).cuda()
+    for _ in range(args.warmup + args.steps):
+        net.infer_torch(rp_t, idx_t, None)
+    torch.cuda.synchronize()
+    print(json.dumps({"oneshot": args.config, "stats": {k: v for k, v in net.stats().items()
+                                                         if k != "live_rows"}}))
+    net.close()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -334,11 +352,15 @@ def main():
     ap.add_argument("--cpu-rows", type=int, default=16)
     ap.add_argument("--ref-rows", type=int, default=0)
     ap.add_argument("--load-threads", type=int, default=8)
+    ap.add_argument("--oneshot", action="store_true",
+                    help="profiling helper: load, run warmup+steps inferences, print timing only")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "sdnn":
         print("warning: the contract asks for >= 3 warm-up steps", file=sys.stderr)
     if args.impl == "reference":
         run_reference(args)
+    elif args.oneshot:
+        run_oneshot(args)
     else:
         run_gpu(args)
 

@@ -83,8 +83,10 @@ enum {
                                     instead of one captured CUDA Graph (f1 study)        */
   SDNN_F_NO_RESIDENT = 1u << 3,  /* disable the SMEM-resident multi-layer kernel        */
   SDNN_F_TRUST_INPUT = 1u << 4,  /* sdnn_infer: skip host validation of Y0              */
-  SDNN_F_PROFILE = 1u << 5       /* record a CUDA event pair around every layer kernel
+  SDNN_F_PROFILE = 1u << 5,      /* record a CUDA event pair around every layer kernel
                                     (read back with sdnn_layer_times)                    */
+  SDNN_F_NO_BULK = 1u << 6       /* uniform layers: use the register-staged gather kernel
+                                    instead of the TMA bulk-copy pipeline                */
 };
 
 typedef struct sdnn_opts {

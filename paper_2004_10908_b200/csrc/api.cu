@@ -159,7 +159,8 @@ void free_ws(sdnn_net *net) {
 }
 
 sdnn_status ensure_ws(sdnn_net *net, int64_t batch) {
-  const int64_t stride = std::max<int64_t>(128, (batch + 127) / 128 * 128);
+  const int64_t q = bulk_stride_quantum();
+  const int64_t stride = std::max<int64_t>(q, (batch + q - 1) / q * q);
   if (net->ws_cap >= stride) return SDNN_OK;
   free_ws(net);
   if ((int64_t)net->n * stride > (int64_t(1) << 36)) return fail(SDNN_E_UNSUPPORTED, "batch too large");
@@ -373,6 +374,8 @@ sdnn_status sdnn_create_empty(int32_t neurons, int32_t layers, const sdnn_opts *
   net->cfg.sms = sms;
   net->cfg.layer_blocks = sms * 2;   // 2 resident 256-thread CTAs per SM (128 regs)
   net->cfg.copy_blocks = sms * 4;
+  net->cfg.bulk = !(o.flags & SDNN_F_NO_BULK);
+  configure_kernels();
   if (cudaStreamCreateWithFlags(&net->own, cudaStreamNonBlocking) != cudaSuccess) {
     cudaGetLastError();
     delete net;

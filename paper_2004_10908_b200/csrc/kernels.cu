@@ -170,6 +170,147 @@ __global__ void __launch_bounds__(256, 2) k_layer_uniform(DevLayer L, const Laye
 }
 
 // ---------------------------------------------------------------------------
+// Layer kernel, uniform weights, TMA bulk-copy pipeline (sm_90+/sm_100a).
+// Persistent CTAs: warp 0 is the producer -- lane t issues one
+// cp.async.bulk (global -> shared, completion on an mbarrier) for the group's
+// t-th source row segment [tile*T, tile*T + T) -- and warps 1..4 consume: the
+// canonical chain over the K_g staged rows (conflict-free LDS.128), then one
+// bias-add + clamp + STG.128 per member column.  kStages stages of
+// 32 rows x T floats keep ~3 x 64 KB of HBM reads in flight per SM without
+// costing registers (the register-staged kernel above is latency bound).
+// ---------------------------------------------------------------------------
+constexpr int kBulkT = 512;                      // positions per item (2 KB per row)
+constexpr int kBulkStages = 3;
+constexpr int kBulkConsumers = 4;                // 4 warps x 32 lanes x 4 positions = 512
+constexpr int kBulkThreads = 32 * (1 + kBulkConsumers);
+constexpr size_t kBulkSmem = (size_t)kBulkStages * 32 * kBulkT * sizeof(float) + 2 * kBulkStages * 8;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx_arrive(uint64_t *b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred P;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+      " @!P bra WAIT_%=;\n}\n" ::"r"(smem_u32(b)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__global__ void __launch_bounds__(kBulkThreads, 1) k_layer_bulk(DevLayer L, const LayerState *__restrict__ st,
+                                                               int layer, float *Ya, float *Yb,
+                                                               uint32_t *__restrict__ alive,
+                                                               int64_t stride, float ymax) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float *stage = reinterpret_cast<float *>(smem_raw);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem_raw + (size_t)kBulkStages * 32 * kBulkT * 4);
+  uint64_t *empty = full + kBulkStages;
+  const LayerState S = st[layer];
+  const int width = S.width;
+  if (width <= 0) return;
+  const float *__restrict__ Yin = S.in ? Yb : Ya;
+  float *__restrict__ Yout = S.in ? Ya : Yb;
+  const int tiles = (width + kBulkT - 1) / kBulkT;
+  const int64_t items = (int64_t)L.ngroups * tiles;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kBulkStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kBulkConsumers);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == 0) {
+    // ---------------- producer ----------------
+    int s = 0;
+    uint32_t ph = 0;
+    for (int64_t it = blockIdx.x, n = 0; it < items; it += gridDim.x, ++n) {
+      const int g = (int)(it / tiles);
+      const int tile = (int)(it - (int64_t)g * tiles);
+      const int K = L.regular ? L.kmax : L.gk[g];
+      if (n >= kBulkStages) mbar_wait(&empty[s], ph ^ 1);
+      if (lane == 0) mbar_expect_tx_arrive(&full[s], (uint32_t)K * kBulkT * 4);
+      __syncwarp();
+      if (lane < K) {
+        const int k = L.src[(int64_t)g * L.kmax + lane];
+        bulk_g2s(stage + ((size_t)s * 32 + lane) * kBulkT, Yin + (int64_t)k * stride + (int64_t)tile * kBulkT,
+                 kBulkT * 4, &full[s]);
+      }
+      if (++s == kBulkStages) { s = 0; ph ^= 1; }
+    }
+  } else {
+    // ---------------- consumers ----------------
+    const int cw = warp - 1;
+    const float w = L.wu;
+    int s = 0;
+    uint32_t ph = 0;
+    for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+      const int g = (int)(it / tiles);
+      const int tile = (int)(it - (int64_t)g * tiles);
+      const int K = L.regular ? L.kmax : L.gk[g];
+      const int G = L.regular ? L.gmax : L.gg[g];
+      const int mycol = lane < G ? L.col[(int64_t)g * L.gmax + lane] : 0;
+      const float bmy = lane < G ? __ldg(L.bias + mycol) : 0.f;
+      mbar_wait(&full[s], ph);
+      const float *src = stage + (size_t)s * 32 * kBulkT + cw * 128 + lane * 4;
+      float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+      if (K == 32) {
+#pragma unroll
+        for (int t = 0; t < 32; ++t) {
+          const float4 v = *reinterpret_cast<const float4 *>(src + t * kBulkT);
+          a0 = __fmaf_rn(v.x, w, a0);
+          a1 = __fmaf_rn(v.y, w, a1);
+          a2 = __fmaf_rn(v.z, w, a2);
+          a3 = __fmaf_rn(v.w, w, a3);
+        }
+      } else {
+        for (int t = 0; t < K; ++t) {
+          const float4 v = *reinterpret_cast<const float4 *>(src + t * kBulkT);
+          a0 = __fmaf_rn(v.x, w, a0);
+          a1 = __fmaf_rn(v.y, w, a1);
+          a2 = __fmaf_rn(v.z, w, a2);
+          a3 = __fmaf_rn(v.w, w, a3);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (++s == kBulkStages) { s = 0; ph ^= 1; }
+      const int64_t tpos = (int64_t)tile * kBulkT + cw * 128;
+      float *dst = Yout + tpos + lane * 4;
+      uint32_t am = 0;
+      for (int m = 0; m < G; ++m) {
+        const int j = __shfl_sync(FULL, mycol, m);
+        const float b = __shfl_sync(FULL, bmy, m);
+        float4 y;
+        y.x = clampy(__fadd_rn(a0, b), ymax);
+        y.y = clampy(__fadd_rn(a1, b), ymax);
+        y.z = clampy(__fadd_rn(a2, b), ymax);
+        y.w = clampy(__fadd_rn(a3, b), ymax);
+        am |= (y.x > 0.f ? 1u : 0u) | (y.y > 0.f ? 2u : 0u) | (y.z > 0.f ? 4u : 0u) | (y.w > 0.f ? 8u : 0u);
+        *reinterpret_cast<float4 *>(dst + (int64_t)j * stride) = y;
+      }
+      publish_alive<4>(am, lane, tpos, width, alive);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Layer kernel, per-slot weights.  Sources of the group are loaded once into
 // registers (K_g <= 32) and every member runs its own chain with its own
 // weights (warp-uniform loads, L1-resident).  K_g > 32 falls back to reloading
@@ -503,6 +644,12 @@ __global__ void k_yout(const LayerState *__restrict__ st, int sidx, int final_ou
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
+int bulk_stride_quantum() { return kBulkT; }
+
+void configure_kernels() {
+  cudaFuncSetAttribute(k_layer_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBulkSmem);
+}
+
 void launch_densify(const LaunchCfg &c, const Workspace &w, int32_t n, int64_t batch,
                     const int64_t *rowptr, const int32_t *idx, const float *val, bool compact,
                     cudaStream_t s) {
@@ -530,7 +677,10 @@ void launch_layer(const LaunchCfg &c, const Workspace &w, const DevLayer &L, int
                   float ymax, int32_t n, cudaStream_t s) {
   (void)n;
   uint32_t *alive = w.alive[layer & 1];
-  if (L.uniform) {
+  if (L.uniform && L.kmax <= 32 && c.bulk) {
+    k_layer_bulk<<<c.sms, kBulkThreads, kBulkSmem, s>>>(L, w.st, layer, w.Y[0], w.Y[1], alive,
+                                                       w.stride, ymax);
+  } else if (L.uniform) {
     if (L.regular && L.kmax == 32)
       k_layer_uniform<4, true><<<c.layer_blocks, 256, 0, s>>>(L, w.st, layer, w.Y[0], w.Y[1],
                                                                alive, w.stride, ymax);

@@ -105,7 +105,11 @@ struct LaunchCfg {
   int sms = 148;
   int layer_blocks = 148 * 8;
   int copy_blocks = 148 * 4;
+  bool bulk = true;            // TMA bulk-copy pipeline for uniform layers with K <= 32
 };
+
+int bulk_stride_quantum();     // activation row stride must be a multiple of this
+void configure_kernels();      // one-time function attributes (dynamic smem)
 
 void launch_densify(const LaunchCfg &c, const Workspace &w, int32_t n, int64_t batch,
                     const int64_t *rowptr, const int32_t *idx, const float *val, bool compact,
