@@ -98,6 +98,11 @@ def dist_env():
     return ws, rank, local
 
 
+def kernel_name(net):
+    st = net.stats()
+    return "k_layer_bulk" if st.get("path", 0) == 0 else "k_chain"
+
+
 def make_inputs(n, B, rank):
     import sdnngen as g
     seed = g.input_seed(n) if rank == 0 else g.input_seed(n) ^ (0x9E37 * rank)
@@ -177,36 +182,34 @@ def run_gpu(args):
     dev = torch.device("cuda", local)
     if ws > 1:
         dist.init_process_group("nccl", device_id=dev)
+    from paper_2004_10908_b200 import dist as sdist
     n, L, B = CONFIGS[args.config]
-    if args.scaling == "strong" and ws > 1:
-        B_rank = (B + ws - 1) // ws
-    else:
-        B_rank = B
     spec = g.rn_spec(n, L)
     t0 = time.time()
     net = sd.Net.from_spec(spec, fmt="ell", threads=args.load_threads, device=local,
                            flags=sd.SDNN_F_PROFILE)
     t_load = time.time() - t0
-    rp, idx = make_inputs(n, B, rank)
     if args.scaling == "strong" and ws > 1:
-        import oracle as _o  # noqa: F401  (not used: subset by slicing below)
-    if B_rank != B:
-        lo, hi = rank * B_rank, min(B, (rank + 1) * B_rank)
-        base = rp[lo]
-        idx = idx[rp[lo]:rp[hi]].copy()
-        rp = (rp[lo:hi + 1] - base).copy()
+        # one global batch, contiguous word-aligned slices (dist.partition)
+        rp, idx = make_inputs(n, B, 0)
+        lo, hi = sdist.partition(B, ws, rank)
+        rp, idx, _ = sdist.slice_csr(rp, idx, None, lo, hi)
+        words = sdist.words_per_rank(B, ws)
+    else:
+        # weak scaling: every rank its own B-input batch (seeded by rank)
+        rp, idx = make_inputs(n, B, rank)
+        words = (B + 31) // 32
     batch = rp.size - 1
     rp_t = torch.from_numpy(rp).to(dev)
-    idx_t = torch.from_numpy(idx).to(dev)
-    words = (batch + 31) // 32
-    alive = torch.empty(words, dtype=torch.int32, device=dev)
-    gathered = torch.empty(words * ws, dtype=torch.int32, device=dev)
+    idx_t = torch.from_numpy(np.ascontiguousarray(idx)).to(dev)
+    alive = torch.zeros(words, dtype=torch.int32, device=dev)
+    alive_view = alive[: (batch + 31) // 32]
     stream = torch.cuda.current_stream(dev)
 
     def step():
-        net.infer_torch(rp_t, idx_t, None, alive_t=alive, stream=stream)
+        net.infer_torch(rp_t, idx_t, None, alive_t=alive_view, stream=stream)
         if ws > 1:
-            dist.all_gather_into_tensor(gathered, alive)
+            sdist.gather_bitmask(alive)          # the single collective (NCCL all-gather)
 
     for _ in range(args.warmup):
         step()
@@ -243,18 +246,22 @@ def run_gpu(args):
     pk = peaks()
     peak = pk["hbm_gbs"] if pk else 6650.0
     achieved = alg_bytes / kern_s / 1e9 if kern_s > 0 else None
-    traffic = None
+    traffic, traffic_src = None, None
     try:
+        # dram__bytes_read.sum + dram__bytes_write.sum of one captured launch
+        # (ncu --set full, profiles/layer_traffic.json), expressed per average
+        # launch through its ratio to that launch's algorithmic bytes
         prof = json.load(open(os.path.join(ROOT, "profiles", "layer_traffic.json")))
-        if prof.get("config") == args.config:
-            traffic = prof.get("dram_bytes_per_live_row_neuron")
-            traffic = None if traffic is None else traffic * alg_bytes / 8.0 / L
+        if prof.get("config") == args.config and prof.get("kernel") == kernel_name(net):
+            traffic = prof["dram_over_alg"] * alg_bytes / L
+            traffic_src = prof["source"]
     except Exception:
         pass
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-            "kernel": "k_layer_uniform (per-layer launch, avg over the last step's "
-                      f"{L} launches)",
+            "traffic_source": traffic_src,
+            "kernel": f"{kernel_name(net)} (per-layer launch; avg over the last timed step's "
+                      f"{L} launches, CUDA events on the launching stream)",
             "peak_source": "MEASURED_PEAKS.json hbm_gbs" if pk else "fallback 6.65 TB/s",
             "kernel_share_of_step": kern_s / (ms * 1e-3),
             "alg_bytes_per_launch": alg_bytes / L}
