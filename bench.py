@@ -98,6 +98,13 @@ def dist_env():
     return ws, rank, local
 
 
+def lib_flags(sd, names):
+    f = 0
+    for nm in filter(None, names.split(",")):
+        f |= getattr(sd, "SDNN_F_" + nm.upper())
+    return f
+
+
 def kernel_name(net):
     st = net.stats()
     return "k_layer_bulk" if st.get("path", 0) == 0 else "k_chain"
@@ -187,7 +194,7 @@ def run_gpu(args):
     spec = g.rn_spec(n, L)
     t0 = time.time()
     net = sd.Net.from_spec(spec, fmt="ell", threads=args.load_threads, device=local,
-                           flags=sd.SDNN_F_PROFILE)
+                           flags=sd.SDNN_F_PROFILE | lib_flags(sd, args.flags))
     t_load = time.time() - t0
     if args.scaling == "strong" and ws > 1:
         # one global batch, contiguous word-aligned slices (dist.partition)
@@ -320,6 +327,7 @@ def run_gpu(args):
                           "categories": int(live[-1]) if live else None,
                           "category_fraction": (live[-1] / batch) if live and batch else None},
             "load_seconds": t_load,
+            "flags": args.flags or None,
         }
         print(json.dumps(line), flush=True)
     net.close()
@@ -334,7 +342,8 @@ def run_oneshot(args):
     import paper_2004_10908_b200 as sd
     import sdnngen as g
     n, L, B = CONFIGS[args.config]
-    net = sd.Net.from_spec(g.rn_spec(n, L), fmt="ell", threads=args.load_threads, device=0)
+    net = sd.Net.from_spec(g.rn_spec(n, L), fmt="ell", threads=args.load_threads, device=0,
+                           flags=lib_flags(sd, args.flags))
     rp, idx = make_inputs(n, B, 0)
     rp_t, idx_t = torch.from_numpy(rp).cuda(), torch.from_numpy(idx).cuda()
     for _ in range(args.warmup + args.steps):
@@ -359,6 +368,8 @@ def main():
     ap.add_argument("--cpu-rows", type=int, default=16)
     ap.add_argument("--ref-rows", type=int, default=0)
     ap.add_argument("--load-threads", type=int, default=8)
+    ap.add_argument("--flags", default="",
+                    help="comma list of library flags, e.g. no_graph,no_bulk (f1 studies)")
     ap.add_argument("--oneshot", action="store_true",
                     help="profiling helper: load, run warmup+steps inferences, print timing only")
     args = ap.parse_args()

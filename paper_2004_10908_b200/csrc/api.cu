@@ -191,11 +191,15 @@ sdnn_status ensure_ws(sdnn_net *net, int64_t batch) {
 void enqueue_chain(sdnn_net *net, bool compact, cudaStream_t s, int64_t *launches) {
   const float ymax = net->opts.ymax;
   const bool prof = (net->opts.flags & SDNN_F_PROFILE) && (int)net->ev_before.size() == net->L;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &cap);
+  // inside a capture the record must be an explicit (external) event node
+  const unsigned evflags = cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0u;
   int64_t c = 0;
   for (int32_t l = 0; l < net->L; ++l) {
-    if (prof) cudaEventRecordWithFlags(net->ev_before[l], s, cudaEventRecordExternal);
+    if (prof) cudaEventRecordWithFlags(net->ev_before[l], s, evflags);
     launch_layer(net->cfg, net->ws, net->dl[l], l, ymax, net->n, s);
-    if (prof) cudaEventRecordWithFlags(net->ev_after[l], s, cudaEventRecordExternal);
+    if (prof) cudaEventRecordWithFlags(net->ev_after[l], s, evflags);
     ++c;
     if (l + 1 < net->L) {
       launch_scan(net->ws, l, compact, net->n, s);

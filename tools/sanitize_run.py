@@ -1,0 +1,44 @@
+"""Small inferences through the C ABI for compute-sanitizer (memcheck /
+racecheck / synccheck): every kernel path (bulk, register-staged uniform,
+general per-slot, K > 32, compaction on/off, graph/stream loop, L = 0)."""
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2004_10908_b200 as sd  # noqa: E402
+import sdnngen as g  # noqa: E402
+
+
+def run(n, layers, rp, idx, val, flags=0, fmt="csr"):
+    with sd.Net.from_layers(n, layers, fmt=fmt, flags=flags) as net:
+        cats, Y = net.infer(rp, idx, val, want_y=True)
+    return cats, Y
+
+
+def main():
+    out = []
+    spec = g.rn_spec(256, 6)
+    lays = list(g.iter_layers(spec))
+    rp, idx = g.ms_inputs(256, 300)
+    ref = None
+    for flags in (0, sd.SDNN_F_NO_BULK, sd.SDNN_F_NO_GROUPS, sd.SDNN_F_NO_COMPACT, sd.SDNN_F_NO_GRAPH):
+        c, Y = run(256, lays, rp, idx, None, flags, fmt="ell")
+        if ref is None:
+            ref = (c, Y)
+        assert np.array_equal(c, ref[0]) and np.array_equal(Y, ref[1])
+        out.append(c.size)
+    spec = g.random_spec(100, 3, seed=5, kmin=0, kmax=40, bias=(-0.3, 0.05))
+    lays = list(g.iter_layers(spec))
+    rp, idx, val = g.random_inputs(100, 77, seed=5)
+    c, Y = run(100, lays, rp, idx, val)
+    out.append(c.size)
+    with sd.Net(64, 0) as net:
+        c, _ = net.infer(np.array([0, 1, 1], np.int64), np.array([3], np.int32), None)
+    out.append(c.size)
+    print("sanitize_run ok", out)
+
+
+if __name__ == "__main__":
+    main()
