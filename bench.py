@@ -107,7 +107,7 @@ def lib_flags(sd, names):
 
 def kernel_name(net):
     st = net.stats()
-    return "k_layer_bulk" if st.get("path", 0) == 0 else "k_chain"
+    return "k_layer_bulk" if st.get("fused_layers", 0) == 0 else "k_pass+k_layer_bulk"
 
 
 def make_inputs(n, B, rank):
@@ -194,7 +194,8 @@ def run_gpu(args):
     spec = g.rn_spec(n, L)
     t0 = time.time()
     net = sd.Net.from_spec(spec, fmt="ell", threads=args.load_threads, device=local,
-                           flags=sd.SDNN_F_PROFILE | lib_flags(sd, args.flags))
+                           flags=sd.SDNN_F_PROFILE | lib_flags(sd, args.flags),
+                           fuse_rows=args.fuse_rows, fuse_layers=args.fuse_layers)
     t_load = time.time() - t0
     if args.scaling == "strong" and ws > 1:
         # one global batch, contiguous word-aligned slices (dist.partition)
@@ -244,11 +245,17 @@ def run_gpu(args):
     edges_rank = batch * total_nnz
     value = edges_rank * ws / (ms * 1e-3) if args.scaling != "strong" else B * total_nnz / (ms * 1e-3)
 
-    # ---- roofline of the dominant kernel (the layer kernel) --------------------
+    # ---- roofline of the dominant kernels (the layer steps) ---------------------
+    # A step (one kernel) runs m layers: k_layer_bulk (m = 1) or a fused pass
+    # k_pass (m > 1).  Its algorithmic HBM traffic: read every neuron row of the
+    # rows entering the step (4 B) and write every output row (4 B) once,
+    # = 8 * N bytes per live row per STEP (intermediate layers stay in SMEM).
     live = st["live_rows"]
     kept0 = st["kept_rows"]
-    live_in = [kept0] + live[:-1]                    # rows each layer processes (algorithmic)
-    alg_bytes = sum(8.0 * n * r for r in live_in)   # read + write 4 B per live row-neuron per layer
+    live_in = [kept0] + live[:-1]                    # rows entering each layer
+    plan = net.step_plan()
+    starts = np.cumsum([0] + plan[:-1]).tolist()
+    alg_bytes = sum(8.0 * n * live_in[a] for a in starts)
     kern_s = sum(layer_ms) * 1e-3
     pk = peaks()
     peak = pk["hbm_gbs"] if pk else 6650.0
@@ -260,18 +267,21 @@ def run_gpu(args):
         # launch through its ratio to that launch's algorithmic bytes
         prof = json.load(open(os.path.join(ROOT, "profiles", "layer_traffic.json")))
         if prof.get("config") == args.config and prof.get("kernel") == kernel_name(net):
-            traffic = prof["dram_over_alg"] * alg_bytes / L
+            traffic = prof["dram_over_alg"] * alg_bytes / len(plan)
             traffic_src = prof["source"]
     except Exception:
         pass
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": (achieved / peak) if achieved else None, "traffic": traffic,
             "traffic_source": traffic_src,
-            "kernel": f"{kernel_name(net)} (per-layer launch; avg over the last timed step's "
-                      f"{L} launches, CUDA events on the launching stream)",
+            "kernel": f"{kernel_name(net)} ({len(plan)} launches per inference, "
+                      f"{sum(1 for m in plan if m > 1)} fused passes covering "
+                      f"{sum(m for m in plan if m > 1)} layers; avg over the last timed "
+                      "inference, CUDA events on the launching stream)",
             "peak_source": "MEASURED_PEAKS.json hbm_gbs" if pk else "fallback 6.65 TB/s",
             "kernel_share_of_step": kern_s / (ms * 1e-3),
-            "alg_bytes_per_launch": alg_bytes / L}
+            "alg_bytes_per_launch": alg_bytes / len(plan),
+            "alg_bytes_per_live_edge": alg_bytes / max(1, st["live_edges"])}
 
     # ---- e2e through the public host-buffer call --------------------------------
     e2e = None
@@ -328,6 +338,8 @@ def run_gpu(args):
                           "category_fraction": (live[-1] / batch) if live and batch else None},
             "load_seconds": t_load,
             "flags": args.flags or None,
+            "fuse": {"rows": args.fuse_rows, "layers": args.fuse_layers,
+                     "steps": len(plan), "fused_layers": st["fused_layers"]},
         }
         print(json.dumps(line), flush=True)
     net.close()
@@ -343,7 +355,8 @@ def run_oneshot(args):
     import sdnngen as g
     n, L, B = CONFIGS[args.config]
     net = sd.Net.from_spec(g.rn_spec(n, L), fmt="ell", threads=args.load_threads, device=0,
-                           flags=lib_flags(sd, args.flags))
+                           flags=lib_flags(sd, args.flags), fuse_rows=args.fuse_rows,
+                           fuse_layers=args.fuse_layers)
     rp, idx = make_inputs(n, B, 0)
     rp_t, idx_t = torch.from_numpy(rp).cuda(), torch.from_numpy(idx).cuda()
     for _ in range(args.warmup + args.steps):
@@ -368,6 +381,9 @@ def main():
     ap.add_argument("--cpu-rows", type=int, default=16)
     ap.add_argument("--ref-rows", type=int, default=0)
     ap.add_argument("--load-threads", type=int, default=8)
+    ap.add_argument("--fuse-rows", type=int, default=-1,
+                    help="component cap for fused multi-layer passes (0 = off, -1 = library default)")
+    ap.add_argument("--fuse-layers", type=int, default=-1)
     ap.add_argument("--flags", default="",
                     help="comma list of library flags, e.g. no_graph,no_bulk (f1 studies)")
     ap.add_argument("--oneshot", action="store_true",

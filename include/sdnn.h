@@ -94,7 +94,13 @@ typedef struct sdnn_opts {
   uint32_t flags;   /* SDNN_F_*                                                        */
   float ymax;       /* clip value YMAX (> 0, finite); north_star: 32                   */
   void *stream;     /* cudaStream_t for sdnn_infer (NULL = a stream owned by the net) */
-} sdnn_opts;        /* passing opts = NULL means {-1, 0, 32.0f, NULL}                  */
+  int32_t fuse_rows;   /* multi-layer passes ("model decomposition"):
+                          consecutive uniform layers are fused while every connected
+                          component of their union has <= fuse_rows neurons on every
+                          layer boundary (<= 256; 0 or -1 = off: on B200 the fused
+                          kernel measured slower than per-layer streaming, DESIGN 7) */
+  int32_t fuse_layers; /* at most this many layers per pass (<= 16; -1 = 8)           */
+} sdnn_opts;        /* passing opts = NULL means {-1, 0, 32.0f, NULL, -1, -1}          */
 
 /* Create a network handle and load all L layers.
  *   neurons  N, 1 <= N <= 65536 on this build (u16 source indices); larger N
@@ -151,7 +157,8 @@ sdnn_status sdnn_infer_device(sdnn_net *net, const int64_t *d_rowptr, const int3
 typedef struct sdnn_stats {
   int32_t struct_size;        /* caller sets sizeof(sdnn_stats) (versioning)            */
   int32_t neurons, layers;
-  int32_t path;               /* 0 = per-layer streaming kernels, 1 = SMEM-resident     */
+  int32_t path;               /* 0 = one kernel per layer, 1 = some layers run in fused
+                                 multi-layer passes                                     */
   int32_t grouped_layers;     /* layers packed with >1 column per source-list group    */
   int32_t max_group;          /* largest group size (columns sharing a source list)    */
   int32_t max_k;              /* largest column nnz over all layers                    */
@@ -163,6 +170,8 @@ typedef struct sdnn_stats {
   int64_t launches_per_infer; /* kernels (graph nodes) one inference launches          */
   int64_t live_edges;         /* sum_l (rows nonzero before layer l) * nnz_l, last call */
   int64_t kept_rows;          /* rows entering layer 0 (empty rows dropped when exact)   */
+  int32_t steps;              /* kernel steps of the layer chain (fused passes count 1)  */
+  int32_t fused_layers;       /* layers executed inside fused multi-layer passes         */
 } sdnn_stats;
 
 /* live_rows: NULL or [layers] receives the number of rows still nonzero after
@@ -187,6 +196,18 @@ typedef struct sdnn_layer_info {
 } sdnn_layer_info;
 sdnn_status sdnn_validate_layer(int32_t neurons, const sdnn_layer *W_l, const float *bias_l,
                                 uint32_t flags, sdnn_layer_info *info);
+
+/* The execution plan of a handle (valid after the first inference): step_len
+ * [layers] capacity receives the number of layers of each kernel step. */
+sdnn_status sdnn_step_plan(const sdnn_net *net, int32_t *step_len, int32_t *nsteps);
+
+/* Host-only (no device): the execution plan sdnn_create would use for these
+ * layers -- step_len[i] = number of layers of step i (1 = one kernel per
+ * layer, > 1 = a fused multi-layer pass, see sdnn_opts.fuse_rows); *nsteps =
+ * number of steps.  step_len: [layers] capacity. */
+sdnn_status sdnn_plan_steps(int32_t neurons, int32_t layers, const sdnn_layer *W,
+                            const float *bias, const sdnn_opts *opts, int32_t *step_len,
+                            int32_t *nsteps);
 
 void sdnn_destroy(sdnn_net *net);          /* NULL-safe; frees all device memory       */
 const char *sdnn_last_error(void);         /* thread-local, never NULL                 */

@@ -32,7 +32,8 @@ SDNN_F_NO_RESIDENT, SDNN_F_TRUST_INPUT, SDNN_F_PROFILE, SDNN_F_NO_BULK = 8, 16, 
 
 EXPORTS = ["sdnn_create", "sdnn_create_empty", "sdnn_set_layer", "sdnn_infer",
            "sdnn_infer_device", "sdnn_stats_get", "sdnn_validate_layer", "sdnn_destroy",
-           "sdnn_last_error", "sdnn_abi_version", "sdnn_layer_times"]
+           "sdnn_last_error", "sdnn_abi_version", "sdnn_layer_times", "sdnn_plan_steps",
+           "sdnn_step_plan"]
 
 
 class SdnnError(RuntimeError):
@@ -49,7 +50,8 @@ class sdnn_layer(ctypes.Structure):
 
 class sdnn_opts(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int32), ("flags", ctypes.c_uint32),
-                ("ymax", ctypes.c_float), ("stream", ctypes.c_void_p)]
+                ("ymax", ctypes.c_float), ("stream", ctypes.c_void_p),
+                ("fuse_rows", ctypes.c_int32), ("fuse_layers", ctypes.c_int32)]
 
 
 class sdnn_layer_info(ctypes.Structure):
@@ -66,7 +68,8 @@ class sdnn_stats(ctypes.Structure):
                 ("packed_weight_bytes", ctypes.c_int64), ("total_nnz", ctypes.c_int64),
                 ("last_batch", ctypes.c_int64), ("last_n_categories", ctypes.c_int64),
                 ("launches_per_infer", ctypes.c_int64), ("live_edges", ctypes.c_int64),
-                ("kept_rows", ctypes.c_int64)]
+                ("kept_rows", ctypes.c_int64), ("steps", ctypes.c_int32),
+                ("fused_layers", ctypes.c_int32)]
 
 
 _LIB = None
@@ -90,6 +93,8 @@ def lib() -> ctypes.CDLL:
         L.sdnn_stats_get.argtypes = [V, P(sdnn_stats), V]
         L.sdnn_validate_layer.argtypes = [I32, P(sdnn_layer), V, U32, P(sdnn_layer_info)]
         L.sdnn_layer_times.argtypes = [V, V]
+        L.sdnn_plan_steps.argtypes = [I32, I32, P(sdnn_layer), V, P(sdnn_opts), V, P(I32)]
+        L.sdnn_step_plan.argtypes = [V, V, P(I32)]
         L.sdnn_destroy.argtypes = [V]
         L.sdnn_destroy.restype = None
         L.sdnn_last_error.argtypes = []
@@ -97,7 +102,7 @@ def lib() -> ctypes.CDLL:
         L.sdnn_abi_version.restype = I32
         for name in ["sdnn_create", "sdnn_create_empty", "sdnn_set_layer", "sdnn_infer",
                      "sdnn_infer_device", "sdnn_stats_get", "sdnn_validate_layer",
-                     "sdnn_layer_times"]:
+                     "sdnn_layer_times", "sdnn_plan_steps", "sdnn_step_plan"]:
             getattr(L, name).restype = I32
         _LIB = L
     return _LIB
@@ -112,8 +117,9 @@ def _p(a: Optional[np.ndarray]):
     return None if a is None else a.ctypes.data
 
 
-def _opts(device=-1, flags=0, ymax=32.0, stream=None):
-    return sdnn_opts(int(device), int(flags), float(ymax), stream)
+def _opts(device=-1, flags=0, ymax=32.0, stream=None, fuse_rows=-1, fuse_layers=-1):
+    return sdnn_opts(int(device), int(flags), float(ymax), stream, int(fuse_rows),
+                     int(fuse_layers))
 
 
 def make_layer(layer, fmt: str = "csr"):
@@ -142,7 +148,8 @@ def make_layer(layer, fmt: str = "csr"):
 # ----------------------------------------------------------------- raw calls
 
 def sdnn_create(neurons: int, layers: Sequence, bias: np.ndarray, fmt: str = "csr",
-                device: int = -1, flags: int = 0, ymax: float = 32.0):
+                device: int = -1, flags: int = 0, ymax: float = 32.0, fuse_rows: int = -1,
+                fuse_layers: int = -1):
     L = len(layers)
     descs = (sdnn_layer * max(L, 1))()
     keep = []
@@ -151,15 +158,15 @@ def sdnn_create(neurons: int, layers: Sequence, bias: np.ndarray, fmt: str = "cs
         keep.append(k)
     bias = np.ascontiguousarray(bias, np.float32).reshape(-1)
     h = ctypes.c_void_p()
-    o = _opts(device, flags, ymax)
+    o = _opts(device, flags, ymax, None, fuse_rows, fuse_layers)
     _check(lib().sdnn_create(neurons, L, descs, _p(bias), ctypes.byref(o), ctypes.byref(h)))
     return h
 
 
 def sdnn_create_empty(neurons: int, layers: int, device: int = -1, flags: int = 0,
-                      ymax: float = 32.0):
+                      ymax: float = 32.0, fuse_rows: int = -1, fuse_layers: int = -1):
     h = ctypes.c_void_p()
-    o = _opts(device, flags, ymax)
+    o = _opts(device, flags, ymax, None, fuse_rows, fuse_layers)
     _check(lib().sdnn_create_empty(neurons, layers, ctypes.byref(o), ctypes.byref(h)))
     return h
 
@@ -213,6 +220,25 @@ def sdnn_validate_layer(neurons: int, layer, bias_l, fmt: str = "csr", flags: in
     return {f: getattr(info, f) for f, _ in sdnn_layer_info._fields_}
 
 
+def sdnn_plan_steps(neurons: int, layers: Sequence, fmt: str = "csr", flags: int = 0,
+                    fuse_rows: int = -1, fuse_layers: int = -1):
+    """Host-only execution plan: list of step lengths (layers per kernel step)."""
+    L = len(layers)
+    descs = (sdnn_layer * max(L, 1))()
+    keep = []
+    for l, lay in enumerate(layers):
+        descs[l], k = make_layer(lay, fmt)
+        keep.append(k)
+    bias = np.concatenate([np.asarray(l.bias if not isinstance(l, dict) else l["bias"], np.float32)
+                           for l in layers]) if L else np.zeros(1, np.float32)
+    out = np.zeros(max(L, 1), np.int32)
+    ns = ctypes.c_int32()
+    o = _opts(-1, flags, 32.0, None, fuse_rows, fuse_layers)
+    _check(lib().sdnn_plan_steps(int(neurons), L, descs, _p(bias), ctypes.byref(o), _p(out),
+                                 ctypes.byref(ns)))
+    return out[:ns.value].tolist()
+
+
 def sdnn_destroy(handle):
     if handle:
         lib().sdnn_destroy(handle)
@@ -224,9 +250,10 @@ class Net:
     """Owning wrapper around an sdnn_net handle."""
 
     def __init__(self, neurons: int, layers: int, flags: int = 0, ymax: float = 32.0,
-                 device: int = -1):
+                 device: int = -1, fuse_rows: int = -1, fuse_layers: int = -1):
         self.n, self.L = int(neurons), int(layers)
-        self.h = sdnn_create_empty(self.n, self.L, device=device, flags=flags, ymax=ymax)
+        self.h = sdnn_create_empty(self.n, self.L, device=device, flags=flags, ymax=ymax,
+                                   fuse_rows=fuse_rows, fuse_layers=fuse_layers)
 
     @classmethod
     def from_layers(cls, neurons: int, layers: Sequence, fmt: str = "csr", **kw):
@@ -281,6 +308,13 @@ class Net:
 
     def stats(self):
         return sdnn_stats_get(self.h, self.L)
+
+    def step_plan(self):
+        """Layers per kernel step of the execution plan (after the first inference)."""
+        out = np.zeros(max(self.L, 1), np.int32)
+        ns = ctypes.c_int32()
+        _check(lib().sdnn_step_plan(self.h, _p(out), ctypes.byref(ns)))
+        return out[:ns.value].tolist()
 
     def layer_times(self):
         """Per-layer kernel durations (ms) of the last inference (SDNN_F_PROFILE)."""

@@ -66,11 +66,12 @@ struct Arena {
 
 struct sdnn_net {
   int32_t n = 0, L = 0;
-  sdnn_opts opts{-1, 0u, 32.f, nullptr};
+  sdnn_opts opts{-1, 0u, 32.f, nullptr, -1, -1};
   int device = 0;
   cudaStream_t own = nullptr;
   Arena arena;
   std::vector<DevLayer> dl;
+  std::vector<PackedLayer> host;   // host copy of every packed layer (pass planning)
   std::vector<uint8_t> set;        // layer loaded?
   std::vector<uint8_t> bias_nonpos;
   std::vector<int64_t> nnz;
@@ -82,6 +83,12 @@ struct sdnn_net {
   // workspace
   Workspace ws;
   int64_t ws_cap = -1;             // stride the workspace was sized for
+  // execution plan: steps of one layer or one fused multi-layer pass
+  std::vector<Step> steps;
+  std::vector<DevPass> passes;
+  Arena pass_arena;
+  bool plan_dirty = true;
+  int32_t fused_layers = 0;
   // captured layer chain
   cudaGraphExec_t chain = nullptr;
   bool chain_compact = false;
@@ -124,8 +131,10 @@ bool compact_enabled(const sdnn_net *net) {
 }
 
 sdnn_status check_opts(const sdnn_opts *o, sdnn_opts &out) {
-  out = sdnn_opts{-1, 0u, 32.f, nullptr};
+  out = sdnn_opts{-1, 0u, 32.f, nullptr, -1, -1};
   if (o) out = *o;
+  if (out.fuse_rows > kMaxPassRows) return fail(SDNN_E_ARG, "fuse_rows > 256");
+  if (out.fuse_layers > kMaxPassLayers) return fail(SDNN_E_ARG, "fuse_layers > 16");
   if (!(out.ymax > 0.f) || !std::isfinite(out.ymax)) return fail(SDNN_E_ARG, "ymax must be finite and > 0");
   return SDNN_OK;
 }
@@ -175,7 +184,7 @@ sdnn_status ensure_ws(sdnn_net *net, int64_t batch) {
       return fail(SDNN_E_NOMEM, "cannot allocate activation buffers (" + std::to_string(2 * ybytes) + " B)");
     }
     CK(cudaMalloc(&w.rid[i], sizeof(int32_t) * stride));
-    CK(cudaMalloc(&w.alive[i], sizeof(uint32_t) * w.words));
+    CK(cudaMalloc(&w.alive[i], sizeof(uint32_t) * w.words * kMaxPassLayers));
   }
   CK(cudaMemset(w.Y[1], 0, ybytes));
   CK(cudaMalloc(&w.inmask, sizeof(uint32_t) * w.words));
@@ -188,6 +197,89 @@ sdnn_status ensure_ws(sdnn_net *net, int64_t batch) {
   return SDNN_OK;
 }
 
+int nthreads_default() {
+  unsigned h = std::thread::hardware_concurrency();
+  return (int)std::max(1u, std::min(h, 32u));
+}
+
+// Plan the steps (fused passes where the component cap allows) and upload the
+// pass descriptors.  Create-time work, redone only when layers change.
+sdnn_status make_plan(sdnn_net *net) {
+  if (!net->plan_dirty) return SDNN_OK;
+  // fused passes are opt-in: measured slower than per-layer streaming on B200
+  const int cap = std::min(net->opts.fuse_rows < 0 ? 0 : net->opts.fuse_rows, kMaxPassRows);
+  const int maxm = net->opts.fuse_layers < 0 ? 8 : net->opts.fuse_layers;
+  std::vector<const PackedLayer *> lp(net->L);
+  for (int l = 0; l < net->L; ++l) lp[l] = &net->host[l];
+  net->steps = plan_steps(lp, net->n, cap, maxm);
+  std::vector<int> fused;
+  for (int i = 0; i < (int)net->steps.size(); ++i)
+    if (net->steps[i].m > 1) fused.push_back(i);
+  std::vector<PassHost> ph(fused.size());
+  {
+    std::atomic<int> next{0};
+    std::vector<std::thread> th;
+    const int nt = std::max(1, std::min<int>(nthreads_default(), (int)fused.size()));
+    for (int t = 0; t < nt; ++t)
+      th.emplace_back([&] {
+        for (int q = next++; q < (int)fused.size(); q = next++)
+          build_pass(lp, net->n, net->steps[fused[q]], pass_buffer_floats(), 32, ph[q]);
+      });
+    for (auto &x : th) x.join();
+  }
+  net->pass_arena.release();
+  net->passes.clear();
+  net->fused_layers = 0;
+  auto up = [&](const void *h, size_t bytes, void **d) -> sdnn_status {
+    cudaError_t e = net->pass_arena.alloc(std::max<size_t>(bytes, 4), d);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(SDNN_E_NOMEM, "device allocation for pass descriptors failed");
+    }
+    if (bytes) CK(cudaMemcpy(*d, h, bytes, cudaMemcpyHostToDevice));
+    return SDNN_OK;
+  };
+  for (size_t q = 0; q < fused.size(); ++q) {
+    PassHost &H = ph[q];
+    DevPass D{};
+    D.a = H.a;
+    D.m = H.m;
+    D.ncomp = H.ncomp;
+    D.rin = H.rin;
+    D.rout = H.rout;
+    D.R = H.R;
+    D.T = H.T;
+    void *p1, *p2, *p3, *p4;
+    sdnn_status st;
+    if ((st = up(H.in_rows.data(), H.in_rows.size() * 4, &p1)) ||
+        (st = up(H.in_count.data(), H.in_count.size() * 4, &p2)) ||
+        (st = up(H.out_rows.data(), H.out_rows.size() * 4, &p3)))
+      return st;
+    D.in_rows = (const int32_t *)p1;
+    D.in_count = (const int32_t *)p2;
+    D.out_rows = (const int32_t *)p3;
+    std::vector<PassLayerDev> pl(H.m);
+    for (int j = 0; j < H.m; ++j) {
+      PassHostLayer &HL = H.layers[j];
+      void *s1, *s2, *s3, *s4, *s5;
+      if ((st = up(HL.src.data(), HL.src.size() * 2, &s1)) ||
+          (st = up(HL.dst.data(), HL.dst.size() * 2, &s2)) ||
+          (st = up(HL.bias.data(), HL.bias.size() * 4, &s3)) ||
+          (st = up(HL.k.data(), HL.k.size(), &s4)) || (st = up(HL.g.data(), HL.g.size(), &s5)))
+        return st;
+      pl[j] = PassLayerDev{(const uint16_t *)s1, (const uint16_t *)s2, (const float *)s3,
+                           (const uint8_t *)s4, (const uint8_t *)s5, HL.NG, HL.wu};
+    }
+    if ((st = up(pl.data(), sizeof(PassLayerDev) * pl.size(), &p4))) return st;
+    D.layers = (const PassLayerDev *)p4;
+    net->steps[fused[q]].pass = (int32_t)net->passes.size();
+    net->passes.push_back(D);
+    net->fused_layers += H.m;
+  }
+  net->plan_dirty = false;
+  return SDNN_OK;
+}
+
 void enqueue_chain(sdnn_net *net, bool compact, cudaStream_t s, int64_t *launches) {
   const float ymax = net->opts.ymax;
   const bool prof = (net->opts.flags & SDNN_F_PROFILE) && (int)net->ev_before.size() == net->L;
@@ -195,16 +287,24 @@ void enqueue_chain(sdnn_net *net, bool compact, cudaStream_t s, int64_t *launche
   cudaStreamIsCapturing(s, &cap);
   // inside a capture the record must be an explicit (external) event node
   const unsigned evflags = cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0u;
+  const Workspace &w = net->ws;
+  const int ns = (int)net->steps.size();
   int64_t c = 0;
-  for (int32_t l = 0; l < net->L; ++l) {
-    if (prof) cudaEventRecordWithFlags(net->ev_before[l], s, evflags);
-    launch_layer(net->cfg, net->ws, net->dl[l], l, ymax, net->n, s);
-    if (prof) cudaEventRecordWithFlags(net->ev_after[l], s, evflags);
-    ++c;
-    if (l + 1 < net->L) {
-      launch_scan(net->ws, l, compact, net->n, s);
-      launch_compact_copy(net->cfg, net->ws, l, net->n, s);
-      c += 2;
+  for (int si = 0; si < ns; ++si) {
+    const Step &S = net->steps[si];
+    const bool last = si + 1 == ns;
+    if (prof) cudaEventRecordWithFlags(net->ev_before[S.a], s, evflags);
+    if (S.m == 1)
+      launch_layer(net->cfg, w, net->dl[S.a], S.a, w.alive_row(si, 0), ymax, s);
+    else
+      launch_pass(net->cfg, w, net->passes[S.pass], w.alive_set(si), ymax, s);
+    if (prof) cudaEventRecordWithFlags(net->ev_after[S.a], s, evflags);
+    // survivor counts for every layer of the step; compaction between steps
+    launch_scan(w, S.a, S.m, w.alive_set(si), w.alive_set(si + 1), compact && !last, s);
+    c += 2;
+    if (!last) {
+      launch_compact_copy(net->cfg, w, S.a, S.m, w.alive_row(si, S.m - 1), net->n, s);
+      ++c;
     }
   }
   if (launches) *launches = c;
@@ -212,6 +312,8 @@ void enqueue_chain(sdnn_net *net, bool compact, cudaStream_t s, int64_t *launche
 
 sdnn_status run_chain(sdnn_net *net, bool compact, cudaStream_t s) {
   if (net->L == 0) return SDNN_OK;
+  sdnn_status st0 = make_plan(net);
+  if (st0) return st0;
   if (net->opts.flags & SDNN_F_NO_GRAPH) {
     enqueue_chain(net, compact, s, &net->chain_launches);
     CK(cudaGetLastError());
@@ -237,6 +339,13 @@ sdnn_status run_chain(sdnn_net *net, bool compact, cudaStream_t s) {
   return SDNN_OK;
 }
 
+void launch_final_yout(sdnn_net *net, int64_t batch, float *d_yout, cudaStream_t s) {
+  if (net->L == 0)
+    launch_yout(net->ws, 0, false, net->n, batch, d_yout, s);
+  else
+    launch_yout(net->ws, net->steps.back().a, true, net->n, batch, d_yout, s);
+}
+
 // Everything of one inference after Y0 is on the device.
 sdnn_status infer_device_impl(sdnn_net *net, const int64_t *d_rowptr, const int32_t *d_idx,
                               const float *d_val, int64_t batch, uint32_t *d_alive,
@@ -255,11 +364,16 @@ sdnn_status infer_device_impl(sdnn_net *net, const int64_t *d_rowptr, const int3
     if (st) return st;
     launches += net->chain_launches;
   }
-  const int32_t last = net->L == 0 ? 0 : net->L - 1;
-  launch_readout(net->ws, last, net->L > 0, d_alive, batch, s);
+  if (net->L == 0) {
+    launch_readout(net->ws, 0, net->ws.alive_row(0, 0), d_alive, batch, s);
+  } else {
+    const int si = (int)net->steps.size() - 1;
+    const Step &S = net->steps[si];
+    launch_readout(net->ws, S.a, net->ws.alive_row(si, S.m - 1), d_alive, batch, s);
+  }
   launches += 1 + (d_alive ? 1 : 0);
   if (d_yout) {
-    launch_yout(net->ws, net->L == 0 ? -1 : last, net->n, batch, d_yout, s);
+    launch_final_yout(net, batch, d_yout, s);
     launches += 2;
   }
   CK(cudaGetLastError());
@@ -269,10 +383,6 @@ sdnn_status infer_device_impl(sdnn_net *net, const int64_t *d_rowptr, const int3
   return SDNN_OK;
 }
 
-int nthreads_default() {
-  unsigned h = std::thread::hardware_concurrency();
-  return (int)std::max(1u, std::min(h, 32u));
-}
 
 template <class F>
 void parallel_for(int64_t n, int nt, F f) {
@@ -369,6 +479,7 @@ sdnn_status sdnn_create_empty(int32_t neurons, int32_t layers, const sdnn_opts *
   net->opts = o;
   net->device = dev;
   net->dl.resize(layers);
+  net->host.resize(layers);
   net->set.assign(layers, 0);
   net->bias_nonpos.assign(layers, 1);
   net->nnz.assign(layers, 0);
@@ -448,11 +559,13 @@ sdnn_status sdnn_set_layer(sdnn_net *net, int32_t l, const sdnn_layer *W, const 
     std::lock_guard<std::mutex> g(net->stat_mu);
     const bool was = net->set[l];
     net->dl[l] = d;
-    net->bias_nonpos[l] = p.bias_nonpos ? 1 : 0;
-    net->nnz[l] = p.nnz;
-    if (p.gmax > 1) net->grouped_layers += was ? 0 : 1;
-    net->max_group = std::max(net->max_group, p.gmax);
-    net->max_k = std::max(net->max_k, p.kmax);
+    net->host[l] = std::move(p);
+    net->plan_dirty = true;
+    net->bias_nonpos[l] = net->host[l].bias_nonpos ? 1 : 0;
+    net->nnz[l] = net->host[l].nnz;
+    if (net->host[l].gmax > 1) net->grouped_layers += was ? 0 : 1;
+    net->max_group = std::max(net->max_group, net->host[l].gmax);
+    net->max_k = std::max(net->max_k, net->host[l].kmax);
     if (!was) {
       net->set[l] = 1;
       net->nset.fetch_add(1);
@@ -591,7 +704,7 @@ sdnn_status sdnn_infer(sdnn_net *net, const int64_t *y0_rowptr, const int32_t *y
   float *d_yout = nullptr;
   if (y_out && batch > 0) {
     CK(cudaMalloc(&d_yout, sizeof(float) * (size_t)net->n * (size_t)batch));
-    launch_yout(net->ws, net->L == 0 ? -1 : net->L - 1, net->n, batch, d_yout, s);
+    launch_final_yout(net, batch, d_yout, s);
   }
   int32_t ncat = 0;
   CK(cudaMemcpyAsync(&ncat, net->ws.ncat, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
@@ -635,10 +748,47 @@ sdnn_status sdnn_layer_times(const sdnn_net *cnet, float *ms) {
   if (!net->profiled) return fail(SDNN_E_STATE, "no profiled inference yet");
   sdnn_status st = set_device(net);
   if (st) return st;
-  for (int l = 0; l < net->L; ++l) {
-    CK(cudaEventSynchronize(net->ev_after[l]));
-    CK(cudaEventElapsedTime(&ms[l], net->ev_before[l], net->ev_after[l]));
+  for (const Step &S : net->steps) {            // a fused pass is one kernel: split evenly
+    float t = 0.f;
+    CK(cudaEventSynchronize(net->ev_after[S.a]));
+    CK(cudaEventElapsedTime(&t, net->ev_before[S.a], net->ev_after[S.a]));
+    for (int j = 0; j < S.m; ++j) ms[S.a + j] = t / S.m;
   }
+  return SDNN_OK;
+}
+
+sdnn_status sdnn_step_plan(const sdnn_net *net, int32_t *step_len, int32_t *nsteps) {
+  if (!net || !nsteps || !step_len) return fail(SDNN_E_ARG, "NULL argument");
+  if (net->plan_dirty && net->L > 0) return fail(SDNN_E_STATE, "no plan yet (run an inference first)");
+  for (size_t i = 0; i < net->steps.size(); ++i) step_len[i] = net->steps[i].m;
+  *nsteps = (int32_t)net->steps.size();
+  return SDNN_OK;
+}
+
+sdnn_status sdnn_plan_steps(int32_t neurons, int32_t layers, const sdnn_layer *W,
+                            const float *bias, const sdnn_opts *opts, int32_t *step_len,
+                            int32_t *nsteps) {
+  if (!nsteps || (layers > 0 && (!W || !bias || !step_len))) return fail(SDNN_E_ARG, "NULL argument");
+  if (neurons < 1 || layers < 0) return fail(SDNN_E_ARG, "bad sizes");
+  if (neurons > 65536) return fail(SDNN_E_UNSUPPORTED, "neurons > 65536");
+  sdnn_opts o;
+  sdnn_status st = check_opts(opts, o);
+  if (st) return st;
+  std::vector<PackedLayer> host(layers);
+  for (int l = 0; l < layers; ++l) {
+    LayerIn in{W[l].format, W[l].ell_k, W[l].rowptr, W[l].idx, W[l].val, W[l].uniform_value};
+    std::string msg;
+    const int rc = pack_layer(neurons, in, bias + (int64_t)l * neurons,
+                              !(o.flags & SDNN_F_NO_GROUPS), host[l], msg);
+    if (rc) return fail(rc, "layer " + std::to_string(l) + ": " + msg);
+  }
+  std::vector<const PackedLayer *> lp(layers);
+  for (int l = 0; l < layers; ++l) lp[l] = &host[l];
+  const int cap = std::min(o.fuse_rows < 0 ? 0 : o.fuse_rows, kMaxPassRows);
+  const int maxm = o.fuse_layers < 0 ? 8 : o.fuse_layers;
+  const std::vector<Step> steps = plan_steps(lp, neurons, cap, maxm);
+  for (size_t i = 0; i < steps.size(); ++i) step_len[i] = steps[i].m;
+  *nsteps = (int32_t)steps.size();
   return SDNN_OK;
 }
 
@@ -650,7 +800,9 @@ sdnn_status sdnn_stats_get(const sdnn_net *cnet, sdnn_stats *out, int64_t *live_
   s.struct_size = sizeof(sdnn_stats);
   s.neurons = net->n;
   s.layers = net->L;
-  s.path = 0;
+  s.path = net->fused_layers > 0 ? 1 : 0;
+  s.steps = (int32_t)net->steps.size();
+  s.fused_layers = net->fused_layers;
   s.grouped_layers = net->grouped_layers;
   s.max_group = net->max_group;
   s.max_k = net->max_k;
@@ -687,6 +839,7 @@ void sdnn_destroy(sdnn_net *net) {
   cudaDeviceSynchronize();
   free_ws(net);
   net->arena.release();
+  net->pass_arena.release();
   cudaFree(net->d_rowptr);
   cudaFree(net->d_idx);
   cudaFree(net->d_val);

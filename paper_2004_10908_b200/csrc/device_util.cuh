@@ -1,0 +1,112 @@
+// device_util.cuh -- small device helpers shared by the product kernels
+// (kernels.cu, chain.cu): canonical clamp, vector load/store, liveness-bit
+// publication, mbarrier and cp.async.bulk (TMA bulk copy) wrappers.
+#pragma once
+#include <cstdint>
+
+namespace sdnn {
+
+#define FULL 0xffffffffu
+
+__device__ __forceinline__ float clampy(float z, float ymax) {
+  return z > 0.f ? fminf(z, ymax) : 0.f;
+}
+
+template <int VEC>
+struct VecT;
+template <>
+struct VecT<1> {
+  using T = float;
+  __device__ static T ld(const float *p) { return __ldg(p); }
+  __device__ static void st(float *p, const float (&v)[1]) { *p = v[0]; }
+  __device__ static void unpack(const T &x, float (&v)[1]) { v[0] = x; }
+};
+template <>
+struct VecT<2> {
+  using T = float2;
+  __device__ static T ld(const float *p) { return __ldg(reinterpret_cast<const float2 *>(p)); }
+  __device__ static void st(float *p, const float (&v)[2]) {
+    *reinterpret_cast<float2 *>(p) = make_float2(v[0], v[1]);
+  }
+  __device__ static void unpack(const T &x, float (&v)[2]) { v[0] = x.x; v[1] = x.y; }
+};
+template <>
+struct VecT<4> {
+  using T = float4;
+  __device__ static T ld(const float *p) { return __ldg(reinterpret_cast<const float4 *>(p)); }
+  __device__ static void st(float *p, const float (&v)[4]) {
+    *reinterpret_cast<float4 *>(p) = make_float4(v[0], v[1], v[2], v[3]);
+  }
+  __device__ static void unpack(const T &x, float (&v)[4]) {
+    v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+  }
+};
+
+// Combine per-lane liveness bits (lane covers positions lane*VEC + e of a
+// 32*VEC-wide tile) into the tile's VEC 32-bit words and OR them into alive[].
+template <int VEC>
+__device__ __forceinline__ void publish_alive(uint32_t am, int lane, int64_t tile_pos, int width,
+                                              uint32_t *alive) {
+  uint32_t bal[VEC];
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) bal[e] = __ballot_sync(FULL, (am >> e) & 1u);
+  if (lane < VEC) {
+    uint32_t word = 0;
+#pragma unroll
+    for (int q = 0; q < 32; ++q) {
+      const int pos = lane * 32 + q;         // position inside the tile
+      const int src_lane = pos / VEC, e = pos % VEC;
+      uint32_t b = 0;
+#pragma unroll
+      for (int ee = 0; ee < VEC; ++ee)
+        if (ee == e) b = (bal[ee] >> src_lane) & 1u;
+      word |= b << q;
+    }
+    const int64_t base = tile_pos + lane * 32;
+    if (base < width) {
+      const int64_t rem = width - base;
+      if (rem < 32) word &= (1u << rem) - 1u;
+      if (word) atomicOr(&alive[base >> 5], word);
+    }
+  }
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx_arrive(uint64_t *b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred P;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+      " @!P bra WAIT_%=;\n}\n" ::"r"(smem_u32(b)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+
+// 16-byte cp.async (LDGSTS, L2 only) global -> shared
+__device__ __forceinline__ void cp_async16(void *dst, const void *src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+// arrive on `bar` once all of this thread's prior cp.async have landed (the
+// barrier's expected count must include one arrival per calling thread)
+__device__ __forceinline__ void cp_async_arrive(uint64_t *bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+}  // namespace sdnn

@@ -16,73 +16,9 @@
 #include <cstdio>
 
 #include "sdnn_internal.h"
+#include "device_util.cuh"
 
 namespace sdnn {
-
-#define FULL 0xffffffffu
-
-__device__ __forceinline__ float clampy(float z, float ymax) {
-  return z > 0.f ? fminf(z, ymax) : 0.f;
-}
-
-template <int VEC>
-struct VecT;
-template <>
-struct VecT<1> {
-  using T = float;
-  __device__ static T ld(const float *p) { return __ldg(p); }
-  __device__ static void st(float *p, const float (&v)[1]) { *p = v[0]; }
-  __device__ static void unpack(const T &x, float (&v)[1]) { v[0] = x; }
-};
-template <>
-struct VecT<2> {
-  using T = float2;
-  __device__ static T ld(const float *p) { return __ldg(reinterpret_cast<const float2 *>(p)); }
-  __device__ static void st(float *p, const float (&v)[2]) {
-    *reinterpret_cast<float2 *>(p) = make_float2(v[0], v[1]);
-  }
-  __device__ static void unpack(const T &x, float (&v)[2]) { v[0] = x.x; v[1] = x.y; }
-};
-template <>
-struct VecT<4> {
-  using T = float4;
-  __device__ static T ld(const float *p) { return __ldg(reinterpret_cast<const float4 *>(p)); }
-  __device__ static void st(float *p, const float (&v)[4]) {
-    *reinterpret_cast<float4 *>(p) = make_float4(v[0], v[1], v[2], v[3]);
-  }
-  __device__ static void unpack(const T &x, float (&v)[4]) {
-    v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
-  }
-};
-
-// Combine per-lane liveness bits (lane covers positions lane*VEC + e of a
-// 32*VEC-wide tile) into the tile's VEC 32-bit words and OR them into alive[].
-template <int VEC>
-__device__ __forceinline__ void publish_alive(uint32_t am, int lane, int64_t tile_pos, int width,
-                                              uint32_t *alive) {
-  uint32_t bal[VEC];
-#pragma unroll
-  for (int e = 0; e < VEC; ++e) bal[e] = __ballot_sync(FULL, (am >> e) & 1u);
-  if (lane < VEC) {
-    uint32_t word = 0;
-#pragma unroll
-    for (int q = 0; q < 32; ++q) {
-      const int pos = lane * 32 + q;         // position inside the tile
-      const int src_lane = pos / VEC, e = pos % VEC;
-      uint32_t b = 0;
-#pragma unroll
-      for (int ee = 0; ee < VEC; ++ee)
-        if (ee == e) b = (bal[ee] >> src_lane) & 1u;
-      word |= b << q;
-    }
-    const int64_t base = tile_pos + lane * 32;
-    if (base < width) {
-      const int64_t rem = width - base;
-      if (rem < 32) word &= (1u << rem) - 1u;
-      if (word) atomicOr(&alive[base >> 5], word);
-    }
-  }
-}
 
 // ---------------------------------------------------------------------------
 // Layer kernel, uniform weights (every stored value of W_l equals wu).
@@ -184,33 +120,6 @@ constexpr int kBulkStages = 3;
 constexpr int kBulkConsumers = 4;                // 4 warps x 32 lanes x 4 positions = 512
 constexpr int kBulkThreads = 32 * (1 + kBulkConsumers);
 constexpr size_t kBulkSmem = (size_t)kBulkStages * 32 * kBulkT * sizeof(float) + 2 * kBulkStages * 8;
-
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx_arrive(uint64_t *b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t *b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
-  asm volatile(
-      "{\n .reg .pred P;\n WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
-      " @!P bra WAIT_%=;\n}\n" ::"r"(smem_u32(b)), "r"(parity) : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
 
 __global__ void __launch_bounds__(kBulkThreads, 1) k_layer_bulk(DevLayer L, const LayerState *__restrict__ st,
                                                                int layer, float *Ya, float *Yb,
@@ -534,24 +443,184 @@ __global__ void k_y0_positive(int64_t batch, const int64_t *__restrict__ rowptr,
 }
 
 // ---------------------------------------------------------------------------
-// Liveness scan + compaction decision (row a4).  Single CTA.
+// Fused multi-layer pass (model decomposition, fuse.cpp) -- opt-in
+// (sdnn_opts.fuse_rows > 0).  Persistent CTAs; an item is (component c, batch
+// tile of T positions), T = 8192 / R so that a component tile is one 32 KB
+// buffer.  Warp 0 streams the component's input rows into kPassIn input
+// buffers with 16-byte cp.async (row segments of 128 B - 1 KB, too small to
+// pay one TMA bulk copy each), so up to kPassIn-1 items load while one
+// computes.  8 consumer warps run the m layers out of shared memory: layer 0
+// reads the input buffer and writes the shared work buffer, layer 1 writes back
+// into the (consumed) input buffer, and so on; the last layer stores straight
+// to the output rows in HBM.  A work unit is (group, 32-position slice), lane =
+// position.  HBM traffic per layer drops by m versus k_layer_bulk, but on B200
+// the kernel is issue/latency bound (one position per lane, CTA barriers
+// between layers): measured slower than streaming, see DESIGN.md section 7.
+// ---------------------------------------------------------------------------
+constexpr int kPassConsumers = 8;
+constexpr int kPassThreads = 32 * (1 + kPassConsumers);
+constexpr int kPassBuf = 8192;                   // floats per buffer (R * T)
+constexpr int kPassIn = 5;                       // input buffers (+1 shared work buffer)
+constexpr size_t kPassSmem =
+    (size_t)(kPassIn + 1) * kPassBuf * 4 + (kPassIn + 1) * 8 + kMaxPassLayers * 8 * 4;
+
+template <int T>
+__global__ void __launch_bounds__(kPassThreads, 1) k_pass(DevPass P, const LayerState *__restrict__ st,
+                                                         float *Ya, float *Yb,
+                                                         uint32_t *__restrict__ alive,
+                                                         int64_t wstride, int64_t stride, float ymax) {
+  constexpr int S = T / 32;                      // 32-position slices per tile
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float *buf = reinterpret_cast<float *>(smem_raw);
+  float *workb = buf + (size_t)kPassIn * kPassBuf;
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem_raw + (size_t)(kPassIn + 1) * kPassBuf * 4);
+  volatile int *done = reinterpret_cast<volatile int *>(full + kPassIn);
+  uint32_t *aw = reinterpret_cast<uint32_t *>(full + kPassIn + 1);   // [kMaxPassLayers][S]
+  const LayerState Sx = st[P.a];
+  const int width = Sx.width;
+  if (width <= 0) return;
+  const float *__restrict__ Yin = Sx.in ? Yb : Ya;
+  float *__restrict__ Yout = Sx.in ? Ya : Yb;
+  const int tiles = (width + T - 1) / T;
+  const int64_t items = (int64_t)P.ncomp * tiles;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int x = 0; x < kPassIn; ++x) mbar_init(&full[x], 32);   // one cp.async arrival per lane
+    *done = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int q = threadIdx.x; q < kMaxPassLayers * S; q += blockDim.x) aw[q] = 0u;
+  __syncthreads();
+  if (warp == 0) {
+    // ------------------------------ producer ------------------------------
+    int64_t i = 0;
+    for (int64_t it = blockIdx.x; it < items; it += gridDim.x, ++i) {
+      const int c = (int)(it / tiles);
+      const int tile = (int)(it - (int64_t)c * tiles);
+      const int x = (int)(i % kPassIn);
+      if (i >= kPassIn) {                      // buffer x held item i - kPassIn
+        if (lane == 0)
+          while (*done < i - kPassIn + 1) __nanosleep(20);
+        __syncwarp();
+      }
+      const int cnt = P.in_count[c];
+      float *dstb = buf + (size_t)x * kPassBuf;
+      const int32_t *rows = P.in_rows + (int64_t)c * P.rin;
+      constexpr int CH = T / 4;                  // 16-byte chunks per row segment
+      const float *src0 = Yin + (int64_t)tile * T;
+      for (int q = lane; q < cnt * CH; q += 32) {
+        const int r = q / CH, ch = q - r * CH;
+        cp_async16(dstb + (size_t)r * T + ch * 4, src0 + (int64_t)rows[r] * stride + ch * 4);
+      }
+      cp_async_arrive(&full[x]);
+    }
+  } else {
+    // ------------------------------ consumers -----------------------------
+    const int cw = warp - 1;
+    int64_t i = 0;
+    for (int64_t it = blockIdx.x; it < items; it += gridDim.x, ++i) {
+      const int c = (int)(it / tiles);
+      const int tile = (int)(it - (int64_t)c * tiles);
+      float *inb = buf + (size_t)(i % kPassIn) * kPassBuf;
+      mbar_wait(&full[i % kPassIn], (uint32_t)((i / kPassIn) & 1));
+      for (int j = 0; j < P.m; ++j) {
+        const PassLayerDev PL = P.layers[j];
+        const float *srcb = (j & 1) ? workb : inb;
+        float *dstb = (j & 1) ? inb : workb;
+        const bool last = j == P.m - 1;
+        const float wu = PL.wu;
+        for (int u = cw; u < PL.NG * S; u += kPassConsumers) {
+          const int gi = u / S, sl = u - gi * S;
+          const int64_t rec = (int64_t)c * PL.NG + gi;
+          const int G = PL.g[rec];
+          if (G == 0) continue;
+          const int K = PL.k[rec];
+          const int mysrc = lane < K ? (int)PL.src[rec * 32 + lane] : 0;
+          const int mydst = lane < G ? (int)PL.dst[rec * 32 + lane] : 0;
+          const float mybias = lane < G ? PL.bias[rec * 32 + lane] : 0.f;
+          const int pofs = sl * 32 + lane;
+          float acc = 0.f;
+          if (K == 32) {
+#pragma unroll 8
+            for (int t = 0; t < 32; ++t) acc = __fmaf_rn(srcb[__shfl_sync(FULL, mysrc, t) * T + pofs], wu, acc);
+          } else {
+            for (int t = 0; t < K; ++t) acc = __fmaf_rn(srcb[__shfl_sync(FULL, mysrc, t) * T + pofs], wu, acc);
+          }
+          float mx = 0.f;                          // max over this slice's outputs
+          if (last) {
+            // lane v holds member v's output row pointer: no dependent load per member
+            float *myrow = Yout + (int64_t)tile * T + sl * 32 +
+                           (lane < G ? (int64_t)P.out_rows[(int64_t)c * P.rout + mydst] * stride : 0);
+            for (int v = 0; v < G; ++v) {
+              float *row = reinterpret_cast<float *>(__shfl_sync(FULL, reinterpret_cast<uintptr_t>(myrow), v));
+              const float b = __shfl_sync(FULL, mybias, v);
+              const float y = clampy(__fadd_rn(acc, b), ymax);
+              mx = fmaxf(mx, y);
+              row[lane] = y;
+            }
+          } else {
+            const int myoff = (lane < G ? mydst : 0) * T + sl * 32;
+            for (int v = 0; v < G; ++v) {
+              const int off = __shfl_sync(FULL, myoff, v);
+              const float b = __shfl_sync(FULL, mybias, v);
+              const float y = clampy(__fadd_rn(acc, b), ymax);
+              mx = fmaxf(mx, y);
+              dstb[off + lane] = y;
+            }
+          }
+          const uint32_t word = __ballot_sync(FULL, mx > 0.f);
+          if (lane == 0 && word) atomicOr(&aw[j * S + sl], word);
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kPassConsumers) : "memory");
+      }
+      if (threadIdx.x == 32) {
+        for (int j = 0; j < P.m; ++j)
+          for (int v = 0; v < S; ++v) {
+            uint32_t word = aw[j * S + v];
+            aw[j * S + v] = 0u;
+            const int64_t base = (int64_t)tile * T + v * 32;
+            if (base >= width) word = 0u;
+            else if (width - base < 32) word &= (1u << (width - base)) - 1u;
+            if (word) atomicOr(&alive[j * wstride + (base >> 5)], word);
+          }
+        *done = (int)(i + 1);
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * kPassConsumers) : "memory");
+    }
+  }
+}
+
+int pass_buffer_floats() { return kPassBuf; }
+
+// ---------------------------------------------------------------------------
+// After a step [a, a+m): survivor counts of its layers, compaction decision
+// (row a4) from the last layer's bits, zeroing of the next step's bit set.
+// Single CTA.
 // ---------------------------------------------------------------------------
 constexpr int kCompactMin = 128;
 
-__global__ void __launch_bounds__(1024) k_scan_layer(LayerState *st, int layer,
-                                                     const uint32_t *alive_cur,
-                                                     uint32_t *alive_next, int32_t *wpre,
-                                                     int32_t *live, int compact) {
-  const LayerState S = st[layer];
+__global__ void __launch_bounds__(1024) k_scan_step(LayerState *st, int a, int m,
+                                                    const uint32_t *alive_cur,
+                                                    uint32_t *alive_next, int64_t wstride,
+                                                    int32_t *wpre, int32_t *live, int compact) {
+  const LayerState S = st[a];
   const int64_t words = ((int64_t)S.width + 31) >> 5;
-  const int64_t count = scan_words(alive_cur, words, wpre);
-  for (int64_t q = threadIdx.x; q < words; q += blockDim.x) alive_next[q] = 0u;
+  for (int j = 0; j < m - 1; ++j) {
+    int64_t cnt = 0;
+    for (int64_t q = threadIdx.x; q < words; q += blockDim.x) cnt += __popc(alive_cur[j * wstride + q]);
+    int64_t total;
+    block_exclusive_scan(cnt, &total);
+    if (threadIdx.x == 0) live[a + j] = (int32_t)total;
+  }
+  const int64_t count = scan_words(alive_cur + (int64_t)(m - 1) * wstride, words, wpre);
+  for (int j = 0; j < kMaxPassLayers; ++j)
+    for (int64_t q = threadIdx.x; q < words; q += blockDim.x) alive_next[j * wstride + q] = 0u;
   if (threadIdx.x == 0) {
-    live[layer] = (int32_t)count;
+    live[a + m - 1] = (int32_t)count;
     const int64_t dead = S.width - count;
     LayerState n;
     if (compact && dead >= kCompactMin && dead * 16 >= S.width) {
-      n.in = S.in;               // layer l's input buffer is free: compact into it
+      n.in = S.in;               // the step's input buffer is free: compact into it
       n.width = (int32_t)count;
       n.rid = 1 - S.rid;
       n.compacted = 1;
@@ -561,19 +630,19 @@ __global__ void __launch_bounds__(1024) k_scan_layer(LayerState *st, int layer,
       n.rid = S.rid;
       n.compacted = 0;
     }
-    st[layer + 1] = n;
+    st[a + m] = n;
   }
 }
 
-// Move the live batch columns of layer l's output into the free buffer.
-__global__ void k_compact(const LayerState *__restrict__ st, int layer, float *Ya, float *Yb,
+// Move the live batch columns of the step's output into the free buffer.
+__global__ void k_compact(const LayerState *__restrict__ st, int a, int m, float *Ya, float *Yb,
                           int32_t *ridA, int32_t *ridB, const uint32_t *__restrict__ alive,
                           const int32_t *__restrict__ wpre, int32_t n, int64_t stride) {
-  const LayerState N1 = st[layer + 1];
+  const LayerState N1 = st[a + m];
   if (!N1.compacted) return;
-  const LayerState S = st[layer];
-  const float *__restrict__ src = S.in ? Ya : Yb;   // layer output = Y[1 - S.in]
-  float *__restrict__ dst = S.in ? Yb : Ya;         // layer input buffer
+  const LayerState S = st[a];
+  const float *__restrict__ src = S.in ? Ya : Yb;   // step output = Y[1 - S.in]
+  float *__restrict__ dst = S.in ? Yb : Ya;         // step input buffer
   const int32_t *__restrict__ rsrc = S.rid ? ridB : ridA;
   int32_t *__restrict__ rdst = S.rid ? ridA : ridB;
   const int64_t words = ((int64_t)S.width + 31) >> 5;
@@ -597,13 +666,12 @@ __global__ void k_compact(const LayerState *__restrict__ st, int layer, float *Y
 // Readout (row a6).  Single CTA: ascending ids (positions are in ascending
 // original-row order because densify and compaction are stable).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(1024) k_readout(const LayerState *__restrict__ st, int sidx,
+__global__ void __launch_bounds__(1024) k_readout(const LayerState *__restrict__ st, int a,
                                                   const uint32_t *__restrict__ alive,
                                                   const int32_t *ridA, const int32_t *ridB,
                                                   int32_t *wpre, int32_t *cats, int32_t *ncat,
-                                                  uint32_t *d_alive_out, int32_t *live,
-                                                  int live_idx) {
-  const LayerState S = st[sidx];
+                                                  uint32_t *d_alive_out) {
+  const LayerState S = st[a];
   const int64_t words = ((int64_t)S.width + 31) >> 5;
   const int32_t *rid = S.rid ? ridB : ridA;
   const int64_t total = scan_words(alive, words, wpre);
@@ -619,17 +687,14 @@ __global__ void __launch_bounds__(1024) k_readout(const LayerState *__restrict__
       if (d_alive_out) atomicOr(&d_alive_out[id >> 5], 1u << (id & 31));
     }
   }
-  if (threadIdx.x == 0) {
-    *ncat = (int32_t)total;
-    if (live_idx >= 0) live[live_idx] = (int32_t)total;
-  }
+  if (threadIdx.x == 0) *ncat = (int32_t)total;
 }
 
 // Y_L (neuron-major, positions) -> row-major [batch][n] (rows not present are 0)
-__global__ void k_yout(const LayerState *__restrict__ st, int sidx, int final_out,
+__global__ void k_yout(const LayerState *__restrict__ st, int a, int final_out,
                        const float *Ya, const float *Yb, const int32_t *ridA,
                        const int32_t *ridB, int32_t n, int64_t stride, float *yout) {
-  const LayerState S = st[sidx];
+  const LayerState S = st[a];
   const int bufsel = final_out ? 1 - S.in : S.in;
   const float *Y = bufsel ? Yb : Ya;
   const int32_t *rid = S.rid ? ridB : ridA;
@@ -648,6 +713,10 @@ int bulk_stride_quantum() { return kBulkT; }
 
 void configure_kernels() {
   cudaFuncSetAttribute(k_layer_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBulkSmem);
+  cudaFuncSetAttribute(k_pass<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPassSmem);
+  cudaFuncSetAttribute(k_pass<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPassSmem);
+  cudaFuncSetAttribute(k_pass<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPassSmem);
+  cudaFuncSetAttribute(k_pass<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPassSmem);
 }
 
 void launch_densify(const LaunchCfg &c, const Workspace &w, int32_t n, int64_t batch,
@@ -655,6 +724,7 @@ void launch_densify(const LaunchCfg &c, const Workspace &w, int32_t n, int64_t b
                     cudaStream_t s) {
   const int64_t words = (batch + 31) / 32;
   cudaMemsetAsync(w.Y[0], 0, sizeof(float) * (size_t)n * (size_t)w.stride, s);
+  cudaMemsetAsync(w.alive[0], 0, sizeof(uint32_t) * (size_t)kMaxPassLayers * w.words, s);
   if (words > 0) {
     const int blocks = (int)std::min<int64_t>((words * 32 + 255) / 256, c.sms * 8);
     k_rowflags<<<blocks, 256, 0, s>>>(batch, rowptr, val, compact ? 1 : 0, w.inmask, words);
@@ -673,52 +743,62 @@ void launch_zero_layers_alive(const Workspace &w, int64_t batch, const int64_t *
         batch, rowptr, val, w.alive[0], words);
 }
 
-void launch_layer(const LaunchCfg &c, const Workspace &w, const DevLayer &L, int32_t layer,
-                  float ymax, int32_t n, cudaStream_t s) {
-  (void)n;
-  uint32_t *alive = w.alive[layer & 1];
+void launch_layer(const LaunchCfg &c, const Workspace &w, const DevLayer &L, int32_t a,
+                  uint32_t *alive, float ymax, cudaStream_t s) {
   if (L.uniform && L.kmax <= 32 && c.bulk) {
-    k_layer_bulk<<<c.sms, kBulkThreads, kBulkSmem, s>>>(L, w.st, layer, w.Y[0], w.Y[1], alive,
+    k_layer_bulk<<<c.sms, kBulkThreads, kBulkSmem, s>>>(L, w.st, a, w.Y[0], w.Y[1], alive,
                                                        w.stride, ymax);
   } else if (L.uniform) {
     if (L.regular && L.kmax == 32)
-      k_layer_uniform<4, true><<<c.layer_blocks, 256, 0, s>>>(L, w.st, layer, w.Y[0], w.Y[1],
+      k_layer_uniform<4, true><<<c.layer_blocks, 256, 0, s>>>(L, w.st, a, w.Y[0], w.Y[1],
                                                                alive, w.stride, ymax);
     else
-      k_layer_uniform<4, false><<<c.layer_blocks, 256, 0, s>>>(L, w.st, layer, w.Y[0], w.Y[1],
+      k_layer_uniform<4, false><<<c.layer_blocks, 256, 0, s>>>(L, w.st, a, w.Y[0], w.Y[1],
                                                                 alive, w.stride, ymax);
   } else {
-    k_layer_general<2><<<c.layer_blocks, 256, 0, s>>>(L, w.st, layer, w.Y[0], w.Y[1], alive,
+    k_layer_general<2><<<c.layer_blocks, 256, 0, s>>>(L, w.st, a, w.Y[0], w.Y[1], alive,
                                                       w.stride, ymax);
   }
 }
 
-void launch_scan(const Workspace &w, int32_t layer, bool compact, int32_t n, cudaStream_t s) {
-  (void)n;
-  k_scan_layer<<<1, 1024, 0, s>>>(w.st, layer, w.alive[layer & 1], w.alive[(layer + 1) & 1],
-                                  w.wpre, w.live, compact ? 1 : 0);
+void launch_pass(const LaunchCfg &c, const Workspace &w, const DevPass &P, uint32_t *alive,
+                 float ymax, cudaStream_t s) {
+#define SDNN_PASS(TT)                                                                          \
+  k_pass<TT><<<c.sms, kPassThreads, kPassSmem, s>>>(P, w.st, w.Y[0], w.Y[1], alive, w.words, \
+                                                    w.stride, ymax)
+  switch (P.T) {
+    case 256: SDNN_PASS(256); break;
+    case 128: SDNN_PASS(128); break;
+    case 64: SDNN_PASS(64); break;
+    default: SDNN_PASS(32); break;
+  }
+#undef SDNN_PASS
 }
 
-void launch_compact_copy(const LaunchCfg &c, const Workspace &w, int32_t layer, int32_t n,
-                         cudaStream_t s) {
-  k_compact<<<c.copy_blocks, 256, 0, s>>>(w.st, layer, w.Y[0], w.Y[1], w.rid[0], w.rid[1],
-                                          w.alive[layer & 1], w.wpre, n, w.stride);
+void launch_scan(const Workspace &w, int32_t a, int32_t m, const uint32_t *alive_cur,
+                 uint32_t *alive_next, bool compact, cudaStream_t s) {
+  k_scan_step<<<1, 1024, 0, s>>>(w.st, a, m, alive_cur, alive_next, w.words, w.wpre, w.live,
+                                 compact ? 1 : 0);
 }
 
-void launch_readout(const Workspace &w, int32_t last_state, bool after_layer,
+void launch_compact_copy(const LaunchCfg &c, const Workspace &w, int32_t a, int32_t m,
+                         const uint32_t *alive_last, int32_t n, cudaStream_t s) {
+  k_compact<<<c.copy_blocks, 256, 0, s>>>(w.st, a, m, w.Y[0], w.Y[1], w.rid[0], w.rid[1],
+                                          alive_last, w.wpre, n, w.stride);
+}
+
+void launch_readout(const Workspace &w, int32_t a, const uint32_t *alive_last,
                     uint32_t *d_alive_out, int64_t batch, cudaStream_t s) {
   if (d_alive_out) cudaMemsetAsync(d_alive_out, 0, sizeof(uint32_t) * (size_t)((batch + 31) / 32), s);
-  k_readout<<<1, 1024, 0, s>>>(w.st, last_state, w.alive[last_state & 1], w.rid[0], w.rid[1],
-                               w.wpre, w.cats, w.ncat, d_alive_out, w.live,
-                               after_layer ? last_state : -1);
+  k_readout<<<1, 1024, 0, s>>>(w.st, a, alive_last, w.rid[0], w.rid[1], w.wpre, w.cats, w.ncat,
+                               d_alive_out);
 }
 
-void launch_yout(const Workspace &w, int32_t last_state, int32_t n, int64_t batch,
+void launch_yout(const Workspace &w, int32_t a, bool final_out, int32_t n, int64_t batch,
                  float *d_yout, cudaStream_t s) {
   cudaMemsetAsync(d_yout, 0, sizeof(float) * (size_t)n * (size_t)batch, s);
-  (void)batch;
-  k_yout<<<148 * 4, 256, 0, s>>>(w.st, last_state < 0 ? 0 : last_state, last_state < 0 ? 0 : 1,
-                                 w.Y[0], w.Y[1], w.rid[0], w.rid[1], n, w.stride, d_yout);
+  k_yout<<<148 * 4, 256, 0, s>>>(w.st, a, final_out ? 1 : 0, w.Y[0], w.Y[1], w.rid[0], w.rid[1],
+                                 n, w.stride, d_yout);
 }
 
 }  // namespace sdnn

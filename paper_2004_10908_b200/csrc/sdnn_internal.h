@@ -84,18 +84,75 @@ struct LayerState {
   int32_t compacted; // 1 if the scan before this layer compacted
 };
 
+// ---------------------------------------------------------------------------
+// Multi-layer passes ("model decomposition").
+// A step runs layers [a, a+m).  For m > 1 the union of the m layers' bipartite
+// graphs splits into small connected components (for RadiX-Net butterflies:
+// 2^(5+2(m-1)) neurons); every component is closed, so one CTA can load a
+// component's input rows for a batch tile, run all m layers out of shared
+// memory, and write only the last layer's rows back to HBM.  Each output's
+// chain is still the canonical ascending-source fmaf sequence.
+// ---------------------------------------------------------------------------
+constexpr int kMaxPassLayers = 16;
+constexpr int kMaxPassRows = 256;      // rows per component per boundary (smem)
+
+struct Step {
+  int32_t a = 0, m = 1;                // layers [a, a+m)
+  int32_t pass = -1;                   // index into the fused-pass table, -1 = single layer
+};
+
+// plan greedy fused passes: extend while every component stays <= cap rows at
+// every boundary and the layers are uniform with K <= 32
+std::vector<Step> plan_steps(const std::vector<const PackedLayer *> &layers, int32_t n, int cap,
+                             int max_m);
+
+struct PassHostLayer {
+  int32_t NG = 0;                      // group slots per component (max over components)
+  float wu = 0.f;
+  std::vector<uint16_t> src, dst;      // [ncomp][NG][32] local row indices
+  std::vector<float> bias;             // [ncomp][NG][32] bias of each member
+  std::vector<uint8_t> k, g;           // [ncomp][NG] sources / members (0 = empty slot)
+};
+struct PassHost {
+  int32_t a = 0, m = 0, ncomp = 0, rin = 0, rout = 0, R = 0, T = 0;
+  std::vector<int32_t> in_rows;        // [ncomp][rin]  global neuron ids at boundary a, -1 pad
+  std::vector<int32_t> in_count;       // [ncomp]
+  std::vector<int32_t> out_rows;       // [ncomp][rout] global neuron ids at boundary a+m, -1 pad
+  std::vector<PassHostLayer> layers;   // [m]
+};
+void build_pass(const std::vector<const PackedLayer *> &layers, int32_t n, const Step &s,
+                int buf_floats, int min_t, PassHost &out);
+
+struct PassLayerDev {
+  const uint16_t *src, *dst;
+  const float *bias;
+  const uint8_t *k, *g;
+  int32_t NG;
+  float wu;
+};
+struct DevPass {
+  int32_t a, m, ncomp, rin, rout, R, T;
+  const int32_t *in_rows, *in_count, *out_rows;
+  const PassLayerDev *layers;          // device array [m]
+};
+
+// ---------------------------------------------------------------------------
+// Workspace
+// ---------------------------------------------------------------------------
 struct Workspace {
   float *Y[2] = {nullptr, nullptr};   // [n][stride] neuron-major activations
   int32_t *rid[2] = {nullptr, nullptr};
-  uint32_t *alive[2] = {nullptr, nullptr};  // [stride/32]
+  uint32_t *alive[2] = {nullptr, nullptr};  // two sets of [kMaxPassLayers][words] bitmasks
   uint32_t *inmask = nullptr;         // densify: rows kept
-  int32_t *wpre = nullptr;            // [stride/32 + 1] exclusive prefix of popcounts
+  int32_t *wpre = nullptr;            // [words + 1] exclusive prefix of popcounts
   LayerState *st = nullptr;           // [L + 1]
   int32_t *live = nullptr;            // [L] live rows after each layer
   int32_t *cats = nullptr;            // [stride] category list
   int32_t *ncat = nullptr;            // [1]
-  int64_t stride = 0;                 // row stride (capacity in batch columns, mult of 128)
+  int64_t stride = 0;                 // row stride (capacity in batch columns)
   int64_t words = 0;                  // stride / 32
+  uint32_t *alive_set(int s) const { return alive[s & 1]; }
+  uint32_t *alive_row(int s, int j) const { return alive[s & 1] + (int64_t)j * words; }
 };
 
 // ---------------------------------------------------------------------------
@@ -114,16 +171,26 @@ void configure_kernels();      // one-time function attributes (dynamic smem)
 void launch_densify(const LaunchCfg &c, const Workspace &w, int32_t n, int64_t batch,
                     const int64_t *rowptr, const int32_t *idx, const float *val, bool compact,
                     cudaStream_t s);
-void launch_layer(const LaunchCfg &c, const Workspace &w, const DevLayer &L, int32_t layer,
-                  float ymax, int32_t n, cudaStream_t s);
-void launch_scan(const Workspace &w, int32_t layer, bool compact, int32_t n, cudaStream_t s);
-void launch_compact_copy(const LaunchCfg &c, const Workspace &w, int32_t layer, int32_t n,
-                         cudaStream_t s);
+// one layer: reads state st[a], writes its liveness bits to `alive`
+void launch_layer(const LaunchCfg &c, const Workspace &w, const DevLayer &L, int32_t a,
+                  uint32_t *alive, float ymax, cudaStream_t s);
+int pass_buffer_floats();      // smem floats per component tile (tile T = this / R)
+// a fused pass: reads st[P.a], liveness of layer a+j to alive + j*words
+void launch_pass(const LaunchCfg &c, const Workspace &w, const DevPass &P, uint32_t *alive,
+                 float ymax, cudaStream_t s);
+// after a step [a, a+m): live counts of its m layers, compaction decision -> st[a+m],
+// zero the next step's bitmask set
+void launch_scan(const Workspace &w, int32_t a, int32_t m, const uint32_t *alive_cur,
+                 uint32_t *alive_next, bool compact, cudaStream_t s);
+void launch_compact_copy(const LaunchCfg &c, const Workspace &w, int32_t a, int32_t m,
+                         const uint32_t *alive_last, int32_t n, cudaStream_t s);
 void launch_zero_layers_alive(const Workspace &w, int64_t batch, const int64_t *rowptr,
                               const float *val, cudaStream_t s);
-void launch_readout(const Workspace &w, int32_t last_state, bool after_layer,
+// categories from the final liveness bits `alive_last` of the step entered with st[a]
+void launch_readout(const Workspace &w, int32_t a, const uint32_t *alive_last,
                     uint32_t *d_alive_out, int64_t batch, cudaStream_t s);
-void launch_yout(const Workspace &w, int32_t last_state, int32_t n, int64_t batch,
+// Y_L: final_out = the output buffer of the step entered with st[a] (L > 0), else Y_0
+void launch_yout(const Workspace &w, int32_t a, bool final_out, int32_t n, int64_t batch,
                  float *d_yout, cudaStream_t s);
 
 }  // namespace sdnn

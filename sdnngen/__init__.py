@@ -19,7 +19,8 @@ Families
         32 ids equal to m except in bits [p_l, p_l+5).  Hence every column has
         exactly 32 distinct sources, every row exactly 32 out-edges, and the
         layer is a (relabelled) set of N/32 dense 32x32 blocks.  The field
-        schedule is p_l = (2 l) mod (log2 N - 4) (overlapping fields; see
+        schedule is p_l = (2 l + floor(l / c)) mod (log2 N - 4), c =
+        ceil((log2 N - 4) / 2) (overlapping fields that reach every offset; see
         DESIGN.md reading R-W2 for why the non-overlapping radix-32 schedule is
         not used).  Neurons are relabelled at every internal layer boundary by
         a seeded permutation pi_l applied consistently to the outputs of layer
@@ -166,9 +167,14 @@ def _inv(p: np.ndarray) -> np.ndarray:
 
 
 def rn_field(n: int, l: int) -> int:
+    """Offset of layer l's 5-bit butterfly field: steps of 2 (consecutive fields
+    overlap in 3 bits, which keeps image locality for a few layers) and every
+    cycle of ceil(span/2) layers shifted by one, so odd offsets -- and with them
+    the top id bit -- are mixed too."""
     bits = n.bit_length() - 1
     span = bits - 4                      # valid offsets 0 .. bits-5
-    return (2 * l) % span
+    c = (span + 1) // 2
+    return (2 * l + l // c) % span
 
 
 def _rn_sets(n: int, l: int, m: np.ndarray) -> np.ndarray:

@@ -147,3 +147,43 @@ def test_product_path_never_touches_oracle():
             if f.endswith((".cu", ".cpp", ".h", ".py")):
                 txt = open(p).read()
                 assert "sdnn_oracle" not in txt and "liboracle" not in txt, p
+
+
+def test_plan_steps_rn_and_rr(sd):
+    """Fused multi-layer passes: RadiX-Net layers (5-bit butterfly fields that
+    overlap) have connected components of 2^(union of the fields' bits) neurons
+    over consecutive layers, so the planner fuses several layers per pass;
+    random-regular layers have one giant component and are never fused."""
+    rn = list(g.iter_layers(g.rn_spec(1024, 24)))
+    fields = [g.rn_field(1024, l) for l in range(24)]
+
+    def comp_bits(ls):
+        bits = set()
+        for p in ls:
+            bits |= set(range(p, p + 5))
+        return len(bits)
+    for cap in (256, 128):
+        plan = sd.sdnn_plan_steps(1024, rn, fuse_rows=cap)
+        assert sum(plan) == 24 and max(plan) > 1
+        a = 0
+        for m in plan:                      # every pass fits, and is maximal (greedy)
+            assert 2 ** comp_bits(fields[a:a + m]) <= cap or m == 1
+            if a + m < 24 and m < 8:
+                assert 2 ** comp_bits(fields[a:a + m + 1]) > cap
+            a += m
+    assert sd.sdnn_plan_steps(1024, rn) == [1] * 24                   # opt-in: default off
+    assert sd.sdnn_plan_steps(1024, rn, fuse_rows=0) == [1] * 24
+    assert sd.sdnn_plan_steps(1024, rn, fuse_rows=64) == [1] * 24    # 2 layers need 128 rows
+    assert max(sd.sdnn_plan_steps(1024, rn, fuse_rows=256, fuse_layers=2)) == 2
+    rr = list(g.iter_layers(g.rr_spec(1024, 5)))
+    assert sd.sdnn_plan_steps(1024, rr, fuse_rows=256) == [1] * 5
+    ka = list(g.iter_layers(g.ka_spec(1024, 20)))
+    assert sd.sdnn_plan_steps(1024, ka, fuse_rows=256, fuse_layers=16) == [16, 4]
+    big = [g.gen_layer(g.rn_spec(65536, 12), l, fmt="ell") for l in range(12)]
+    plan = sd.sdnn_plan_steps(65536, big, fmt="ell", fuse_rows=256)
+    assert sum(plan) == 12 and min(plan) >= 2
+
+
+def test_plan_steps_nonuniform_not_fused(sd):
+    lays = list(g.iter_layers(g.rn_spec(1024, 4, wdist="random")))
+    assert sd.sdnn_plan_steps(1024, lays, fuse_rows=256) == [1, 1, 1, 1]

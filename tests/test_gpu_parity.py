@@ -31,8 +31,10 @@ def assert_parity(cats_gpu, Y_gpu, cats_or, Y_or):
         assert np.array_equal(Y_gpu.view(np.uint32), Y_or.view(np.uint32))
 
 
-def run_gpu(sd, n, layers, rp, idx, val, fmt="csr", flags=0, ymax=32.0, want_y=True):
-    with sd.Net.from_layers(n, layers, fmt=fmt, flags=flags, ymax=ymax) as net:
+def run_gpu(sd, n, layers, rp, idx, val, fmt="csr", flags=0, ymax=32.0, want_y=True,
+            fuse_rows=-1, fuse_layers=-1):
+    with sd.Net.from_layers(n, layers, fmt=fmt, flags=flags, ymax=ymax, fuse_rows=fuse_rows,
+                            fuse_layers=fuse_layers) as net:
         cats, Y = net.infer(rp, idx, val, want_y=want_y)
         st = net.stats()
     return cats, Y, st
@@ -70,6 +72,50 @@ def test_c1_full(sd, c1, fmt, flags):
     assert_parity(cg, Yg, cats, Y)
     assert st["live_rows"] == prof
     assert 0 < cats.sum() < cats.size
+
+
+@pytest.mark.parametrize("fuse_rows,fuse_layers", [(0, -1), (128, -1), (256, -1),
+                                                   (256, 2), (256, 16)])
+def test_fused_passes_rn(sd, fuse_rows, fuse_layers):
+    """Multi-layer passes (model decomposition): T = 128 / 64 / 32 variants,
+    pass lengths 2..16, compaction between passes, ragged batch."""
+    n, L, B = 1024, 40, 700
+    spec = g.rn_spec(n, L)
+    layers = list(g.iter_layers(spec))
+    rp, idx = g.ms_inputs(n, B, seed=31)
+    cats, Y, prof = oracle.infer(n, layers, rp, idx, None, profile=True)
+    for flags in (0, 4):
+        cg, Yg, st = run_gpu(sd, n, layers, rp, idx, None, fmt="ell", flags=flags,
+                             fuse_rows=fuse_rows, fuse_layers=fuse_layers)
+        assert (st["fused_layers"] > 0) == (fuse_rows > 0)
+        assert_parity(cg, Yg, cats, Y)
+        assert st["live_rows"] == prof
+
+
+def test_fused_t64_and_irregular_components(sd):
+    """N = 512: component sizes 128 / 256 -> tiles of T = 64 / 32 positions."""
+    n, L = 512, 30
+    spec = g.rn_spec(n, L)
+    layers = list(g.iter_layers(spec))
+    rp, idx, val = g.random_inputs(n, 333, seed=12, density=0.4, lo=0.0, hi=1.5)
+    cats, Y, _ = oracle.infer(n, layers, rp, idx, val)
+    for cap in (128, 256):
+        cg, Yg, st = run_gpu(sd, n, layers, rp, idx, val, fuse_rows=cap)
+        assert st["fused_layers"] > 0
+        assert_parity(cg, Yg, cats, Y)
+
+
+def test_fused_ka_long_passes(sd):
+    from test_oracle_pins import ka_expected
+    spec = g.ka_spec(2048, 40)
+    layers = list(g.iter_layers(spec))
+    rp, idx, cnt = g.ka_inputs(2048, 999, seed=5)
+    cg, Yg, st = run_gpu(sd, 2048, layers, rp, idx, None, fmt="ell", fuse_rows=256,
+                         fuse_layers=16)
+    assert st["steps"] == 3 and st["fused_layers"] == 40
+    Yx = ka_expected(spec, cnt)
+    assert np.array_equal(Yg.view(np.uint32), Yx.view(np.uint32))
+    assert np.array_equal(cg, np.flatnonzero((Yx > 0).any(1)))
 
 
 def test_ka_known_answer(sd):

@@ -5,7 +5,8 @@ radix-32 butterfly nets under three field schedules, evaluated with the CPU
 oracle (test infrastructure; this is a workload study, not part of the product):
   r32     non-overlapping fields 0, 5, 10, ... (full mixing in ceil(log2N/5) layers)
   shift1  p_l = l mod (log2N - 4)
-  shift2  p_l = 2l mod (log2N - 4)      <- used by sdnngen.rn_spec
+  shift2  p_l = 2l mod (log2N - 4)      (first version: never mixes the top bit)
+  rn      sdnngen.rn_field: p_l = (2l + l // ceil(span/2)) mod span   <- used by sdnngen.rn_spec
 Run: python tools/schedule_study.py [N] [L] [B]
 """
 import os
@@ -32,7 +33,7 @@ def main():
     B = int(sys.argv[3]) if len(sys.argv) > 3 else 500
     bits = n.bit_length() - 1
     rp, idx = g.ms_inputs(n, B, sentinels=False)
-    for name in ["r32", "shift1", "shift2"]:
+    for name in ["r32", "shift1", "shift2", "rn"]:
         o = oracle.Oracle(n, rp, idx, None)
         prof = []
         for l in range(L):
@@ -43,8 +44,10 @@ def main():
                 p = offs[l % len(offs)]
             elif name == "shift1":
                 p = l % (bits - 4)
-            else:
+            elif name == "shift2":
                 p = (2 * l) % (bits - 4)
+            else:
+                p = g.rn_field(n, l)
             lay = layer(n, p, g.bias_value(n))
             o.layer(lay["rowptr"], lay["colidx"], None, lay["uniform"], lay["bias"])
             prof.append(o.live_rows())
