@@ -7,6 +7,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -168,15 +169,23 @@ void free_ws(sdnn_net *net) {
 }
 
 sdnn_status ensure_ws(sdnn_net *net, int64_t batch) {
+  // row stride: whole tiles plus a skew so that row starts are not aligned to a
+  // large power of two (the 32 source segments of an item would otherwise share
+  // their low address bits); one extra tile at the end keeps the last row's tail
+  // tile inside the allocation
   const int64_t q = bulk_stride_quantum();
-  const int64_t stride = std::max<int64_t>(q, (batch + q - 1) / q * q);
+  static const int64_t skew = [] {
+    const char *e = getenv("SDNN_SKEW");
+    return e ? std::max<int64_t>(0, atoll(e)) / 32 * 32 : int64_t(1024);
+  }();
+  const int64_t stride = std::max<int64_t>(q, (batch + q - 1) / q * q) + skew;
   if (net->ws_cap >= stride) return SDNN_OK;
   free_ws(net);
   if ((int64_t)net->n * stride > (int64_t(1) << 36)) return fail(SDNN_E_UNSUPPORTED, "batch too large");
   Workspace &w = net->ws;
   w.stride = stride;
   w.words = stride / 32;
-  const size_t ybytes = sizeof(float) * (size_t)net->n * (size_t)stride;
+  const size_t ybytes = sizeof(float) * ((size_t)net->n * (size_t)stride + (size_t)q);
   for (int i = 0; i < 2; ++i) {
     if (cudaMalloc(&w.Y[i], ybytes) != cudaSuccess) {
       cudaGetLastError();

@@ -14,6 +14,7 @@
 // The explicit _rn intrinsics forbid the compiler from contracting or
 // reassociating; the chain order is the group's ascending source order.
 #include <cstdio>
+#include <cstdlib>
 
 #include "sdnn_internal.h"
 #include "device_util.cuh"
@@ -115,32 +116,33 @@ __global__ void __launch_bounds__(256, 2) k_layer_uniform(DevLayer L, const Laye
 // 32 rows x T floats keep ~3 x 64 KB of HBM reads in flight per SM without
 // costing registers (the register-staged kernel above is latency bound).
 // ---------------------------------------------------------------------------
-constexpr int kBulkT = 512;                      // positions per item (2 KB per row)
-constexpr int kBulkStages = 3;
-constexpr int kBulkConsumers = 4;                // 4 warps x 32 lanes x 4 positions = 512
-constexpr int kBulkThreads = 32 * (1 + kBulkConsumers);
-constexpr size_t kBulkSmem = (size_t)kBulkStages * 32 * kBulkT * sizeof(float) + 2 * kBulkStages * 8;
+constexpr int kBulkMaxT = 2048;                  // stride quantum (largest tile)
 
-__global__ void __launch_bounds__(kBulkThreads, 1) k_layer_bulk(DevLayer L, const LayerState *__restrict__ st,
-                                                               int layer, float *Ya, float *Yb,
-                                                               uint32_t *__restrict__ alive,
-                                                               int64_t stride, float ymax) {
+// T positions per item (4 per lane, T/128 consumer warps); an item's K source
+// rows arrive in sub-stages of RPS rows, STAGES sub-stages deep, so the loads of
+// the next item overlap the chain of the current one while each cp.async.bulk
+// still moves a T*4-byte row segment (4 KB at T = 1024: DRAM-friendly).
+template <int T, int RPS, int STAGES, bool CS>
+__global__ void __launch_bounds__(32 * (1 + T / 128), 1)
+    k_layer_bulk(DevLayer L, const LayerState *__restrict__ st, int layer, float *Ya, float *Yb,
+                 uint32_t *__restrict__ alive, int64_t stride, float ymax) {
+  constexpr int NC = T / 128;                      // consumer warps, 4 positions per lane
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float *stage = reinterpret_cast<float *>(smem_raw);
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem_raw + (size_t)kBulkStages * 32 * kBulkT * 4);
-  uint64_t *empty = full + kBulkStages;
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem_raw + (size_t)STAGES * RPS * T * 4);
+  uint64_t *empty = full + STAGES;
   const LayerState S = st[layer];
   const int width = S.width;
   if (width <= 0) return;
   const float *__restrict__ Yin = S.in ? Yb : Ya;
   float *__restrict__ Yout = S.in ? Ya : Yb;
-  const int tiles = (width + kBulkT - 1) / kBulkT;
+  const int tiles = (width + T - 1) / T;
   const int64_t items = (int64_t)L.ngroups * tiles;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kBulkStages; ++s) {
+    for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kBulkConsumers);
+      mbar_init(&empty[s], NC);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -149,19 +151,23 @@ __global__ void __launch_bounds__(kBulkThreads, 1) k_layer_bulk(DevLayer L, cons
     // ---------------- producer ----------------
     int s = 0;
     uint32_t ph = 0;
-    for (int64_t it = blockIdx.x, n = 0; it < items; it += gridDim.x, ++n) {
+    int64_t n = 0;                                   // sub-stages issued
+    for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
       const int g = (int)(it / tiles);
       const int tile = (int)(it - (int64_t)g * tiles);
       const int K = L.regular ? L.kmax : L.gk[g];
-      if (n >= kBulkStages) mbar_wait(&empty[s], ph ^ 1);
-      if (lane == 0) mbar_expect_tx_arrive(&full[s], (uint32_t)K * kBulkT * 4);
-      __syncwarp();
-      if (lane < K) {
-        const int k = L.src[(int64_t)g * L.kmax + lane];
-        bulk_g2s(stage + ((size_t)s * 32 + lane) * kBulkT, Yin + (int64_t)k * stride + (int64_t)tile * kBulkT,
-                 kBulkT * 4, &full[s]);
+      const int mysrc = lane < K ? (int)L.src[(int64_t)g * L.kmax + lane] : 0;
+      for (int r0 = 0; r0 < K; r0 += RPS, ++n) {
+        const int rows = min(RPS, K - r0);
+        if (n >= STAGES) mbar_wait(&empty[s], ph ^ 1);
+        if (lane == 0) mbar_expect_tx_arrive(&full[s], (uint32_t)rows * T * 4);
+        __syncwarp();
+        const int k = __shfl_sync(FULL, mysrc, (r0 + lane) & 31);
+        if (lane < rows)
+          bulk_g2s(stage + ((size_t)s * RPS + lane) * T, Yin + (int64_t)k * stride + (int64_t)tile * T,
+                   T * 4, &full[s]);
+        if (++s == STAGES) { s = 0; ph ^= 1; }
       }
-      if (++s == kBulkStages) { s = 0; ph ^= 1; }
     }
   } else {
     // ---------------- consumers ----------------
@@ -176,31 +182,34 @@ __global__ void __launch_bounds__(kBulkThreads, 1) k_layer_bulk(DevLayer L, cons
       const int G = L.regular ? L.gmax : L.gg[g];
       const int mycol = lane < G ? L.col[(int64_t)g * L.gmax + lane] : 0;
       const float bmy = lane < G ? __ldg(L.bias + mycol) : 0.f;
-      mbar_wait(&full[s], ph);
-      const float *src = stage + (size_t)s * 32 * kBulkT + cw * 128 + lane * 4;
       float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-      if (K == 32) {
+      for (int r0 = 0; r0 < K; r0 += RPS) {          // ascending sources, sub-stage by sub-stage
+        const int rows = min(RPS, K - r0);
+        mbar_wait(&full[s], ph);
+        const float *src = stage + (size_t)s * RPS * T + cw * 128 + lane * 4;
+        if (rows == RPS) {
 #pragma unroll
-        for (int t = 0; t < 32; ++t) {
-          const float4 v = *reinterpret_cast<const float4 *>(src + t * kBulkT);
-          a0 = __fmaf_rn(v.x, w, a0);
-          a1 = __fmaf_rn(v.y, w, a1);
-          a2 = __fmaf_rn(v.z, w, a2);
-          a3 = __fmaf_rn(v.w, w, a3);
+          for (int t = 0; t < RPS; ++t) {
+            const float4 v = *reinterpret_cast<const float4 *>(src + t * T);
+            a0 = __fmaf_rn(v.x, w, a0);
+            a1 = __fmaf_rn(v.y, w, a1);
+            a2 = __fmaf_rn(v.z, w, a2);
+            a3 = __fmaf_rn(v.w, w, a3);
+          }
+        } else {
+          for (int t = 0; t < rows; ++t) {
+            const float4 v = *reinterpret_cast<const float4 *>(src + t * T);
+            a0 = __fmaf_rn(v.x, w, a0);
+            a1 = __fmaf_rn(v.y, w, a1);
+            a2 = __fmaf_rn(v.z, w, a2);
+            a3 = __fmaf_rn(v.w, w, a3);
+          }
         }
-      } else {
-        for (int t = 0; t < K; ++t) {
-          const float4 v = *reinterpret_cast<const float4 *>(src + t * kBulkT);
-          a0 = __fmaf_rn(v.x, w, a0);
-          a1 = __fmaf_rn(v.y, w, a1);
-          a2 = __fmaf_rn(v.z, w, a2);
-          a3 = __fmaf_rn(v.w, w, a3);
-        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        if (++s == STAGES) { s = 0; ph ^= 1; }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-      if (++s == kBulkStages) { s = 0; ph ^= 1; }
-      const int64_t tpos = (int64_t)tile * kBulkT + cw * 128;
+      const int64_t tpos = (int64_t)tile * T + cw * 128;
       float *dst = Yout + tpos + lane * 4;
       uint32_t am = 0;
       for (int m = 0; m < G; ++m) {
@@ -212,12 +221,30 @@ __global__ void __launch_bounds__(kBulkThreads, 1) k_layer_bulk(DevLayer L, cons
         y.z = clampy(__fadd_rn(a2, b), ymax);
         y.w = clampy(__fadd_rn(a3, b), ymax);
         am |= (y.x > 0.f ? 1u : 0u) | (y.y > 0.f ? 2u : 0u) | (y.z > 0.f ? 4u : 0u) | (y.w > 0.f ? 8u : 0u);
-        *reinterpret_cast<float4 *>(dst + (int64_t)j * stride) = y;
+        if (CS)
+          __stcs(reinterpret_cast<float4 *>(dst + (int64_t)j * stride), y);
+        else
+          *reinterpret_cast<float4 *>(dst + (int64_t)j * stride) = y;
       }
       publish_alive<4>(am, lane, tpos, width, alive);
     }
   }
 }
+
+template <int T, int RPS, int STAGES>
+constexpr size_t bulk_smem() {
+  return (size_t)STAGES * RPS * T * sizeof(float) + 2 * STAGES * 8;
+}
+
+// bulk-kernel variant (tile positions, rows per sub-stage, sub-stages, CTAs per
+// SM, streaming stores); SDNN_BULK="T,RPS,STAGES,CTAS,CS" selects another
+// instantiated variant.  Measured on B200 (C4, tools/gpu_job_bulk_sweep.sh):
+// 4 KB row segments (T = 1024) with one whole item per stage reach ~0.91 of
+// the measured HBM copy peak; 2 KB segments 0.83; 1 KB 0.59 (1 CTA/SM).
+struct BulkCfg {
+  int t, rps, stages, ctas, cs;
+};
+static BulkCfg g_bulk = {1024, 32, 1, 1, 0};
 
 // ---------------------------------------------------------------------------
 // Layer kernel, per-slot weights.  Sources of the group are loaded once into
@@ -709,10 +736,39 @@ __global__ void k_yout(const LayerState *__restrict__ st, int a, int final_out,
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
-int bulk_stride_quantum() { return kBulkT; }
+int bulk_stride_quantum() { return kBulkMaxT; }
+
+#define SDNN_BULK_VARIANTS(X)                                                                     \
+  X(512, 32, 3, false) X(1024, 32, 1, false) X(1024, 16, 3, false) X(1024, 16, 1, false)          \
+  X(1024, 8, 6, false) X(2048, 8, 3, false) X(2048, 16, 1, false)
+
+static void launch_bulk(const LaunchCfg &c, const Workspace &w, const DevLayer &L, int32_t a,
+                        uint32_t *alive, float ymax, cudaStream_t s) {
+  const BulkCfg &b = g_bulk;
+#define X(TT, RR, SS, CC)                                                                          \
+  if (b.t == TT && b.rps == RR && b.stages == SS && (b.cs != 0) == CC) {                            \
+    k_layer_bulk<TT, RR, SS, CC><<<c.sms * b.ctas, 32 * (1 + TT / 128), bulk_smem<TT, RR, SS>(),    \
+                                   s>>>(L, w.st, a, w.Y[0], w.Y[1], alive, w.stride, ymax);         \
+    return;                                                                                         \
+  }
+  SDNN_BULK_VARIANTS(X)
+#undef X
+  k_layer_bulk<1024, 32, 1, false><<<c.sms, 288, bulk_smem<1024, 32, 1>(), s>>>(
+      L, w.st, a, w.Y[0], w.Y[1], alive, w.stride, ymax);
+}
 
 void configure_kernels() {
-  cudaFuncSetAttribute(k_layer_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBulkSmem);
+#define X(TT, RR, SS, CC)                                                                      \
+  cudaFuncSetAttribute(k_layer_bulk<TT, RR, SS, CC>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                       (int)bulk_smem<TT, RR, SS>());
+  SDNN_BULK_VARIANTS(X)
+#undef X
+  if (const char *e = getenv("SDNN_BULK")) {
+    BulkCfg b = g_bulk;
+    if (sscanf(e, "%d,%d,%d,%d,%d", &b.t, &b.rps, &b.stages, &b.ctas, &b.cs) == 5 && b.ctas >= 1 &&
+        b.ctas <= 4)
+      g_bulk = b;
+  }
   cudaFuncSetAttribute(k_pass<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPassSmem);
   cudaFuncSetAttribute(k_pass<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPassSmem);
   cudaFuncSetAttribute(k_pass<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPassSmem);
@@ -746,8 +802,7 @@ void launch_zero_layers_alive(const Workspace &w, int64_t batch, const int64_t *
 void launch_layer(const LaunchCfg &c, const Workspace &w, const DevLayer &L, int32_t a,
                   uint32_t *alive, float ymax, cudaStream_t s) {
   if (L.uniform && L.kmax <= 32 && c.bulk) {
-    k_layer_bulk<<<c.sms, kBulkThreads, kBulkSmem, s>>>(L, w.st, a, w.Y[0], w.Y[1], alive,
-                                                       w.stride, ymax);
+    launch_bulk(c, w, L, a, alive, ymax, s);
   } else if (L.uniform) {
     if (L.regular && L.kmax == 32)
       k_layer_uniform<4, true><<<c.layer_blocks, 256, 0, s>>>(L, w.st, a, w.Y[0], w.Y[1],
