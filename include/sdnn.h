@@ -100,7 +100,12 @@ typedef struct sdnn_opts {
                           layer boundary (<= 256; 0 or -1 = off: on B200 the fused
                           kernel measured slower than per-layer streaming, DESIGN 7) */
   int32_t fuse_layers; /* at most this many layers per pass (<= 16; -1 = 8)           */
-} sdnn_opts;        /* passing opts = NULL means {-1, 0, 32.0f, NULL, -1, -1}          */
+  int32_t resident_from; /* N <= 4096: layers [resident_from, L) run in one kernel that
+                          keeps each CTA's batch tile resident in shared memory
+                          (earlier layers stream with dead-row compaction);
+                          -1 = 24 when L > 32 (else off); >= L or SDNN_F_NO_RESIDENT
+                          = off                                                      */
+} sdnn_opts;        /* opts = NULL means {-1, 0, 32.0f, NULL, -1, -1, -1}              */
 
 /* Create a network handle and load all L layers.
  *   neurons  N, 1 <= N <= 65536 on this build (u16 source indices); larger N
@@ -157,8 +162,8 @@ sdnn_status sdnn_infer_device(sdnn_net *net, const int64_t *d_rowptr, const int3
 typedef struct sdnn_stats {
   int32_t struct_size;        /* caller sets sizeof(sdnn_stats) (versioning)            */
   int32_t neurons, layers;
-  int32_t path;               /* 0 = one kernel per layer, 1 = some layers run in fused
-                                 multi-layer passes                                     */
+  int32_t path;               /* bit 0: fused multi-layer passes used; bit 1: the
+                                 SMEM-resident kernel runs the last layers              */
   int32_t grouped_layers;     /* layers packed with >1 column per source-list group    */
   int32_t max_group;          /* largest group size (columns sharing a source list)    */
   int32_t max_k;              /* largest column nnz over all layers                    */
@@ -172,6 +177,7 @@ typedef struct sdnn_stats {
   int64_t kept_rows;          /* rows entering layer 0 (empty rows dropped when exact)   */
   int32_t steps;              /* kernel steps of the layer chain (fused passes count 1)  */
   int32_t fused_layers;       /* layers executed inside fused multi-layer passes         */
+  int32_t resident_layers;    /* layers executed by the SMEM-resident kernel             */
 } sdnn_stats;
 
 /* live_rows: NULL or [layers] receives the number of rows still nonzero after

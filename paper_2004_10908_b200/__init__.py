@@ -51,7 +51,8 @@ class sdnn_layer(ctypes.Structure):
 class sdnn_opts(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int32), ("flags", ctypes.c_uint32),
                 ("ymax", ctypes.c_float), ("stream", ctypes.c_void_p),
-                ("fuse_rows", ctypes.c_int32), ("fuse_layers", ctypes.c_int32)]
+                ("fuse_rows", ctypes.c_int32), ("fuse_layers", ctypes.c_int32),
+                ("resident_from", ctypes.c_int32)]
 
 
 class sdnn_layer_info(ctypes.Structure):
@@ -69,7 +70,7 @@ class sdnn_stats(ctypes.Structure):
                 ("last_batch", ctypes.c_int64), ("last_n_categories", ctypes.c_int64),
                 ("launches_per_infer", ctypes.c_int64), ("live_edges", ctypes.c_int64),
                 ("kept_rows", ctypes.c_int64), ("steps", ctypes.c_int32),
-                ("fused_layers", ctypes.c_int32)]
+                ("fused_layers", ctypes.c_int32), ("resident_layers", ctypes.c_int32)]
 
 
 _LIB = None
@@ -117,9 +118,10 @@ def _p(a: Optional[np.ndarray]):
     return None if a is None else a.ctypes.data
 
 
-def _opts(device=-1, flags=0, ymax=32.0, stream=None, fuse_rows=-1, fuse_layers=-1):
+def _opts(device=-1, flags=0, ymax=32.0, stream=None, fuse_rows=-1, fuse_layers=-1,
+          resident_from=-1):
     return sdnn_opts(int(device), int(flags), float(ymax), stream, int(fuse_rows),
-                     int(fuse_layers))
+                     int(fuse_layers), int(resident_from))
 
 
 def make_layer(layer, fmt: str = "csr"):
@@ -149,7 +151,7 @@ def make_layer(layer, fmt: str = "csr"):
 
 def sdnn_create(neurons: int, layers: Sequence, bias: np.ndarray, fmt: str = "csr",
                 device: int = -1, flags: int = 0, ymax: float = 32.0, fuse_rows: int = -1,
-                fuse_layers: int = -1):
+                fuse_layers: int = -1, resident_from: int = -1):
     L = len(layers)
     descs = (sdnn_layer * max(L, 1))()
     keep = []
@@ -158,15 +160,16 @@ def sdnn_create(neurons: int, layers: Sequence, bias: np.ndarray, fmt: str = "cs
         keep.append(k)
     bias = np.ascontiguousarray(bias, np.float32).reshape(-1)
     h = ctypes.c_void_p()
-    o = _opts(device, flags, ymax, None, fuse_rows, fuse_layers)
+    o = _opts(device, flags, ymax, None, fuse_rows, fuse_layers, resident_from)
     _check(lib().sdnn_create(neurons, L, descs, _p(bias), ctypes.byref(o), ctypes.byref(h)))
     return h
 
 
 def sdnn_create_empty(neurons: int, layers: int, device: int = -1, flags: int = 0,
-                      ymax: float = 32.0, fuse_rows: int = -1, fuse_layers: int = -1):
+                      ymax: float = 32.0, fuse_rows: int = -1, fuse_layers: int = -1,
+                      resident_from: int = -1):
     h = ctypes.c_void_p()
-    o = _opts(device, flags, ymax, None, fuse_rows, fuse_layers)
+    o = _opts(device, flags, ymax, None, fuse_rows, fuse_layers, resident_from)
     _check(lib().sdnn_create_empty(neurons, layers, ctypes.byref(o), ctypes.byref(h)))
     return h
 
@@ -250,10 +253,12 @@ class Net:
     """Owning wrapper around an sdnn_net handle."""
 
     def __init__(self, neurons: int, layers: int, flags: int = 0, ymax: float = 32.0,
-                 device: int = -1, fuse_rows: int = -1, fuse_layers: int = -1):
+                 device: int = -1, fuse_rows: int = -1, fuse_layers: int = -1,
+                 resident_from: int = -1):
         self.n, self.L = int(neurons), int(layers)
         self.h = sdnn_create_empty(self.n, self.L, device=device, flags=flags, ymax=ymax,
-                                   fuse_rows=fuse_rows, fuse_layers=fuse_layers)
+                                   fuse_rows=fuse_rows, fuse_layers=fuse_layers,
+                                   resident_from=resident_from)
 
     @classmethod
     def from_layers(cls, neurons: int, layers: Sequence, fmt: str = "csr", **kw):

@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 SO = os.path.join(HERE, "libsdnn.so")
-SOURCES = ["api.cu", "kernels.cu", "pack.cpp", "fuse.cpp"]
+SOURCES = ["api.cu", "kernels.cu", "resident.cu", "pack.cpp", "fuse.cpp"]
 HEADERS = ["sdnn_internal.h", "device_util.cuh", os.path.join("..", "..", "include", "sdnn.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2,-pthread",

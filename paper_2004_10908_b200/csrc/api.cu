@@ -67,7 +67,7 @@ struct Arena {
 
 struct sdnn_net {
   int32_t n = 0, L = 0;
-  sdnn_opts opts{-1, 0u, 32.f, nullptr, -1, -1};
+  sdnn_opts opts{-1, 0u, 32.f, nullptr, -1, -1, -1};
   int device = 0;
   cudaStream_t own = nullptr;
   Arena arena;
@@ -90,6 +90,8 @@ struct sdnn_net {
   Arena pass_arena;
   bool plan_dirty = true;
   int32_t fused_layers = 0;
+  int32_t resident_layers = 0;
+  ResLayerDev *d_res = nullptr;        // device table for the resident step (pass_arena)
   // captured layer chain
   cudaGraphExec_t chain = nullptr;
   bool chain_compact = false;
@@ -132,7 +134,7 @@ bool compact_enabled(const sdnn_net *net) {
 }
 
 sdnn_status check_opts(const sdnn_opts *o, sdnn_opts &out) {
-  out = sdnn_opts{-1, 0u, 32.f, nullptr, -1, -1};
+  out = sdnn_opts{-1, 0u, 32.f, nullptr, -1, -1, -1};
   if (o) out = *o;
   if (out.fuse_rows > kMaxPassRows) return fail(SDNN_E_ARG, "fuse_rows > 256");
   if (out.fuse_layers > kMaxPassLayers) return fail(SDNN_E_ARG, "fuse_layers > 16");
@@ -285,6 +287,45 @@ sdnn_status make_plan(sdnn_net *net) {
     net->passes.push_back(D);
     net->fused_layers += H.m;
   }
+  // SMEM-resident tail: layers [ar, L) in one persistent kernel when the width fits
+  net->resident_layers = 0;
+  net->d_res = nullptr;
+  if (!(net->opts.flags & SDNN_F_NO_RESIDENT) && resident_positions(net->n) > 0) {
+    int ar = net->opts.resident_from >= 0 ? net->opts.resident_from : (net->L > 32 ? 24 : net->L);
+    ar = std::min(ar, net->L);
+    // the resident step must start on a step boundary and every layer must fit
+    bool ok = ar < net->L;
+    std::vector<std::vector<unsigned char>> blobs(ok ? net->L - ar : 0);
+    std::vector<ResLayerDev> rl(blobs.size());
+    for (int l = ar; ok && l < net->L; ++l) ok = build_resident_blob(net->host[l], blobs[l - ar], rl[l - ar]);
+    int cut = -1;
+    for (int i = 0; ok && i < (int)net->steps.size(); ++i)
+      if (net->steps[i].a == ar) cut = i;
+    if (ok && cut >= 0) {
+      for (size_t q = 0; q < rl.size(); ++q) {
+        void *d;
+        sdnn_status st2 = up(blobs[q].data(), blobs[q].size(), &d);
+        if (st2) return st2;
+        rl[q].blob = (const unsigned char *)d;
+      }
+      // the kernel indexes the table by absolute layer: pad the front
+      std::vector<ResLayerDev> full(net->L);
+      for (size_t q = 0; q < rl.size(); ++q) full[ar + q] = rl[q];
+      void *d;
+      sdnn_status st2 = up(full.data(), sizeof(ResLayerDev) * full.size(), &d);
+      if (st2) return st2;
+      net->d_res = (ResLayerDev *)d;
+      for (int i = cut; i < (int)net->steps.size(); ++i)
+        if (net->steps[i].pass >= 0) net->fused_layers -= net->steps[i].m;
+      net->steps.resize(cut);
+      Step r;
+      r.a = ar;
+      r.m = net->L - ar;
+      r.pass = kResidentStep;
+      net->steps.push_back(r);
+      net->resident_layers = r.m;
+    }
+  }
   net->plan_dirty = false;
   return SDNN_OK;
 }
@@ -303,6 +344,12 @@ void enqueue_chain(sdnn_net *net, bool compact, cudaStream_t s, int64_t *launche
     const Step &S = net->steps[si];
     const bool last = si + 1 == ns;
     if (prof) cudaEventRecordWithFlags(net->ev_before[S.a], s, evflags);
+    if (S.pass == kResidentStep) {            // always the last step
+      launch_resident(w, net->d_res, S.a, net->L, net->n, w.alive_row(si, 0), compact, ymax, s);
+      if (prof) cudaEventRecordWithFlags(net->ev_after[S.a], s, evflags);
+      c += 2;
+      continue;
+    }
     if (S.m == 1)
       launch_layer(net->cfg, w, net->dl[S.a], S.a, w.alive_row(si, 0), ymax, s);
     else
@@ -378,7 +425,8 @@ sdnn_status infer_device_impl(sdnn_net *net, const int64_t *d_rowptr, const int3
   } else {
     const int si = (int)net->steps.size() - 1;
     const Step &S = net->steps[si];
-    launch_readout(net->ws, S.a, net->ws.alive_row(si, S.m - 1), d_alive, batch, s);
+    const int row = S.pass == kResidentStep ? 0 : S.m - 1;
+    launch_readout(net->ws, S.a, net->ws.alive_row(si, row), d_alive, batch, s);
   }
   launches += 1 + (d_alive ? 1 : 0);
   if (d_yout) {
@@ -500,6 +548,7 @@ sdnn_status sdnn_create_empty(int32_t neurons, int32_t layers, const sdnn_opts *
   net->cfg.copy_blocks = sms * 4;
   net->cfg.bulk = !(o.flags & SDNN_F_NO_BULK);
   configure_kernels();
+  configure_resident();
   if (cudaStreamCreateWithFlags(&net->own, cudaStreamNonBlocking) != cudaSuccess) {
     cudaGetLastError();
     delete net;
@@ -809,9 +858,10 @@ sdnn_status sdnn_stats_get(const sdnn_net *cnet, sdnn_stats *out, int64_t *live_
   s.struct_size = sizeof(sdnn_stats);
   s.neurons = net->n;
   s.layers = net->L;
-  s.path = net->fused_layers > 0 ? 1 : 0;
+  s.path = (net->fused_layers > 0 ? 1 : 0) | (net->resident_layers > 0 ? 2 : 0);
   s.steps = (int32_t)net->steps.size();
   s.fused_layers = net->fused_layers;
+  s.resident_layers = net->resident_layers;
   s.grouped_layers = net->grouped_layers;
   s.max_group = net->max_group;
   s.max_k = net->max_k;

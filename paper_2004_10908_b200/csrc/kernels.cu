@@ -205,6 +205,9 @@ __global__ void __launch_bounds__(32 * (1 + T / 128), 1)
             a3 = __fmaf_rn(v.w, w, a3);
           }
         }
+        // order this warp's generic-proxy reads before the TMA (async-proxy)
+        // writes that refill the stage once every consumer warp has arrived
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
         if (++s == STAGES) { s = 0; ph ^= 1; }

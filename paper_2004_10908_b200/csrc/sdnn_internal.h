@@ -98,8 +98,9 @@ constexpr int kMaxPassRows = 256;      // rows per component per boundary (smem)
 
 struct Step {
   int32_t a = 0, m = 1;                // layers [a, a+m)
-  int32_t pass = -1;                   // index into the fused-pass table, -1 = single layer
+  int32_t pass = -1;                   // fused-pass table index; -1 single layer; kResidentStep
 };
+constexpr int32_t kResidentStep = -2;  // layers [a, L) in the SMEM-resident kernel
 
 // plan greedy fused passes: extend while every component stays <= cap rows at
 // every boundary and the layers are uniform with K <= 32
@@ -135,6 +136,20 @@ struct DevPass {
   const int32_t *in_rows, *in_count, *out_rows;
   const PassLayerDev *layers;          // device array [m]
 };
+
+// SMEM-resident multi-layer kernel (resident.cu), N <= 4096
+struct ResLayerDev {
+  const unsigned char *blob;           // device weight image of the layer (see resident.cu)
+  int32_t G, bytes;
+  float wu;
+  int32_t regular, bias_uniform;
+  float bias0;
+  int32_t off_col, off_bias, off_counts;
+};
+int resident_positions(int n);         // batch positions per CTA (0 = not eligible)
+int resident_max_blob();
+bool build_resident_blob(const PackedLayer &p, std::vector<unsigned char> &blob, ResLayerDev &d);
+void configure_resident();
 
 // ---------------------------------------------------------------------------
 // Workspace
@@ -192,5 +207,7 @@ void launch_readout(const Workspace &w, int32_t a, const uint32_t *alive_last,
 // Y_L: final_out = the output buffer of the step entered with st[a] (L > 0), else Y_0
 void launch_yout(const Workspace &w, int32_t a, bool final_out, int32_t n, int64_t batch,
                  float *d_yout, cudaStream_t s);
+void launch_resident(const Workspace &w, const ResLayerDev *layers, int a, int L, int n,
+                     uint32_t *alive_final, bool compact, float ymax, cudaStream_t s);
 
 }  // namespace sdnn

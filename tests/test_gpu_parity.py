@@ -32,9 +32,9 @@ def assert_parity(cats_gpu, Y_gpu, cats_or, Y_or):
 
 
 def run_gpu(sd, n, layers, rp, idx, val, fmt="csr", flags=0, ymax=32.0, want_y=True,
-            fuse_rows=-1, fuse_layers=-1):
+            fuse_rows=-1, fuse_layers=-1, resident_from=-1):
     with sd.Net.from_layers(n, layers, fmt=fmt, flags=flags, ymax=ymax, fuse_rows=fuse_rows,
-                            fuse_layers=fuse_layers) as net:
+                            fuse_layers=fuse_layers, resident_from=resident_from) as net:
         cats, Y = net.infer(rp, idx, val, want_y=want_y)
         st = net.stats()
     return cats, Y, st
@@ -72,6 +72,60 @@ def test_c1_full(sd, c1, fmt, flags):
     assert_parity(cg, Yg, cats, Y)
     assert st["live_rows"] == prof
     assert 0 < cats.sum() < cats.size
+
+
+@pytest.mark.parametrize("resident_from", [0, 1, 7, 24, 119])
+def test_c1_smem_resident(sd, c1, resident_from):
+    """SMEM-resident tail (P = 16 positions per CTA at N = 1024): layers before
+    resident_from stream with compaction, the rest stay in shared memory."""
+    spec, layers, rp, idx, cats, Y, prof = c1
+    for flags in (0, 1):                                  # with / without compaction
+        cg, Yg, st = run_gpu(sd, 1024, layers, rp, idx, None, fmt="ell", flags=flags,
+                             resident_from=resident_from)
+        assert st["resident_layers"] == 120 - resident_from and st["path"] & 2
+        assert_parity(cg, Yg, cats, Y)
+        assert st["live_rows"] == prof
+
+
+@pytest.mark.parametrize("n,L,B", [(4096, 12, 301), (2048, 9, 77), (512, 10, 500), (256, 6, 65)])
+def test_smem_resident_widths(sd, n, L, B):
+    """P = 4 / 8 / 32 / 32 positions per CTA; ragged last CTA."""
+    spec = g.rn_spec(n, L)
+    layers = list(g.iter_layers(spec))
+    rp, idx = g.ms_inputs(n, B, seed=n)
+    cats, Y, prof = oracle.infer(n, layers, rp, idx, None, profile=True)
+    cg, Yg, st = run_gpu(sd, n, layers, rp, idx, None, fmt="ell", resident_from=2)
+    assert st["resident_layers"] == L - 2
+    assert_parity(cg, Yg, cats, Y)
+    assert st["live_rows"] == prof
+
+
+def test_smem_resident_irregular_and_positive_bias(sd):
+    """Uniform-valued irregular layers (1..32 sources per column, singleton
+    groups, per-neuron bias including positive values -> no compaction, no
+    early stop)."""
+    n, L = 384, 6
+    spec = g.random_spec(n, L, seed=77, kmin=1, kmax=32, wdist="uniform", bias=(-0.4, 0.1))
+    layers = list(g.iter_layers(spec))
+    for lay in layers:
+        lay.uniform = 0.1875
+    rp, idx, val = g.random_inputs(n, 200, seed=78, density=0.3, lo=0.0, hi=2.0)
+    cats, Y, _ = oracle.infer(n, layers, rp, idx, val)
+    cg, Yg, st = run_gpu(sd, n, layers, rp, idx, val, resident_from=0)
+    assert st["resident_layers"] == L and st["compaction"] == 0
+    assert_parity(cg, Yg, cats, Y)
+
+
+def test_smem_resident_ka(sd):
+    from test_oracle_pins import ka_expected
+    spec = g.ka_spec(1024, 40)
+    layers = list(g.iter_layers(spec))
+    rp, idx, cnt = g.ka_inputs(1024, 1500, seed=9)
+    cg, Yg, st = run_gpu(sd, 1024, layers, rp, idx, None, fmt="ell", resident_from=3)
+    assert st["resident_layers"] == 37
+    Yx = ka_expected(spec, cnt)
+    assert np.array_equal(Yg.view(np.uint32), Yx.view(np.uint32))
+    assert np.array_equal(cg, np.flatnonzero((Yx > 0).any(1)))
 
 
 @pytest.mark.parametrize("fuse_rows,fuse_layers", [(0, -1), (128, -1), (256, -1),

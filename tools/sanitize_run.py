@@ -33,6 +33,10 @@ def main():
         with sd.Net.from_layers(256, lays, fmt="ell", fuse_rows=cap) as net:
             c, Y = net.infer(rp, idx, None, want_y=True)
         assert np.array_equal(c, ref[0]) and np.array_equal(Y, ref[1])
+    for rf in (0, 3):                                # SMEM-resident tail (P = 32 at N = 256)
+        with sd.Net.from_layers(256, lays, fmt="ell", resident_from=rf) as net:
+            c, Y = net.infer(rp, idx, None, want_y=True)
+        assert np.array_equal(c, ref[0]) and np.array_equal(Y, ref[1])
     spec = g.random_spec(100, 3, seed=5, kmin=0, kmax=40, bias=(-0.3, 0.05))
     lays = list(g.iter_layers(spec))
     rp, idx, val = g.random_inputs(100, 77, seed=5)
