@@ -185,10 +185,15 @@ def run_gpu(args):
     import sdnngen as g
 
     ws, rank, local = dist_env()
+    local = local % max(1, torch.cuda.device_count())   # >1 rank per GPU only in tests
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("SDNN_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     from paper_2004_10908_b200 import dist as sdist
     n, L, B = CONFIGS[args.config]
     spec = g.rn_spec(n, L)

@@ -54,9 +54,10 @@ def gather_bitmask(local_words, group=None):
                           device=local_words.device)
         dist.all_gather_into_tensor(out, local_words, group=group)
         return out
-    parts = [torch.empty_like(local_words) for _ in range(ws)]      # gloo (CPU tests)
-    dist.all_gather(parts, local_words, group=group)
-    return torch.cat(parts)
+    host = local_words.cpu()                                        # gloo (CPU / single-GPU tests)
+    parts = [torch.empty_like(host) for _ in range(ws)]
+    dist.all_gather(parts, host, group=group)
+    return torch.cat(parts).to(local_words.device)
 
 
 def decode(words, batch: int) -> np.ndarray:
