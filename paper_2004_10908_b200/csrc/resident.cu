@@ -103,8 +103,8 @@ __global__ void __launch_bounds__(kResThreads, 1)
     const int G = Ld.G;
     const float wu = Ld.wu;
     const uint16_t *src16 = reinterpret_cast<const uint16_t *>(wcur);          // [32][G]
-    const uint16_t *col16 = reinterpret_cast<const uint16_t *>(wcur + Ld.off_col); // [gmax][G]
-    const float *biasm = reinterpret_cast<const float *>(wcur + Ld.off_bias);     // [gmax][G]
+    const uint16_t *col16 = reinterpret_cast<const uint16_t *>(wcur + Ld.off_col); // [G][gmax]
+    const float *biasm = reinterpret_cast<const float *>(wcur + Ld.off_bias);     // [G][gmax]
     const uint8_t *k8 = wcur + Ld.off_counts;                                    // [G] K_g
     const uint8_t *g8 = k8 + G;                                                  // [G] G_g
     uint32_t bits = 0;
@@ -119,15 +119,40 @@ __global__ void __launch_bounds__(kResThreads, 1)
       } else {
         for (int t = 0; t < K; ++t) acc = __fmaf_rn(yc[src16[t * G + g] * RS + p], wu, acc);
       }
-      // the P lanes of group g hold its P chains; gather them, then this lane
-      // writes members m = p, p+P, ... for all P positions
+      // the P lanes of group g hold its P chains; gather them, then lane p
+      // writes the contiguous member block [p*MPL, p*MPL + MPL) for all P
+      // positions (member arrays are group-major: one vector load per lane)
       float av[P];
 #pragma unroll
       for (int q = 0; q < P; ++q) av[q] = __shfl_sync(FULL, acc, (lane & ~(P - 1)) | q);
-      for (int m = p; m < Gg; m += P) {
-        const int c = col16[m * G + g];
-        const float b = Ld.bias_uniform ? Ld.bias0 : biasm[m * G + g];
-        float *dst = yn + c * RS;
+      constexpr int MPL = 32 / P;                 // members per lane when G_g = 32
+      const int GM = Ld.gmax;
+      uint16_t cols[MPL];
+      float bs[MPL];
+      const int m0 = p * MPL;
+      if (Ld.regular) {
+        const uint16_t *cg = col16 + g * 32 + m0;
+        if (MPL == 8) {
+          const uint4 v = *reinterpret_cast<const uint4 *>(cg);
+          const uint16_t *h = reinterpret_cast<const uint16_t *>(&v);
+#pragma unroll
+          for (int i = 0; i < MPL; ++i) cols[i] = h[i];
+        } else {
+#pragma unroll
+          for (int i = 0; i < MPL; ++i) cols[i] = cg[i];
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < MPL; ++i) cols[i] = (m0 + i < Gg) ? col16[g * GM + m0 + i] : 0;
+      }
+#pragma unroll
+      for (int i = 0; i < MPL; ++i)
+        bs[i] = Ld.bias_uniform ? Ld.bias0 : ((m0 + i < Gg) ? biasm[g * GM + m0 + i] : 0.f);
+#pragma unroll
+      for (int i = 0; i < MPL; ++i) {
+        if (m0 + i >= Gg) break;
+        const float b = bs[i];
+        float *dst = yn + cols[i] * RS;
 #pragma unroll
         for (int q = 0; q < P; q += 4) {
           float4 y;
@@ -245,23 +270,24 @@ bool build_resident_blob(const PackedLayer &p, std::vector<unsigned char> &blob,
   const size_t bytes = al(off_cnt + 2 * (size_t)G);
   if (bytes > (size_t)kResMaxBlob) return false;
   blob.assign(bytes, 0);
-  uint16_t *src = reinterpret_cast<uint16_t *>(blob.data());
-  uint16_t *col = reinterpret_cast<uint16_t *>(blob.data() + off_col);
-  float *bias = reinterpret_cast<float *>(blob.data() + off_bias);
+  uint16_t *src = reinterpret_cast<uint16_t *>(blob.data());              // [KM][G] slot-major
+  uint16_t *col = reinterpret_cast<uint16_t *>(blob.data() + off_col);    // [G][GM] group-major
+  float *bias = reinterpret_cast<float *>(blob.data() + off_bias);        // [G][GM]
   uint8_t *cnt = blob.data() + off_cnt;
   for (int g = 0; g < G; ++g) {
     const int K = p.gk[g], Gg = p.gg[g];
     for (int t = 0; t < K; ++t) src[t * G + g] = p.src[(size_t)g * p.kmax + t];
     for (int m = 0; m < Gg; ++m) {
       const int j = p.col[(size_t)g * p.gmax + m];
-      col[m * G + g] = (uint16_t)j;
-      if (!bu) bias[m * G + g] = p.bias[j];
+      col[g * GM + m] = (uint16_t)j;
+      if (!bu) bias[g * GM + m] = p.bias[j];
     }
     cnt[g] = (uint8_t)K;
     cnt[G + g] = (uint8_t)Gg;
   }
   d.blob = nullptr;
   d.G = G;
+  d.gmax = GM;
   d.bytes = (int32_t)bytes;
   d.wu = p.wu;
   d.regular = p.regular && p.kmax == 32 && p.gmax == 32 ? 1 : 0;

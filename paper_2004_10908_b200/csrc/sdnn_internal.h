@@ -140,7 +140,7 @@ struct DevPass {
 // SMEM-resident multi-layer kernel (resident.cu), N <= 4096
 struct ResLayerDev {
   const unsigned char *blob;           // device weight image of the layer (see resident.cu)
-  int32_t G, bytes;
+  int32_t G, gmax, bytes;
   float wu;
   int32_t regular, bias_uniform;
   float bias0;
