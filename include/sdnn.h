@@ -85,8 +85,16 @@ enum {
   SDNN_F_TRUST_INPUT = 1u << 4,  /* sdnn_infer: skip host validation of Y0              */
   SDNN_F_PROFILE = 1u << 5,      /* record a CUDA event pair around every layer kernel
                                     (read back with sdnn_layer_times)                    */
-  SDNN_F_NO_BULK = 1u << 6       /* uniform layers: use the register-staged gather kernel
+  SDNN_F_NO_BULK = 1u << 6,      /* uniform layers: use the register-staged gather kernel
                                     instead of the TMA bulk-copy pipeline                */
+  SDNN_F_SATURATE = 1u << 8      /* f2 (reported separately): a row whose
+                                    every output equals YMAX before a suffix of layers
+                                    that map all-YMAX rows to all-YMAX rows (checked per
+                                    layer with the canonical fmaf chain at create time)
+                                    is a category with Y_L = YMAX: it is retired from
+                                    the working set like a dead row.  Exact; it changes
+                                    the work, so its numbers are not the headline.
+                                    Streaming path only (no resident/fused steps)       */
 };
 
 typedef struct sdnn_opts {
@@ -178,6 +186,7 @@ typedef struct sdnn_stats {
   int32_t steps;              /* kernel steps of the layer chain (fused passes count 1)  */
   int32_t fused_layers;       /* layers executed inside fused multi-layer passes         */
   int32_t resident_layers;    /* layers executed by the SMEM-resident kernel             */
+  int64_t retired_rows;       /* SDNN_F_SATURATE: rows retired as saturated categories    */
 } sdnn_stats;
 
 /* live_rows: NULL or [layers] receives the number of rows still nonzero after

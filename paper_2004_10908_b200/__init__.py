@@ -29,6 +29,7 @@ SDNN_E_NOMEM, SDNN_E_CUDA, SDNN_E_STATE = -4, -5, -6
 SDNN_W_CSR, SDNN_W_ELLCOL = 0, 1
 SDNN_F_NO_COMPACT, SDNN_F_NO_GROUPS, SDNN_F_NO_GRAPH = 1, 2, 4
 SDNN_F_NO_RESIDENT, SDNN_F_TRUST_INPUT, SDNN_F_PROFILE, SDNN_F_NO_BULK = 8, 16, 32, 64
+SDNN_F_SATURATE = 256
 
 EXPORTS = ["sdnn_create", "sdnn_create_empty", "sdnn_set_layer", "sdnn_infer",
            "sdnn_infer_device", "sdnn_stats_get", "sdnn_validate_layer", "sdnn_destroy",
@@ -70,7 +71,8 @@ class sdnn_stats(ctypes.Structure):
                 ("last_batch", ctypes.c_int64), ("last_n_categories", ctypes.c_int64),
                 ("launches_per_infer", ctypes.c_int64), ("live_edges", ctypes.c_int64),
                 ("kept_rows", ctypes.c_int64), ("steps", ctypes.c_int32),
-                ("fused_layers", ctypes.c_int32), ("resident_layers", ctypes.c_int32)]
+                ("fused_layers", ctypes.c_int32), ("resident_layers", ctypes.c_int32),
+                ("retired_rows", ctypes.c_int64)]
 
 
 _LIB = None

@@ -92,6 +92,7 @@ struct sdnn_net {
   int32_t fused_layers = 0;
   int32_t resident_layers = 0;
   ResLayerDev *d_res = nullptr;        // device table for the resident step (pass_arena)
+  std::vector<uint8_t> sat_suffix;     // f2: layers [l, L) all saturation-preserving
   // captured layer chain
   cudaGraphExec_t chain = nullptr;
   bool chain_compact = false;
@@ -164,6 +165,12 @@ void free_ws(sdnn_net *net) {
   cudaFree(w.live);
   cudaFree(w.cats);
   cudaFree(w.ncat);
+  cudaFree(w.sat[0]);
+  cudaFree(w.sat[1]);
+  cudaFree(w.retired);
+  cudaFree(w.pret);
+  cudaFree(w.nretired);
+  cudaFree(w.orig);
   w = Workspace();
   if (net->chain) cudaGraphExecDestroy(net->chain);
   net->chain = nullptr;
@@ -204,6 +211,14 @@ sdnn_status ensure_ws(sdnn_net *net, int64_t batch) {
   CK(cudaMalloc(&w.live, sizeof(int32_t) * std::max(1, net->L)));
   CK(cudaMalloc(&w.cats, sizeof(int32_t) * stride));
   CK(cudaMalloc(&w.ncat, sizeof(int32_t)));
+  if (net->opts.flags & SDNN_F_SATURATE) {
+    CK(cudaMalloc(&w.sat[0], sizeof(uint32_t) * w.words));
+    CK(cudaMalloc(&w.sat[1], sizeof(uint32_t) * w.words));
+    CK(cudaMalloc(&w.retired, sizeof(uint32_t) * w.words));
+    CK(cudaMalloc(&w.pret, sizeof(uint32_t) * w.words));
+    CK(cudaMalloc(&w.nretired, sizeof(int32_t)));
+    CK(cudaMalloc(&w.orig, sizeof(uint32_t) * w.words));
+  }
   net->ws_cap = stride;
   return SDNN_OK;
 }
@@ -218,7 +233,11 @@ int nthreads_default() {
 sdnn_status make_plan(sdnn_net *net) {
   if (!net->plan_dirty) return SDNN_OK;
   // fused passes are opt-in: measured slower than per-layer streaming on B200
-  const int cap = std::min(net->opts.fuse_rows < 0 ? 0 : net->opts.fuse_rows, kMaxPassRows);
+  const bool sat = net->opts.flags & SDNN_F_SATURATE;
+  const int cap = sat ? 0 : std::min(net->opts.fuse_rows < 0 ? 0 : net->opts.fuse_rows, kMaxPassRows);
+  net->sat_suffix.assign(net->L + 1, 1);
+  for (int l = net->L - 1; l >= 0; --l)
+    net->sat_suffix[l] = net->sat_suffix[l + 1] && saturation_preserving(net->host[l], net->opts.ymax);
   const int maxm = net->opts.fuse_layers < 0 ? 8 : net->opts.fuse_layers;
   std::vector<const PackedLayer *> lp(net->L);
   for (int l = 0; l < net->L; ++l) lp[l] = &net->host[l];
@@ -290,7 +309,7 @@ sdnn_status make_plan(sdnn_net *net) {
   // SMEM-resident tail: layers [ar, L) in one persistent kernel when the width fits
   net->resident_layers = 0;
   net->d_res = nullptr;
-  if (!(net->opts.flags & SDNN_F_NO_RESIDENT) && resident_positions(net->n) > 0) {
+  if (!(net->opts.flags & (SDNN_F_NO_RESIDENT | SDNN_F_SATURATE)) && resident_positions(net->n) > 0) {
     int ar = net->opts.resident_from >= 0 ? net->opts.resident_from : (net->L > 32 ? 24 : net->L);
     ar = std::min(ar, net->L);
     // the resident step must start on a step boundary and every layer must fit
@@ -350,13 +369,20 @@ void enqueue_chain(sdnn_net *net, bool compact, cudaStream_t s, int64_t *launche
       c += 2;
       continue;
     }
+    const bool sat = (net->opts.flags & SDNN_F_SATURATE) && S.m == 1 &&
+                     layer_tracks_saturation(net->cfg, net->dl[S.a]);
     if (S.m == 1)
-      launch_layer(net->cfg, w, net->dl[S.a], S.a, w.alive_row(si, 0), ymax, s);
+      launch_layer(net->cfg, w, net->dl[S.a], S.a, w.alive_row(si, 0), ymax, s,
+                   sat ? w.sat[si & 1] : nullptr);
     else
       launch_pass(net->cfg, w, net->passes[S.pass], w.alive_set(si), ymax, s);
     if (prof) cudaEventRecordWithFlags(net->ev_after[S.a], s, evflags);
-    // survivor counts for every layer of the step; compaction between steps
-    launch_scan(w, S.a, S.m, w.alive_set(si), w.alive_set(si + 1), compact && !last, s);
+    // survivor counts for every layer of the step; compaction between steps;
+    // f2: retire rows saturated before a saturation-preserving suffix
+    const bool retire = sat && net->sat_suffix[S.a + 1];
+    launch_scan(w, S.a, S.m, w.alive_set(si), w.alive_set(si + 1), compact && !last, s,
+                retire ? w.sat[si & 1] : nullptr,
+                (net->opts.flags & SDNN_F_SATURATE) ? w.sat[(si + 1) & 1] : nullptr);
     c += 2;
     if (!last) {
       launch_compact_copy(net->cfg, w, S.a, S.m, w.alive_row(si, S.m - 1), net->n, s);
@@ -396,10 +422,13 @@ sdnn_status run_chain(sdnn_net *net, bool compact, cudaStream_t s) {
 }
 
 void launch_final_yout(sdnn_net *net, int64_t batch, float *d_yout, cudaStream_t s) {
-  if (net->L == 0)
+  if (net->L == 0) {
     launch_yout(net->ws, 0, false, net->n, batch, d_yout, s);
-  else
+  } else {
     launch_yout(net->ws, net->steps.back().a, true, net->n, batch, d_yout, s);
+    if (net->opts.flags & SDNN_F_SATURATE)
+      launch_yout_retired(net->ws, net->n, batch, net->opts.ymax, d_yout, s);
+  }
 }
 
 // Everything of one inference after Y0 is on the device.
@@ -426,7 +455,10 @@ sdnn_status infer_device_impl(sdnn_net *net, const int64_t *d_rowptr, const int3
     const int si = (int)net->steps.size() - 1;
     const Step &S = net->steps[si];
     const int row = S.pass == kResidentStep ? 0 : S.m - 1;
-    launch_readout(net->ws, S.a, net->ws.alive_row(si, row), d_alive, batch, s);
+    if (net->opts.flags & SDNN_F_SATURATE)
+      launch_readout_retired(net->ws, S.a, net->ws.alive_row(si, row), d_alive, batch, s);
+    else
+      launch_readout(net->ws, S.a, net->ws.alive_row(si, row), d_alive, batch, s);
   }
   launches += 1 + (d_alive ? 1 : 0);
   if (d_yout) {
@@ -885,6 +917,11 @@ sdnn_status sdnn_stats_get(const sdnn_net *cnet, sdnn_stats *out, int64_t *live_
     CK(cudaMemcpy(&s0, net->ws.st, sizeof(LayerState), cudaMemcpyDeviceToHost));
     kept0 = s0.width;
     s.kept_rows = kept0;
+    if (net->ws.nretired) {
+      int32_t r = 0;
+      CK(cudaMemcpy(&r, net->ws.nretired, sizeof(int32_t), cudaMemcpyDeviceToHost));
+      s.retired_rows = r;
+    }
     for (int l = 0; l < net->L; ++l)
       s.live_edges += (int64_t)(l == 0 ? kept0 : live[l - 1]) * net->nnz[l];
   }

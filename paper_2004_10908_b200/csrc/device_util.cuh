@@ -71,6 +71,31 @@ __device__ __forceinline__ void publish_alive(uint32_t am, int lane, int64_t til
   }
 }
 
+// AND per-lane "all outputs saturated" bits of a tile into sat[] (only words
+// that lose a bit are touched)
+template <int VEC>
+__device__ __forceinline__ void publish_sat(uint32_t sm, int lane, int64_t tile_pos, int width,
+                                            uint32_t *sat) {
+  uint32_t bal[VEC];
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) bal[e] = __ballot_sync(FULL, (sm >> e) & 1u);
+  if (lane < VEC) {
+    uint32_t word = 0;
+#pragma unroll
+    for (int q = 0; q < 32; ++q) {
+      const int pos = lane * 32 + q;
+      const int src_lane = pos / VEC, e = pos % VEC;
+      uint32_t b = 0;
+#pragma unroll
+      for (int ee = 0; ee < VEC; ++ee)
+        if (ee == e) b = (bal[ee] >> src_lane) & 1u;
+      word |= b << q;
+    }
+    const int64_t base = tile_pos + lane * 32;
+    if (base < width && word != 0xffffffffu) atomicAnd(&sat[base >> 5], word);
+  }
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }

@@ -125,7 +125,8 @@ constexpr int kBulkMaxT = 2048;                  // stride quantum (largest tile
 template <int T, int RPS, int STAGES, bool CS>
 __global__ void __launch_bounds__(32 * (1 + T / 128), 1)
     k_layer_bulk(DevLayer L, const LayerState *__restrict__ st, int layer, float *Ya, float *Yb,
-                 uint32_t *__restrict__ alive, int64_t stride, float ymax) {
+                 uint32_t *__restrict__ alive, int64_t stride, float ymax,
+                 uint32_t *__restrict__ satw) {
   constexpr int NC = T / 128;                      // consumer warps, 4 positions per lane
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float *stage = reinterpret_cast<float *>(smem_raw);
@@ -214,7 +215,7 @@ __global__ void __launch_bounds__(32 * (1 + T / 128), 1)
       }
       const int64_t tpos = (int64_t)tile * T + cw * 128;
       float *dst = Yout + tpos + lane * 4;
-      uint32_t am = 0;
+      uint32_t am = 0, sm = 0xfu;                    // alive / all-members-saturated bits
       for (int m = 0; m < G; ++m) {
         const int j = __shfl_sync(FULL, mycol, m);
         const float b = __shfl_sync(FULL, bmy, m);
@@ -224,12 +225,15 @@ __global__ void __launch_bounds__(32 * (1 + T / 128), 1)
         y.z = clampy(__fadd_rn(a2, b), ymax);
         y.w = clampy(__fadd_rn(a3, b), ymax);
         am |= (y.x > 0.f ? 1u : 0u) | (y.y > 0.f ? 2u : 0u) | (y.z > 0.f ? 4u : 0u) | (y.w > 0.f ? 8u : 0u);
+        sm &= (y.x == ymax ? 1u : 0u) | (y.y == ymax ? 2u : 0u) | (y.z == ymax ? 4u : 0u) |
+              (y.w == ymax ? 8u : 0u);
         if (CS)
           __stcs(reinterpret_cast<float4 *>(dst + (int64_t)j * stride), y);
         else
           *reinterpret_cast<float4 *>(dst + (int64_t)j * stride) = y;
       }
       publish_alive<4>(am, lane, tpos, width, alive);
+      if (satw) publish_sat<4>(sm, lane, tpos, width, satw);
     }
   }
 }
@@ -630,23 +634,60 @@ int pass_buffer_floats() { return kPassBuf; }
 constexpr int kCompactMin = 128;
 
 __global__ void __launch_bounds__(1024) k_scan_step(LayerState *st, int a, int m,
-                                                    const uint32_t *alive_cur,
+                                                    uint32_t *alive_cur,
                                                     uint32_t *alive_next, int64_t wstride,
-                                                    int32_t *wpre, int32_t *live, int compact) {
+                                                    int32_t *wpre, int32_t *live, int compact,
+                                                    const uint32_t *sat_cur, uint32_t *sat_next,
+                                                    const int32_t *ridA, const int32_t *ridB,
+                                                    uint32_t *retired, int32_t *nretired,
+                                                    uint32_t *pret) {
+  __shared__ int s_compacted;
   const LayerState S = st[a];
   const int64_t words = ((int64_t)S.width + 31) >> 5;
+  const int32_t before = nretired ? *nretired : 0;   // rows retired by earlier steps
   for (int j = 0; j < m - 1; ++j) {
     int64_t cnt = 0;
     for (int64_t q = threadIdx.x; q < words; q += blockDim.x) cnt += __popc(alive_cur[j * wstride + q]);
     int64_t total;
     block_exclusive_scan(cnt, &total);
-    if (threadIdx.x == 0) live[a + j] = (int32_t)total;
+    if (threadIdx.x == 0) live[a + j] = (int32_t)total + before;
   }
-  const int64_t count = scan_words(alive_cur + (int64_t)(m - 1) * wstride, words, wpre);
+  uint32_t *last = alive_cur + (int64_t)(m - 1) * wstride;
+  int64_t alive_cnt = 0, newly = 0;
+  if (pret) {
+    // f2 (SDNN_F_SATURATE): positions retired earlier but not yet compacted
+    // away (pret) are out of the working set; rows saturated at YMAX before a
+    // suffix of saturation-preserving layers (sat_cur) are final categories --
+    // record them by original row id and drop them like dead rows
+    const int32_t *rid = S.rid ? ridB : ridA;
+    for (int64_t q = threadIdx.x; q < words; q += blockDim.x) {
+      const uint32_t eff = last[q] & ~pret[q];
+      alive_cnt += __popc(eff);
+      uint32_t r = sat_cur ? (eff & sat_cur[q]) : 0u;
+      last[q] = eff & ~r;
+      pret[q] |= r;
+      newly += __popc(r);
+      while (r) {
+        const int b = __ffs(r) - 1;
+        r &= r - 1;
+        const int32_t id = rid[q * 32 + b];
+        atomicOr(&retired[id >> 5], 1u << (id & 31));
+      }
+    }
+    int64_t t0, t1;
+    block_exclusive_scan(alive_cnt, &t0);
+    block_exclusive_scan(newly, &t1);
+    alive_cnt = t0;
+    newly = t1;
+  }
+  const int64_t count = scan_words(last, words, wpre);
   for (int j = 0; j < kMaxPassLayers; ++j)
     for (int64_t q = threadIdx.x; q < words; q += blockDim.x) alive_next[j * wstride + q] = 0u;
+  if (sat_next)
+    for (int64_t q = threadIdx.x; q < words; q += blockDim.x) sat_next[q] = 0xffffffffu;
   if (threadIdx.x == 0) {
-    live[a + m - 1] = (int32_t)count;
+    live[a + m - 1] = (int32_t)(pret ? alive_cnt : count) + before;
+    if (nretired) *nretired = before + (int32_t)newly;
     const int64_t dead = S.width - count;
     LayerState n;
     if (compact && dead >= kCompactMin && dead * 16 >= S.width) {
@@ -661,7 +702,11 @@ __global__ void __launch_bounds__(1024) k_scan_step(LayerState *st, int a, int m
       n.compacted = 0;
     }
     st[a + m] = n;
+    s_compacted = n.compacted;
   }
+  __syncthreads();
+  if (pret && s_compacted)                           // retired positions were dropped
+    for (int64_t q = threadIdx.x; q < words; q += blockDim.x) pret[q] = 0u;
 }
 
 // Move the live batch columns of the step's output into the free buffer.
@@ -720,6 +765,56 @@ __global__ void __launch_bounds__(1024) k_readout(const LayerState *__restrict__
   if (threadIdx.x == 0) *ncat = (int32_t)total;
 }
 
+// f2 readout: categories = final live positions (mapped to original rows) OR
+// the retired (saturated) rows; one bitmask over original rows, then listed.
+__global__ void k_orig_bits(const LayerState *__restrict__ st, int a, const uint32_t *__restrict__ alive,
+                            const int32_t *ridA, const int32_t *ridB, uint32_t *orig) {
+  const LayerState S = st[a];
+  const int32_t *rid = S.rid ? ridB : ridA;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < S.width;
+       p += (int64_t)gridDim.x * blockDim.x)
+    if ((alive[p >> 5] >> (p & 31)) & 1u) {
+      const int32_t id = rid[p];
+      atomicOr(&orig[id >> 5], 1u << (id & 31));
+    }
+}
+
+__global__ void __launch_bounds__(1024) k_list_bits(const uint32_t *__restrict__ orig,
+                                                    const uint32_t *__restrict__ retired,
+                                                    int64_t words, int32_t *wpre, int32_t *cats,
+                                                    int32_t *ncat, uint32_t *d_alive_out) {
+  __shared__ int dummy;
+  (void)dummy;
+  // merge (in place into a scratch copy is not needed: OR on the fly)
+  const int64_t per = (words + blockDim.x - 1) / blockDim.x;
+  const int64_t w0 = min(words, (int64_t)threadIdx.x * per), w1 = min(words, w0 + per);
+  int64_t sum = 0;
+  for (int64_t q = w0; q < w1; ++q) sum += __popc(orig[q] | retired[q]);
+  int64_t total;
+  int64_t run = block_exclusive_scan(sum, &total);
+  for (int64_t q = w0; q < w1; ++q) {
+    uint32_t bits = orig[q] | retired[q];
+    if (d_alive_out) d_alive_out[q] = bits;
+    while (bits) {
+      const int b = __ffs(bits) - 1;
+      bits &= bits - 1;
+      cats[run++] = (int32_t)(q * 32 + b);
+    }
+  }
+  (void)wpre;
+  if (threadIdx.x == 0) *ncat = (int32_t)total;
+}
+
+// f2: rows retired as saturated are all-YMAX in Y_L
+__global__ void k_yout_retired(const uint32_t *__restrict__ retired, int64_t batch, int32_t n,
+                               float ymax, float *yout) {
+  for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < batch * (int64_t)n;
+       it += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = it / n;
+    if ((retired[r >> 5] >> (r & 31)) & 1u) yout[it] = ymax;
+  }
+}
+
 // Y_L (neuron-major, positions) -> row-major [batch][n] (rows not present are 0)
 __global__ void k_yout(const LayerState *__restrict__ st, int a, int final_out,
                        const float *Ya, const float *Yb, const int32_t *ridA,
@@ -746,18 +841,18 @@ int bulk_stride_quantum() { return kBulkMaxT; }
   X(1024, 8, 6, false) X(2048, 8, 3, false) X(2048, 16, 1, false)
 
 static void launch_bulk(const LaunchCfg &c, const Workspace &w, const DevLayer &L, int32_t a,
-                        uint32_t *alive, float ymax, cudaStream_t s) {
+                        uint32_t *alive, float ymax, uint32_t *sat, cudaStream_t s) {
   const BulkCfg &b = g_bulk;
 #define X(TT, RR, SS, CC)                                                                          \
   if (b.t == TT && b.rps == RR && b.stages == SS && (b.cs != 0) == CC) {                            \
     k_layer_bulk<TT, RR, SS, CC><<<c.sms * b.ctas, 32 * (1 + TT / 128), bulk_smem<TT, RR, SS>(),    \
-                                   s>>>(L, w.st, a, w.Y[0], w.Y[1], alive, w.stride, ymax);         \
+                                   s>>>(L, w.st, a, w.Y[0], w.Y[1], alive, w.stride, ymax, sat);    \
     return;                                                                                         \
   }
   SDNN_BULK_VARIANTS(X)
 #undef X
   k_layer_bulk<1024, 32, 1, false><<<c.sms, 288, bulk_smem<1024, 32, 1>(), s>>>(
-      L, w.st, a, w.Y[0], w.Y[1], alive, w.stride, ymax);
+      L, w.st, a, w.Y[0], w.Y[1], alive, w.stride, ymax, sat);
 }
 
 void configure_kernels() {
@@ -789,6 +884,12 @@ void launch_densify(const LaunchCfg &c, const Workspace &w, int32_t n, int64_t b
     k_rowflags<<<blocks, 256, 0, s>>>(batch, rowptr, val, compact ? 1 : 0, w.inmask, words);
   }
   k_scan_input<<<1, 1024, 0, s>>>(w.inmask, words, w.wpre, w.st, w.alive[0]);
+  if (w.sat[0]) {
+    cudaMemsetAsync(w.sat[0], 0xff, sizeof(uint32_t) * (size_t)w.words, s);
+    cudaMemsetAsync(w.retired, 0, sizeof(uint32_t) * (size_t)w.words, s);
+    cudaMemsetAsync(w.pret, 0, sizeof(uint32_t) * (size_t)w.words, s);
+    cudaMemsetAsync(w.nretired, 0, sizeof(int32_t), s);
+  }
   if (batch > 0)
     k_scatter<<<c.sms * 8, 256, 0, s>>>(batch, rowptr, idx, val, w.inmask, w.wpre, w.Y[0],
                                         w.rid[0], w.stride);
@@ -802,10 +903,14 @@ void launch_zero_layers_alive(const Workspace &w, int64_t batch, const int64_t *
         batch, rowptr, val, w.alive[0], words);
 }
 
+bool layer_tracks_saturation(const LaunchCfg &c, const DevLayer &L) {
+  return L.uniform && L.kmax <= 32 && c.bulk;
+}
+
 void launch_layer(const LaunchCfg &c, const Workspace &w, const DevLayer &L, int32_t a,
-                  uint32_t *alive, float ymax, cudaStream_t s) {
+                  uint32_t *alive, float ymax, cudaStream_t s, uint32_t *sat) {
   if (L.uniform && L.kmax <= 32 && c.bulk) {
-    launch_bulk(c, w, L, a, alive, ymax, s);
+    launch_bulk(c, w, L, a, alive, ymax, sat, s);
   } else if (L.uniform) {
     if (L.regular && L.kmax == 32)
       k_layer_uniform<4, true><<<c.layer_blocks, 256, 0, s>>>(L, w.st, a, w.Y[0], w.Y[1],
@@ -833,10 +938,25 @@ void launch_pass(const LaunchCfg &c, const Workspace &w, const DevPass &P, uint3
 #undef SDNN_PASS
 }
 
-void launch_scan(const Workspace &w, int32_t a, int32_t m, const uint32_t *alive_cur,
-                 uint32_t *alive_next, bool compact, cudaStream_t s) {
+void launch_scan(const Workspace &w, int32_t a, int32_t m, uint32_t *alive_cur,
+                 uint32_t *alive_next, bool compact, cudaStream_t s, const uint32_t *sat_cur,
+                 uint32_t *sat_next) {
   k_scan_step<<<1, 1024, 0, s>>>(w.st, a, m, alive_cur, alive_next, w.words, w.wpre, w.live,
-                                 compact ? 1 : 0);
+                                 compact ? 1 : 0, sat_cur, sat_next, w.rid[0], w.rid[1],
+                                 w.retired, w.nretired, w.sat[0] ? w.pret : nullptr);
+}
+
+void launch_readout_retired(const Workspace &w, int32_t a, const uint32_t *alive_last,
+                            uint32_t *d_alive_out, int64_t batch, cudaStream_t s) {
+  const int64_t words = (batch + 31) / 32;
+  cudaMemsetAsync(w.orig, 0, sizeof(uint32_t) * (size_t)std::max<int64_t>(words, 1), s);
+  k_orig_bits<<<148 * 2, 256, 0, s>>>(w.st, a, alive_last, w.rid[0], w.rid[1], w.orig);
+  k_list_bits<<<1, 1024, 0, s>>>(w.orig, w.retired, words, w.wpre, w.cats, w.ncat, d_alive_out);
+}
+
+void launch_yout_retired(const Workspace &w, int32_t n, int64_t batch, float ymax, float *d_yout,
+                         cudaStream_t s) {
+  k_yout_retired<<<148 * 4, 256, 0, s>>>(w.retired, batch, n, ymax, d_yout);
 }
 
 void launch_compact_copy(const LaunchCfg &c, const Workspace &w, int32_t a, int32_t m,

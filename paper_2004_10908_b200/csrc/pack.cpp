@@ -235,4 +235,21 @@ int pack_layer(int32_t n, const LayerIn &in, const float *bias, bool allow_group
   return SDNN_OK;
 }
 
+bool saturation_preserving(const PackedLayer &p, float ymax) {
+  for (int32_t g = 0; g < p.ngroups; ++g) {
+    const int K = p.gk[g], G = p.gg[g];
+    for (int m = 0; m < G; ++m) {
+      float acc = 0.f;                           // the canonical chain on all-ymax inputs
+      for (int t = 0; t < K; ++t) {
+        const float w = p.uniform ? p.wu : p.val[((size_t)g * p.gmax + m) * p.kmax + t];
+        acc = std::fmaf(ymax, w, acc);
+      }
+      const float z = acc + p.bias[p.col[(size_t)g * p.gmax + m]];
+      if (!(z >= ymax)) return false;
+    }
+  }
+  // a column outside every group cannot exist (each output belongs to one group)
+  return true;
+}
+
 }  // namespace sdnn

@@ -53,6 +53,10 @@ struct LayerIn {              // mirrors sdnn_layer
   float uniform_value;
 };
 
+// f2: does an all-ymax input row give an all-ymax output row (every column's
+// canonical chain on ymax inputs plus its bias >= ymax)?
+bool saturation_preserving(const PackedLayer &p, float ymax);
+
 // Validate and pack one layer.  Returns 0 or a negative sdnn_status with msg.
 int pack_layer(int32_t n, const LayerIn &in, const float *bias, bool allow_groups,
                PackedLayer &out, std::string &msg);
@@ -164,6 +168,13 @@ struct Workspace {
   int32_t *live = nullptr;            // [L] live rows after each layer
   int32_t *cats = nullptr;            // [stride] category list
   int32_t *ncat = nullptr;            // [1]
+  // f2 (SDNN_F_SATURATE): all-outputs-saturated bits per step parity, rows
+  // retired as saturated (original-row bitmask), their count, readout scratch
+  uint32_t *sat[2] = {nullptr, nullptr};
+  uint32_t *retired = nullptr;         // original-row bitmask of retired rows
+  uint32_t *pret = nullptr;            // positions retired but not yet compacted away
+  int32_t *nretired = nullptr;
+  uint32_t *orig = nullptr;
   int64_t stride = 0;                 // row stride (capacity in batch columns)
   int64_t words = 0;                  // stride / 32
   uint32_t *alive_set(int s) const { return alive[s & 1]; }
@@ -188,15 +199,21 @@ void launch_densify(const LaunchCfg &c, const Workspace &w, int32_t n, int64_t b
                     cudaStream_t s);
 // one layer: reads state st[a], writes its liveness bits to `alive`
 void launch_layer(const LaunchCfg &c, const Workspace &w, const DevLayer &L, int32_t a,
-                  uint32_t *alive, float ymax, cudaStream_t s);
+                  uint32_t *alive, float ymax, cudaStream_t s, uint32_t *sat = nullptr);
+bool layer_tracks_saturation(const LaunchCfg &c, const DevLayer &L);
 int pass_buffer_floats();      // smem floats per component tile (tile T = this / R)
 // a fused pass: reads st[P.a], liveness of layer a+j to alive + j*words
 void launch_pass(const LaunchCfg &c, const Workspace &w, const DevPass &P, uint32_t *alive,
                  float ymax, cudaStream_t s);
 // after a step [a, a+m): live counts of its m layers, compaction decision -> st[a+m],
 // zero the next step's bitmask set
-void launch_scan(const Workspace &w, int32_t a, int32_t m, const uint32_t *alive_cur,
-                 uint32_t *alive_next, bool compact, cudaStream_t s);
+void launch_scan(const Workspace &w, int32_t a, int32_t m, uint32_t *alive_cur,
+                 uint32_t *alive_next, bool compact, cudaStream_t s,
+                 const uint32_t *sat_cur = nullptr, uint32_t *sat_next = nullptr);
+void launch_readout_retired(const Workspace &w, int32_t a, const uint32_t *alive_last,
+                            uint32_t *d_alive_out, int64_t batch, cudaStream_t s);
+void launch_yout_retired(const Workspace &w, int32_t n, int64_t batch, float ymax, float *d_yout,
+                         cudaStream_t s);
 void launch_compact_copy(const LaunchCfg &c, const Workspace &w, int32_t a, int32_t m,
                          const uint32_t *alive_last, int32_t n, cudaStream_t s);
 void launch_zero_layers_alive(const Workspace &w, int64_t batch, const int64_t *rowptr,

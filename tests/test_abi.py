@@ -187,3 +187,17 @@ def test_plan_steps_rn_and_rr(sd):
 def test_plan_steps_nonuniform_not_fused(sd):
     lays = list(g.iter_layers(g.rn_spec(1024, 4, wdist="random")))
     assert sd.sdnn_plan_steps(1024, lays, fuse_rows=256) == [1, 1, 1, 1]
+
+
+def test_binding_constants_match_header(sd):
+    """Every SDNN_F_* / SDNN_E_* / SDNN_W_* value in include/sdnn.h is mirrored
+    exactly by the Python binding."""
+    src = open(os.path.join(ROOT, "include", "sdnn.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    vals = {}
+    for name, expr in re.findall(r"\b(SDNN_[FEW]_[A-Z_]+|SDNN_OK)\s*=\s*([^,}\n]+)", src):
+        expr = expr.strip().replace("u <<", " <<")
+        vals[name] = eval(expr)
+    assert len(vals) >= 15
+    for name, v in vals.items():
+        assert getattr(sd, name) == v, name

@@ -172,6 +172,51 @@ def test_fused_ka_long_passes(sd):
     assert np.array_equal(cg, np.flatnonzero((Yx > 0).any(1)))
 
 
+# ---------------------------------------------------------------------------
+# f2: exact saturated-row retirement (SDNN_F_SATURATE)
+# ---------------------------------------------------------------------------
+def test_saturate_c1(sd, c1):
+    spec, layers, rp, idx, cats, Y, prof = c1
+    cg, Yg, st = run_gpu(sd, 1024, layers, rp, idx, None, fmt="ell", flags=sd.SDNN_F_SATURATE)
+    assert_parity(cg, Yg, cats, Y)
+    # RN survivors saturate to all-32 rows and are retired; the survivor profile
+    # still counts them
+    assert 0 < st["retired_rows"] <= cats.sum() and st["live_rows"] == prof
+
+
+def test_saturate_ka_and_device_bitmask(sd):
+    import torch
+    from test_oracle_pins import ka_expected
+    spec = g.ka_spec(1024, 30)
+    layers = list(g.iter_layers(spec))
+    rp, idx, cnt = g.ka_inputs(1024, 1200, seed=13)
+    Yx = ka_expected(spec, cnt)
+    with sd.Net.from_layers(1024, layers, fmt="ell", flags=sd.SDNN_F_SATURATE) as net:
+        cg, Yg = net.infer(rp, idx, None, want_y=True)
+        # KA rows keep one saturated group and zeros elsewhere: never all-YMAX
+        assert net.stats()["retired_rows"] == 0
+        dev = torch.device("cuda", 0)
+        alive = net.infer_torch(torch.from_numpy(rp).to(dev), torch.from_numpy(idx).to(dev))
+        torch.cuda.synchronize()
+        assert np.array_equal(sd.bitmask_to_ids(alive.cpu().numpy(), 1200), cg)
+    assert np.array_equal(Yg.view(np.uint32), Yx.view(np.uint32))
+    assert np.array_equal(cg, np.flatnonzero((Yx > 0).any(1)))
+
+
+def test_saturate_respects_non_preserving_suffix(sd):
+    """A late layer with some bias < -32 maps all-32 rows to non-saturated rows,
+    so nothing may be retired before it."""
+    n, L = 1024, 30
+    spec = g.rn_spec(n, L)
+    layers = list(g.iter_layers(spec))
+    layers[25].bias = layers[25].bias.copy()
+    layers[25].bias[::7] = -40.0                         # 64 - 40 = 24 < 32 = YMAX
+    rp, idx = g.ms_inputs(n, 600, seed=3)
+    cats, Y, _ = oracle.infer(n, layers, rp, idx, None)
+    cg, Yg, st = run_gpu(sd, n, layers, rp, idx, None, fmt="ell", flags=sd.SDNN_F_SATURATE)
+    assert_parity(cg, Yg, cats, Y)
+
+
 def test_ka_known_answer(sd):
     from test_oracle_pins import ka_expected
     spec = g.ka_spec(1024, 24)
