@@ -105,8 +105,8 @@ typedef struct sdnn_opts {
   int32_t fuse_rows;   /* multi-layer passes ("model decomposition"):
                           consecutive uniform layers are fused while every connected
                           component of their union has <= fuse_rows neurons on every
-                          layer boundary (<= 256; 0 or -1 = off: on B200 the fused
-                          kernel measured slower than per-layer streaming, DESIGN 7) */
+                          layer boundary (<= 128, larger values are clamped; 0 =
+                          off; -1 = 128)                                            */
   int32_t fuse_layers; /* at most this many layers per pass (<= 16; -1 = 8)           */
   int32_t resident_from; /* N <= 4096: layers [resident_from, L) run in one kernel that
                           keeps each CTA's batch tile resident in shared memory
@@ -216,10 +216,11 @@ sdnn_status sdnn_validate_layer(int32_t neurons, const sdnn_layer *W_l, const fl
  * [layers] capacity receives the number of layers of each kernel step. */
 sdnn_status sdnn_step_plan(const sdnn_net *net, int32_t *step_len, int32_t *nsteps);
 
-/* Host-only (no device): the execution plan sdnn_create would use for these
- * layers -- step_len[i] = number of layers of step i (1 = one kernel per
- * layer, > 1 = a fused multi-layer pass, see sdnn_opts.fuse_rows); *nsteps =
- * number of steps.  step_len: [layers] capacity. */
+/* Host-only (no device): the fused-pass plan sdnn_create would use for these
+ * layers, before the SMEM-resident tail (N <= 4096) replaces the last ones --
+ * step_len[i] = number of layers of step i (1 = one kernel per layer, > 1 = a
+ * fused multi-layer pass, see sdnn_opts.fuse_rows); *nsteps = number of
+ * steps.  step_len: [layers] capacity. */
 sdnn_status sdnn_plan_steps(int32_t neurons, int32_t layers, const sdnn_layer *W,
                             const float *bias, const sdnn_opts *opts, int32_t *step_len,
                             int32_t *nsteps);

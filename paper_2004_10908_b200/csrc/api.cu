@@ -137,7 +137,7 @@ bool compact_enabled(const sdnn_net *net) {
 sdnn_status check_opts(const sdnn_opts *o, sdnn_opts &out) {
   out = sdnn_opts{-1, 0u, 32.f, nullptr, -1, -1, -1};
   if (o) out = *o;
-  if (out.fuse_rows > kMaxPassRows) return fail(SDNN_E_ARG, "fuse_rows > 256");
+  if (out.fuse_rows > kMaxPassRows) out.fuse_rows = kMaxPassRows;
   if (out.fuse_layers > kMaxPassLayers) return fail(SDNN_E_ARG, "fuse_layers > 16");
   if (!(out.ymax > 0.f) || !std::isfinite(out.ymax)) return fail(SDNN_E_ARG, "ymax must be finite and > 0");
   return SDNN_OK;
@@ -232,16 +232,30 @@ int nthreads_default() {
 // pass descriptors.  Create-time work, redone only when layers change.
 sdnn_status make_plan(sdnn_net *net) {
   if (!net->plan_dirty) return SDNN_OK;
-  // fused passes are opt-in: measured slower than per-layer streaming on B200
   const bool sat = net->opts.flags & SDNN_F_SATURATE;
-  const int cap = sat ? 0 : std::min(net->opts.fuse_rows < 0 ? 0 : net->opts.fuse_rows, kMaxPassRows);
+  const int cap = sat ? 0 : std::min(net->opts.fuse_rows < 0 ? kMaxPassRows : net->opts.fuse_rows,
+                                     kMaxPassRows);
   net->sat_suffix.assign(net->L + 1, 1);
   for (int l = net->L - 1; l >= 0; --l)
     net->sat_suffix[l] = net->sat_suffix[l + 1] && saturation_preserving(net->host[l], net->opts.ymax);
   const int maxm = net->opts.fuse_layers < 0 ? 8 : net->opts.fuse_layers;
+  // the SMEM-resident tail (N <= 4096) starts at layer ar; fused passes never cross it
+  int ar = net->L;
+  std::vector<std::vector<unsigned char>> blobs;
+  std::vector<ResLayerDev> rl;
+  if (!(net->opts.flags & (SDNN_F_NO_RESIDENT | SDNN_F_SATURATE)) && resident_positions(net->n) > 0) {
+    int a0 = net->opts.resident_from >= 0 ? net->opts.resident_from : (net->L > 32 ? 24 : net->L);
+    a0 = std::min(a0, net->L);
+    bool ok = a0 < net->L;
+    blobs.resize(ok ? net->L - a0 : 0);
+    rl.resize(blobs.size());
+    for (int l = a0; ok && l < net->L; ++l) ok = build_resident_blob(net->host[l], blobs[l - a0], rl[l - a0]);
+    if (ok) ar = a0;
+  }
   std::vector<const PackedLayer *> lp(net->L);
   for (int l = 0; l < net->L; ++l) lp[l] = &net->host[l];
-  net->steps = plan_steps(lp, net->n, cap, maxm);
+  std::vector<const PackedLayer *> head(lp.begin(), lp.begin() + ar);
+  net->steps = plan_steps(head, net->n, cap, maxm);
   std::vector<int> fused;
   for (int i = 0; i < (int)net->steps.size(); ++i)
     if (net->steps[i].m > 1) fused.push_back(i);
@@ -253,7 +267,7 @@ sdnn_status make_plan(sdnn_net *net) {
     for (int t = 0; t < nt; ++t)
       th.emplace_back([&] {
         for (int q = next++; q < (int)fused.size(); q = next++)
-          build_pass(lp, net->n, net->steps[fused[q]], pass_buffer_floats(), 32, ph[q]);
+          build_pass(lp, net->n, net->steps[fused[q]], pass_tile_floats(), ph[q]);
       });
     for (auto &x : th) x.join();
   }
@@ -276,28 +290,25 @@ sdnn_status make_plan(sdnn_net *net) {
     D.m = H.m;
     D.ncomp = H.ncomp;
     D.rin = H.rin;
-    D.rout = H.rout;
     D.R = H.R;
     D.T = H.T;
-    void *p1, *p2, *p3, *p4;
+    void *p1, *p2, *p4;
     sdnn_status st;
     if ((st = up(H.in_rows.data(), H.in_rows.size() * 4, &p1)) ||
-        (st = up(H.in_count.data(), H.in_count.size() * 4, &p2)) ||
-        (st = up(H.out_rows.data(), H.out_rows.size() * 4, &p3)))
+        (st = up(H.in_count.data(), H.in_count.size() * 4, &p2)))
       return st;
     D.in_rows = (const int32_t *)p1;
     D.in_count = (const int32_t *)p2;
-    D.out_rows = (const int32_t *)p3;
     std::vector<PassLayerDev> pl(H.m);
     for (int j = 0; j < H.m; ++j) {
       PassHostLayer &HL = H.layers[j];
-      void *s1, *s2, *s3, *s4, *s5;
+      void *s1, *s3, *s4, *s5, *s6 = nullptr;
       if ((st = up(HL.src.data(), HL.src.size() * 2, &s1)) ||
-          (st = up(HL.dst.data(), HL.dst.size() * 2, &s2)) ||
           (st = up(HL.bias.data(), HL.bias.size() * 4, &s3)) ||
           (st = up(HL.k.data(), HL.k.size(), &s4)) || (st = up(HL.g.data(), HL.g.size(), &s5)))
         return st;
-      pl[j] = PassLayerDev{(const uint16_t *)s1, (const uint16_t *)s2, (const float *)s3,
+      if (!HL.orow.empty() && (st = up(HL.orow.data(), HL.orow.size() * 4, &s6))) return st;
+      pl[j] = PassLayerDev{(const uint16_t *)s1, (const float *)s3, (const int32_t *)s6,
                            (const uint8_t *)s4, (const uint8_t *)s5, HL.NG, HL.wu};
     }
     if ((st = up(pl.data(), sizeof(PassLayerDev) * pl.size(), &p4))) return st;
@@ -309,41 +320,25 @@ sdnn_status make_plan(sdnn_net *net) {
   // SMEM-resident tail: layers [ar, L) in one persistent kernel when the width fits
   net->resident_layers = 0;
   net->d_res = nullptr;
-  if (!(net->opts.flags & (SDNN_F_NO_RESIDENT | SDNN_F_SATURATE)) && resident_positions(net->n) > 0) {
-    int ar = net->opts.resident_from >= 0 ? net->opts.resident_from : (net->L > 32 ? 24 : net->L);
-    ar = std::min(ar, net->L);
-    // the resident step must start on a step boundary and every layer must fit
-    bool ok = ar < net->L;
-    std::vector<std::vector<unsigned char>> blobs(ok ? net->L - ar : 0);
-    std::vector<ResLayerDev> rl(blobs.size());
-    for (int l = ar; ok && l < net->L; ++l) ok = build_resident_blob(net->host[l], blobs[l - ar], rl[l - ar]);
-    int cut = -1;
-    for (int i = 0; ok && i < (int)net->steps.size(); ++i)
-      if (net->steps[i].a == ar) cut = i;
-    if (ok && cut >= 0) {
-      for (size_t q = 0; q < rl.size(); ++q) {
-        void *d;
-        sdnn_status st2 = up(blobs[q].data(), blobs[q].size(), &d);
-        if (st2) return st2;
-        rl[q].blob = (const unsigned char *)d;
-      }
-      // the kernel indexes the table by absolute layer: pad the front
-      std::vector<ResLayerDev> full(net->L);
-      for (size_t q = 0; q < rl.size(); ++q) full[ar + q] = rl[q];
+  if (ar < net->L) {
+    for (size_t q = 0; q < rl.size(); ++q) {
       void *d;
-      sdnn_status st2 = up(full.data(), sizeof(ResLayerDev) * full.size(), &d);
+      sdnn_status st2 = up(blobs[q].data(), blobs[q].size(), &d);
       if (st2) return st2;
-      net->d_res = (ResLayerDev *)d;
-      for (int i = cut; i < (int)net->steps.size(); ++i)
-        if (net->steps[i].pass >= 0) net->fused_layers -= net->steps[i].m;
-      net->steps.resize(cut);
-      Step r;
-      r.a = ar;
-      r.m = net->L - ar;
-      r.pass = kResidentStep;
-      net->steps.push_back(r);
-      net->resident_layers = r.m;
+      rl[q].blob = (const unsigned char *)d;
     }
+    std::vector<ResLayerDev> full(net->L);      // indexed by absolute layer
+    for (size_t q = 0; q < rl.size(); ++q) full[ar + q] = rl[q];
+    void *d;
+    sdnn_status st2 = up(full.data(), sizeof(ResLayerDev) * full.size(), &d);
+    if (st2) return st2;
+    net->d_res = (ResLayerDev *)d;
+    Step r;
+    r.a = ar;
+    r.m = net->L - ar;
+    r.pass = kResidentStep;
+    net->steps.push_back(r);
+    net->resident_layers = r.m;
   }
   net->plan_dirty = false;
   return SDNN_OK;
@@ -874,7 +869,9 @@ sdnn_status sdnn_plan_steps(int32_t neurons, int32_t layers, const sdnn_layer *W
   }
   std::vector<const PackedLayer *> lp(layers);
   for (int l = 0; l < layers; ++l) lp[l] = &host[l];
-  const int cap = std::min(o.fuse_rows < 0 ? 0 : o.fuse_rows, kMaxPassRows);
+  const int cap = (o.flags & SDNN_F_SATURATE)
+                      ? 0
+                      : std::min(o.fuse_rows < 0 ? kMaxPassRows : o.fuse_rows, kMaxPassRows);
   const int maxm = o.fuse_layers < 0 ? 8 : o.fuse_layers;
   const std::vector<Step> steps = plan_steps(lp, neurons, cap, maxm);
   for (size_t i = 0; i < steps.size(); ++i) step_len[i] = steps[i].m;

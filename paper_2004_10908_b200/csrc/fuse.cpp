@@ -40,6 +40,21 @@ struct UF {
 
 bool fusable(const PackedLayer &p) { return p.uniform && p.kmax <= 32 && p.gmax <= 32; }
 
+// a layer whose groups can overwrite their own source slots: every source row
+// feeds at most one group, and no group has more members than sources
+bool inplace(const PackedLayer &p) {
+  std::vector<uint8_t> seen(p.n, 0);
+  for (int32_t g = 0; g < p.ngroups; ++g) {
+    if (p.gg[g] > p.gk[g]) return false;
+    for (int t = 0; t < p.gk[g]; ++t) {
+      uint8_t &s = seen[p.src[(size_t)g * p.kmax + t]];
+      if (s) return false;
+      s = 1;
+    }
+  }
+  return true;
+}
+
 // join layer (boundary b -> b+1) into the union-find
 void add_layer(UF &uf, const PackedLayer &p, int32_t n, int b) {
   const int64_t in0 = (int64_t)b * n, out0 = (int64_t)(b + 1) * n;
@@ -86,7 +101,8 @@ std::vector<Step> plan_steps(const std::vector<const PackedLayer *> &layers, int
       stamp.assign(nodes, 0);
       add_layer(uf, *layers[a], n, 0);
       if (within_cap(uf, n, 1, cap, cnt, stamp)) {
-        while (a + m < L && m < max_m && fusable(*layers[a + m])) {
+        // layer a+m-1 stops being the last layer of the pass: it must allow in-place slots
+        while (a + m < L && m < max_m && fusable(*layers[a + m]) && inplace(*layers[a + m - 1])) {
           add_layer(uf, *layers[a + m], n, m);
           std::fill(stamp.begin(), stamp.end(), 0);
           if (!within_cap(uf, n, m + 1, cap, cnt, stamp)) break;
@@ -104,12 +120,12 @@ std::vector<Step> plan_steps(const std::vector<const PackedLayer *> &layers, int
 }
 
 void build_pass(const std::vector<const PackedLayer *> &layers, int32_t n, const Step &s,
-                int buf_floats, int min_t, PassHost &out) {
+                int tile_floats, PassHost &out) {
   const int m = s.m;
   UF uf;
   uf.init((int64_t)(m + 1) * n);
   for (int b = 0; b < m; ++b) add_layer(uf, *layers[s.a + b], n, b);
-  // components that own at least one group (have outputs); dense ids by smallest node
+  // components that own at least one group (have outputs); dense ids
   std::vector<int32_t> comp_of_root((size_t)(m + 1) * n, -1);
   int ncomp = 0;
   for (int b = 0; b < m; ++b) {
@@ -119,49 +135,36 @@ void build_pass(const std::vector<const PackedLayer *> &layers, int32_t n, const
       if (comp_of_root[r] < 0) comp_of_root[r] = ncomp++;
     }
   }
-  // local row index of every node: order by neuron id within (component, boundary)
-  std::vector<int32_t> local((size_t)(m + 1) * n, -1);
-  std::vector<std::vector<int32_t>> rows_in(ncomp), rows_out(ncomp);
-  std::vector<int32_t> fill((size_t)ncomp * (m + 1), 0);
-  int R = 0;
-  for (int b = 0; b <= m; ++b)
-    for (int32_t i = 0; i < n; ++i) {
-      const int64_t node = (int64_t)b * n + i;
-      const int32_t c = comp_of_root[uf.find((int32_t)node)];
-      if (c < 0) continue;                      // input neuron feeding nothing in this pass
-      const int32_t li = fill[(size_t)c * (m + 1) + b]++;
-      local[node] = li;
-      R = std::max(R, li + 1);
-      if (b == 0) rows_in[c].push_back(i);
-      if (b == m) rows_out[c].push_back(i);
-    }
+  // boundary-0 rows of each component -> smem slots 0..cnt-1 (ascending neuron id)
+  std::vector<int32_t> slot((size_t)(m + 1) * n, -1);
+  std::vector<std::vector<int32_t>> rows_in(ncomp);
+  for (int32_t i = 0; i < n; ++i) {
+    const int32_t c = comp_of_root[uf.find(i)];
+    if (c < 0) continue;                          // input neuron feeding nothing in this pass
+    slot[i] = (int32_t)rows_in[c].size();
+    rows_in[c].push_back(i);
+  }
   out = PassHost();
   out.a = s.a;
   out.m = m;
   out.ncomp = ncomp;
+  int R = 1;
+  for (auto &v : rows_in) R = std::max<int>(R, (int)v.size());
   out.R = R;
-  int rin = 0, rout = 0;
-  for (int c = 0; c < ncomp; ++c) {
-    rin = std::max<int>(rin, (int)rows_in[c].size());
-    rout = std::max<int>(rout, (int)rows_out[c].size());
-  }
-  out.rin = std::max(rin, 1);
-  out.rout = std::max(rout, 1);
-  // positions per item: one smem buffer (buf_floats) per component tile
-  int T = 512;
-  while (T > min_t && (int64_t)R * T > buf_floats) T >>= 1;
+  out.rin = R;
+  int T = 512;                                    // one tile of tile_floats per component
+  while (T > 128 && (int64_t)R * T > tile_floats) T >>= 1;
   out.T = T;
-  out.in_rows.assign((size_t)ncomp * out.rin, -1);
+  out.in_rows.assign((size_t)ncomp * R, -1);
   out.in_count.assign(ncomp, 0);
-  out.out_rows.assign((size_t)ncomp * out.rout, -1);
   for (int c = 0; c < ncomp; ++c) {
-    std::copy(rows_in[c].begin(), rows_in[c].end(), out.in_rows.begin() + (size_t)c * out.rin);
+    std::copy(rows_in[c].begin(), rows_in[c].end(), out.in_rows.begin() + (size_t)c * R);
     out.in_count[c] = (int32_t)rows_in[c].size();
-    std::copy(rows_out[c].begin(), rows_out[c].end(), out.out_rows.begin() + (size_t)c * out.rout);
   }
   out.layers.resize(m);
   for (int b = 0; b < m; ++b) {
     const PackedLayer &p = *layers[s.a + b];
+    const bool last = b == m - 1;
     std::vector<std::vector<int32_t>> groups(ncomp);
     for (int32_t g = 0; g < p.ngroups; ++g) {
       const int32_t c =
@@ -174,10 +177,10 @@ void build_pass(const std::vector<const PackedLayer *> &layers, int32_t n, const
     H.NG = NG;
     H.wu = p.wu;
     H.src.assign((size_t)ncomp * NG * 32, 0);
-    H.dst.assign((size_t)ncomp * NG * 32, 0);
     H.bias.assign((size_t)ncomp * NG * 32, 0.f);
     H.k.assign((size_t)ncomp * NG, 0);
     H.g.assign((size_t)ncomp * NG, 0);
+    if (last) H.orow.assign((size_t)ncomp * NG * 32, 0);
     const int64_t in0 = (int64_t)b * n, out0 = (int64_t)(b + 1) * n;
     for (int c = 0; c < ncomp; ++c)
       for (size_t q = 0; q < groups[c].size(); ++q) {
@@ -187,11 +190,14 @@ void build_pass(const std::vector<const PackedLayer *> &layers, int32_t n, const
         H.k[rec] = (uint8_t)K;
         H.g[rec] = (uint8_t)G;
         for (int t = 0; t < K; ++t)        // keeps the ascending source order (canonical chain)
-          H.src[rec * 32 + t] = (uint16_t)local[in0 + p.src[(size_t)g * p.kmax + t]];
+          H.src[rec * 32 + t] = (uint16_t)slot[in0 + p.src[(size_t)g * p.kmax + t]];
         for (int u = 0; u < G; ++u) {
           const int32_t j = p.col[(size_t)g * p.gmax + u];
-          H.dst[rec * 32 + u] = (uint16_t)local[out0 + j];
           H.bias[rec * 32 + u] = p.bias[j];
+          if (last)
+            H.orow[rec * 32 + u] = j;
+          else                             // member u overwrites the slot of source u
+            slot[out0 + j] = H.src[rec * 32 + u];
         }
       }
   }

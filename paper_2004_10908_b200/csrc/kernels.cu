@@ -478,38 +478,33 @@ __global__ void k_y0_positive(int64_t batch, const int64_t *__restrict__ rowptr,
 
 // ---------------------------------------------------------------------------
 // Fused multi-layer pass (model decomposition, fuse.cpp) -- opt-in
-// (sdnn_opts.fuse_rows > 0).  Persistent CTAs; an item is (component c, batch
-// tile of T positions), T = 8192 / R so that a component tile is one 32 KB
-// buffer.  Warp 0 streams the component's input rows into kPassIn input
-// buffers with 16-byte cp.async (row segments of 128 B - 1 KB, too small to
-// pay one TMA bulk copy each), so up to kPassIn-1 items load while one
-// computes.  8 consumer warps run the m layers out of shared memory: layer 0
-// reads the input buffer and writes the shared work buffer, layer 1 writes back
-// into the (consumed) input buffer, and so on; the last layer stores straight
-// to the output rows in HBM.  A work unit is (group, 32-position slice), lane =
-// position.  HBM traffic per layer drops by m versus k_layer_bulk, but on B200
-// the kernel is issue/latency bound (one position per lane, CTA barriers
-// between layers): measured slower than streaming, see DESIGN.md section 7.
+// (sdnn_opts.fuse_rows > 0).  An item is (component c, batch tile of T
+// positions); its R <= 128 input rows are one 64 KB shared-memory tile loaded
+// with one cp.async.bulk per row (T*4 = 512 B - 2 KB).  Four warps run the m
+// layers in place: a group's chain reads its source slots, then its members
+// overwrite those same slots (legal because the planner only fuses layers whose
+// source rows each feed one group); the last layer stores the member rows
+// straight to HBM.  No second buffer, so three CTAs share an SM and hide each
+// other's load latency.  Four positions per lane (float4), one warp per
+// (group, 128-position slice).  HBM traffic per layer drops by m.
 // ---------------------------------------------------------------------------
-constexpr int kPassConsumers = 8;
-constexpr int kPassThreads = 32 * (1 + kPassConsumers);
-constexpr int kPassBuf = 8192;                   // floats per buffer (R * T)
-constexpr int kPassIn = 5;                       // input buffers (+1 shared work buffer)
-constexpr size_t kPassSmem =
-    (size_t)(kPassIn + 1) * kPassBuf * 4 + (kPassIn + 1) * 8 + kMaxPassLayers * 8 * 4;
+constexpr int kPassWarps = 4;
+constexpr int kPassTile = 16384;                 // floats per component tile (R * T)
+constexpr int kPassMaxT = 512;
+constexpr size_t kPassSmem = (size_t)kPassTile * 4 + 16 + kMaxPassLayers * (kPassMaxT / 32) * 4;
+
+int pass_tile_floats() { return kPassTile; }
 
 template <int T>
-__global__ void __launch_bounds__(kPassThreads, 1) k_pass(DevPass P, const LayerState *__restrict__ st,
-                                                         float *Ya, float *Yb,
-                                                         uint32_t *__restrict__ alive,
-                                                         int64_t wstride, int64_t stride, float ymax) {
-  constexpr int S = T / 32;                      // 32-position slices per tile
+__global__ void __launch_bounds__(32 * kPassWarps, 3)
+    k_pass(DevPass P, const LayerState *__restrict__ st, float *Ya, float *Yb,
+           uint32_t *__restrict__ alive, int64_t wstride, int64_t stride, float ymax) {
+  constexpr int S = T / 128;                     // 128-position slices per tile
+  constexpr int W = T / 32;                      // liveness words per tile
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  float *buf = reinterpret_cast<float *>(smem_raw);
-  float *workb = buf + (size_t)kPassIn * kPassBuf;
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem_raw + (size_t)(kPassIn + 1) * kPassBuf * 4);
-  volatile int *done = reinterpret_cast<volatile int *>(full + kPassIn);
-  uint32_t *aw = reinterpret_cast<uint32_t *>(full + kPassIn + 1);   // [kMaxPassLayers][S]
+  float *tile_s = reinterpret_cast<float *>(smem_raw);
+  uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw + (size_t)kPassTile * 4);
+  uint32_t *aw = reinterpret_cast<uint32_t *>(bar + 2);                 // [kMaxPassLayers][W]
   const LayerState Sx = st[P.a];
   const int width = Sx.width;
   if (width <= 0) return;
@@ -517,114 +512,135 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(DevPass P, const Layer
   float *__restrict__ Yout = Sx.in ? Ya : Yb;
   const int tiles = (width + T - 1) / T;
   const int64_t items = (int64_t)P.ncomp * tiles;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    for (int x = 0; x < kPassIn; ++x) mbar_init(&full[x], 32);   // one cp.async arrival per lane
-    *done = 0;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    mbar_init(bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (int q = threadIdx.x; q < kMaxPassLayers * S; q += blockDim.x) aw[q] = 0u;
+  for (int q = tid; q < kMaxPassLayers * W; q += blockDim.x) aw[q] = 0u;
   __syncthreads();
-  if (warp == 0) {
-    // ------------------------------ producer ------------------------------
-    int64_t i = 0;
-    for (int64_t it = blockIdx.x; it < items; it += gridDim.x, ++i) {
-      const int c = (int)(it / tiles);
-      const int tile = (int)(it - (int64_t)c * tiles);
-      const int x = (int)(i % kPassIn);
-      if (i >= kPassIn) {                      // buffer x held item i - kPassIn
-        if (lane == 0)
-          while (*done < i - kPassIn + 1) __nanosleep(20);
-        __syncwarp();
-      }
-      const int cnt = P.in_count[c];
-      float *dstb = buf + (size_t)x * kPassBuf;
-      const int32_t *rows = P.in_rows + (int64_t)c * P.rin;
-      constexpr int CH = T / 4;                  // 16-byte chunks per row segment
-      const float *src0 = Yin + (int64_t)tile * T;
-      for (int q = lane; q < cnt * CH; q += 32) {
-        const int r = q / CH, ch = q - r * CH;
-        cp_async16(dstb + (size_t)r * T + ch * 4, src0 + (int64_t)rows[r] * stride + ch * 4);
-      }
-      cp_async_arrive(&full[x]);
-    }
-  } else {
-    // ------------------------------ consumers -----------------------------
-    const int cw = warp - 1;
-    int64_t i = 0;
-    for (int64_t it = blockIdx.x; it < items; it += gridDim.x, ++i) {
-      const int c = (int)(it / tiles);
-      const int tile = (int)(it - (int64_t)c * tiles);
-      float *inb = buf + (size_t)(i % kPassIn) * kPassBuf;
-      mbar_wait(&full[i % kPassIn], (uint32_t)((i / kPassIn) & 1));
-      for (int j = 0; j < P.m; ++j) {
-        const PassLayerDev PL = P.layers[j];
-        const float *srcb = (j & 1) ? workb : inb;
-        float *dstb = (j & 1) ? inb : workb;
-        const bool last = j == P.m - 1;
-        const float wu = PL.wu;
-        for (int u = cw; u < PL.NG * S; u += kPassConsumers) {
-          const int gi = u / S, sl = u - gi * S;
-          const int64_t rec = (int64_t)c * PL.NG + gi;
-          const int G = PL.g[rec];
-          if (G == 0) continue;
-          const int K = PL.k[rec];
-          const int mysrc = lane < K ? (int)PL.src[rec * 32 + lane] : 0;
-          const int mydst = lane < G ? (int)PL.dst[rec * 32 + lane] : 0;
-          const float mybias = lane < G ? PL.bias[rec * 32 + lane] : 0.f;
-          const int pofs = sl * 32 + lane;
-          float acc = 0.f;
-          if (K == 32) {
-#pragma unroll 8
-            for (int t = 0; t < 32; ++t) acc = __fmaf_rn(srcb[__shfl_sync(FULL, mysrc, t) * T + pofs], wu, acc);
-          } else {
-            for (int t = 0; t < K; ++t) acc = __fmaf_rn(srcb[__shfl_sync(FULL, mysrc, t) * T + pofs], wu, acc);
-          }
-          float mx = 0.f;                          // max over this slice's outputs
-          if (last) {
-            // lane v holds member v's output row pointer: no dependent load per member
-            float *myrow = Yout + (int64_t)tile * T + sl * 32 +
-                           (lane < G ? (int64_t)P.out_rows[(int64_t)c * P.rout + mydst] * stride : 0);
-            for (int v = 0; v < G; ++v) {
-              float *row = reinterpret_cast<float *>(__shfl_sync(FULL, reinterpret_cast<uintptr_t>(myrow), v));
-              const float b = __shfl_sync(FULL, mybias, v);
-              const float y = clampy(__fadd_rn(acc, b), ymax);
-              mx = fmaxf(mx, y);
-              row[lane] = y;
-            }
-          } else {
-            const int myoff = (lane < G ? mydst : 0) * T + sl * 32;
-            for (int v = 0; v < G; ++v) {
-              const int off = __shfl_sync(FULL, myoff, v);
-              const float b = __shfl_sync(FULL, mybias, v);
-              const float y = clampy(__fadd_rn(acc, b), ymax);
-              mx = fmaxf(mx, y);
-              dstb[off + lane] = y;
-            }
-          }
-          const uint32_t word = __ballot_sync(FULL, mx > 0.f);
-          if (lane == 0 && word) atomicOr(&aw[j * S + sl], word);
+  // one cp.async.bulk per input row of the component tile (all threads issue)
+  auto issue_load = [&](int64_t it) {
+    const int c = (int)(it / tiles);
+    const int tile = (int)(it - (int64_t)c * tiles);
+    const int cnt = P.in_count[c];
+    const int32_t *rows = P.in_rows + (int64_t)c * P.rin;
+    if (tid == 0) mbar_expect_tx_arrive(bar, (uint32_t)cnt * T * 4);
+    for (int r = tid; r < cnt; r += blockDim.x)
+      bulk_g2s(tile_s + (size_t)r * T, Yin + (int64_t)rows[r] * stride + (int64_t)tile * T, T * 4, bar);
+  };
+  const PassLayerDev PLast = P.layers[P.m - 1];
+  // the last layer releases the tile before its HBM stores when every warp owns
+  // at most one (group, slice) unit of it
+  const bool early = PLast.NG * S <= kPassWarps;
+  if (blockIdx.x < items) issue_load(blockIdx.x);
+  uint32_t ph = 0;
+  for (int64_t it = blockIdx.x; it < items; it += gridDim.x, ph ^= 1u) {
+    const int c = (int)(it / tiles);
+    const int tile = (int)(it - (int64_t)c * tiles);
+    const int64_t next = it + gridDim.x;
+    bool issued = false;
+    mbar_wait(bar, ph);
+    for (int j = 0; j < P.m; ++j) {
+      const PassLayerDev PL = P.layers[j];
+      const bool last = j == P.m - 1;
+      const float wu = PL.wu;
+      const int units = PL.NG * S;
+      for (int u0 = 0; u0 < (last && early ? kPassWarps : units); u0 += kPassWarps) {
+        const int u = u0 + warp;
+        const bool active = u < units;
+        int G = 0, K = 0, sl = 0;
+        int64_t rec = 0;
+        if (active) {
+          const int gi = u / S;
+          sl = u - gi * S;
+          rec = (int64_t)c * PL.NG + gi;
+          G = PL.g[rec];
+          K = PL.k[rec];
         }
-        asm volatile("bar.sync 1, %0;" ::"n"(32 * kPassConsumers) : "memory");
-      }
-      if (threadIdx.x == 32) {
-        for (int j = 0; j < P.m; ++j)
-          for (int v = 0; v < S; ++v) {
-            uint32_t word = aw[j * S + v];
-            aw[j * S + v] = 0u;
-            const int64_t base = (int64_t)tile * T + v * 32;
-            if (base >= width) word = 0u;
-            else if (width - base < 32) word &= (1u << (width - base)) - 1u;
-            if (word) atomicOr(&alive[j * wstride + (base >> 5)], word);
+        const int mysrc = (active && lane < K) ? (int)PL.src[rec * 32 + lane] * T : 0;
+        const float mybias = (active && lane < G) ? PL.bias[rec * 32 + lane] : 0.f;
+        const int pofs = sl * 128 + lane * 4;
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+        if (G > 0) {
+#pragma unroll 8
+          for (int t = 0; t < K; ++t) {
+            const float4 v = *reinterpret_cast<const float4 *>(tile_s + __shfl_sync(FULL, mysrc, t) + pofs);
+            a0 = __fmaf_rn(v.x, wu, a0);
+            a1 = __fmaf_rn(v.y, wu, a1);
+            a2 = __fmaf_rn(v.z, wu, a2);
+            a3 = __fmaf_rn(v.w, wu, a3);
           }
-        *done = (int)(i + 1);
+        }
+        if (last && early) {
+          // every chain of the pass has read the tile: hand it to the next load
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncthreads();
+          if (next < items) issue_load(next);
+          issued = true;
+        }
+        if (G == 0) continue;
+        uint32_t am = 0;
+        if (last) {
+          // lane v holds member v's output row base: no dependent load per member
+          float *myrow = Yout + (int64_t)tile * T + pofs - lane * 4 +
+                         (lane < G ? (int64_t)PL.orow[rec * 32 + lane] * stride : 0);
+          for (int v = 0; v < G; ++v) {
+            float *row = reinterpret_cast<float *>(__shfl_sync(FULL, reinterpret_cast<uintptr_t>(myrow), v));
+            const float b = __shfl_sync(FULL, mybias, v);
+            float4 y;
+            y.x = clampy(__fadd_rn(a0, b), ymax);
+            y.y = clampy(__fadd_rn(a1, b), ymax);
+            y.z = clampy(__fadd_rn(a2, b), ymax);
+            y.w = clampy(__fadd_rn(a3, b), ymax);
+            am |= (y.x > 0.f ? 1u : 0u) | (y.y > 0.f ? 2u : 0u) | (y.z > 0.f ? 4u : 0u) | (y.w > 0.f ? 8u : 0u);
+            *reinterpret_cast<float4 *>(row + lane * 4) = y;
+          }
+        } else {
+          for (int v = 0; v < G; ++v) {          // member v overwrites source slot v (in place)
+            const int off = __shfl_sync(FULL, mysrc, v);
+            const float b = __shfl_sync(FULL, mybias, v);
+            float4 y;
+            y.x = clampy(__fadd_rn(a0, b), ymax);
+            y.y = clampy(__fadd_rn(a1, b), ymax);
+            y.z = clampy(__fadd_rn(a2, b), ymax);
+            y.w = clampy(__fadd_rn(a3, b), ymax);
+            am |= (y.x > 0.f ? 1u : 0u) | (y.y > 0.f ? 2u : 0u) | (y.z > 0.f ? 4u : 0u) | (y.w > 0.f ? 8u : 0u);
+            *reinterpret_cast<float4 *>(tile_s + off + pofs) = y;
+          }
+        }
+        // liveness: lane covers positions sl*128 + lane*4 + e -> word sl*4 + lane/8
+        uint32_t bal[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) bal[e] = __ballot_sync(FULL, (am >> e) & 1u);
+        if (lane < 4) {
+          uint32_t word = 0;
+#pragma unroll
+          for (int q = 0; q < 32; ++q) word |= ((bal[q & 3] >> (lane * 8 + (q >> 2))) & 1u) << q;
+          if (word) atomicOr(&aw[j * W + sl * 4 + lane], word);
+        }
       }
-      asm volatile("bar.sync 1, %0;" ::"n"(32 * kPassConsumers) : "memory");
+      __syncthreads();                           // the next layer reads slots other warps wrote
     }
+    if (tid < W) {
+      for (int j = 0; j < P.m; ++j) {
+        uint32_t word = aw[j * W + tid];
+        aw[j * W + tid] = 0u;
+        const int64_t base = (int64_t)tile * T + tid * 32;
+        if (base >= width) word = 0u;
+        else if (width - base < 32) word &= (1u << (width - base)) - 1u;
+        if (word) atomicOr(&alive[j * wstride + (base >> 5)], word);
+      }
+    }
+    if (!issued) {
+      // generic-proxy smem writes of this item before the next item's TMA writes
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();
+      if (next < items) issue_load(next);
+    }
+    __syncthreads();                             // aw published before the next item uses it
   }
 }
-
-int pass_buffer_floats() { return kPassBuf; }
 
 // ---------------------------------------------------------------------------
 // After a step [a, a+m): survivor counts of its layers, compaction decision
@@ -867,10 +883,9 @@ void configure_kernels() {
         b.ctas <= 4)
       g_bulk = b;
   }
-  cudaFuncSetAttribute(k_pass<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPassSmem);
-  cudaFuncSetAttribute(k_pass<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPassSmem);
   cudaFuncSetAttribute(k_pass<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPassSmem);
   cudaFuncSetAttribute(k_pass<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPassSmem);
+  cudaFuncSetAttribute(k_pass<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPassSmem);
 }
 
 void launch_densify(const LaunchCfg &c, const Workspace &w, int32_t n, int64_t batch,
@@ -926,14 +941,13 @@ void launch_layer(const LaunchCfg &c, const Workspace &w, const DevLayer &L, int
 
 void launch_pass(const LaunchCfg &c, const Workspace &w, const DevPass &P, uint32_t *alive,
                  float ymax, cudaStream_t s) {
-#define SDNN_PASS(TT)                                                                          \
-  k_pass<TT><<<c.sms, kPassThreads, kPassSmem, s>>>(P, w.st, w.Y[0], w.Y[1], alive, w.words, \
-                                                    w.stride, ymax)
+#define SDNN_PASS(TT)                                                                             \
+  k_pass<TT><<<c.sms * 3, 32 * kPassWarps, kPassSmem, s>>>(P, w.st, w.Y[0], w.Y[1], alive, w.words, \
+                                                          w.stride, ymax)
   switch (P.T) {
+    case 512: SDNN_PASS(512); break;
     case 256: SDNN_PASS(256); break;
-    case 128: SDNN_PASS(128); break;
-    case 64: SDNN_PASS(64); break;
-    default: SDNN_PASS(32); break;
+    default: SDNN_PASS(128); break;
   }
 #undef SDNN_PASS
 }

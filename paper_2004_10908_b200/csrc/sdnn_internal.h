@@ -94,11 +94,14 @@ struct LayerState {
 // graphs splits into small connected components (for RadiX-Net butterflies:
 // 2^(5+2(m-1)) neurons); every component is closed, so one CTA can load a
 // component's input rows for a batch tile, run all m layers out of shared
-// memory, and write only the last layer's rows back to HBM.  Each output's
-// chain is still the canonical ascending-source fmaf sequence.
+// memory, and write only the last layer's rows back to HBM.  When every source
+// row of a (non-last) layer feeds exactly one group and no group has more
+// members than sources, each group overwrites its own source slots in place, so
+// a component tile needs no second buffer.  Each output's chain is still the
+// canonical ascending-source fmaf sequence.
 // ---------------------------------------------------------------------------
 constexpr int kMaxPassLayers = 16;
-constexpr int kMaxPassRows = 256;      // rows per component per boundary (smem)
+constexpr int kMaxPassRows = 128;      // rows per component (one 64 KB tile of >= 128 positions)
 
 struct Step {
   int32_t a = 0, m = 1;                // layers [a, a+m)
@@ -107,37 +110,39 @@ struct Step {
 constexpr int32_t kResidentStep = -2;  // layers [a, L) in the SMEM-resident kernel
 
 // plan greedy fused passes: extend while every component stays <= cap rows at
-// every boundary and the layers are uniform with K <= 32
+// every boundary, the layers are uniform with K <= 32, and every layer but the
+// last of a pass allows in-place slots (exclusive sources, G_g <= K_g)
 std::vector<Step> plan_steps(const std::vector<const PackedLayer *> &layers, int32_t n, int cap,
                              int max_m);
 
 struct PassHostLayer {
   int32_t NG = 0;                      // group slots per component (max over components)
   float wu = 0.f;
-  std::vector<uint16_t> src, dst;      // [ncomp][NG][32] local row indices
+  std::vector<uint16_t> src;           // [ncomp][NG][32] smem slots of the sources
   std::vector<float> bias;             // [ncomp][NG][32] bias of each member
+  std::vector<int32_t> orow;           // last layer only: [ncomp][NG][32] global output rows
   std::vector<uint8_t> k, g;           // [ncomp][NG] sources / members (0 = empty slot)
 };
 struct PassHost {
-  int32_t a = 0, m = 0, ncomp = 0, rin = 0, rout = 0, R = 0, T = 0;
-  std::vector<int32_t> in_rows;        // [ncomp][rin]  global neuron ids at boundary a, -1 pad
+  int32_t a = 0, m = 0, ncomp = 0, rin = 0, R = 0, T = 0;
+  std::vector<int32_t> in_rows;        // [ncomp][rin]  global neuron ids at boundary a
   std::vector<int32_t> in_count;       // [ncomp]
-  std::vector<int32_t> out_rows;       // [ncomp][rout] global neuron ids at boundary a+m, -1 pad
   std::vector<PassHostLayer> layers;   // [m]
 };
 void build_pass(const std::vector<const PackedLayer *> &layers, int32_t n, const Step &s,
-                int buf_floats, int min_t, PassHost &out);
+                int tile_floats, PassHost &out);
 
 struct PassLayerDev {
-  const uint16_t *src, *dst;
+  const uint16_t *src;
   const float *bias;
+  const int32_t *orow;
   const uint8_t *k, *g;
   int32_t NG;
   float wu;
 };
 struct DevPass {
-  int32_t a, m, ncomp, rin, rout, R, T;
-  const int32_t *in_rows, *in_count, *out_rows;
+  int32_t a, m, ncomp, rin, R, T;
+  const int32_t *in_rows, *in_count;
   const PassLayerDev *layers;          // device array [m]
 };
 
@@ -201,7 +206,7 @@ void launch_densify(const LaunchCfg &c, const Workspace &w, int32_t n, int64_t b
 void launch_layer(const LaunchCfg &c, const Workspace &w, const DevLayer &L, int32_t a,
                   uint32_t *alive, float ymax, cudaStream_t s, uint32_t *sat = nullptr);
 bool layer_tracks_saturation(const LaunchCfg &c, const DevLayer &L);
-int pass_buffer_floats();      // smem floats per component tile (tile T = this / R)
+int pass_tile_floats();        // smem floats per component tile (tile T = this / R)
 // a fused pass: reads st[P.a], liveness of layer a+j to alive + j*words
 void launch_pass(const LaunchCfg &c, const Workspace &w, const DevPass &P, uint32_t *alive,
                  float ymax, cudaStream_t s);

@@ -152,8 +152,9 @@ def test_product_path_never_touches_oracle():
 def test_plan_steps_rn_and_rr(sd):
     """Fused multi-layer passes: RadiX-Net layers (5-bit butterfly fields that
     overlap) have connected components of 2^(union of the fields' bits) neurons
-    over consecutive layers, so the planner fuses several layers per pass;
-    random-regular layers have one giant component and are never fused."""
+    over consecutive layers, so the planner fuses layers while a component fits
+    the 128-row tile; random-regular layers have one giant component and are
+    never fused."""
     rn = list(g.iter_layers(g.rn_spec(1024, 24)))
     fields = [g.rn_field(1024, l) for l in range(24)]
 
@@ -162,7 +163,10 @@ def test_plan_steps_rn_and_rr(sd):
         for p in ls:
             bits |= set(range(p, p + 5))
         return len(bits)
-    for cap in (256, 128):
+    default = sd.sdnn_plan_steps(1024, rn)                         # fusion on by default
+    assert default == sd.sdnn_plan_steps(1024, rn, fuse_rows=128)
+    assert sd.sdnn_plan_steps(1024, rn, fuse_rows=4096) == default   # clamped to 128
+    for cap in (128,):
         plan = sd.sdnn_plan_steps(1024, rn, fuse_rows=cap)
         assert sum(plan) == 24 and max(plan) > 1
         a = 0
@@ -171,22 +175,30 @@ def test_plan_steps_rn_and_rr(sd):
             if a + m < 24 and m < 8:
                 assert 2 ** comp_bits(fields[a:a + m + 1]) > cap
             a += m
-    assert sd.sdnn_plan_steps(1024, rn) == [1] * 24                   # opt-in: default off
     assert sd.sdnn_plan_steps(1024, rn, fuse_rows=0) == [1] * 24
     assert sd.sdnn_plan_steps(1024, rn, fuse_rows=64) == [1] * 24    # 2 layers need 128 rows
-    assert max(sd.sdnn_plan_steps(1024, rn, fuse_rows=256, fuse_layers=2)) == 2
+    assert sd.sdnn_plan_steps(1024, rn, flags=sd.SDNN_F_SATURATE) == [1] * 24
     rr = list(g.iter_layers(g.rr_spec(1024, 5)))
-    assert sd.sdnn_plan_steps(1024, rr, fuse_rows=256) == [1] * 5
+    assert sd.sdnn_plan_steps(1024, rr) == [1] * 5
     ka = list(g.iter_layers(g.ka_spec(1024, 20)))
-    assert sd.sdnn_plan_steps(1024, ka, fuse_rows=256, fuse_layers=16) == [16, 4]
+    assert sd.sdnn_plan_steps(1024, ka, fuse_layers=16) == [16, 4]
+    assert max(sd.sdnn_plan_steps(1024, ka, fuse_layers=2)) == 2
     big = [g.gen_layer(g.rn_spec(65536, 12), l, fmt="ell") for l in range(12)]
-    plan = sd.sdnn_plan_steps(65536, big, fmt="ell", fuse_rows=256)
-    assert sum(plan) == 12 and min(plan) >= 2
+    plan = sd.sdnn_plan_steps(65536, big, fmt="ell")
+    assert sum(plan) == 12 and max(plan) == 2
+
+
+def test_plan_steps_not_in_place_not_fused(sd):
+    """A layer whose source rows feed several groups cannot be the non-last
+    layer of a pass (its groups could not overwrite their source slots)."""
+    n = 256
+    lays = list(g.iter_layers(g.random_spec(n, 3, seed=4, kmin=2, kmax=4, wdist="uniform")))
+    assert sd.sdnn_plan_steps(n, lays, fuse_rows=128) == [1, 1, 1]
 
 
 def test_plan_steps_nonuniform_not_fused(sd):
     lays = list(g.iter_layers(g.rn_spec(1024, 4, wdist="random")))
-    assert sd.sdnn_plan_steps(1024, lays, fuse_rows=256) == [1, 1, 1, 1]
+    assert sd.sdnn_plan_steps(1024, lays) == [1, 1, 1, 1]
 
 
 def test_binding_constants_match_header(sd):

@@ -165,7 +165,7 @@ def test_fused_ka_long_passes(sd):
     layers = list(g.iter_layers(spec))
     rp, idx, cnt = g.ka_inputs(2048, 999, seed=5)
     cg, Yg, st = run_gpu(sd, 2048, layers, rp, idx, None, fmt="ell", fuse_rows=256,
-                         fuse_layers=16)
+                         fuse_layers=16, flags=sd.SDNN_F_NO_RESIDENT)
     assert st["steps"] == 3 and st["fused_layers"] == 40
     Yx = ka_expected(spec, cnt)
     assert np.array_equal(Yg.view(np.uint32), Yx.view(np.uint32))
