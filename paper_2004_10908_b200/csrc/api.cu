@@ -255,22 +255,8 @@ sdnn_status make_plan(sdnn_net *net) {
   std::vector<const PackedLayer *> lp(net->L);
   for (int l = 0; l < net->L; ++l) lp[l] = &net->host[l];
   std::vector<const PackedLayer *> head(lp.begin(), lp.begin() + ar);
-  net->steps = plan_steps(head, net->n, cap, maxm);
-  std::vector<int> fused;
-  for (int i = 0; i < (int)net->steps.size(); ++i)
-    if (net->steps[i].m > 1) fused.push_back(i);
-  std::vector<PassHost> ph(fused.size());
-  {
-    std::atomic<int> next{0};
-    std::vector<std::thread> th;
-    const int nt = std::max(1, std::min<int>(nthreads_default(), (int)fused.size()));
-    for (int t = 0; t < nt; ++t)
-      th.emplace_back([&] {
-        for (int q = next++; q < (int)fused.size(); q = next++)
-          build_pass(lp, net->n, net->steps[fused[q]], pass_tile_floats(), ph[q]);
-      });
-    for (auto &x : th) x.join();
-  }
+  std::vector<PassHost> ph;
+  net->steps = plan_passes(head, net->n, cap, maxm, pass_tile_floats(), nthreads_default(), &ph);
   net->pass_arena.release();
   net->passes.clear();
   net->fused_layers = 0;
@@ -283,7 +269,8 @@ sdnn_status make_plan(sdnn_net *net) {
     if (bytes) CK(cudaMemcpy(*d, h, bytes, cudaMemcpyHostToDevice));
     return SDNN_OK;
   };
-  for (size_t q = 0; q < fused.size(); ++q) {
+  for (size_t q = 0; q < net->steps.size(); ++q) {
+    if (net->steps[q].m == 1) continue;
     PassHost &H = ph[q];
     DevPass D{};
     D.a = H.a;
@@ -292,28 +279,21 @@ sdnn_status make_plan(sdnn_net *net) {
     D.rin = H.rin;
     D.R = H.R;
     D.T = H.T;
-    void *p1, *p2, *p4;
+    D.rec_bytes = H.rec_bytes;
+    void *p1, *p2, *p3;
     sdnn_status st;
     if ((st = up(H.in_rows.data(), H.in_rows.size() * 4, &p1)) ||
-        (st = up(H.in_count.data(), H.in_count.size() * 4, &p2)))
+        (st = up(H.in_count.data(), H.in_count.size() * 4, &p2)) ||
+        (st = up(H.rec.data(), H.rec.size(), &p3)))
       return st;
     D.in_rows = (const int32_t *)p1;
     D.in_count = (const int32_t *)p2;
-    std::vector<PassLayerDev> pl(H.m);
+    D.rec = (const unsigned char *)p3;
     for (int j = 0; j < H.m; ++j) {
-      PassHostLayer &HL = H.layers[j];
-      void *s1, *s3, *s4, *s5, *s6 = nullptr;
-      if ((st = up(HL.src.data(), HL.src.size() * 2, &s1)) ||
-          (st = up(HL.bias.data(), HL.bias.size() * 4, &s3)) ||
-          (st = up(HL.k.data(), HL.k.size(), &s4)) || (st = up(HL.g.data(), HL.g.size(), &s5)))
-        return st;
-      if (!HL.orow.empty() && (st = up(HL.orow.data(), HL.orow.size() * 4, &s6))) return st;
-      pl[j] = PassLayerDev{(const uint16_t *)s1, (const float *)s3, (const int32_t *)s6,
-                           (const uint8_t *)s4, (const uint8_t *)s5, HL.NG, HL.wu};
+      const PassHostLayer &HL = H.layers[j];
+      D.layers[j] = PassLayerDev{HL.off_kg, HL.off_src, HL.off_bias, HL.off_orow, HL.NG, HL.wu};
     }
-    if ((st = up(pl.data(), sizeof(PassLayerDev) * pl.size(), &p4))) return st;
-    D.layers = (const PassLayerDev *)p4;
-    net->steps[fused[q]].pass = (int32_t)net->passes.size();
+    net->steps[q].pass = (int32_t)net->passes.size();
     net->passes.push_back(D);
     net->fused_layers += H.m;
   }
@@ -873,7 +853,7 @@ sdnn_status sdnn_plan_steps(int32_t neurons, int32_t layers, const sdnn_layer *W
                       ? 0
                       : std::min(o.fuse_rows < 0 ? kMaxPassRows : o.fuse_rows, kMaxPassRows);
   const int maxm = o.fuse_layers < 0 ? 8 : o.fuse_layers;
-  const std::vector<Step> steps = plan_steps(lp, neurons, cap, maxm);
+  const std::vector<Step> steps = plan_passes(lp, neurons, cap, maxm, pass_tile_floats(), 1, nullptr);
   for (size_t i = 0; i < steps.size(); ++i) step_len[i] = steps[i].m;
   *nsteps = (int32_t)steps.size();
   return SDNN_OK;

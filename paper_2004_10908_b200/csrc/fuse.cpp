@@ -9,7 +9,10 @@
 // component has at most `cap` nodes on every boundary; the greedy planner
 // extends a pass layer by layer while that holds.
 #include <algorithm>
+#include <atomic>
+#include <cstring>
 #include <numeric>
+#include <thread>
 
 #include "sdnn_internal.h"
 
@@ -201,6 +204,87 @@ void build_pass(const std::vector<const PackedLayer *> &layers, int32_t n, const
         }
       }
   }
+  // ---- per-component records ----
+  int32_t off = 0;
+  for (int b = 0; b < m; ++b) {
+    PassHostLayer &H = out.layers[b];
+    H.off_kg = off;
+    off += (H.NG * 2 + 15) / 16 * 16;
+    H.off_src = off;
+    off += H.NG * 64;
+    H.off_bias = off;
+    off += H.NG * 128;
+    if (b == m - 1) {
+      H.off_orow = off;
+      off += H.NG * 128;
+    }
+  }
+  out.rec_bytes = off;
+  out.rec.assign((size_t)ncomp * off, 0);
+  for (int c = 0; c < ncomp; ++c) {
+    unsigned char *r = out.rec.data() + (size_t)c * off;
+    for (int b = 0; b < m; ++b) {
+      const PassHostLayer &H = out.layers[b];
+      const size_t g0 = (size_t)c * H.NG;
+      for (int q = 0; q < H.NG; ++q) {
+        const uint16_t kg = (uint16_t)(H.k[g0 + q] | (H.g[g0 + q] << 8));
+        std::memcpy(r + H.off_kg + 2 * q, &kg, 2);
+      }
+      std::memcpy(r + H.off_src, H.src.data() + g0 * 32, (size_t)H.NG * 64);
+      std::memcpy(r + H.off_bias, H.bias.data() + g0 * 32, (size_t)H.NG * 128);
+      if (H.off_orow >= 0) std::memcpy(r + H.off_orow, H.orow.data() + g0 * 32, (size_t)H.NG * 128);
+    }
+  }
+}
+
+std::vector<Step> plan_passes(const std::vector<const PackedLayer *> &layers, int32_t n, int cap,
+                              int max_m, int tile_floats, int threads,
+                              std::vector<PassHost> *built) {
+  std::vector<Step> steps = plan_steps(layers, n, cap, max_m);
+  std::vector<PassHost> ph(steps.size());
+  std::vector<char> done(steps.size(), 0);
+  for (;;) {
+    std::vector<int> todo;
+    for (int i = 0; i < (int)steps.size(); ++i)
+      if (steps[i].m > 1 && !done[i]) todo.push_back(i);
+    if (todo.empty()) break;
+    std::atomic<int> next{0};
+    std::vector<std::thread> th;
+    const int nt = std::max(1, std::min<int>(threads, (int)todo.size()));
+    for (int t = 0; t < nt; ++t)
+      th.emplace_back([&] {
+        for (int q = next++; q < (int)todo.size(); q = next++)
+          build_pass(layers, n, steps[todo[q]], tile_floats, ph[todo[q]]);
+      });
+    for (auto &x : th) x.join();
+    // split passes whose record does not fit (any sub-range of a pass is a pass)
+    std::vector<Step> s2;
+    std::vector<PassHost> p2;
+    std::vector<char> d2;
+    for (int i = 0; i < (int)steps.size(); ++i) {
+      const Step &S = steps[i];
+      if (S.m > 1 && ph[i].rec_bytes > kPassRecMax) {
+        Step lo = S, hi = S;
+        lo.m = S.m / 2;
+        hi.a = S.a + lo.m;
+        hi.m = S.m - lo.m;
+        for (const Step &x : {lo, hi}) {
+          s2.push_back(x);
+          p2.emplace_back();
+          d2.push_back(x.m == 1);
+        }
+      } else {
+        s2.push_back(S);
+        p2.push_back(std::move(ph[i]));
+        d2.push_back(1);                    // built in this round or before
+      }
+    }
+    steps.swap(s2);
+    ph.swap(p2);
+    done.swap(d2);
+  }
+  if (built) built->swap(ph);
+  return steps;
 }
 
 }  // namespace sdnn

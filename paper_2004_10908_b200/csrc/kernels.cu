@@ -491,19 +491,26 @@ __global__ void k_y0_positive(int64_t batch, const int64_t *__restrict__ rowptr,
 constexpr int kPassWarps = 4;
 constexpr int kPassTile = 16384;                 // floats per component tile (R * T)
 constexpr int kPassMaxT = 512;
-constexpr size_t kPassSmem = (size_t)kPassTile * 4 + 16 + kMaxPassLayers * (kPassMaxT / 32) * 4;
+constexpr size_t kPassSmem =
+    (size_t)kPassTile * 4 + kPassRecMax + 16 + kMaxPassLayers * (kPassMaxT / 32) * 4;
 
 int pass_tile_floats() { return kPassTile; }
 
+// One CTA per (component, tile) item at a time: the component's metadata record
+// and its input rows for T batch positions arrive by bulk copy on one mbarrier;
+// the layers run in place in shared memory; the last layer writes HBM.  The
+// next item's copies are issued as soon as the last layer's chains have read
+// the tile (before its stores), and its row ids are prefetched into registers.
 template <int T>
 __global__ void __launch_bounds__(32 * kPassWarps, 3)
-    k_pass(DevPass P, const LayerState *__restrict__ st, float *Ya, float *Yb,
+    k_pass(const DevPass P, const LayerState *__restrict__ st, float *Ya, float *Yb,
            uint32_t *__restrict__ alive, int64_t wstride, int64_t stride, float ymax) {
   constexpr int S = T / 128;                     // 128-position slices per tile
   constexpr int W = T / 32;                      // liveness words per tile
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float *tile_s = reinterpret_cast<float *>(smem_raw);
-  uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw + (size_t)kPassTile * 4);
+  unsigned char *rec_s = smem_raw + (size_t)kPassTile * 4;
+  uint64_t *bar = reinterpret_cast<uint64_t *>(rec_s + kPassRecMax);
   uint32_t *aw = reinterpret_cast<uint32_t *>(bar + 2);                 // [kMaxPassLayers][W]
   const LayerState Sx = st[P.a];
   const int width = Sx.width;
@@ -519,26 +526,36 @@ __global__ void __launch_bounds__(32 * kPassWarps, 3)
   }
   for (int q = tid; q < kMaxPassLayers * W; q += blockDim.x) aw[q] = 0u;
   __syncthreads();
-  // one cp.async.bulk per input row of the component tile (all threads issue)
+  // rin <= kMaxPassRows == blockDim.x: thread r owns input row r of an item
+  int nrow = 0, ncnt = 0;
+  auto fetch_rows = [&](int64_t it) {
+    const int c = (int)(it / tiles);
+    ncnt = __ldg(P.in_count + c);
+    nrow = tid < P.rin ? __ldg(P.in_rows + (int64_t)c * P.rin + tid) : 0;
+  };
   auto issue_load = [&](int64_t it) {
     const int c = (int)(it / tiles);
     const int tile = (int)(it - (int64_t)c * tiles);
-    const int cnt = P.in_count[c];
-    const int32_t *rows = P.in_rows + (int64_t)c * P.rin;
-    if (tid == 0) mbar_expect_tx_arrive(bar, (uint32_t)cnt * T * 4);
-    for (int r = tid; r < cnt; r += blockDim.x)
-      bulk_g2s(tile_s + (size_t)r * T, Yin + (int64_t)rows[r] * stride + (int64_t)tile * T, T * 4, bar);
+    if (tid == 0) {
+      mbar_expect_tx_arrive(bar, (uint32_t)ncnt * T * 4 + (uint32_t)P.rec_bytes);
+      bulk_g2s(rec_s, P.rec + (int64_t)c * P.rec_bytes, P.rec_bytes, bar);
+    }
+    if (tid < ncnt)
+      bulk_g2s(tile_s + (size_t)tid * T, Yin + (int64_t)nrow * stride + (int64_t)tile * T, T * 4, bar);
   };
-  const PassLayerDev PLast = P.layers[P.m - 1];
   // the last layer releases the tile before its HBM stores when every warp owns
   // at most one (group, slice) unit of it
-  const bool early = PLast.NG * S <= kPassWarps;
-  if (blockIdx.x < items) issue_load(blockIdx.x);
+  const bool early = P.layers[P.m - 1].NG * S <= kPassWarps;
+  if (blockIdx.x < items) {
+    fetch_rows(blockIdx.x);
+    issue_load(blockIdx.x);
+  }
   uint32_t ph = 0;
   for (int64_t it = blockIdx.x; it < items; it += gridDim.x, ph ^= 1u) {
     const int c = (int)(it / tiles);
     const int tile = (int)(it - (int64_t)c * tiles);
     const int64_t next = it + gridDim.x;
+    if (next < items) fetch_rows(next);          // in flight while this item computes
     bool issued = false;
     mbar_wait(bar, ph);
     for (int j = 0; j < P.m; ++j) {
@@ -546,21 +563,29 @@ __global__ void __launch_bounds__(32 * kPassWarps, 3)
       const bool last = j == P.m - 1;
       const float wu = PL.wu;
       const int units = PL.NG * S;
+      const uint16_t *kg_s = reinterpret_cast<const uint16_t *>(rec_s + PL.off_kg);
+      const uint16_t *src_s = reinterpret_cast<const uint16_t *>(rec_s + PL.off_src);
+      const float *bias_s = reinterpret_cast<const float *>(rec_s + PL.off_bias);
       for (int u0 = 0; u0 < (last && early ? kPassWarps : units); u0 += kPassWarps) {
         const int u = u0 + warp;
         const bool active = u < units;
-        int G = 0, K = 0, sl = 0;
-        int64_t rec = 0;
+        int G = 0, K = 0, sl = 0, gi = 0;
         if (active) {
-          const int gi = u / S;
+          gi = u / S;
           sl = u - gi * S;
-          rec = (int64_t)c * PL.NG + gi;
-          G = PL.g[rec];
-          K = PL.k[rec];
+          const uint32_t kg = kg_s[gi];
+          K = kg & 0xffu;
+          G = kg >> 8;
         }
-        const int mysrc = (active && lane < K) ? (int)PL.src[rec * 32 + lane] * T : 0;
-        const float mybias = (active && lane < G) ? PL.bias[rec * 32 + lane] : 0.f;
+        const int mysrc = (active && lane < K) ? (int)src_s[gi * 32 + lane] * T : 0;
+        const float mybias = (active && lane < G) ? bias_s[gi * 32 + lane] : 0.f;
         const int pofs = sl * 128 + lane * 4;
+        float *myrow = nullptr;
+        if (last)
+          myrow = Yout + (int64_t)tile * T + pofs - lane * 4 +
+                  ((active && lane < G)
+                       ? (int64_t)reinterpret_cast<const int32_t *>(rec_s + PL.off_orow)[gi * 32 + lane] * stride
+                       : 0);
         float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
         if (G > 0) {
 #pragma unroll 8
@@ -573,7 +598,7 @@ __global__ void __launch_bounds__(32 * kPassWarps, 3)
           }
         }
         if (last && early) {
-          // every chain of the pass has read the tile: hand it to the next load
+          // every chain of the pass has read the tile and the record: next load
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncthreads();
           if (next < items) issue_load(next);
@@ -583,8 +608,6 @@ __global__ void __launch_bounds__(32 * kPassWarps, 3)
         uint32_t am = 0;
         if (last) {
           // lane v holds member v's output row base: no dependent load per member
-          float *myrow = Yout + (int64_t)tile * T + pofs - lane * 4 +
-                         (lane < G ? (int64_t)PL.orow[rec * 32 + lane] * stride : 0);
           for (int v = 0; v < G; ++v) {
             float *row = reinterpret_cast<float *>(__shfl_sync(FULL, reinterpret_cast<uintptr_t>(myrow), v));
             const float b = __shfl_sync(FULL, mybias, v);

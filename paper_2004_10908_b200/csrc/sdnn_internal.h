@@ -118,6 +118,7 @@ std::vector<Step> plan_steps(const std::vector<const PackedLayer *> &layers, int
 struct PassHostLayer {
   int32_t NG = 0;                      // group slots per component (max over components)
   float wu = 0.f;
+  int32_t off_kg = 0, off_src = 0, off_bias = 0, off_orow = -1;  // byte offsets in a record
   std::vector<uint16_t> src;           // [ncomp][NG][32] smem slots of the sources
   std::vector<float> bias;             // [ncomp][NG][32] bias of each member
   std::vector<int32_t> orow;           // last layer only: [ncomp][NG][32] global output rows
@@ -128,22 +129,31 @@ struct PassHost {
   std::vector<int32_t> in_rows;        // [ncomp][rin]  global neuron ids at boundary a
   std::vector<int32_t> in_count;       // [ncomp]
   std::vector<PassHostLayer> layers;   // [m]
+  // per-component metadata record (one bulk copy next to the tile):
+  //   for each layer j: kg[NG_j] u16 (K | G << 8) padded to 16 B, src[NG_j][32] u16,
+  //   bias[NG_j][32] f32; last layer: orow[NG][32] i32
+  int32_t rec_bytes = 0;
+  std::vector<unsigned char> rec;      // [ncomp][rec_bytes]
 };
+constexpr int kPassRecMax = 8192;      // record bytes per component (3 CTAs per SM)
 void build_pass(const std::vector<const PackedLayer *> &layers, int32_t n, const Step &s,
                 int tile_floats, PassHost &out);
+// plan_steps, build every fused pass, and split (in halves) any pass whose
+// record exceeds kPassRecMax; `built[i]` is the PassHost of steps[i] (m > 1)
+std::vector<Step> plan_passes(const std::vector<const PackedLayer *> &layers, int32_t n, int cap,
+                              int max_m, int tile_floats, int threads,
+                              std::vector<PassHost> *built);
 
 struct PassLayerDev {
-  const uint16_t *src;
-  const float *bias;
-  const int32_t *orow;
-  const uint8_t *k, *g;
+  int32_t off_kg, off_src, off_bias, off_orow;   // byte offsets in the component record
   int32_t NG;
   float wu;
 };
 struct DevPass {
-  int32_t a, m, ncomp, rin, R, T;
+  int32_t a, m, ncomp, rin, R, T, rec_bytes;
   const int32_t *in_rows, *in_count;
-  const PassLayerDev *layers;          // device array [m]
+  const unsigned char *rec;            // [ncomp][rec_bytes]
+  PassLayerDev layers[kMaxPassLayers]; // by value: the kernel parameter carries them
 };
 
 // SMEM-resident multi-layer kernel (resident.cu), N <= 4096

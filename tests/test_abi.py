@@ -188,6 +188,27 @@ def test_plan_steps_rn_and_rr(sd):
     assert sum(plan) == 12 and max(plan) == 2
 
 
+def identity_layer(n):
+    """W = I, uniform 1, bias 0: Y -> min(max(Y, 0), 32) (the identity on Y in [0, 32])."""
+    from types import SimpleNamespace
+    return SimpleNamespace(rowptr=np.arange(n + 1, dtype=np.int64), colidx=np.arange(n, dtype=np.int32),
+                           val=None, uniform=1.0, bias=np.zeros(n, np.float32),
+                           ell=np.arange(n, dtype=np.int32).reshape(n, 1), ell_val=None)
+
+
+def test_plan_splits_oversized_records(sd):
+    """A pass's per-component metadata record must fit kPassRecMax (8 KB):
+    [identity, rn0, rn1] forms 128-row components (plan [3] by the component cap
+    alone) but the identity layer has 128 singleton groups per component (~25 KB
+    of record), so the pass is split in halves -> [1, 2]."""
+    n = 1024
+    rn = [g.gen_layer(g.rn_spec(n, 2), l) for l in range(2)]
+    assert sd.sdnn_plan_steps(n, rn) == [2]
+    assert sd.sdnn_plan_steps(n, [identity_layer(n)] + rn) == [1, 2]
+    # two layers [identity, rn0]: 32-row components, 32 singletons (~6.5 KB) fit
+    assert sd.sdnn_plan_steps(n, [identity_layer(n)] + rn, fuse_layers=2) == [2, 1]
+
+
 def test_plan_steps_not_in_place_not_fused(sd):
     """A layer whose source rows feed several groups cannot be the non-last
     layer of a pass (its groups could not overwrite their source slots)."""

@@ -172,6 +172,23 @@ def test_fused_ka_long_passes(sd):
     assert np.array_equal(cg, np.flatnonzero((Yx > 0).any(1)))
 
 
+def test_fused_record_split_and_singletons(sd):
+    """Identity layers (singleton groups, K = G = 1) inside fused passes: a pass
+    whose metadata record would exceed 8 KB is split; [identity, rn0] fuses
+    with 32 singleton groups per component."""
+    from test_abi import identity_layer
+    n, B = 1024, 613
+    rn = [g.gen_layer(g.rn_spec(n, 6), l) for l in range(6)]
+    layers = [identity_layer(n)] + rn[:3] + [identity_layer(n)] + rn[3:]
+    rp, idx = g.ms_inputs(n, B, seed=41)
+    cats, Y, prof = oracle.infer(n, layers, rp, idx, None, profile=True)
+    for fl in (2, -1):
+        cg, Yg, st = run_gpu(sd, n, layers, rp, idx, None, fuse_layers=fl, flags=sd.SDNN_F_NO_RESIDENT)
+        assert st["fused_layers"] > 0
+        assert_parity(cg, Yg, cats, Y)
+        assert st["live_rows"] == prof
+
+
 # ---------------------------------------------------------------------------
 # f2: exact saturated-row retirement (SDNN_F_SATURATE)
 # ---------------------------------------------------------------------------
