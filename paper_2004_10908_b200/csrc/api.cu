@@ -219,6 +219,7 @@ sdnn_status ensure_ws(sdnn_net *net, int64_t batch) {
     CK(cudaMalloc(&w.nretired, sizeof(int32_t)));
     CK(cudaMalloc(&w.orig, sizeof(uint32_t) * w.words));
   }
+  encode_pass_maps(w, net->n);                  // row gathers for fused passes (optional)
   net->ws_cap = stride;
   return SDNN_OK;
 }

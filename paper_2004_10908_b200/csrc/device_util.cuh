@@ -124,6 +124,17 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 }
 
 
+// TMA row gather (sm_100): rows r0..r3 of a 2-D tensor map with box {C, 1},
+// columns [c, c + C) -> 4 consecutive C-element rows at dst
+__device__ __forceinline__ void gather4_g2s(void *dst, const void *tmap, int c, int r0, int r1,
+                                            int r2, int r3, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
+      "l"(tmap), "r"(c), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // 16-byte cp.async (LDGSTS, L2 only) global -> shared
 __device__ __forceinline__ void cp_async16(void *dst, const void *src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");

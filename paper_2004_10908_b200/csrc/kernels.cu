@@ -503,8 +503,10 @@ int pass_tile_floats() { return kPassTile; }
 // the tile (before its stores), and its row ids are prefetched into registers.
 template <int T>
 __global__ void __launch_bounds__(32 * kPassWarps, 3)
-    k_pass(const DevPass P, const LayerState *__restrict__ st, float *Ya, float *Yb,
-           uint32_t *__restrict__ alive, int64_t wstride, int64_t stride, float ymax) {
+    k_pass(const DevPass P, const __grid_constant__ CUtensorMap tmA,
+           const __grid_constant__ CUtensorMap tmB, const LayerState *__restrict__ st, float *Ya,
+           float *Yb, uint32_t *__restrict__ alive, int64_t wstride, int64_t stride, float ymax,
+           int use_gather) {
   constexpr int S = T / 128;                     // 128-position slices per tile
   constexpr int W = T / 32;                      // liveness words per tile
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -533,9 +535,27 @@ __global__ void __launch_bounds__(32 * kPassWarps, 3)
     ncnt = __ldg(P.in_count + c);
     nrow = tid < P.rin ? __ldg(P.in_rows + (int64_t)c * P.rin + tid) : 0;
   };
+  const void *tm = Sx.in ? (const void *)&tmB : (const void *)&tmA;
+  const bool gather = T <= 256 && use_gather;
   auto issue_load = [&](int64_t it) {
     const int c = (int)(it / tiles);
     const int tile = (int)(it - (int64_t)c * tiles);
+    if (gather) {
+      // lanes 4i..4i+3 hold the rows of gather i; a padded tail repeats the
+      // quad's first row into slots >= ncnt (inside the tile, never read)
+      const int qb = lane & ~3;
+      const int r0 = __shfl_sync(FULL, nrow, qb), r1 = __shfl_sync(FULL, nrow, qb + 1);
+      const int r2 = __shfl_sync(FULL, nrow, qb + 2), r3 = __shfl_sync(FULL, nrow, qb + 3);
+      if (tid == 0) {
+        mbar_expect_tx_arrive(bar, (uint32_t)((ncnt + 3) & ~3) * T * 4 + (uint32_t)P.rec_bytes);
+        bulk_g2s(rec_s, P.rec + (int64_t)c * P.rec_bytes, P.rec_bytes, bar);
+      }
+      const int q = tid & ~3;
+      if ((lane & 3) == 0 && q < ncnt)
+        gather4_g2s(tile_s + (size_t)q * T, tm, tile * T, r0, q + 1 < ncnt ? r1 : r0,
+                    q + 2 < ncnt ? r2 : r0, q + 3 < ncnt ? r3 : r0, bar);
+      return;
+    }
     if (tid == 0) {
       mbar_expect_tx_arrive(bar, (uint32_t)ncnt * T * 4 + (uint32_t)P.rec_bytes);
       bulk_g2s(rec_s, P.rec + (int64_t)c * P.rec_bytes, P.rec_bytes, bar);
@@ -964,15 +984,56 @@ void launch_layer(const LaunchCfg &c, const Workspace &w, const DevLayer &L, int
 
 void launch_pass(const LaunchCfg &c, const Workspace &w, const DevPass &P, uint32_t *alive,
                  float ymax, cudaStream_t s) {
-#define SDNN_PASS(TT)                                                                             \
-  k_pass<TT><<<c.sms * 3, 32 * kPassWarps, kPassSmem, s>>>(P, w.st, w.Y[0], w.Y[1], alive, w.words, \
-                                                          w.stride, ymax)
+  static const int gather_env = [] {
+    // opt-in: measured slower than per-row bulk copies on C4 (k_pass 2.48 vs
+    // 2.36 ms per launch, profiles/r01_v7_gather_c4.txt)
+    const char *e = getenv("SDNN_PASS_GATHER");
+    return e ? atoi(e) : 0;
+  }();
+  const int tb = P.T == 256 ? 1 : 0;
+  const int g = (w.tm_ok && gather_env && P.T <= 256) ? 1 : 0;
+#define SDNN_PASS(TT)                                                                    \
+  k_pass<TT><<<c.sms * 3, 32 * kPassWarps, kPassSmem, s>>>(P, w.tmY[0][tb], w.tmY[1][tb], \
+                                                          w.st, w.Y[0], w.Y[1], alive,    \
+                                                          w.words, w.stride, ymax, g)
   switch (P.T) {
     case 512: SDNN_PASS(512); break;
     case 256: SDNN_PASS(256); break;
     default: SDNN_PASS(128); break;
   }
 #undef SDNN_PASS
+}
+
+bool encode_pass_maps(Workspace &w, int32_t n) {
+  using EncodeFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static EncodeFn encode = [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      p = nullptr;
+    }
+    return reinterpret_cast<EncodeFn>(p);
+  }();
+  w.tm_ok = false;
+  if (!encode) return false;
+  for (int b = 0; b < 2; ++b)
+    for (int t = 0; t < 2; ++t) {
+      const cuuint64_t dims[2] = {(cuuint64_t)w.stride, (cuuint64_t)n};
+      const cuuint64_t strides[1] = {(cuuint64_t)w.stride * 4};
+      const cuuint32_t box[2] = {t ? 256u : 128u, 1u};
+      const cuuint32_t estr[2] = {1u, 1u};
+      if (encode(&w.tmY[b][t], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, w.Y[b], dims, strides, box, estr,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    }
+  w.tm_ok = true;
+  return true;
 }
 
 void launch_scan(const Workspace &w, int32_t a, int32_t m, uint32_t *alive_cur,

@@ -6,6 +6,7 @@
 #include <string>
 #include <vector>
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace sdnn {
@@ -190,6 +191,10 @@ struct Workspace {
   uint32_t *pret = nullptr;            // positions retired but not yet compacted away
   int32_t *nretired = nullptr;
   uint32_t *orig = nullptr;
+  // TMA tensor maps of Y[b] as a 2-D [n][stride] fp32 tensor with a box of
+  // {T, 1}: tmY[b][0] for T = 128, tmY[b][1] for T = 256 (fused-pass row gathers)
+  CUtensorMap tmY[2][2];
+  bool tm_ok = false;
   int64_t stride = 0;                 // row stride (capacity in batch columns)
   int64_t words = 0;                  // stride / 32
   uint32_t *alive_set(int s) const { return alive[s & 1]; }
@@ -220,6 +225,9 @@ int pass_tile_floats();        // smem floats per component tile (tile T = this 
 // a fused pass: reads st[P.a], liveness of layer a+j to alive + j*words
 void launch_pass(const LaunchCfg &c, const Workspace &w, const DevPass &P, uint32_t *alive,
                  float ymax, cudaStream_t s);
+// build w.tmY for the current Y buffers (false: no driver entry point; passes
+// then use per-row bulk copies)
+bool encode_pass_maps(Workspace &w, int32_t n);
 // after a step [a, a+m): live counts of its m layers, compaction decision -> st[a+m],
 // zero the next step's bitmask set
 void launch_scan(const Workspace &w, int32_t a, int32_t m, uint32_t *alive_cur,
