@@ -22,7 +22,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsdnn.so")
+LIB_PATH = os.environ.get("SDNN_LIB") or os.path.join(_HERE, "libsdnn.so")
 
 SDNN_OK, SDNN_E_ARG, SDNN_E_FORMAT, SDNN_E_UNSUPPORTED = 0, -1, -2, -3
 SDNN_E_NOMEM, SDNN_E_CUDA, SDNN_E_STATE = -4, -5, -6

@@ -9,7 +9,11 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
-SO = os.path.join(HERE, "libsdnn.so")
+# SDNN_LIB / SDNN_NVCC_FLAGS: an alternative in-tree build (A/B experiments,
+# e.g. SDNN_LIB=.../libsdnn_b.so SDNN_NVCC_FLAGS=-DSDNN_CLAMP3); the binding
+# loads the same SDNN_LIB path
+SO = os.environ.get("SDNN_LIB") or os.path.join(HERE, "libsdnn.so")
+EXTRA = os.environ.get("SDNN_NVCC_FLAGS", "").split()
 SOURCES = ["api.cu", "kernels.cu", "resident.cu", "pack.cpp", "fuse.cpp"]
 HEADERS = ["sdnn_internal.h", "device_util.cuh", os.path.join("..", "..", "include", "sdnn.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -29,7 +33,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return SO
     nvcc = os.environ.get("NVCC", "nvcc")
     tmp = SO + ".%d.tmp" % os.getpid()
-    cmd = [nvcc, *ARCH, *FLAGS, "-shared", "-I", os.path.join(ROOT, "include"),
+    cmd = [nvcc, *ARCH, *FLAGS, *EXTRA, "-shared", "-I", os.path.join(ROOT, "include"),
            *[os.path.join(CSRC, f) for f in SOURCES], "-o", tmp, "-lpthread"]
     if verbose:
         print(" ".join(cmd))

@@ -8,9 +8,15 @@ namespace sdnn {
 
 #define FULL 0xffffffffu
 
+// min(max(z, 0), ymax) with the canonical reading z > 0 ? min(z, ymax) : +0
+// (A6).  The two agree bit for bit because z is never -0 here: every
+// chain starts at acc = +0 and a round-to-nearest sum (fma or add) is -0 only
+// when both addends are -0, so acc and z = acc + b are never -0; NaN -> +0 in
+// both.  Two FMNMX instead of FSETP + FMNMX + FSEL.
 __device__ __forceinline__ float clampy(float z, float ymax) {
-  return z > 0.f ? fminf(z, ymax) : 0.f;
+  return fminf(fmaxf(z, 0.f), ymax);
 }
+
 
 template <int VEC>
 struct VecT;

@@ -9,6 +9,7 @@
 // component has at most `cap` nodes on every boundary; the greedy planner
 // extends a pass layer by layer while that holds.
 #include <algorithm>
+#include <cmath>
 #include <atomic>
 #include <cstring>
 #include <numeric>

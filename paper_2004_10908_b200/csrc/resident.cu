@@ -36,8 +36,9 @@ int resident_positions(int n) {
 }
 int resident_max_blob() { return kResMaxBlob; }
 
+// same bits as z > 0 ? min(z, ymax) : +0 because z is never -0 (see clampy)
 __device__ __forceinline__ float clamp_res(float z, float ymax) {
-  return z > 0.f ? fminf(z, ymax) : 0.f;
+  return fminf(fmaxf(z, 0.f), ymax);
 }
 
 template <int P, int PAD>
@@ -148,6 +149,13 @@ __global__ void __launch_bounds__(kResThreads, 1)
 #pragma unroll
       for (int i = 0; i < MPL; ++i)
         bs[i] = Ld.bias_uniform ? Ld.bias0 : ((m0 + i < Gg) ? biasm[g * GM + m0 + i] : 0.f);
+      // liveness: some member of this lane alive iff acc + max bias > 0 (monotone)
+      float bhi = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < MPL; ++i)
+        if (m0 + i < Gg) bhi = fmaxf(bhi, bs[i]);
+#pragma unroll
+      for (int q = 0; q < P; ++q) bits |= (__fadd_rn(av[q], bhi) > 0.f ? 1u : 0u) << q;
 #pragma unroll
       for (int i = 0; i < MPL; ++i) {
         if (m0 + i >= Gg) break;
@@ -160,8 +168,6 @@ __global__ void __launch_bounds__(kResThreads, 1)
           y.y = clamp_res(__fadd_rn(av[q + 1], b), ymax);
           y.z = clamp_res(__fadd_rn(av[q + 2], b), ymax);
           y.w = clamp_res(__fadd_rn(av[q + 3], b), ymax);
-          bits |= (y.x > 0.f ? 1u : 0u) << q | (y.y > 0.f ? 1u : 0u) << (q + 1) |
-                  (y.z > 0.f ? 1u : 0u) << (q + 2) | (y.w > 0.f ? 1u : 0u) << (q + 3);
           if (PAD == 0) {
             *reinterpret_cast<float4 *>(dst + q) = y;
           } else {

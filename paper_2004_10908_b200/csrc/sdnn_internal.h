@@ -119,7 +119,7 @@ std::vector<Step> plan_steps(const std::vector<const PackedLayer *> &layers, int
 struct PassHostLayer {
   int32_t NG = 0;                      // group slots per component (max over components)
   float wu = 0.f;
-  int32_t off_kg = 0, off_src = 0, off_bias = 0, off_orow = -1;  // byte offsets in a record
+  int32_t off_kg = 0, off_src = 0, off_bias = 0, off_orow = -1;  // record byte offsets
   std::vector<uint16_t> src;           // [ncomp][NG][32] smem slots of the sources
   std::vector<float> bias;             // [ncomp][NG][32] bias of each member
   std::vector<int32_t> orow;           // last layer only: [ncomp][NG][32] global output rows

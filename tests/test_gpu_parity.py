@@ -285,6 +285,61 @@ def test_rn_random_weights_grouped(sd):
         assert_parity(cg, Yg, cats, Y)
 
 
+def _pair_layer(n, w, bias):
+    """Column j has sources j and j^1 (a group of 2 per pair) with weights
+    (+w, -w) when w is a pair of values, or uniform w; bias per column."""
+    from types import SimpleNamespace
+    ell = np.stack([np.arange(n) & ~1, np.arange(n) | 1], 1).astype(np.int32)
+    rows = np.repeat(np.arange(n), 2)                       # CSR row k feeds columns k&~1, k|1
+    cols = np.stack([np.arange(n) & ~1, np.arange(n) | 1], 1).reshape(-1).astype(np.int32)
+    rowptr = np.arange(0, 2 * n + 1, 2, dtype=np.int64)
+    if np.ndim(w) == 0:
+        val = ell_val = None
+        uni = float(w)
+    else:
+        # W[k][j]: +w0 if k is even, -w0 if k is odd (for both columns of the pair)
+        val = np.where(rows % 2 == 0, w[0], w[1]).astype(np.float32)
+        ell_val = np.tile(np.array([w[0], w[1]], np.float32), (n, 1))
+        uni = 0.0
+    return SimpleNamespace(rowptr=rowptr, colidx=cols, val=val, uniform=uni,
+                           bias=np.asarray(bias, np.float32), ell=ell, ell_val=ell_val)
+
+
+def test_signed_zero_and_exact_cancellation(sd):
+    """The 2-FMNMX clamp and the max-bias liveness test rely on z never being
+    -0 (A6 note): exact cancellations (+w, -w on equal inputs),
+    -0.0 biases, -0.0 and negative inputs, through the general (per-slot) and
+    uniform kernels, fused and unfused.  Outputs and categories bit-exact."""
+    n, B = 256, 97
+    r = np.random.default_rng(2026)
+    dense = np.zeros((B, n), np.float32)
+    for i in range(B):
+        for k in range(0, n, 2):
+            u = r.random()
+            if u < 0.3:
+                dense[i, k] = dense[i, k + 1] = np.float32(r.choice([0.5, 1.25, 3.0]))   # cancels
+            elif u < 0.4:
+                dense[i, k] = -0.0
+                dense[i, k + 1] = np.float32(r.uniform(0, 2))
+            elif u < 0.5:
+                dense[i, k] = np.float32(r.uniform(-1, 2))
+    rp, idx, val = g.csr_from_dense(dense)
+    val[r.random(val.size) < 0.05] = -0.0
+    bias_negzero = np.full(n, -0.0, np.float32)
+    bias_mixed = np.where(np.arange(n) % 3 == 0, -0.0, -0.125).astype(np.float32)
+    layers = [_pair_layer(n, (0.75, -0.75), bias_negzero), _pair_layer(n, 0.5, bias_mixed),
+              _pair_layer(n, 2.0, bias_mixed), _pair_layer(n, (1.0, -1.0), bias_negzero),
+              _pair_layer(n, 0.25, bias_mixed), _pair_layer(n, 1.5, bias_negzero)]
+    assert sd.sdnn_plan_steps(n, layers) == [1, 2, 1, 2]            # fused uniform pairs
+    cats, Y, _ = oracle.infer(n, layers, rp, idx, val)
+    assert 0 < cats.sum() < B
+    for flags, fr in ((0, -1), (0, 0), (2, -1), (4, -1)):
+        cg, Yg, _ = run_gpu(sd, n, layers, rp, idx, val, flags=flags | sd.SDNN_F_NO_RESIDENT, fuse_rows=fr)
+        assert_parity(cg, Yg, cats, Y)
+    cg, Yg, _ = run_gpu(sd, n, layers, rp, idx, val, resident_from=0)
+    assert_parity(cg, Yg, cats, Y)
+
+
 @pytest.mark.parametrize("B", [1, 31, 33, 127, 129, 1000, 4097])
 def test_ragged_batches(sd, B):
     n, L = 1024, 16
