@@ -200,7 +200,8 @@ def run_gpu(args):
     t0 = time.time()
     net = sd.Net.from_spec(spec, fmt="ell", threads=args.load_threads, device=local,
                            flags=sd.SDNN_F_PROFILE | lib_flags(sd, args.flags),
-                           fuse_rows=args.fuse_rows, fuse_layers=args.fuse_layers)
+                           fuse_rows=args.fuse_rows, fuse_layers=args.fuse_layers,
+                           stream_slots=args.stream_slots)
     t_load = time.time() - t0
     if args.scaling == "strong" and ws > 1:
         # one global batch, contiguous word-aligned slices (dist.partition)
@@ -345,6 +346,8 @@ def run_gpu(args):
             "flags": args.flags or None,
             "fuse": {"rows": args.fuse_rows, "layers": args.fuse_layers,
                      "steps": len(plan), "fused_layers": st["fused_layers"]},
+            "weight_streaming": ({"slots": args.stream_slots, "h2d_bytes_per_step": st["stream_bytes"],
+                                  "slot_bytes": st["stream_slot_bytes"]} if args.stream_slots else None),
         }
         print(json.dumps(line), flush=True)
     net.close()
@@ -361,7 +364,7 @@ def run_oneshot(args):
     n, L, B = CONFIGS[args.config]
     net = sd.Net.from_spec(g.rn_spec(n, L), fmt="ell", threads=args.load_threads, device=0,
                            flags=lib_flags(sd, args.flags), fuse_rows=args.fuse_rows,
-                           fuse_layers=args.fuse_layers)
+                           fuse_layers=args.fuse_layers, stream_slots=args.stream_slots)
     rp, idx = make_inputs(n, B, 0)
     rp_t, idx_t = torch.from_numpy(rp).cuda(), torch.from_numpy(idx).cuda()
     for _ in range(args.warmup + args.steps):
@@ -389,6 +392,8 @@ def main():
     ap.add_argument("--fuse-rows", type=int, default=-1,
                     help="component cap for fused multi-layer passes (0 = off, -1 = library default)")
     ap.add_argument("--fuse-layers", type=int, default=-1)
+    ap.add_argument("--stream-slots", type=int, default=0,
+                    help="f3 weight streaming: ring of S device slots (0 = weights resident)")
     ap.add_argument("--flags", default="",
                     help="comma list of library flags, e.g. no_graph,no_bulk (f1 studies)")
     ap.add_argument("--oneshot", action="store_true",

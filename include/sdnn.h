@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define SDNN_ABI_VERSION 1
+#define SDNN_ABI_VERSION 2
 
 typedef struct sdnn_net sdnn_net;
 typedef int32_t sdnn_status;
@@ -113,7 +113,18 @@ typedef struct sdnn_opts {
                           (earlier layers stream with dead-row compaction);
                           -1 = 24 when L > 32 (else off); >= L or SDNN_F_NO_RESIDENT
                           = off                                                      */
-} sdnn_opts;        /* opts = NULL means {-1, 0, 32.0f, NULL, -1, -1, -1}              */
+  int32_t stream_slots; /* weight streaming (the paper streams weight
+                          partitions because "preloading ... is impossible",
+                          PAPER.md:2560-2569).  0 = every packed layer and pass
+                          descriptor resident in HBM.  S >= 1: they stay in pinned
+                          host memory and each step's block is copied into a ring
+                          of S device slots on a copy stream, step i+S's copy
+                          issued as soon as step i's kernel has released its slot,
+                          so the upload of later steps overlaps the compute of
+                          earlier ones (inside the same captured graph).  Device
+                          footprint: S x the largest step block.  The SMEM-resident
+                          tail is not used in this mode.  Results are identical. */
+} sdnn_opts;        /* opts = NULL means {-1, 0, 32.0f, NULL, -1, -1, -1, 0}           */
 
 /* Create a network handle and load all L layers.
  *   neurons  N, 1 <= N <= 65536 on this build (u16 source indices); larger N
@@ -187,6 +198,9 @@ typedef struct sdnn_stats {
   int32_t fused_layers;       /* layers executed inside fused multi-layer passes         */
   int32_t resident_layers;    /* layers executed by the SMEM-resident kernel             */
   int64_t retired_rows;       /* SDNN_F_SATURATE: rows retired as saturated categories    */
+  int64_t stream_bytes;       /* stream_slots > 0: host->device weight bytes per inference
+                                 (0 when every layer is resident)                        */
+  int64_t stream_slot_bytes;  /* stream_slots > 0: device bytes of one ring slot            */
 } sdnn_stats;
 
 /* live_rows: NULL or [layers] receives the number of rows still nonzero after

@@ -53,7 +53,7 @@ class sdnn_opts(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int32), ("flags", ctypes.c_uint32),
                 ("ymax", ctypes.c_float), ("stream", ctypes.c_void_p),
                 ("fuse_rows", ctypes.c_int32), ("fuse_layers", ctypes.c_int32),
-                ("resident_from", ctypes.c_int32)]
+                ("resident_from", ctypes.c_int32), ("stream_slots", ctypes.c_int32)]
 
 
 class sdnn_layer_info(ctypes.Structure):
@@ -72,7 +72,8 @@ class sdnn_stats(ctypes.Structure):
                 ("launches_per_infer", ctypes.c_int64), ("live_edges", ctypes.c_int64),
                 ("kept_rows", ctypes.c_int64), ("steps", ctypes.c_int32),
                 ("fused_layers", ctypes.c_int32), ("resident_layers", ctypes.c_int32),
-                ("retired_rows", ctypes.c_int64)]
+                ("retired_rows", ctypes.c_int64), ("stream_bytes", ctypes.c_int64),
+                ("stream_slot_bytes", ctypes.c_int64)]
 
 
 _LIB = None
@@ -121,9 +122,9 @@ def _p(a: Optional[np.ndarray]):
 
 
 def _opts(device=-1, flags=0, ymax=32.0, stream=None, fuse_rows=-1, fuse_layers=-1,
-          resident_from=-1):
+          resident_from=-1, stream_slots=0):
     return sdnn_opts(int(device), int(flags), float(ymax), stream, int(fuse_rows),
-                     int(fuse_layers), int(resident_from))
+                     int(fuse_layers), int(resident_from), int(stream_slots))
 
 
 def make_layer(layer, fmt: str = "csr"):
@@ -153,7 +154,7 @@ def make_layer(layer, fmt: str = "csr"):
 
 def sdnn_create(neurons: int, layers: Sequence, bias: np.ndarray, fmt: str = "csr",
                 device: int = -1, flags: int = 0, ymax: float = 32.0, fuse_rows: int = -1,
-                fuse_layers: int = -1, resident_from: int = -1):
+                fuse_layers: int = -1, resident_from: int = -1, stream_slots: int = 0):
     L = len(layers)
     descs = (sdnn_layer * max(L, 1))()
     keep = []
@@ -162,16 +163,16 @@ def sdnn_create(neurons: int, layers: Sequence, bias: np.ndarray, fmt: str = "cs
         keep.append(k)
     bias = np.ascontiguousarray(bias, np.float32).reshape(-1)
     h = ctypes.c_void_p()
-    o = _opts(device, flags, ymax, None, fuse_rows, fuse_layers, resident_from)
+    o = _opts(device, flags, ymax, None, fuse_rows, fuse_layers, resident_from, stream_slots)
     _check(lib().sdnn_create(neurons, L, descs, _p(bias), ctypes.byref(o), ctypes.byref(h)))
     return h
 
 
 def sdnn_create_empty(neurons: int, layers: int, device: int = -1, flags: int = 0,
                       ymax: float = 32.0, fuse_rows: int = -1, fuse_layers: int = -1,
-                      resident_from: int = -1):
+                      resident_from: int = -1, stream_slots: int = 0):
     h = ctypes.c_void_p()
-    o = _opts(device, flags, ymax, None, fuse_rows, fuse_layers, resident_from)
+    o = _opts(device, flags, ymax, None, fuse_rows, fuse_layers, resident_from, stream_slots)
     _check(lib().sdnn_create_empty(neurons, layers, ctypes.byref(o), ctypes.byref(h)))
     return h
 
@@ -256,11 +257,11 @@ class Net:
 
     def __init__(self, neurons: int, layers: int, flags: int = 0, ymax: float = 32.0,
                  device: int = -1, fuse_rows: int = -1, fuse_layers: int = -1,
-                 resident_from: int = -1):
+                 resident_from: int = -1, stream_slots: int = 0):
         self.n, self.L = int(neurons), int(layers)
         self.h = sdnn_create_empty(self.n, self.L, device=device, flags=flags, ymax=ymax,
                                    fuse_rows=fuse_rows, fuse_layers=fuse_layers,
-                                   resident_from=resident_from)
+                                   resident_from=resident_from, stream_slots=stream_slots)
 
     @classmethod
     def from_layers(cls, neurons: int, layers: Sequence, fmt: str = "csr", **kw):

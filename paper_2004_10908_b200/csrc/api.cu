@@ -67,7 +67,7 @@ struct Arena {
 
 struct sdnn_net {
   int32_t n = 0, L = 0;
-  sdnn_opts opts{-1, 0u, 32.f, nullptr, -1, -1, -1};
+  sdnn_opts opts{-1, 0u, 32.f, nullptr, -1, -1, -1, 0};
   int device = 0;
   cudaStream_t own = nullptr;
   Arena arena;
@@ -93,6 +93,17 @@ struct sdnn_net {
   int32_t resident_layers = 0;
   ResLayerDev *d_res = nullptr;        // device table for the resident step (pass_arena)
   std::vector<uint8_t> sat_suffix;     // f2: layers [l, L) all saturation-preserving
+  // f3 weight streaming (opts.stream_slots > 0): every step's weight block in one
+  // pinned host buffer, copied into a ring of device slots during the chain
+  std::vector<DevLayer> step_dl;       // per step: layer view into its slot
+  unsigned char *h_wblob = nullptr;
+  std::vector<size_t> wb_off, wb_bytes;
+  unsigned char *d_slots = nullptr;    // [stream_slots][slot_bytes] (pass_arena)
+  size_t slot_bytes = 0;
+  int64_t stream_bytes = 0;
+  cudaStream_t copy_s = nullptr;
+  std::vector<cudaEvent_t> ev_ready, ev_done;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // captured layer chain
   cudaGraphExec_t chain = nullptr;
   bool chain_compact = false;
@@ -135,8 +146,9 @@ bool compact_enabled(const sdnn_net *net) {
 }
 
 sdnn_status check_opts(const sdnn_opts *o, sdnn_opts &out) {
-  out = sdnn_opts{-1, 0u, 32.f, nullptr, -1, -1, -1};
+  out = sdnn_opts{-1, 0u, 32.f, nullptr, -1, -1, -1, 0};
   if (o) out = *o;
+  if (out.stream_slots < 0 || out.stream_slots > 64) return fail(SDNN_E_ARG, "stream_slots must be in [0, 64]");
   if (out.fuse_rows > kMaxPassRows) out.fuse_rows = kMaxPassRows;
   if (out.fuse_layers > kMaxPassLayers) return fail(SDNN_E_ARG, "fuse_layers > 16");
   if (!(out.ymax > 0.f) || !std::isfinite(out.ymax)) return fail(SDNN_E_ARG, "ymax must be finite and > 0");
@@ -229,6 +241,109 @@ int nthreads_default() {
   return (int)std::max(1u, std::min(h, 32u));
 }
 
+bool weight_streaming(const sdnn_net *net) { return net->opts.stream_slots > 0; }
+
+void free_stream(sdnn_net *net) {
+  if (net->h_wblob) cudaFreeHost(net->h_wblob);
+  net->h_wblob = nullptr;
+  for (auto e : net->ev_ready) cudaEventDestroy(e);
+  for (auto e : net->ev_done) cudaEventDestroy(e);
+  net->ev_ready.clear();
+  net->ev_done.clear();
+  net->d_slots = nullptr;                          // lives in pass_arena
+  net->slot_bytes = 0;
+  net->stream_bytes = 0;
+}
+
+constexpr size_t kBlobAlign = 256;
+size_t blob_align(size_t x) { return (x + kBlobAlign - 1) & ~(kBlobAlign - 1); }
+
+// f3: lay out every step's weight block (a layer's packed arrays or a fused
+// pass's row lists and records) in one pinned host buffer; point the per-step
+// device views into ring slot (step mod S)
+sdnn_status build_stream_blobs(sdnn_net *net, const std::vector<PassHost> &ph) {
+  const int ns = (int)net->steps.size();
+  const int S = net->opts.stream_slots;
+  net->wb_off.assign(ns, 0);
+  net->wb_bytes.assign(ns, 0);
+  net->step_dl.assign(ns, DevLayer{});
+  // per-step part sizes
+  struct Part { const void *h; size_t bytes; };
+  std::vector<std::vector<Part>> parts(ns);
+  for (int i = 0; i < ns; ++i) {
+    const Step &S_ = net->steps[i];
+    if (S_.m == 1) {
+      const PackedLayer &p = net->host[S_.a];
+      parts[i] = {{p.src.data(), p.src.size() * 2}, {p.col.data(), p.col.size() * 4},
+                  {p.gk.data(), p.gk.size() * 4}, {p.gg.data(), p.gg.size() * 4},
+                  {p.val.data(), p.uniform ? 0 : p.val.size() * 4}, {p.bias.data(), p.bias.size() * 4}};
+    } else {
+      const PassHost &H = ph[i];
+      parts[i] = {{H.in_rows.data(), H.in_rows.size() * 4}, {H.in_count.data(), H.in_count.size() * 4},
+                  {H.rec.data(), H.rec.size()}};
+    }
+  }
+  size_t total = 0, smax = 0;
+  for (int i = 0; i < ns; ++i) {
+    size_t b = 0;
+    for (auto &q : parts[i]) b += blob_align(q.bytes);
+    net->wb_off[i] = total;
+    net->wb_bytes[i] = b;
+    total += b;
+    smax = std::max(smax, b);
+  }
+  if (cudaHostAlloc((void **)&net->h_wblob, std::max<size_t>(total, 1), cudaHostAllocDefault) != cudaSuccess) {
+    cudaGetLastError();
+    net->h_wblob = nullptr;
+    return fail(SDNN_E_NOMEM, "pinned host allocation for weight streaming failed");
+  }
+  void *d = nullptr;
+  if (net->pass_arena.alloc(std::max<size_t>(smax, 1) * S, &d) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(SDNN_E_NOMEM, "device allocation for the weight-streaming ring failed");
+  }
+  net->d_slots = (unsigned char *)d;
+  net->slot_bytes = smax;
+  net->stream_bytes = (int64_t)total;
+  for (int i = 0; i < ns; ++i) {
+    unsigned char *h = net->h_wblob + net->wb_off[i];
+    unsigned char *dv = net->d_slots + (size_t)(i % S) * smax;
+    std::vector<unsigned char *> at;
+    size_t o = 0;
+    for (auto &q : parts[i]) {
+      if (q.bytes) std::memcpy(h + o, q.h, q.bytes);
+      at.push_back(q.bytes ? dv + o : nullptr);
+      o += blob_align(q.bytes);
+    }
+    const Step &S_ = net->steps[i];
+    if (S_.m == 1) {
+      DevLayer dl = net->dl[S_.a];                 // metadata (sizes, uniform value)
+      dl.src = (const uint16_t *)at[0];
+      dl.col = (const int32_t *)at[1];
+      dl.gk = (const int32_t *)at[2];
+      dl.gg = (const int32_t *)at[3];
+      dl.val = net->host[S_.a].uniform ? nullptr : (const float *)at[4];
+      dl.bias = (const float *)at[5];
+      net->step_dl[i] = dl;
+    } else {
+      DevPass &D = net->passes[S_.pass];
+      D.in_rows = (const int32_t *)at[0];
+      D.in_count = (const int32_t *)at[1];
+      D.rec = (const unsigned char *)at[2];
+    }
+  }
+  net->ev_ready.resize(ns);
+  net->ev_done.resize(ns);
+  for (int i = 0; i < ns; ++i) {
+    CK(cudaEventCreateWithFlags(&net->ev_ready[i], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&net->ev_done[i], cudaEventDisableTiming));
+  }
+  if (!net->copy_s) CK(cudaStreamCreateWithFlags(&net->copy_s, cudaStreamNonBlocking));
+  if (!net->ev_fork) CK(cudaEventCreateWithFlags(&net->ev_fork, cudaEventDisableTiming));
+  if (!net->ev_join) CK(cudaEventCreateWithFlags(&net->ev_join, cudaEventDisableTiming));
+  return SDNN_OK;
+}
+
 // Plan the steps (fused passes where the component cap allows) and upload the
 // pass descriptors.  Create-time work, redone only when layers change.
 sdnn_status make_plan(sdnn_net *net) {
@@ -244,7 +359,8 @@ sdnn_status make_plan(sdnn_net *net) {
   int ar = net->L;
   std::vector<std::vector<unsigned char>> blobs;
   std::vector<ResLayerDev> rl;
-  if (!(net->opts.flags & (SDNN_F_NO_RESIDENT | SDNN_F_SATURATE)) && resident_positions(net->n) > 0) {
+  if (!(net->opts.flags & (SDNN_F_NO_RESIDENT | SDNN_F_SATURATE)) && !weight_streaming(net) &&
+      resident_positions(net->n) > 0) {
     int a0 = net->opts.resident_from >= 0 ? net->opts.resident_from : (net->L > 32 ? 24 : net->L);
     a0 = std::min(a0, net->L);
     bool ok = a0 < net->L;
@@ -259,8 +375,10 @@ sdnn_status make_plan(sdnn_net *net) {
   std::vector<PassHost> ph;
   net->steps = plan_passes(head, net->n, cap, maxm, pass_tile_floats(), nthreads_default(), &ph);
   net->pass_arena.release();
+  free_stream(net);
   net->passes.clear();
   net->fused_layers = 0;
+  const bool streaming = weight_streaming(net);
   auto up = [&](const void *h, size_t bytes, void **d) -> sdnn_status {
     cudaError_t e = net->pass_arena.alloc(std::max<size_t>(bytes, 4), d);
     if (e != cudaSuccess) {
@@ -281,15 +399,17 @@ sdnn_status make_plan(sdnn_net *net) {
     D.R = H.R;
     D.T = H.T;
     D.rec_bytes = H.rec_bytes;
-    void *p1, *p2, *p3;
-    sdnn_status st;
-    if ((st = up(H.in_rows.data(), H.in_rows.size() * 4, &p1)) ||
-        (st = up(H.in_count.data(), H.in_count.size() * 4, &p2)) ||
-        (st = up(H.rec.data(), H.rec.size(), &p3)))
-      return st;
-    D.in_rows = (const int32_t *)p1;
-    D.in_count = (const int32_t *)p2;
-    D.rec = (const unsigned char *)p3;
+    if (!streaming) {                            // else: pointers into the slot ring
+      void *p1, *p2, *p3;
+      sdnn_status st;
+      if ((st = up(H.in_rows.data(), H.in_rows.size() * 4, &p1)) ||
+          (st = up(H.in_count.data(), H.in_count.size() * 4, &p2)) ||
+          (st = up(H.rec.data(), H.rec.size(), &p3)))
+        return st;
+      D.in_rows = (const int32_t *)p1;
+      D.in_count = (const int32_t *)p2;
+      D.rec = (const unsigned char *)p3;
+    }
     for (int j = 0; j < H.m; ++j) {
       const PassHostLayer &HL = H.layers[j];
       D.layers[j] = PassLayerDev{HL.off_kg, HL.off_src, HL.off_bias, HL.off_orow, HL.NG, HL.wu};
@@ -297,6 +417,10 @@ sdnn_status make_plan(sdnn_net *net) {
     net->steps[q].pass = (int32_t)net->passes.size();
     net->passes.push_back(D);
     net->fused_layers += H.m;
+  }
+  if (streaming) {
+    sdnn_status st2 = build_stream_blobs(net, ph);
+    if (st2) return st2;
   }
   // SMEM-resident tail: layers [ar, L) in one persistent kernel when the width fits
   net->resident_layers = 0;
@@ -335,9 +459,26 @@ void enqueue_chain(sdnn_net *net, bool compact, cudaStream_t s, int64_t *launche
   const Workspace &w = net->ws;
   const int ns = (int)net->steps.size();
   int64_t c = 0;
+  // f3: the copy stream forks from s; step j's block goes into slot j mod S once
+  // step j - S has released it; step j waits for its own block
+  const bool streaming = weight_streaming(net);
+  const int nslot = net->opts.stream_slots;
+  auto issue_copy = [&](int j) {
+    if (j >= ns) return;
+    if (j >= nslot) cudaStreamWaitEvent(net->copy_s, net->ev_done[j - nslot], 0);
+    cudaMemcpyAsync(net->d_slots + (size_t)(j % nslot) * net->slot_bytes, net->h_wblob + net->wb_off[j],
+                    net->wb_bytes[j], cudaMemcpyHostToDevice, net->copy_s);
+    cudaEventRecord(net->ev_ready[j], net->copy_s);
+  };
+  if (streaming) {
+    cudaEventRecord(net->ev_fork, s);
+    cudaStreamWaitEvent(net->copy_s, net->ev_fork, 0);
+    for (int j = 0; j < nslot; ++j) issue_copy(j);
+  }
   for (int si = 0; si < ns; ++si) {
     const Step &S = net->steps[si];
     const bool last = si + 1 == ns;
+    if (streaming) cudaStreamWaitEvent(s, net->ev_ready[si], 0);
     if (prof) cudaEventRecordWithFlags(net->ev_before[S.a], s, evflags);
     if (S.pass == kResidentStep) {            // always the last step
       launch_resident(w, net->d_res, S.a, net->L, net->n, w.alive_row(si, 0), compact, ymax, s);
@@ -345,14 +486,18 @@ void enqueue_chain(sdnn_net *net, bool compact, cudaStream_t s, int64_t *launche
       c += 2;
       continue;
     }
+    const DevLayer &dl = streaming ? net->step_dl[si] : net->dl[S.a];
     const bool sat = (net->opts.flags & SDNN_F_SATURATE) && S.m == 1 &&
-                     layer_tracks_saturation(net->cfg, net->dl[S.a]);
+                     layer_tracks_saturation(net->cfg, dl);
     if (S.m == 1)
-      launch_layer(net->cfg, w, net->dl[S.a], S.a, w.alive_row(si, 0), ymax, s,
-                   sat ? w.sat[si & 1] : nullptr);
+      launch_layer(net->cfg, w, dl, S.a, w.alive_row(si, 0), ymax, s, sat ? w.sat[si & 1] : nullptr);
     else
       launch_pass(net->cfg, w, net->passes[S.pass], w.alive_set(si), ymax, s);
     if (prof) cudaEventRecordWithFlags(net->ev_after[S.a], s, evflags);
+    if (streaming) {                              // slot si mod S is free again
+      cudaEventRecord(net->ev_done[si], s);
+      issue_copy(si + nslot);
+    }
     // survivor counts for every layer of the step; compaction between steps;
     // f2: retire rows saturated before a saturation-preserving suffix
     const bool retire = sat && net->sat_suffix[S.a + 1];
@@ -364,6 +509,10 @@ void enqueue_chain(sdnn_net *net, bool compact, cudaStream_t s, int64_t *launche
       launch_compact_copy(net->cfg, w, S.a, S.m, w.alive_row(si, S.m - 1), net->n, s);
       ++c;
     }
+  }
+  if (streaming) {                                // join the copy stream back
+    cudaEventRecord(net->ev_join, net->copy_s);
+    cudaStreamWaitEvent(s, net->ev_join, 0);      // (memcpy nodes are not kernel launches)
   }
   if (launches) *launches = c;
 }
@@ -604,9 +753,10 @@ sdnn_status sdnn_set_layer(sdnn_net *net, int32_t l, const sdnn_layer *W, const 
   };
   DevLayer d{};
   void *ps = nullptr, *pc = nullptr, *pk = nullptr, *pg = nullptr, *pv = nullptr, *pb = nullptr;
-  if ((st = up(p.src.data(), b_src, &ps)) || (st = up(p.col.data(), b_col, &pc)) ||
-      (st = up(p.gk.data(), b_gk, &pk)) || (st = up(p.gg.data(), b_gk, &pg)) ||
-      (st = up(p.val.data(), b_val, &pv)) || (st = up(p.bias.data(), b_bias, &pb)))
+  if (!weight_streaming(net) &&                   // f3: the blocks stay on the host
+      ((st = up(p.src.data(), b_src, &ps)) || (st = up(p.col.data(), b_col, &pc)) ||
+       (st = up(p.gk.data(), b_gk, &pk)) || (st = up(p.gg.data(), b_gk, &pg)) ||
+       (st = up(p.val.data(), b_val, &pv)) || (st = up(p.bias.data(), b_bias, &pb))))
     return st;
   d.src = (const uint16_t *)ps;
   d.col = (const int32_t *)pc;
@@ -877,6 +1027,8 @@ sdnn_status sdnn_stats_get(const sdnn_net *cnet, sdnn_stats *out, int64_t *live_
   s.max_k = net->max_k;
   s.compaction = compact_enabled(net) ? 1 : 0;
   s.packed_weight_bytes = (int64_t)net->arena.total;
+  s.stream_bytes = weight_streaming(net) ? net->stream_bytes : 0;
+  s.stream_slot_bytes = weight_streaming(net) ? (int64_t)net->slot_bytes : 0;
   for (int l = 0; l < net->L; ++l) s.total_nnz += net->nnz[l];
   s.last_batch = net->last_batch;
   s.last_n_categories = net->last_ncat;
@@ -913,7 +1065,11 @@ void sdnn_destroy(sdnn_net *net) {
   cudaDeviceSynchronize();
   free_ws(net);
   net->arena.release();
+  free_stream(net);
   net->pass_arena.release();
+  if (net->copy_s) cudaStreamDestroy(net->copy_s);
+  if (net->ev_fork) cudaEventDestroy(net->ev_fork);
+  if (net->ev_join) cudaEventDestroy(net->ev_join);
   cudaFree(net->d_rowptr);
   cudaFree(net->d_idx);
   cudaFree(net->d_val);

@@ -36,7 +36,32 @@ def test_exports_every_declared_symbol(sd):
     for name in declared:
         assert hasattr(L, name), name
     assert sorted(sd.EXPORTS) == declared
-    assert L.sdnn_abi_version() == 1
+    assert L.sdnn_abi_version() == 2
+
+
+def test_struct_layouts_match_header(sd, tmp_path):
+    """The ctypes mirrors of sdnn_layer / sdnn_opts / sdnn_stats /
+    sdnn_layer_info have the C header's size and field offsets (compiled with
+    gcc against include/sdnn.h)."""
+    import ctypes
+    import subprocess
+    structs = {"sdnn_layer": sd.sdnn_layer, "sdnn_opts": sd.sdnn_opts, "sdnn_stats": sd.sdnn_stats,
+               "sdnn_layer_info": sd.sdnn_layer_info}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "sdnn.h"', "int main(void) {"]
+    for name, cls in structs.items():
+        lines.append(f'  printf("{name} %zu\\n", sizeof({name}));')
+        for f, _ in cls._fields_:
+            lines.append(f'  printf("{name}.{f} %zu\\n", offsetof({name}, {f}));')
+    lines += ["  return 0;", "}"]
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)])
+    got = dict(l.split() for l in subprocess.check_output([str(exe)]).decode().splitlines())
+    for name, cls in structs.items():
+        assert int(got[name]) == ctypes.sizeof(cls), name
+        for f, _ in cls._fields_:
+            assert int(got[f"{name}.{f}"]) == getattr(cls, f).offset, f"{name}.{f}"
 
 
 def test_destroy_null_is_safe(sd):

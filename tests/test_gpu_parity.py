@@ -32,9 +32,10 @@ def assert_parity(cats_gpu, Y_gpu, cats_or, Y_or):
 
 
 def run_gpu(sd, n, layers, rp, idx, val, fmt="csr", flags=0, ymax=32.0, want_y=True,
-            fuse_rows=-1, fuse_layers=-1, resident_from=-1):
+            fuse_rows=-1, fuse_layers=-1, resident_from=-1, stream_slots=0):
     with sd.Net.from_layers(n, layers, fmt=fmt, flags=flags, ymax=ymax, fuse_rows=fuse_rows,
-                            fuse_layers=fuse_layers, resident_from=resident_from) as net:
+                            fuse_layers=fuse_layers, resident_from=resident_from,
+                            stream_slots=stream_slots) as net:
         cats, Y = net.infer(rp, idx, val, want_y=want_y)
         st = net.stats()
     return cats, Y, st
@@ -187,6 +188,46 @@ def test_fused_record_split_and_singletons(sd):
         assert st["fused_layers"] > 0
         assert_parity(cg, Yg, cats, Y)
         assert st["live_rows"] == prof
+
+
+# ---------------------------------------------------------------------------
+# f3: weight streaming through a ring of device slots (stream_slots > 0)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("slots", [1, 2, 3])
+@pytest.mark.parametrize("flags", [0, 4])
+def test_weight_streaming_c1(sd, c1, slots, flags):
+    """Fused passes and single layers with their weight blocks copied into S
+    slots during the chain (graph and stream loop): bit-exact, and every step's
+    block crosses the host link once per inference."""
+    spec, layers, rp, idx, cats, Y, prof = c1
+    cg, Yg, st = run_gpu(sd, 1024, layers, rp, idx, None, fmt="ell", flags=flags, stream_slots=slots)
+    assert_parity(cg, Yg, cats, Y)
+    assert st["live_rows"] == prof
+    assert st["resident_layers"] == 0 and st["fused_layers"] > 0
+    assert st["stream_bytes"] > 0 and st["packed_weight_bytes"] == 0
+    assert 0 < st["stream_slot_bytes"] < st["stream_bytes"]
+
+
+def test_weight_streaming_general_and_saturate(sd):
+    """Per-slot weights (general kernel) and f2 saturation tracking read their
+    arrays from the slot ring; repeated inferences reuse the captured graph."""
+    n, L = 300, 7
+    spec = g.random_spec(n, L, seed=91, kmin=0, kmax=40, bias=(-0.3, 0.0))
+    layers = list(g.iter_layers(spec))
+    rp, idx, val = g.random_inputs(n, 257, seed=92)
+    cats, Y, _ = oracle.infer(n, layers, rp, idx, val)
+    with sd.Net.from_layers(n, layers, stream_slots=2) as net:
+        for _ in range(3):
+            cg, Yg = net.infer(rp, idx, val, want_y=True)
+            assert_parity(cg, Yg, cats, Y)
+    spec = g.rn_spec(1024, 40)
+    layers = list(g.iter_layers(spec))
+    rp, idx = g.ms_inputs(1024, 640, seed=93)
+    cats, Y, _ = oracle.infer(1024, layers, rp, idx, None)
+    cg, Yg, st = run_gpu(sd, 1024, layers, rp, idx, None, fmt="ell", flags=sd.SDNN_F_SATURATE,
+                         stream_slots=2)
+    assert_parity(cg, Yg, cats, Y)
+    assert st["retired_rows"] > 0
 
 
 # ---------------------------------------------------------------------------
