@@ -103,10 +103,15 @@ typedef struct sdnn_opts {
   float ymax;       /* clip value YMAX (> 0, finite); north_star: 32                   */
   void *stream;     /* cudaStream_t for sdnn_infer (NULL = a stream owned by the net) */
   int32_t fuse_rows;   /* multi-layer passes ("model decomposition"):
-                          consecutive uniform layers are fused while every connected
-                          component of their union has <= fuse_rows neurons on every
-                          layer boundary (<= 128, larger values are clamped; 0 =
-                          off; -1 = 128)                                            */
+                          consecutive uniform layers run as one pass over the
+                          connected components of their union.  All layers but the
+                          last stay inside one CTA (sub-components of <= 128
+                          neurons, updated in place in shared memory); the last
+                          layer reads across a thread-block cluster of up to
+                          fuse_rows / 128 CTAs (distributed shared memory), so a
+                          component has <= fuse_rows neurons (<= 512, larger
+                          values are clamped; <= 128: single-CTA passes; 0 = off;
+                          -1 = 512)                                                */
   int32_t fuse_layers; /* at most this many layers per pass (<= 16; -1 = 8)           */
   int32_t resident_from; /* N <= 4096: layers [resident_from, L) run in one kernel that
                           keeps each CTA's batch tile resident in shared memory

@@ -149,7 +149,7 @@ sdnn_status check_opts(const sdnn_opts *o, sdnn_opts &out) {
   out = sdnn_opts{-1, 0u, 32.f, nullptr, -1, -1, -1, 0};
   if (o) out = *o;
   if (out.stream_slots < 0 || out.stream_slots > 64) return fail(SDNN_E_ARG, "stream_slots must be in [0, 64]");
-  if (out.fuse_rows > kMaxPassRows) out.fuse_rows = kMaxPassRows;
+  if (out.fuse_rows > kMaxPassRows * kMaxPassCluster) out.fuse_rows = kMaxPassRows * kMaxPassCluster;
   if (out.fuse_layers > kMaxPassLayers) return fail(SDNN_E_ARG, "fuse_layers > 16");
   if (!(out.ymax > 0.f) || !std::isfinite(out.ymax)) return fail(SDNN_E_ARG, "ymax must be finite and > 0");
   return SDNN_OK;
@@ -231,7 +231,6 @@ sdnn_status ensure_ws(sdnn_net *net, int64_t batch) {
     CK(cudaMalloc(&w.nretired, sizeof(int32_t)));
     CK(cudaMalloc(&w.orig, sizeof(uint32_t) * w.words));
   }
-  encode_pass_maps(w, net->n);                  // row gathers for fused passes (optional)
   net->ws_cap = stride;
   return SDNN_OK;
 }
@@ -349,8 +348,9 @@ sdnn_status build_stream_blobs(sdnn_net *net, const std::vector<PassHost> &ph) {
 sdnn_status make_plan(sdnn_net *net) {
   if (!net->plan_dirty) return SDNN_OK;
   const bool sat = net->opts.flags & SDNN_F_SATURATE;
-  const int cap = sat ? 0 : std::min(net->opts.fuse_rows < 0 ? kMaxPassRows : net->opts.fuse_rows,
-                                     kMaxPassRows);
+  const int cap = sat ? 0 : std::min(net->opts.fuse_rows < 0 ? kMaxPassRows * kMaxPassCluster
+                                                              : net->opts.fuse_rows,
+                                     kMaxPassRows * kMaxPassCluster);
   net->sat_suffix.assign(net->L + 1, 1);
   for (int l = net->L - 1; l >= 0; --l)
     net->sat_suffix[l] = net->sat_suffix[l + 1] && saturation_preserving(net->host[l], net->opts.ymax);
@@ -398,6 +398,7 @@ sdnn_status make_plan(sdnn_net *net) {
     D.rin = H.rin;
     D.R = H.R;
     D.T = H.T;
+    D.C = H.C;
     D.rec_bytes = H.rec_bytes;
     if (!streaming) {                            // else: pointers into the slot ring
       void *p1, *p2, *p3;
@@ -1002,7 +1003,8 @@ sdnn_status sdnn_plan_steps(int32_t neurons, int32_t layers, const sdnn_layer *W
   for (int l = 0; l < layers; ++l) lp[l] = &host[l];
   const int cap = (o.flags & SDNN_F_SATURATE)
                       ? 0
-                      : std::min(o.fuse_rows < 0 ? kMaxPassRows : o.fuse_rows, kMaxPassRows);
+                      : std::min(o.fuse_rows < 0 ? kMaxPassRows * kMaxPassCluster : o.fuse_rows,
+                                 kMaxPassRows * kMaxPassCluster);
   const int maxm = o.fuse_layers < 0 ? 8 : o.fuse_layers;
   const std::vector<Step> steps = plan_passes(lp, neurons, cap, maxm, pass_tile_floats(), 1, nullptr);
   for (size_t i = 0; i < steps.size(); ++i) step_len[i] = steps[i].m;

@@ -87,31 +87,82 @@ bool within_cap(UF &uf, int32_t n, int m, int cap, std::vector<int32_t> &cnt,
   return true;
 }
 
+// first-fit-decreasing of the sub-component sizes of every full component into
+// bins of `cap_cta` slots; returns the largest bin count (0 if a sub-component
+// alone exceeds a bin)
+int bins_needed(UF &full, UF &sub, int32_t n, int cap_cta, std::vector<int32_t> &size,
+                std::vector<int32_t> &owner) {
+  // size[sub root] = rows at boundary 0; owner[] lists sub roots per full root
+  std::vector<std::pair<int32_t, int32_t>> roots;      // (full root, sub root)
+  for (int32_t i = 0; i < n; ++i) {
+    const int32_t sr = sub.find(i);
+    if (size[sr]++ == 0) roots.push_back({full.find(i), sr});
+  }
+  std::sort(roots.begin(), roots.end(), [&](const auto &x, const auto &y) {
+    return x.first != y.first ? x.first < y.first : size[x.second] > size[y.second];
+  });
+  int worst = 1;
+  std::vector<int32_t> bins;
+  for (size_t q = 0; q < roots.size();) {
+    size_t e = q;
+    bins.clear();
+    while (e < roots.size() && roots[e].first == roots[q].first) {
+      const int32_t sz = size[roots[e].second];
+      if (sz > cap_cta) worst = 0;
+      bool placed = false;
+      for (auto &b : bins)
+        if (b + sz <= cap_cta) {
+          b += sz;
+          placed = true;
+          break;
+        }
+      if (!placed) bins.push_back(sz);
+      ++e;
+    }
+    if (worst) worst = std::max<int>(worst, (int)bins.size());
+    q = e;
+  }
+  for (auto &r : roots) size[r.second] = 0;
+  (void)owner;
+  return worst;
+}
+
 }  // namespace
 
+// A pass [a, a+m) keeps every layer but the last inside one CTA: the
+// sub-components of layers a..a+m-2 must fit kMaxPassRows slots.  The last
+// layer may read across a cluster of up to kMaxPassCluster CTAs, so the
+// sub-components of a full component are bin-packed into at most
+// cap / kMaxPassRows CTAs (cap <= kMaxPassRows: one CTA of cap slots).
 std::vector<Step> plan_steps(const std::vector<const PackedLayer *> &layers, int32_t n, int cap,
                              int max_m) {
   std::vector<Step> steps;
   const int L = (int)layers.size();
   max_m = std::max(1, std::min(max_m, kMaxPassLayers));
-  UF uf;
-  std::vector<int32_t> cnt, stamp;
+  cap = std::min(cap, kMaxPassRows * kMaxPassCluster);
+  const int cap_cta = std::min(cap, kMaxPassRows);
+  const int max_bins = std::max(1, cap / kMaxPassRows);
+  UF full, sub;
+  std::vector<int32_t> cnt, stamp, size, owner;
   for (int a = 0; a < L;) {
     int m = 1;
     if (cap > 0 && max_m > 1 && fusable(*layers[a])) {
       const int64_t nodes = (int64_t)(max_m + 1) * n;
-      uf.init(nodes);
+      full.init(nodes);
+      sub.init(nodes);
       cnt.assign(nodes, 0);
       stamp.assign(nodes, 0);
-      add_layer(uf, *layers[a], n, 0);
-      if (within_cap(uf, n, 1, cap, cnt, stamp)) {
-        // layer a+m-1 stops being the last layer of the pass: it must allow in-place slots
-        while (a + m < L && m < max_m && fusable(*layers[a + m]) && inplace(*layers[a + m - 1])) {
-          add_layer(uf, *layers[a + m], n, m);
-          std::fill(stamp.begin(), stamp.end(), 0);
-          if (!within_cap(uf, n, m + 1, cap, cnt, stamp)) break;
-          ++m;
-        }
+      size.assign(nodes, 0);
+      add_layer(full, *layers[a], n, 0);
+      // layer a+m-1 stops being the last layer of the pass: it must allow in-place slots
+      while (a + m < L && m < max_m && fusable(*layers[a + m]) && inplace(*layers[a + m - 1])) {
+        add_layer(sub, *layers[a + m - 1], n, m - 1);
+        add_layer(full, *layers[a + m], n, m);
+        std::fill(stamp.begin(), stamp.end(), 0);
+        if (!within_cap(sub, n, m, cap_cta, cnt, stamp)) break;
+        const int nb = bins_needed(full, sub, n, cap_cta, size, owner);
+        if (nb == 0 || nb > max_bins) break;
+        ++m;
       }
     }
     Step s;
@@ -126,86 +177,136 @@ std::vector<Step> plan_steps(const std::vector<const PackedLayer *> &layers, int
 void build_pass(const std::vector<const PackedLayer *> &layers, int32_t n, const Step &s,
                 int tile_floats, PassHost &out) {
   const int m = s.m;
-  UF uf;
-  uf.init((int64_t)(m + 1) * n);
-  for (int b = 0; b < m; ++b) add_layer(uf, *layers[s.a + b], n, b);
+  UF full, sub;
+  full.init((int64_t)(m + 1) * n);
+  sub.init((int64_t)(m + 1) * n);
+  for (int b = 0; b < m; ++b) add_layer(full, *layers[s.a + b], n, b);
+  for (int b = 0; b + 1 < m; ++b) add_layer(sub, *layers[s.a + b], n, b);
   // components that own at least one group (have outputs); dense ids
   std::vector<int32_t> comp_of_root((size_t)(m + 1) * n, -1);
   int ncomp = 0;
   for (int b = 0; b < m; ++b) {
     const PackedLayer &p = *layers[s.a + b];
     for (int32_t g = 0; g < p.ngroups; ++g) {
-      const int32_t r = uf.find((int32_t)((int64_t)(b + 1) * n + p.col[(size_t)g * p.gmax]));
+      const int32_t r = full.find((int32_t)((int64_t)(b + 1) * n + p.col[(size_t)g * p.gmax]));
       if (comp_of_root[r] < 0) comp_of_root[r] = ncomp++;
     }
   }
-  // boundary-0 rows of each component -> smem slots 0..cnt-1 (ascending neuron id)
-  std::vector<int32_t> slot((size_t)(m + 1) * n, -1);
-  std::vector<std::vector<int32_t>> rows_in(ncomp);
-  for (int32_t i = 0; i < n; ++i) {
-    const int32_t c = comp_of_root[uf.find(i)];
-    if (c < 0) continue;                          // input neuron feeding nothing in this pass
-    slot[i] = (int32_t)rows_in[c].size();
-    rows_in[c].push_back(i);
+  // boundary-0 rows of each component, grouped by sub-component, bin-packed
+  // (first fit decreasing) into CTAs of kMaxPassRows slots
+  std::vector<std::vector<std::vector<int32_t>>> subs(ncomp);   // [comp][sub] rows
+  {
+    std::vector<int32_t> sub_idx((size_t)(m + 1) * n, -1);
+    for (int32_t i = 0; i < n; ++i) {
+      const int32_t c = comp_of_root[full.find(i)];
+      if (c < 0) continue;                        // input neuron feeding nothing in this pass
+      const int32_t sr = sub.find(i);
+      if (sub_idx[sr] < 0) {
+        sub_idx[sr] = (int32_t)subs[c].size();
+        subs[c].emplace_back();
+      }
+      subs[c][sub_idx[sr]].push_back(i);
+    }
   }
+  std::vector<std::vector<std::vector<int32_t>>> bins(ncomp);   // [comp][bin] rows
+  int C = 1, R = 1;
+  for (int c = 0; c < ncomp; ++c) {
+    auto &v = subs[c];
+    std::stable_sort(v.begin(), v.end(), [](const auto &x, const auto &y) { return x.size() > y.size(); });
+    for (auto &sv : v) {
+      bool placed = false;
+      for (auto &b : bins[c])
+        if ((int)(b.size() + sv.size()) <= kMaxPassRows) {
+          b.insert(b.end(), sv.begin(), sv.end());
+          placed = true;
+          break;
+        }
+      if (!placed) bins[c].push_back(sv);
+    }
+    for (auto &b : bins[c]) {
+      std::sort(b.begin(), b.end());              // slots in ascending neuron id
+      R = std::max<int>(R, (int)b.size());
+    }
+    C = std::max<int>(C, (int)bins[c].size());
+  }
+  if (C > 1) C = C <= 2 ? 2 : 4;                  // cluster sizes 2 / 4
+  // slot code of a boundary node: (bin << 8) | slot within the bin
+  std::vector<int32_t> slot((size_t)(m + 1) * n, -1);
+  std::vector<int32_t> bin_of_sub((size_t)(m + 1) * n, 0);
   out = PassHost();
   out.a = s.a;
   out.m = m;
   out.ncomp = ncomp;
-  int R = 1;
-  for (auto &v : rows_in) R = std::max<int>(R, (int)v.size());
+  out.C = C;
   out.R = R;
   out.rin = R;
-  int T = 512;                                    // one tile of tile_floats per component
+  int T = 512;                                    // one tile of tile_floats per CTA
   while (T > 128 && (int64_t)R * T > tile_floats) T >>= 1;
+  if (C > 1) T = 128;
   out.T = T;
-  out.in_rows.assign((size_t)ncomp * R, -1);
-  out.in_count.assign(ncomp, 0);
-  for (int c = 0; c < ncomp; ++c) {
-    std::copy(rows_in[c].begin(), rows_in[c].end(), out.in_rows.begin() + (size_t)c * R);
-    out.in_count[c] = (int32_t)rows_in[c].size();
-  }
+  out.in_rows.assign((size_t)ncomp * C * R, -1);
+  out.in_count.assign((size_t)ncomp * C, 0);
+  for (int c = 0; c < ncomp; ++c)
+    for (int b = 0; b < (int)bins[c].size(); ++b) {
+      const auto &rows = bins[c][b];
+      for (size_t q = 0; q < rows.size(); ++q) {
+        slot[rows[q]] = (b << 8) | (int32_t)q;
+        bin_of_sub[sub.find(rows[q])] = b;
+        out.in_rows[((size_t)c * C + b) * R + q] = rows[q];
+      }
+      out.in_count[(size_t)c * C + b] = (int32_t)rows.size();
+    }
   out.layers.resize(m);
   for (int b = 0; b < m; ++b) {
     const PackedLayer &p = *layers[s.a + b];
     const bool last = b == m - 1;
-    std::vector<std::vector<int32_t>> groups(ncomp);
+    // groups of each (component, bin): non-last layers by their sub-component's
+    // bin (all sources local), the last layer round robin over the bins
+    std::vector<std::vector<int32_t>> groups((size_t)ncomp * C);
+    std::vector<int32_t> rr(ncomp, 0);
     for (int32_t g = 0; g < p.ngroups; ++g) {
-      const int32_t c =
-          comp_of_root[uf.find((int32_t)((int64_t)(b + 1) * n + p.col[(size_t)g * p.gmax]))];
-      groups[c].push_back(g);
+      const int32_t node = (int32_t)((int64_t)(b + 1) * n + p.col[(size_t)g * p.gmax]);
+      const int32_t c = comp_of_root[full.find(node)];
+      const int bin = last ? (rr[c]++ % C) : bin_of_sub[sub.find(node)];
+      groups[(size_t)c * C + bin].push_back(g);
     }
     int NG = 1;
     for (auto &v : groups) NG = std::max<int>(NG, (int)v.size());
     PassHostLayer &H = out.layers[b];
     H.NG = NG;
     H.wu = p.wu;
-    H.src.assign((size_t)ncomp * NG * 32, 0);
-    H.bias.assign((size_t)ncomp * NG * 32, 0.f);
-    H.k.assign((size_t)ncomp * NG, 0);
-    H.g.assign((size_t)ncomp * NG, 0);
-    if (last) H.orow.assign((size_t)ncomp * NG * 32, 0);
+    const size_t units = (size_t)ncomp * C;
+    H.src.assign(units * NG * 32, 0);
+    H.bias.assign(units * NG * 32, 0.f);
+    H.k.assign(units * NG, 0);
+    H.g.assign(units * NG, 0);
+    if (last) H.orow.assign(units * NG * 32, 0);
     const int64_t in0 = (int64_t)b * n, out0 = (int64_t)(b + 1) * n;
-    for (int c = 0; c < ncomp; ++c)
-      for (size_t q = 0; q < groups[c].size(); ++q) {
-        const int32_t g = groups[c][q];
-        const size_t rec = (size_t)c * NG + q;
+    for (size_t cb = 0; cb < units; ++cb)
+      for (size_t q = 0; q < groups[cb].size(); ++q) {
+        const int32_t g = groups[cb][q];
+        const size_t rec = cb * NG + q;
         const int K = p.gk[g], G = p.gg[g];
         H.k[rec] = (uint8_t)K;
         H.g[rec] = (uint8_t)G;
-        for (int t = 0; t < K; ++t)        // keeps the ascending source order (canonical chain)
-          H.src[rec * 32 + t] = (uint16_t)slot[in0 + p.src[(size_t)g * p.kmax + t]];
+        // keeps the ascending source order (canonical chain); non-last layers read
+        // their own CTA's slots, the last layer the (bin << 8 | slot) code
+        int32_t code[32];
+        for (int t = 0; t < K; ++t) {
+          code[t] = slot[in0 + p.src[(size_t)g * p.kmax + t]];
+          H.src[rec * 32 + t] = (uint16_t)(last ? code[t] : (code[t] & 0xff));
+        }
         for (int u = 0; u < G; ++u) {
           const int32_t j = p.col[(size_t)g * p.gmax + u];
           H.bias[rec * 32 + u] = p.bias[j];
           if (last)
             H.orow[rec * 32 + u] = j;
           else                             // member u overwrites the slot of source u
-            slot[out0 + j] = H.src[rec * 32 + u];
+            slot[out0 + j] = code[u];
         }
       }
   }
-  // ---- per-component records ----
+  // ---- per-(component, bin) records ----
   int32_t off = 0;
   for (int b = 0; b < m; ++b) {
     PassHostLayer &H = out.layers[b];
@@ -221,12 +322,13 @@ void build_pass(const std::vector<const PackedLayer *> &layers, int32_t n, const
     }
   }
   out.rec_bytes = off;
-  out.rec.assign((size_t)ncomp * off, 0);
-  for (int c = 0; c < ncomp; ++c) {
-    unsigned char *r = out.rec.data() + (size_t)c * off;
+  const size_t units = (size_t)ncomp * C;
+  out.rec.assign(units * off, 0);
+  for (size_t cb = 0; cb < units; ++cb) {
+    unsigned char *r = out.rec.data() + cb * off;
     for (int b = 0; b < m; ++b) {
       const PassHostLayer &H = out.layers[b];
-      const size_t g0 = (size_t)c * H.NG;
+      const size_t g0 = cb * H.NG;
       for (int q = 0; q < H.NG; ++q) {
         const uint16_t kg = (uint16_t)(H.k[g0 + q] | (H.g[g0 + q] << 8));
         std::memcpy(r + H.off_kg + 2 * q, &kg, 2);

@@ -481,37 +481,125 @@ __global__ void k_y0_positive(int64_t batch, const int64_t *__restrict__ rowptr,
 }
 
 // ---------------------------------------------------------------------------
-// Fused multi-layer pass (model decomposition, fuse.cpp) -- opt-in
-// (sdnn_opts.fuse_rows > 0).  An item is (component c, batch tile of T
-// positions); its R <= 128 input rows are one 64 KB shared-memory tile loaded
-// with one cp.async.bulk per row (T*4 = 512 B - 2 KB).  Four warps run the m
-// layers in place: a group's chain reads its source slots, then its members
-// overwrite those same slots (legal because the planner only fuses layers whose
-// source rows each feed one group); the last layer stores the member rows
-// straight to HBM.  No second buffer, so three CTAs share an SM and hide each
-// other's load latency.  Four positions per lane (float4), one warp per
-// (group, 128-position slice).  HBM traffic per layer drops by m.
+// Fused multi-layer pass (model decomposition, fuse.cpp; the default plan).  An
+// item is (component c, batch tile of T positions).  The component's rows are
+// split over C CTAs (C = 1, or a thread-block cluster of 2 / 4): CTA `rank`
+// owns up to 128 rows -- the sub-components of the pass's first m-1 layers
+// bin-packed at plan time -- as one 64 KB shared-memory tile loaded with one
+// cp.async.bulk per row (T*4 = 512 B - 2 KB), plus its metadata record (source
+// slots, biases, output rows; <= 8 KB) on the same mbarrier.  Layers 0..m-2
+// run in place in the CTA's tile: a group's chain reads its source slots, then
+// its members overwrite those slots (legal because every non-last layer's
+// source rows each feed one group and G_g <= K_g).  The last layer reads its
+// sources from any CTA of the cluster (C > 1: mapa + ld.shared::cluster after a
+// cluster barrier) and stores the member rows straight to HBM.  As soon as the
+// last layer's chains have read the tiles (a second barrier) the next item's
+// copies are issued, before the stores.  NW warps; a unit is (group, slice of
+// 32*V positions), V positions per lane.  HBM traffic per layer drops by m.
 // ---------------------------------------------------------------------------
-constexpr int kPassWarps = 4;
-constexpr int kPassTile = 16384;                 // floats per component tile (R * T)
+constexpr int kPassTile = 16384;                 // floats per CTA tile (R * T)
 constexpr int kPassMaxT = 512;
 constexpr size_t kPassSmem =
     (size_t)kPassTile * 4 + kPassRecMax + 16 + kMaxPassLayers * (kPassMaxT / 32) * 4;
 
 int pass_tile_floats() { return kPassTile; }
 
-// One CTA per (component, tile) item at a time: the component's metadata record
-// and its input rows for T batch positions arrive by bulk copy on one mbarrier;
-// the layers run in place in shared memory; the last layer writes HBM.  The
-// next item's copies are issued as soon as the last layer's chains have read
-// the tile (before its stores), and its row ids are prefetched into registers.
-template <int T>
-__global__ void __launch_bounds__(32 * kPassWarps, 3)
-    k_pass(const DevPass P, const __grid_constant__ CUtensorMap tmA,
-           const __grid_constant__ CUtensorMap tmB, const LayerState *__restrict__ st, float *Ya,
-           float *Yb, uint32_t *__restrict__ alive, int64_t wstride, int64_t stride, float ymax,
-           int use_gather) {
-  constexpr int S = T / 128;                     // 128-position slices per tile
+#define SDNN_PASS_VARIANTS(X)                                                                    \
+  X(128, 4, 4, 1, false) X(256, 4, 4, 1, false) X(512, 4, 4, 1, false) X(128, 4, 4, 1, true)    \
+  X(128, 4, 4, 2, true) X(128, 4, 4, 4, true)                                                   \
+  X(128, 2, 8, 1, true) X(256, 2, 8, 1, true) X(512, 2, 8, 1, true) X(128, 2, 8, 2, true)       \
+  X(128, 2, 8, 4, true)
+
+// X2: packed fp32x2 arithmetic (FFMA2 / FADD2, sm_100; per component identical
+// to __fmaf_rn / __fadd_rn) and liveness from the OR of the output bit patterns
+// (y is +0 exactly when dead: z is never -0, see clampy).  Measured on C4
+// (same box): X2 speeds up the cluster passes (2726 -> 2620 ms/step) but slows
+// the single-CTA passes (2755 -> 2832 at cap 128), whose per-member compare
+// work paces their HBM stores; launch_pass picks X2 = (C > 1).
+template <int V, bool X2>
+struct PassVec;
+template <>
+struct PassVec<4, true> {
+  using T = float4;
+  __device__ static void acc(const T &v, float w, float (&a)[4]) {
+    const float2 w2 = make_float2(w, w);
+    const float2 lo = __ffma2_rn(make_float2(v.x, v.y), w2, make_float2(a[0], a[1]));
+    const float2 hi = __ffma2_rn(make_float2(v.z, v.w), w2, make_float2(a[2], a[3]));
+    a[0] = lo.x;
+    a[1] = lo.y;
+    a[2] = hi.x;
+    a[3] = hi.y;
+  }
+  __device__ static T out(const float (&a)[4], float b, float ymax, uint32_t (&o)[4]) {
+    const float2 b2 = make_float2(b, b);
+    const float2 lo = __fadd2_rn(make_float2(a[0], a[1]), b2);
+    const float2 hi = __fadd2_rn(make_float2(a[2], a[3]), b2);
+    T y;
+    y.x = clampy(lo.x, ymax);
+    y.y = clampy(lo.y, ymax);
+    y.z = clampy(hi.x, ymax);
+    y.w = clampy(hi.y, ymax);
+    o[0] |= __float_as_uint(y.x);
+    o[1] |= __float_as_uint(y.y);
+    o[2] |= __float_as_uint(y.z);
+    o[3] |= __float_as_uint(y.w);
+    return y;
+  }
+  __device__ static uint32_t bits(const uint32_t (&o)[4]) {
+    return (o[0] ? 1u : 0u) | (o[1] ? 2u : 0u) | (o[2] ? 4u : 0u) | (o[3] ? 8u : 0u);
+  }
+  __device__ static T ld_cluster(uint32_t addr) { return ld_cluster_f4(addr); }
+};
+template <>
+struct PassVec<4, false> {
+  using T = float4;
+  __device__ static void acc(const T &v, float w, float (&a)[4]) {
+    a[0] = __fmaf_rn(v.x, w, a[0]);
+    a[1] = __fmaf_rn(v.y, w, a[1]);
+    a[2] = __fmaf_rn(v.z, w, a[2]);
+    a[3] = __fmaf_rn(v.w, w, a[3]);
+  }
+  __device__ static T out(const float (&a)[4], float b, float ymax, uint32_t (&o)[4]) {
+    T y;
+    y.x = clampy(__fadd_rn(a[0], b), ymax);
+    y.y = clampy(__fadd_rn(a[1], b), ymax);
+    y.z = clampy(__fadd_rn(a[2], b), ymax);
+    y.w = clampy(__fadd_rn(a[3], b), ymax);
+    o[0] |= (y.x > 0.f ? 1u : 0u) | (y.y > 0.f ? 2u : 0u) | (y.z > 0.f ? 4u : 0u) | (y.w > 0.f ? 8u : 0u);
+    return y;
+  }
+  __device__ static uint32_t bits(const uint32_t (&o)[4]) { return o[0]; }
+  __device__ static T ld_cluster(uint32_t addr) { return ld_cluster_f4(addr); }
+};
+template <>
+struct PassVec<2, true> {
+  using T = float2;
+  __device__ static void acc(const T &v, float w, float (&a)[2]) {
+    const float2 r = __ffma2_rn(v, make_float2(w, w), make_float2(a[0], a[1]));
+    a[0] = r.x;
+    a[1] = r.y;
+  }
+  __device__ static T out(const float (&a)[2], float b, float ymax, uint32_t (&o)[2]) {
+    const float2 z = __fadd2_rn(make_float2(a[0], a[1]), make_float2(b, b));
+    T y;
+    y.x = clampy(z.x, ymax);
+    y.y = clampy(z.y, ymax);
+    o[0] |= __float_as_uint(y.x);
+    o[1] |= __float_as_uint(y.y);
+    return y;
+  }
+  __device__ static uint32_t bits(const uint32_t (&o)[2]) { return (o[0] ? 1u : 0u) | (o[1] ? 2u : 0u); }
+  __device__ static T ld_cluster(uint32_t addr) { return ld_cluster_f2(addr); }
+};
+
+template <int T, int V, int NW, int C, bool X2>
+__global__ void __launch_bounds__(32 * NW, 3)
+    k_pass(const DevPass P, const LayerState *__restrict__ st, float *Ya, float *Yb,
+           uint32_t *__restrict__ alive, int64_t wstride, int64_t stride, float ymax) {
+  using PV = PassVec<V, X2>;
+  using VT = typename PV::T;
+  constexpr int SW = 32 * V;                     // positions per slice (one warp)
+  constexpr int S = T / SW;                      // slices per tile
   constexpr int W = T / 32;                      // liveness words per tile
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float *tile_s = reinterpret_cast<float *>(smem_raw);
@@ -520,65 +608,56 @@ __global__ void __launch_bounds__(32 * kPassWarps, 3)
   uint32_t *aw = reinterpret_cast<uint32_t *>(bar + 2);                 // [kMaxPassLayers][W]
   const LayerState Sx = st[P.a];
   const int width = Sx.width;
-  if (width <= 0) return;
+  if (width <= 0) return;                        // uniform over the grid
   const float *__restrict__ Yin = Sx.in ? Yb : Ya;
   float *__restrict__ Yout = Sx.in ? Ya : Yb;
   const int tiles = (width + T - 1) / T;
   const int64_t items = (int64_t)P.ncomp * tiles;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t rank = C > 1 ? cluster_rank() : 0u;
+  const int64_t cid = C > 1 ? (int64_t)cluster_id_x() : (int64_t)blockIdx.x;
+  const int64_t ncl = C > 1 ? (int64_t)nclusters_x() : (int64_t)gridDim.x;
+  const uint32_t tile_u32 = smem_u32(tile_s);
   if (tid == 0) {
     mbar_init(bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int q = tid; q < kMaxPassLayers * W; q += blockDim.x) aw[q] = 0u;
   __syncthreads();
-  // rin <= kMaxPassRows == blockDim.x: thread r owns input row r of an item
+  // rin <= 128 <= blockDim.x: thread r owns input row r of an item
   int nrow = 0, ncnt = 0;
   auto fetch_rows = [&](int64_t it) {
-    const int c = (int)(it / tiles);
-    ncnt = __ldg(P.in_count + c);
-    nrow = tid < P.rin ? __ldg(P.in_rows + (int64_t)c * P.rin + tid) : 0;
+    const int64_t cb = (it / tiles) * C + rank;
+    ncnt = __ldg(P.in_count + cb);
+    nrow = tid < P.rin ? __ldg(P.in_rows + cb * P.rin + tid) : 0;
   };
-  const void *tm = Sx.in ? (const void *)&tmB : (const void *)&tmA;
-  const bool gather = T <= 256 && use_gather;
   auto issue_load = [&](int64_t it) {
-    const int c = (int)(it / tiles);
-    const int tile = (int)(it - (int64_t)c * tiles);
-    if (gather) {
-      // lanes 4i..4i+3 hold the rows of gather i; a padded tail repeats the
-      // quad's first row into slots >= ncnt (inside the tile, never read)
-      const int qb = lane & ~3;
-      const int r0 = __shfl_sync(FULL, nrow, qb), r1 = __shfl_sync(FULL, nrow, qb + 1);
-      const int r2 = __shfl_sync(FULL, nrow, qb + 2), r3 = __shfl_sync(FULL, nrow, qb + 3);
-      if (tid == 0) {
-        mbar_expect_tx_arrive(bar, (uint32_t)((ncnt + 3) & ~3) * T * 4 + (uint32_t)P.rec_bytes);
-        bulk_g2s(rec_s, P.rec + (int64_t)c * P.rec_bytes, P.rec_bytes, bar);
-      }
-      const int q = tid & ~3;
-      if ((lane & 3) == 0 && q < ncnt)
-        gather4_g2s(tile_s + (size_t)q * T, tm, tile * T, r0, q + 1 < ncnt ? r1 : r0,
-                    q + 2 < ncnt ? r2 : r0, q + 3 < ncnt ? r3 : r0, bar);
-      return;
-    }
+    const int64_t c = it / tiles;
+    const int tile = (int)(it - c * tiles);
+    const int64_t cb = c * C + rank;
     if (tid == 0) {
       mbar_expect_tx_arrive(bar, (uint32_t)ncnt * T * 4 + (uint32_t)P.rec_bytes);
-      bulk_g2s(rec_s, P.rec + (int64_t)c * P.rec_bytes, P.rec_bytes, bar);
+      bulk_g2s(rec_s, P.rec + cb * P.rec_bytes, P.rec_bytes, bar);
     }
     if (tid < ncnt)
       bulk_g2s(tile_s + (size_t)tid * T, Yin + (int64_t)nrow * stride + (int64_t)tile * T, T * 4, bar);
   };
-  // the last layer releases the tile before its HBM stores when every warp owns
+  auto release = [&]() {                         // every reader of every tile is done
+    if (C > 1) cluster_sync();
+    else __syncthreads();
+  };
+  // the last layer releases the tiles before its HBM stores when every warp owns
   // at most one (group, slice) unit of it
-  const bool early = P.layers[P.m - 1].NG * S <= kPassWarps;
-  if (blockIdx.x < items) {
-    fetch_rows(blockIdx.x);
-    issue_load(blockIdx.x);
+  const bool early = P.layers[P.m - 1].NG * S <= NW;
+  if (cid < items) {
+    fetch_rows(cid);
+    issue_load(cid);
   }
   uint32_t ph = 0;
-  for (int64_t it = blockIdx.x; it < items; it += gridDim.x, ph ^= 1u) {
-    const int c = (int)(it / tiles);
-    const int tile = (int)(it - (int64_t)c * tiles);
-    const int64_t next = it + gridDim.x;
+  for (int64_t it = cid; it < items; it += ncl, ph ^= 1u) {
+    const int64_t c = it / tiles;
+    const int tile = (int)(it - c * tiles);
+    const int64_t next = it + ncl;
     if (next < items) fetch_rows(next);          // in flight while this item computes
     bool issued = false;
     mbar_wait(bar, ph);
@@ -590,7 +669,8 @@ __global__ void __launch_bounds__(32 * kPassWarps, 3)
       const uint16_t *kg_s = reinterpret_cast<const uint16_t *>(rec_s + PL.off_kg);
       const uint16_t *src_s = reinterpret_cast<const uint16_t *>(rec_s + PL.off_src);
       const float *bias_s = reinterpret_cast<const float *>(rec_s + PL.off_bias);
-      for (int u0 = 0; u0 < (last && early ? kPassWarps : units); u0 += kPassWarps) {
+      if (C > 1 && last) cluster_sync();         // every CTA's tile is at boundary m-1
+      for (int u0 = 0; u0 < (last && early ? NW : units); u0 += NW) {
         const int u = u0 + warp;
         const bool active = u < units;
         int G = 0, K = 0, sl = 0, gi = 0;
@@ -601,70 +681,72 @@ __global__ void __launch_bounds__(32 * kPassWarps, 3)
           K = kg & 0xffu;
           G = kg >> 8;
         }
-        const int mysrc = (active && lane < K) ? (int)src_s[gi * 32 + lane] * T : 0;
+        const int pofs = sl * SW + lane * V;
         const float mybias = (active && lane < G) ? bias_s[gi * 32 + lane] : 0.f;
-        const int pofs = sl * 128 + lane * 4;
+        int mysrc = 0;                           // local slot offset (floats)
+        uint32_t myaddr = 0;                     // C > 1, last layer: row base in its owner CTA
+        if (active && lane < K) {
+          const uint32_t code = src_s[gi * 32 + lane];
+          if (C > 1 && last)
+            myaddr = cluster_map(tile_u32 + (code & 0xffu) * (T * 4), code >> 8);
+          else
+            mysrc = (int)(code & 0xffu) * T;
+        }
         float *myrow = nullptr;
-        if (last)
-          myrow = Yout + (int64_t)tile * T + pofs - lane * 4 +
+        if (last)                                // lane v: member v's output row base
+          myrow = Yout + (int64_t)tile * T + sl * SW +
                   ((active && lane < G)
                        ? (int64_t)reinterpret_cast<const int32_t *>(rec_s + PL.off_orow)[gi * 32 + lane] * stride
                        : 0);
-        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+        float acc[V];
+#pragma unroll
+        for (int e = 0; e < V; ++e) acc[e] = 0.f;
         if (G > 0) {
+          if (C > 1 && last) {
 #pragma unroll 8
-          for (int t = 0; t < K; ++t) {
-            const float4 v = *reinterpret_cast<const float4 *>(tile_s + __shfl_sync(FULL, mysrc, t) + pofs);
-            a0 = __fmaf_rn(v.x, wu, a0);
-            a1 = __fmaf_rn(v.y, wu, a1);
-            a2 = __fmaf_rn(v.z, wu, a2);
-            a3 = __fmaf_rn(v.w, wu, a3);
+            for (int t = 0; t < K; ++t)
+              PV::acc(PV::ld_cluster(__shfl_sync(FULL, myaddr, t) + (uint32_t)(pofs * 4)), wu, acc);
+          } else {
+#pragma unroll 8
+            for (int t = 0; t < K; ++t)
+              PV::acc(*reinterpret_cast<const VT *>(tile_s + __shfl_sync(FULL, mysrc, t) + pofs), wu, acc);
           }
         }
         if (last && early) {
-          // every chain of the pass has read the tile and the record: next load
+          // generic-proxy tile reads/writes before the next item's TMA writes
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          __syncthreads();
+          release();
           if (next < items) issue_load(next);
           issued = true;
         }
         if (G == 0) continue;
-        uint32_t am = 0;                         // per member, between the stores (see k_layer_bulk)
+        uint32_t o[V];                           // per member, between the stores
+#pragma unroll
+        for (int e = 0; e < V; ++e) o[e] = 0u;
         if (last) {
-          // lane v holds member v's output row base: no dependent load per member
           for (int v = 0; v < G; ++v) {
             float *row = reinterpret_cast<float *>(__shfl_sync(FULL, reinterpret_cast<uintptr_t>(myrow), v));
-            const float b = __shfl_sync(FULL, mybias, v);
-            float4 y;
-            y.x = clampy(__fadd_rn(a0, b), ymax);
-            y.y = clampy(__fadd_rn(a1, b), ymax);
-            y.z = clampy(__fadd_rn(a2, b), ymax);
-            y.w = clampy(__fadd_rn(a3, b), ymax);
-            am |= (y.x > 0.f ? 1u : 0u) | (y.y > 0.f ? 2u : 0u) | (y.z > 0.f ? 4u : 0u) | (y.w > 0.f ? 8u : 0u);
-            *reinterpret_cast<float4 *>(row + lane * 4) = y;
+            const VT y = PV::out(acc, __shfl_sync(FULL, mybias, v), ymax, o);
+            *reinterpret_cast<VT *>(row + lane * V) = y;
           }
         } else {
           for (int v = 0; v < G; ++v) {          // member v overwrites source slot v (in place)
             const int off = __shfl_sync(FULL, mysrc, v);
-            const float b = __shfl_sync(FULL, mybias, v);
-            float4 y;
-            y.x = clampy(__fadd_rn(a0, b), ymax);
-            y.y = clampy(__fadd_rn(a1, b), ymax);
-            y.z = clampy(__fadd_rn(a2, b), ymax);
-            y.w = clampy(__fadd_rn(a3, b), ymax);
-            am |= (y.x > 0.f ? 1u : 0u) | (y.y > 0.f ? 2u : 0u) | (y.z > 0.f ? 4u : 0u) | (y.w > 0.f ? 8u : 0u);
-            *reinterpret_cast<float4 *>(tile_s + off + pofs) = y;
+            const VT y = PV::out(acc, __shfl_sync(FULL, mybias, v), ymax, o);
+            *reinterpret_cast<VT *>(tile_s + off + pofs) = y;
           }
         }
-        // liveness: lane covers positions sl*128 + lane*4 + e -> word sl*4 + lane/8
-        uint32_t bal[4];
+        const uint32_t am = PV::bits(o);
+        // liveness: lane L holds positions sl*SW + L*V + e; word sl*V + q of the
+        // tile has bit b = position q*32 + b of the slice -> lane (q*32+b)/V, e = b%V
+        uint32_t bal[V];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) bal[e] = __ballot_sync(FULL, (am >> e) & 1u);
-        if (lane < 4) {
+        for (int e = 0; e < V; ++e) bal[e] = __ballot_sync(FULL, (am >> e) & 1u);
+        if (lane < V) {
           uint32_t word = 0;
 #pragma unroll
-          for (int q = 0; q < 32; ++q) word |= ((bal[q & 3] >> (lane * 8 + (q >> 2))) & 1u) << q;
-          if (word) atomicOr(&aw[j * W + sl * 4 + lane], word);
+          for (int b = 0; b < 32; ++b) word |= ((bal[b % V] >> (lane * (32 / V) + b / V)) & 1u) << b;
+          if (word) atomicOr(&aw[j * W + sl * V + lane], word);
         }
       }
       __syncthreads();                           // the next layer reads slots other warps wrote
@@ -680,13 +762,13 @@ __global__ void __launch_bounds__(32 * kPassWarps, 3)
       }
     }
     if (!issued) {
-      // generic-proxy smem writes of this item before the next item's TMA writes
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncthreads();
+      release();
       if (next < items) issue_load(next);
     }
     __syncthreads();                             // aw published before the next item uses it
   }
+  if (C > 1) cluster_sync();                     // no CTA exits while a peer may read its tile
 }
 
 // ---------------------------------------------------------------------------
@@ -930,9 +1012,69 @@ void configure_kernels() {
         b.ctas <= 4)
       g_bulk = b;
   }
-  cudaFuncSetAttribute(k_pass<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPassSmem);
-  cudaFuncSetAttribute(k_pass<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPassSmem);
-  cudaFuncSetAttribute(k_pass<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPassSmem);
+#define X(TT, VV, NN, CC, XX) \
+  cudaFuncSetAttribute(k_pass<TT, VV, NN, CC, XX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPassSmem);
+  SDNN_PASS_VARIANTS(X)
+#undef X
+}
+
+// pass-kernel shape: V positions per lane and NW warps (default V = 4: 4 warps
+// of float4 lanes; SDNN_PASS_V = 2: 8 warps of float2 lanes)
+static int pass_v() {
+  static const int v = [] {
+    const char *e = getenv("SDNN_PASS_V");
+    return (e && atoi(e) == 2) ? 2 : 4;
+  }();
+  return v;
+}
+
+// clusters of C CTAs that can be co-resident
+template <int T, int V, int NW, int C, bool X2>
+static int pass_clusters(int sms) {
+  static int cached = 0;
+  if (cached) return cached;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(C * sms * 3);
+  cfg.blockDim = dim3(32 * NW);
+  cfg.dynamicSmemBytes = kPassSmem;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = C;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, k_pass<T, V, NW, C, X2>, &cfg) != cudaSuccess || n <= 0) {
+    cudaGetLastError();
+    n = sms * 3 / C / 2;                         // conservative
+  }
+  cached = n;
+  return n;
+}
+
+template <int T, int V, int NW, int C, bool X2>
+static void launch_pass_t(const LaunchCfg &c, const Workspace &w, const DevPass &P, uint32_t *alive,
+                          float ymax, cudaStream_t s) {
+  if (C == 1) {
+    k_pass<T, V, NW, 1, X2><<<c.sms * 3, 32 * NW, kPassSmem, s>>>(P, w.st, w.Y[0], w.Y[1], alive, w.words,
+                                                              w.stride, ymax);
+    return;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(C * pass_clusters<T, V, NW, C, X2>(c.sms));
+  cfg.blockDim = dim3(32 * NW);
+  cfg.dynamicSmemBytes = kPassSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = C;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_pass<T, V, NW, C, X2>, P, (const LayerState *)w.st, w.Y[0], w.Y[1], alive,
+                     (int64_t)w.words, (int64_t)w.stride, ymax);
 }
 
 void launch_densify(const LaunchCfg &c, const Workspace &w, int32_t n, int64_t batch,
@@ -988,57 +1130,30 @@ void launch_layer(const LaunchCfg &c, const Workspace &w, const DevLayer &L, int
 
 void launch_pass(const LaunchCfg &c, const Workspace &w, const DevPass &P, uint32_t *alive,
                  float ymax, cudaStream_t s) {
-  static const int gather_env = [] {
-    // opt-in: measured slower than per-row bulk copies on C4 (k_pass 2.48 vs
-    // 2.36 ms per launch, profiles/r01_v7_gather_c4.txt)
-    const char *e = getenv("SDNN_PASS_GATHER");
+  static const int x2_c1 = [] {                  // SDNN_PASS_X2=1: packed path for C = 1 too
+    const char *e = getenv("SDNN_PASS_X2");
     return e ? atoi(e) : 0;
   }();
-  const int tb = P.T == 256 ? 1 : 0;
-  const int g = (w.tm_ok && gather_env && P.T <= 256) ? 1 : 0;
-#define SDNN_PASS(TT)                                                                    \
-  k_pass<TT><<<c.sms * 3, 32 * kPassWarps, kPassSmem, s>>>(P, w.tmY[0][tb], w.tmY[1][tb], \
-                                                          w.st, w.Y[0], w.Y[1], alive,    \
-                                                          w.words, w.stride, ymax, g)
-  switch (P.T) {
-    case 512: SDNN_PASS(512); break;
-    case 256: SDNN_PASS(256); break;
-    default: SDNN_PASS(128); break;
+  const bool v4 = pass_v() == 4;
+  if (P.C == 4) {
+    if (v4) launch_pass_t<128, 4, 4, 4, true>(c, w, P, alive, ymax, s);
+    else launch_pass_t<128, 2, 8, 4, true>(c, w, P, alive, ymax, s);
+  } else if (P.C == 2) {
+    if (v4) launch_pass_t<128, 4, 4, 2, true>(c, w, P, alive, ymax, s);
+    else launch_pass_t<128, 2, 8, 2, true>(c, w, P, alive, ymax, s);
+  } else if (P.T == 512) {
+    if (v4) launch_pass_t<512, 4, 4, 1, false>(c, w, P, alive, ymax, s);
+    else launch_pass_t<512, 2, 8, 1, true>(c, w, P, alive, ymax, s);
+  } else if (P.T == 256) {
+    if (v4) launch_pass_t<256, 4, 4, 1, false>(c, w, P, alive, ymax, s);
+    else launch_pass_t<256, 2, 8, 1, true>(c, w, P, alive, ymax, s);
+  } else {
+    if (!v4) launch_pass_t<128, 2, 8, 1, true>(c, w, P, alive, ymax, s);
+    else if (x2_c1) launch_pass_t<128, 4, 4, 1, true>(c, w, P, alive, ymax, s);
+    else launch_pass_t<128, 4, 4, 1, false>(c, w, P, alive, ymax, s);
   }
-#undef SDNN_PASS
 }
 
-bool encode_pass_maps(Workspace &w, int32_t n) {
-  using EncodeFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
-                                const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
-                                const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
-                                CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-  static EncodeFn encode = [] {
-    void *p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess) {
-      cudaGetLastError();
-      p = nullptr;
-    }
-    return reinterpret_cast<EncodeFn>(p);
-  }();
-  w.tm_ok = false;
-  if (!encode) return false;
-  for (int b = 0; b < 2; ++b)
-    for (int t = 0; t < 2; ++t) {
-      const cuuint64_t dims[2] = {(cuuint64_t)w.stride, (cuuint64_t)n};
-      const cuuint64_t strides[1] = {(cuuint64_t)w.stride * 4};
-      const cuuint32_t box[2] = {t ? 256u : 128u, 1u};
-      const cuuint32_t estr[2] = {1u, 1u};
-      if (encode(&w.tmY[b][t], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, w.Y[b], dims, strides, box, estr,
-                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-        return false;
-    }
-  w.tm_ok = true;
-  return true;
-}
 
 void launch_scan(const Workspace &w, int32_t a, int32_t m, uint32_t *alive_cur,
                  uint32_t *alive_next, bool compact, cudaStream_t s, const uint32_t *sat_cur,

@@ -6,7 +6,6 @@
 #include <string>
 #include <vector>
 
-#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace sdnn {
@@ -102,7 +101,8 @@ struct LayerState {
 // canonical ascending-source fmaf sequence.
 // ---------------------------------------------------------------------------
 constexpr int kMaxPassLayers = 16;
-constexpr int kMaxPassRows = 128;      // rows per component (one 64 KB tile of >= 128 positions)
+constexpr int kMaxPassRows = 128;      // slots per CTA (one 64 KB tile of >= 128 positions)
+constexpr int kMaxPassCluster = 4;     // CTAs per component (thread-block cluster, DSMEM)
 
 struct Step {
   int32_t a = 0, m = 1;                // layers [a, a+m)
@@ -110,9 +110,11 @@ struct Step {
 };
 constexpr int32_t kResidentStep = -2;  // layers [a, L) in the SMEM-resident kernel
 
-// plan greedy fused passes: extend while every component stays <= cap rows at
-// every boundary, the layers are uniform with K <= 32, and every layer but the
-// last of a pass allows in-place slots (exclusive sources, G_g <= K_g)
+// plan greedy fused passes: extend while the layers are uniform with K <= 32,
+// every layer but the last allows in-place slots (exclusive sources,
+// G_g <= K_g), the sub-components of all layers but the last fit one CTA
+// (kMaxPassRows slots) and every component's sub-components pack into
+// cap / kMaxPassRows CTAs (cap <= kMaxPassRows * kMaxPassCluster)
 std::vector<Step> plan_steps(const std::vector<const PackedLayer *> &layers, int32_t n, int cap,
                              int max_m);
 
@@ -127,6 +129,7 @@ struct PassHostLayer {
 };
 struct PassHost {
   int32_t a = 0, m = 0, ncomp = 0, rin = 0, R = 0, T = 0;
+  int32_t C = 1;                       // CTAs per component (cluster size; rows/records per [comp][bin])
   std::vector<int32_t> in_rows;        // [ncomp][rin]  global neuron ids at boundary a
   std::vector<int32_t> in_count;       // [ncomp]
   std::vector<PassHostLayer> layers;   // [m]
@@ -152,6 +155,7 @@ struct PassLayerDev {
 };
 struct DevPass {
   int32_t a, m, ncomp, rin, R, T, rec_bytes;
+  int32_t C;                           // cluster size: in_rows/in_count/rec indexed [comp * C + rank]
   const int32_t *in_rows, *in_count;
   const unsigned char *rec;            // [ncomp][rec_bytes]
   PassLayerDev layers[kMaxPassLayers]; // by value: the kernel parameter carries them
@@ -191,10 +195,6 @@ struct Workspace {
   uint32_t *pret = nullptr;            // positions retired but not yet compacted away
   int32_t *nretired = nullptr;
   uint32_t *orig = nullptr;
-  // TMA tensor maps of Y[b] as a 2-D [n][stride] fp32 tensor with a box of
-  // {T, 1}: tmY[b][0] for T = 128, tmY[b][1] for T = 256 (fused-pass row gathers)
-  CUtensorMap tmY[2][2];
-  bool tm_ok = false;
   int64_t stride = 0;                 // row stride (capacity in batch columns)
   int64_t words = 0;                  // stride / 32
   uint32_t *alive_set(int s) const { return alive[s & 1]; }
@@ -225,9 +225,6 @@ int pass_tile_floats();        // smem floats per component tile (tile T = this 
 // a fused pass: reads st[P.a], liveness of layer a+j to alive + j*words
 void launch_pass(const LaunchCfg &c, const Workspace &w, const DevPass &P, uint32_t *alive,
                  float ymax, cudaStream_t s);
-// build w.tmY for the current Y buffers (false: no driver entry point; passes
-// then use per-row bulk copies)
-bool encode_pass_maps(Workspace &w, int32_t n);
 // after a step [a, a+m): live counts of its m layers, compaction decision -> st[a+m],
 // zero the next step's bitmask set
 void launch_scan(const Workspace &w, int32_t a, int32_t m, uint32_t *alive_cur,

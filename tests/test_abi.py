@@ -175,31 +175,41 @@ def test_product_path_never_touches_oracle():
 
 
 def test_plan_steps_rn_and_rr(sd):
-    """Fused multi-layer passes: RadiX-Net layers (5-bit butterfly fields that
-    overlap) have connected components of 2^(union of the fields' bits) neurons
-    over consecutive layers, so the planner fuses layers while a component fits
-    the 128-row tile; random-regular layers have one giant component and are
-    never fused."""
+    """Fused multi-layer passes: in a RadiX-Net layer every group is a dense
+    32x32 block varying one 5-bit field of the neuron id, so the connected
+    components over layers a..b span 2^|union of their fields' bits| neurons.
+    A pass keeps all layers but the last in one CTA (sub-components of <= 128
+    slots) and lets the last layer read across a cluster of cap/128 CTAs; the
+    planner extends every pass while that holds (greedy, maximal).
+    Random-regular layers have one giant component and are never fused."""
     rn = list(g.iter_layers(g.rn_spec(1024, 24)))
     fields = [g.rn_field(1024, l) for l in range(24)]
 
-    def comp_bits(ls):
+    def comp(a, m):
         bits = set()
-        for p in ls:
+        for p in fields[a:a + m]:
             bits |= set(range(p, p + 5))
-        return len(bits)
+        return 2 ** len(bits)
+
+    def feasible(a, m, cap):
+        sub, full = comp(a, m - 1), comp(a, m)
+        cta = min(cap, 128)
+        return sub <= cta and -(-full // (cta // sub * sub)) <= max(1, cap // 128)
+
     default = sd.sdnn_plan_steps(1024, rn)                         # fusion on by default
-    assert default == sd.sdnn_plan_steps(1024, rn, fuse_rows=128)
-    assert sd.sdnn_plan_steps(1024, rn, fuse_rows=4096) == default   # clamped to 128
-    for cap in (128,):
+    assert default == sd.sdnn_plan_steps(1024, rn, fuse_rows=512)
+    assert sd.sdnn_plan_steps(1024, rn, fuse_rows=4096) == default   # clamped to 512
+    for cap in (128, 256, 512):
         plan = sd.sdnn_plan_steps(1024, rn, fuse_rows=cap)
         assert sum(plan) == 24 and max(plan) > 1
         a = 0
         for m in plan:                      # every pass fits, and is maximal (greedy)
-            assert 2 ** comp_bits(fields[a:a + m]) <= cap or m == 1
+            assert m == 1 or feasible(a, m, cap)
             if a + m < 24 and m < 8:
-                assert 2 ** comp_bits(fields[a:a + m + 1]) > cap
+                assert not feasible(a, m + 1, cap)
             a += m
+    assert max(default) == 3                # 3-layer passes need the 4-CTA cluster
+    assert max(sd.sdnn_plan_steps(1024, rn, fuse_rows=128)) == 2
     assert sd.sdnn_plan_steps(1024, rn, fuse_rows=0) == [1] * 24
     assert sd.sdnn_plan_steps(1024, rn, fuse_rows=64) == [1] * 24    # 2 layers need 128 rows
     assert sd.sdnn_plan_steps(1024, rn, flags=sd.SDNN_F_SATURATE) == [1] * 24
@@ -209,8 +219,8 @@ def test_plan_steps_rn_and_rr(sd):
     assert sd.sdnn_plan_steps(1024, ka, fuse_layers=16) == [16, 4]
     assert max(sd.sdnn_plan_steps(1024, ka, fuse_layers=2)) == 2
     big = [g.gen_layer(g.rn_spec(65536, 12), l, fmt="ell") for l in range(12)]
-    plan = sd.sdnn_plan_steps(65536, big, fmt="ell")
-    assert sum(plan) == 12 and max(plan) == 2
+    assert sd.sdnn_plan_steps(65536, big, fmt="ell") == [3, 3, 3, 3]
+    assert sd.sdnn_plan_steps(65536, big, fmt="ell", fuse_rows=128) == [2] * 6
 
 
 def identity_layer(n):

@@ -130,10 +130,13 @@ def test_smem_resident_ka(sd):
 
 
 @pytest.mark.parametrize("fuse_rows,fuse_layers", [(0, -1), (128, -1), (256, -1),
-                                                   (256, 2), (256, 16)])
+                                                   (256, 2), (256, 16), (512, -1), (512, 3),
+                                                   (512, 16)])
 def test_fused_passes_rn(sd, fuse_rows, fuse_layers):
-    """Multi-layer passes (model decomposition): T = 128 / 64 / 32 variants,
-    pass lengths 2..16, compaction between passes, ragged batch."""
+    """Multi-layer passes (model decomposition): single-CTA passes (cap 128)
+    and 2- / 4-CTA cluster passes whose last layer reads through distributed
+    shared memory (cap 256 / 512), pass lengths 2..16, compaction between
+    passes, ragged batch."""
     n, L, B = 1024, 40, 700
     spec = g.rn_spec(n, L)
     layers = list(g.iter_layers(spec))
