@@ -105,13 +105,13 @@ typedef struct sdnn_opts {
   int32_t fuse_rows;   /* multi-layer passes ("model decomposition"):
                           consecutive uniform layers run as one pass over the
                           connected components of their union.  All layers but the
-                          last stay inside one CTA (sub-components of <= 128
-                          neurons, updated in place in shared memory); the last
-                          layer reads across a thread-block cluster of up to
-                          fuse_rows / 128 CTAs (distributed shared memory), so a
-                          component has <= fuse_rows neurons (<= 512, larger
-                          values are clamped; <= 128: single-CTA passes; 0 = off;
-                          -1 = 512)                                                */
+                          last stay inside one CTA (sub-components of <= 512
+                          neurons, updated in place in a 64 KB shared-memory tile
+                          of 16384/rows batch positions); the last layer reads
+                          across a thread-block cluster of up to fuse_rows / 512
+                          CTAs (distributed shared memory), so a component has
+                          <= fuse_rows neurons (<= 2048, larger values are
+                          clamped; <= 512: single-CTA passes; 0 = off; -1 = 512) */
   int32_t fuse_layers; /* at most this many layers per pass (<= 16; -1 = 8)           */
   int32_t resident_from; /* N <= 4096: layers [resident_from, L) run in one kernel that
                           keeps each CTA's batch tile resident in shared memory

@@ -149,7 +149,7 @@ sdnn_status check_opts(const sdnn_opts *o, sdnn_opts &out) {
   out = sdnn_opts{-1, 0u, 32.f, nullptr, -1, -1, -1, 0};
   if (o) out = *o;
   if (out.stream_slots < 0 || out.stream_slots > 64) return fail(SDNN_E_ARG, "stream_slots must be in [0, 64]");
-  if (out.fuse_rows > kMaxPassRows * kMaxPassCluster) out.fuse_rows = kMaxPassRows * kMaxPassCluster;
+  if (out.fuse_rows > pass_cta_rows() * kMaxPassCluster) out.fuse_rows = pass_cta_rows() * kMaxPassCluster;
   if (out.fuse_layers > kMaxPassLayers) return fail(SDNN_E_ARG, "fuse_layers > 16");
   if (!(out.ymax > 0.f) || !std::isfinite(out.ymax)) return fail(SDNN_E_ARG, "ymax must be finite and > 0");
   return SDNN_OK;
@@ -348,9 +348,9 @@ sdnn_status build_stream_blobs(sdnn_net *net, const std::vector<PassHost> &ph) {
 sdnn_status make_plan(sdnn_net *net) {
   if (!net->plan_dirty) return SDNN_OK;
   const bool sat = net->opts.flags & SDNN_F_SATURATE;
-  const int cap = sat ? 0 : std::min(net->opts.fuse_rows < 0 ? kMaxPassRows * kMaxPassCluster
+  const int cap = sat ? 0 : std::min(net->opts.fuse_rows < 0 ? kDefaultPassRows
                                                               : net->opts.fuse_rows,
-                                     kMaxPassRows * kMaxPassCluster);
+                                     pass_cta_rows() * kMaxPassCluster);
   net->sat_suffix.assign(net->L + 1, 1);
   for (int l = net->L - 1; l >= 0; --l)
     net->sat_suffix[l] = net->sat_suffix[l + 1] && saturation_preserving(net->host[l], net->opts.ymax);
@@ -391,6 +391,9 @@ sdnn_status make_plan(sdnn_net *net) {
   for (size_t q = 0; q < net->steps.size(); ++q) {
     if (net->steps[q].m == 1) continue;
     PassHost &H = ph[q];
+    if (!pass_variant(H.T, H.C))
+      return fail(SDNN_E_UNSUPPORTED, "no fused-pass kernel for tile " + std::to_string(H.T) + " x cluster " +
+                                          std::to_string(H.C));
     DevPass D{};
     D.a = H.a;
     D.m = H.m;
@@ -413,7 +416,7 @@ sdnn_status make_plan(sdnn_net *net) {
     }
     for (int j = 0; j < H.m; ++j) {
       const PassHostLayer &HL = H.layers[j];
-      D.layers[j] = PassLayerDev{HL.off_kg, HL.off_src, HL.off_bias, HL.off_orow, HL.NG, HL.wu};
+      D.layers[j] = PassLayerDev{HL.off_kg, HL.off_src, HL.off_bias, HL.off_orow, HL.NG, HL.wu, HL.bu};
     }
     net->steps[q].pass = (int32_t)net->passes.size();
     net->passes.push_back(D);
@@ -1003,8 +1006,8 @@ sdnn_status sdnn_plan_steps(int32_t neurons, int32_t layers, const sdnn_layer *W
   for (int l = 0; l < layers; ++l) lp[l] = &host[l];
   const int cap = (o.flags & SDNN_F_SATURATE)
                       ? 0
-                      : std::min(o.fuse_rows < 0 ? kMaxPassRows * kMaxPassCluster : o.fuse_rows,
-                                 kMaxPassRows * kMaxPassCluster);
+                      : std::min(o.fuse_rows < 0 ? kDefaultPassRows : o.fuse_rows,
+                                 pass_cta_rows() * kMaxPassCluster);
   const int maxm = o.fuse_layers < 0 ? 8 : o.fuse_layers;
   const std::vector<Step> steps = plan_passes(lp, neurons, cap, maxm, pass_tile_floats(), 1, nullptr);
   for (size_t i = 0; i < steps.size(); ++i) step_len[i] = steps[i].m;

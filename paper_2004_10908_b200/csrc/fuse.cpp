@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cmath>
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <thread>
@@ -129,22 +130,35 @@ int bins_needed(UF &full, UF &sub, int32_t n, int cap_cta, std::vector<int32_t> 
 
 }  // namespace
 
+// slots per CTA of a fused pass (128 / 256 / 512; SDNN_PASS_CTA_ROWS overrides
+// the default for A/B runs): a component larger than this spreads over a
+// cluster of up to kMaxPassCluster CTAs
+int pass_cta_rows() {
+  static const int r = [] {
+    const char *e = getenv("SDNN_PASS_CTA_ROWS");
+    const int v = e ? atoi(e) : kDefaultCtaRows;
+    return (v == 128 || v == 256 || v == 512) ? v : kDefaultCtaRows;
+  }();
+  return r;
+}
+
 // A pass [a, a+m) keeps every layer but the last inside one CTA: the
-// sub-components of layers a..a+m-2 must fit kMaxPassRows slots.  The last
+// sub-components of layers a..a+m-2 must fit pass_cta_rows() slots.  The last
 // layer may read across a cluster of up to kMaxPassCluster CTAs, so the
 // sub-components of a full component are bin-packed into at most
-// cap / kMaxPassRows CTAs (cap <= kMaxPassRows: one CTA of cap slots).
+// cap / pass_cta_rows() CTAs (cap <= pass_cta_rows(): one CTA of cap slots).
 std::vector<Step> plan_steps(const std::vector<const PackedLayer *> &layers, int32_t n, int cap,
-                             int max_m) {
+                             int max_m, int a_begin) {
   std::vector<Step> steps;
   const int L = (int)layers.size();
   max_m = std::max(1, std::min(max_m, kMaxPassLayers));
-  cap = std::min(cap, kMaxPassRows * kMaxPassCluster);
-  const int cap_cta = std::min(cap, kMaxPassRows);
-  const int max_bins = std::max(1, cap / kMaxPassRows);
+  const int cta_rows = pass_cta_rows();
+  cap = std::min(cap, cta_rows * kMaxPassCluster);
+  const int cap_cta = std::min(cap, cta_rows);
+  const int max_bins = std::max(1, cap / cta_rows);
   UF full, sub;
   std::vector<int32_t> cnt, stamp, size, owner;
-  for (int a = 0; a < L;) {
+  for (int a = a_begin; a < L;) {
     int m = 1;
     if (cap > 0 && max_m > 1 && fusable(*layers[a])) {
       const int64_t nodes = (int64_t)(max_m + 1) * n;
@@ -193,7 +207,7 @@ void build_pass(const std::vector<const PackedLayer *> &layers, int32_t n, const
     }
   }
   // boundary-0 rows of each component, grouped by sub-component, bin-packed
-  // (first fit decreasing) into CTAs of kMaxPassRows slots
+  // (first fit decreasing) into CTAs of pass_cta_rows() slots
   std::vector<std::vector<std::vector<int32_t>>> subs(ncomp);   // [comp][sub] rows
   {
     std::vector<int32_t> sub_idx((size_t)(m + 1) * n, -1);
@@ -208,6 +222,7 @@ void build_pass(const std::vector<const PackedLayer *> &layers, int32_t n, const
       subs[c][sub_idx[sr]].push_back(i);
     }
   }
+  const int cta_rows = pass_cta_rows();
   std::vector<std::vector<std::vector<int32_t>>> bins(ncomp);   // [comp][bin] rows
   int C = 1, R = 1;
   for (int c = 0; c < ncomp; ++c) {
@@ -216,7 +231,7 @@ void build_pass(const std::vector<const PackedLayer *> &layers, int32_t n, const
     for (auto &sv : v) {
       bool placed = false;
       for (auto &b : bins[c])
-        if ((int)(b.size() + sv.size()) <= kMaxPassRows) {
+        if ((int)(b.size() + sv.size()) <= cta_rows) {
           b.insert(b.end(), sv.begin(), sv.end());
           placed = true;
           break;
@@ -240,17 +255,16 @@ void build_pass(const std::vector<const PackedLayer *> &layers, int32_t n, const
   out.C = C;
   out.R = R;
   out.rin = R;
-  int T = 512;                                    // one tile of tile_floats per CTA
-  while (T > 128 && (int64_t)R * T > tile_floats) T >>= 1;
-  if (C > 1) T = 128;
-  out.T = T;
+  int Rp = 32;                                    // one tile of tile_floats per CTA
+  while (Rp < R) Rp <<= 1;
+  out.T = std::max(32, std::min(512, tile_floats / Rp));
   out.in_rows.assign((size_t)ncomp * C * R, -1);
   out.in_count.assign((size_t)ncomp * C, 0);
   for (int c = 0; c < ncomp; ++c)
     for (int b = 0; b < (int)bins[c].size(); ++b) {
       const auto &rows = bins[c][b];
       for (size_t q = 0; q < rows.size(); ++q) {
-        slot[rows[q]] = (b << 8) | (int32_t)q;
+        slot[rows[q]] = (b << 10) | (int32_t)q;
         bin_of_sub[sub.find(rows[q])] = b;
         out.in_rows[((size_t)c * C + b) * R + q] = rows[q];
       }
@@ -290,11 +304,11 @@ void build_pass(const std::vector<const PackedLayer *> &layers, int32_t n, const
         H.k[rec] = (uint8_t)K;
         H.g[rec] = (uint8_t)G;
         // keeps the ascending source order (canonical chain); non-last layers read
-        // their own CTA's slots, the last layer the (bin << 8 | slot) code
+        // their own CTA's slots, the last layer the (bin << 10 | slot) code
         int32_t code[32];
         for (int t = 0; t < K; ++t) {
           code[t] = slot[in0 + p.src[(size_t)g * p.kmax + t]];
-          H.src[rec * 32 + t] = (uint16_t)(last ? code[t] : (code[t] & 0xff));
+          H.src[rec * 32 + t] = (uint16_t)(last ? code[t] : (code[t] & 0x3ff));
         }
         for (int u = 0; u < G; ++u) {
           const int32_t j = p.col[(size_t)g * p.gmax + u];
@@ -307,6 +321,26 @@ void build_pass(const std::vector<const PackedLayer *> &layers, int32_t n, const
       }
   }
   // ---- per-(component, bin) records ----
+  // a layer whose members all carry the same bias (bitwise) stores it once (bu)
+  for (int b = 0; b < m; ++b) {
+    PassHostLayer &H = out.layers[b];
+    bool first = true, uni = true;
+    uint32_t ref = 0;
+    for (size_t r = 0; r < H.g.size() && uni; ++r)
+      for (int u = 0; u < H.g[r]; ++u) {
+        uint32_t bits;
+        std::memcpy(&bits, &H.bias[r * 32 + u], 4);
+        if (first) {
+          ref = bits;
+          first = false;
+        } else if (bits != ref) {
+          uni = false;
+          break;
+        }
+      }
+    H.bias_uniform = uni;
+    std::memcpy(&H.bu, &ref, 4);
+  }
   int32_t off = 0;
   for (int b = 0; b < m; ++b) {
     PassHostLayer &H = out.layers[b];
@@ -314,8 +348,11 @@ void build_pass(const std::vector<const PackedLayer *> &layers, int32_t n, const
     off += (H.NG * 2 + 15) / 16 * 16;
     H.off_src = off;
     off += H.NG * 64;
-    H.off_bias = off;
-    off += H.NG * 128;
+    H.off_bias = -1;
+    if (!H.bias_uniform) {
+      H.off_bias = off;
+      off += H.NG * 128;
+    }
     if (b == m - 1) {
       H.off_orow = off;
       off += H.NG * 128;
@@ -334,7 +371,7 @@ void build_pass(const std::vector<const PackedLayer *> &layers, int32_t n, const
         std::memcpy(r + H.off_kg + 2 * q, &kg, 2);
       }
       std::memcpy(r + H.off_src, H.src.data() + g0 * 32, (size_t)H.NG * 64);
-      std::memcpy(r + H.off_bias, H.bias.data() + g0 * 32, (size_t)H.NG * 128);
+      if (H.off_bias >= 0) std::memcpy(r + H.off_bias, H.bias.data() + g0 * 32, (size_t)H.NG * 128);
       if (H.off_orow >= 0) std::memcpy(r + H.off_orow, H.orow.data() + g0 * 32, (size_t)H.NG * 128);
     }
   }
@@ -343,48 +380,42 @@ void build_pass(const std::vector<const PackedLayer *> &layers, int32_t n, const
 std::vector<Step> plan_passes(const std::vector<const PackedLayer *> &layers, int32_t n, int cap,
                               int max_m, int tile_floats, int threads,
                               std::vector<PassHost> *built) {
-  std::vector<Step> steps = plan_steps(layers, n, cap, max_m);
+  std::vector<Step> steps = plan_steps(layers, n, cap, max_m, 0);
   std::vector<PassHost> ph(steps.size());
   std::vector<char> done(steps.size(), 0);
   for (;;) {
     std::vector<int> todo;
     for (int i = 0; i < (int)steps.size(); ++i)
       if (steps[i].m > 1 && !done[i]) todo.push_back(i);
-    if (todo.empty()) break;
     std::atomic<int> next{0};
     std::vector<std::thread> th;
     const int nt = std::max(1, std::min<int>(threads, (int)todo.size()));
-    for (int t = 0; t < nt; ++t)
+    for (int t = 0; t < nt && !todo.empty(); ++t)
       th.emplace_back([&] {
         for (int q = next++; q < (int)todo.size(); q = next++)
           build_pass(layers, n, steps[todo[q]], tile_floats, ph[todo[q]]);
       });
     for (auto &x : th) x.join();
-    // split passes whose record does not fit (any sub-range of a pass is a pass)
-    std::vector<Step> s2;
-    std::vector<PassHost> p2;
-    std::vector<char> d2;
-    for (int i = 0; i < (int)steps.size(); ++i) {
-      const Step &S = steps[i];
-      if (S.m > 1 && ph[i].rec_bytes > kPassRecMax) {
-        Step lo = S, hi = S;
-        lo.m = S.m / 2;
-        hi.a = S.a + lo.m;
-        hi.m = S.m - lo.m;
-        for (const Step &x : {lo, hi}) {
-          s2.push_back(x);
-          p2.emplace_back();
-          d2.push_back(x.m == 1);
-        }
-      } else {
-        s2.push_back(S);
-        p2.push_back(std::move(ph[i]));
-        d2.push_back(1);                    // built in this round or before
-      }
+    for (int i : todo) done[i] = 1;
+    // the first pass whose record does not fit loses its last layer, and the
+    // layers after it are planned again (any prefix of a pass is a pass)
+    int bad = -1;
+    for (int i = 0; i < (int)steps.size() && bad < 0; ++i)
+      if (steps[i].m > 1 && ph[i].rec_bytes > kPassRecMax) bad = i;
+    if (bad < 0) break;
+    Step &S = steps[bad];
+    S.m -= 1;
+    const int resume = S.a + S.m;
+    steps.resize(bad + 1);
+    ph.resize(bad + 1);
+    done.resize(bad + 1);
+    done[bad] = S.m == 1;
+    ph[bad] = PassHost();
+    for (const Step &x : plan_steps(layers, n, cap, max_m, resume)) {
+      steps.push_back(x);
+      ph.emplace_back();
+      done.push_back(0);
     }
-    steps.swap(s2);
-    ph.swap(p2);
-    done.swap(d2);
   }
   if (built) built->swap(ph);
   return steps;

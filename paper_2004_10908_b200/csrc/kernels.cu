@@ -484,44 +484,54 @@ __global__ void k_y0_positive(int64_t batch, const int64_t *__restrict__ rowptr,
 // Fused multi-layer pass (model decomposition, fuse.cpp; the default plan).  An
 // item is (component c, batch tile of T positions).  The component's rows are
 // split over C CTAs (C = 1, or a thread-block cluster of 2 / 4): CTA `rank`
-// owns up to 128 rows -- the sub-components of the pass's first m-1 layers
-// bin-packed at plan time -- as one 64 KB shared-memory tile loaded with one
-// cp.async.bulk per row (T*4 = 512 B - 2 KB), plus its metadata record (source
-// slots, biases, output rows; <= 8 KB) on the same mbarrier.  Layers 0..m-2
-// run in place in the CTA's tile: a group's chain reads its source slots, then
-// its members overwrite those slots (legal because every non-last layer's
-// source rows each feed one group and G_g <= K_g).  The last layer reads its
-// sources from any CTA of the cluster (C > 1: mapa + ld.shared::cluster after a
-// cluster barrier) and stores the member rows straight to HBM.  As soon as the
-// last layer's chains have read the tiles (a second barrier) the next item's
-// copies are issued, before the stores.  NW warps; a unit is (group, slice of
-// 32*V positions), V positions per lane.  HBM traffic per layer drops by m.
+// owns up to 512 rows -- the sub-components of the pass's first m-1 layers
+// bin-packed at plan time -- as one 64 KB shared-memory tile (R rows x T
+// positions, R*T = 16384, T = 32..512) loaded with one cp.async.bulk per row
+// (128 B - 2 KB segments; tools/segbench.cu: 0.70 / 0.88 / 0.88 / 0.92 of the
+// copy peak at 128 / 256 / 512 / 1024 B), plus its metadata record (source
+// slots, biases unless uniform, output rows; <= 8 KB) on the same mbarrier.
+// Layers 0..m-2 run in place in the CTA's tile: a group's chain reads its
+// source slots, then its members overwrite those slots (legal because every
+// non-last layer's source rows each feed one group and G_g <= K_g).  The last
+// layer reads its sources from any CTA of the cluster (C > 1: mapa +
+// ld.shared::cluster after a cluster barrier) and stores the member rows
+// straight to HBM.  As soon as the last layer's chains have read the tiles (a
+// second barrier) the next item's copies are issued, before the stores.  Four
+// warps; a unit is (group, slice of 32*V positions), V = min(4, T/32)
+// positions per lane, UM = 4/V units per warp processed together (independent
+// chains for ILP).  HBM traffic per layer drops by m.
 // ---------------------------------------------------------------------------
 constexpr int kPassTile = 16384;                 // floats per CTA tile (R * T)
 constexpr int kPassMaxT = 512;
+constexpr int kPassNW = 4;                       // warps per CTA
 constexpr size_t kPassSmem =
     (size_t)kPassTile * 4 + kPassRecMax + 16 + kMaxPassLayers * (kPassMaxT / 32) * 4;
 
 int pass_tile_floats() { return kPassTile; }
 
+// (T, C, X2) instances; a cluster pass fills its first CTA beyond half of
+// pass_cta_rows() (first-fit bins), hence T = 16384 / pass_cta_rows().  X2
+// (packed FFMA2/FADD2) is the cluster default; SDNN_PASS_X2=1 selects it for
+// single-CTA passes too.
 #define SDNN_PASS_VARIANTS(X)                                                                    \
-  X(128, 4, 4, 1, false) X(256, 4, 4, 1, false) X(512, 4, 4, 1, false) X(128, 4, 4, 1, true)    \
-  X(128, 4, 4, 2, true) X(128, 4, 4, 4, true)                                                   \
-  X(128, 2, 8, 1, true) X(256, 2, 8, 1, true) X(512, 2, 8, 1, true) X(128, 2, 8, 2, true)       \
-  X(128, 2, 8, 4, true)
+  X(32, 1, false) X(64, 1, false) X(128, 1, false) X(256, 1, false) X(512, 1, false)           \
+  X(32, 1, true) X(64, 1, true) X(128, 1, true) X(256, 1, true) X(512, 1, true) X(32, 2, true) \
+  X(32, 4, true) X(64, 2, true) X(64, 4, true) X(128, 2, true) X(128, 4, true)
 
-// X2: packed fp32x2 arithmetic (FFMA2 / FADD2, sm_100; per component identical
-// to __fmaf_rn / __fadd_rn) and liveness from the OR of the output bit patterns
-// (y is +0 exactly when dead: z is never -0, see clampy).  Measured on C4
-// (same box): X2 speeds up the cluster passes (2726 -> 2620 ms/step) but slows
-// the single-CTA passes (2755 -> 2832 at cap 128), whose per-member compare
-// work paces their HBM stores; launch_pass picks X2 = (C > 1).
-template <int V, bool X2>
-struct PassVec;
-template <>
-struct PassVec<4, true> {
-  using T = float4;
-  __device__ static void acc(const T &v, float w, float (&a)[4]) {
+bool pass_variant(int T, int C) {
+#define X(TT, CC, XX) \
+  if (T == TT && C == CC) return true;
+  SDNN_PASS_VARIANTS(X)
+#undef X
+  return false;
+}
+
+
+// Lane arithmetic on 4 consecutive positions.  X2: packed fp32x2 FFMA2 / FADD2
+// (sm_100; per component identical to __fmaf_rn / __fadd_rn).
+template <bool X2>
+__device__ __forceinline__ void acc4(float (&a)[4], const float4 &v, float w) {
+  if (X2) {
     const float2 w2 = make_float2(w, w);
     const float2 lo = __ffma2_rn(make_float2(v.x, v.y), w2, make_float2(a[0], a[1]));
     const float2 hi = __ffma2_rn(make_float2(v.z, v.w), w2, make_float2(a[2], a[3]));
@@ -529,78 +539,44 @@ struct PassVec<4, true> {
     a[1] = lo.y;
     a[2] = hi.x;
     a[3] = hi.y;
-  }
-  __device__ static T out(const float (&a)[4], float b, float ymax, uint32_t (&o)[4]) {
-    const float2 b2 = make_float2(b, b);
-    const float2 lo = __fadd2_rn(make_float2(a[0], a[1]), b2);
-    const float2 hi = __fadd2_rn(make_float2(a[2], a[3]), b2);
-    T y;
-    y.x = clampy(lo.x, ymax);
-    y.y = clampy(lo.y, ymax);
-    y.z = clampy(hi.x, ymax);
-    y.w = clampy(hi.y, ymax);
-    o[0] |= __float_as_uint(y.x);
-    o[1] |= __float_as_uint(y.y);
-    o[2] |= __float_as_uint(y.z);
-    o[3] |= __float_as_uint(y.w);
-    return y;
-  }
-  __device__ static uint32_t bits(const uint32_t (&o)[4]) {
-    return (o[0] ? 1u : 0u) | (o[1] ? 2u : 0u) | (o[2] ? 4u : 0u) | (o[3] ? 8u : 0u);
-  }
-  __device__ static T ld_cluster(uint32_t addr) { return ld_cluster_f4(addr); }
-};
-template <>
-struct PassVec<4, false> {
-  using T = float4;
-  __device__ static void acc(const T &v, float w, float (&a)[4]) {
+  } else {
     a[0] = __fmaf_rn(v.x, w, a[0]);
     a[1] = __fmaf_rn(v.y, w, a[1]);
     a[2] = __fmaf_rn(v.z, w, a[2]);
     a[3] = __fmaf_rn(v.w, w, a[3]);
   }
-  __device__ static T out(const float (&a)[4], float b, float ymax, uint32_t (&o)[4]) {
-    T y;
-    y.x = clampy(__fadd_rn(a[0], b), ymax);
-    y.y = clampy(__fadd_rn(a[1], b), ymax);
-    y.z = clampy(__fadd_rn(a[2], b), ymax);
-    y.w = clampy(__fadd_rn(a[3], b), ymax);
-    o[0] |= (y.x > 0.f ? 1u : 0u) | (y.y > 0.f ? 2u : 0u) | (y.z > 0.f ? 4u : 0u) | (y.w > 0.f ? 8u : 0u);
-    return y;
+}
+// y = clamp(acc + b); o |= bit pattern (y is +0 exactly when dead: z is never -0)
+template <bool X2>
+__device__ __forceinline__ float4 out4(const float (&a)[4], float b, float ymax, uint32_t &o) {
+  float4 y;
+  if (X2) {
+    const float2 b2 = make_float2(b, b);
+    const float2 lo = __fadd2_rn(make_float2(a[0], a[1]), b2);
+    const float2 hi = __fadd2_rn(make_float2(a[2], a[3]), b2);
+    y = make_float4(clampy(lo.x, ymax), clampy(lo.y, ymax), clampy(hi.x, ymax), clampy(hi.y, ymax));
+  } else {
+    y = make_float4(clampy(__fadd_rn(a[0], b), ymax), clampy(__fadd_rn(a[1], b), ymax),
+                    clampy(__fadd_rn(a[2], b), ymax), clampy(__fadd_rn(a[3], b), ymax));
   }
-  __device__ static uint32_t bits(const uint32_t (&o)[4]) { return o[0]; }
-  __device__ static T ld_cluster(uint32_t addr) { return ld_cluster_f4(addr); }
-};
-template <>
-struct PassVec<2, true> {
-  using T = float2;
-  __device__ static void acc(const T &v, float w, float (&a)[2]) {
-    const float2 r = __ffma2_rn(v, make_float2(w, w), make_float2(a[0], a[1]));
-    a[0] = r.x;
-    a[1] = r.y;
-  }
-  __device__ static T out(const float (&a)[2], float b, float ymax, uint32_t (&o)[2]) {
-    const float2 z = __fadd2_rn(make_float2(a[0], a[1]), make_float2(b, b));
-    T y;
-    y.x = clampy(z.x, ymax);
-    y.y = clampy(z.y, ymax);
-    o[0] |= __float_as_uint(y.x);
-    o[1] |= __float_as_uint(y.y);
-    return y;
-  }
-  __device__ static uint32_t bits(const uint32_t (&o)[2]) { return (o[0] ? 1u : 0u) | (o[1] ? 2u : 0u); }
-  __device__ static T ld_cluster(uint32_t addr) { return ld_cluster_f2(addr); }
-};
+  o |= (__float_as_uint(y.x) ? 1u : 0u) | (__float_as_uint(y.y) ? 2u : 0u) |
+       (__float_as_uint(y.z) ? 4u : 0u) | (__float_as_uint(y.w) ? 8u : 0u);
+  return y;
+}
 
-template <int T, int V, int NW, int C, bool X2>
-__global__ void __launch_bounds__(32 * NW, 3)
+template <int T, int C, bool X2>
+__global__ void __launch_bounds__(32 * kPassNW, 3)
     k_pass(const DevPass P, const LayerState *__restrict__ st, float *Ya, float *Yb,
            uint32_t *__restrict__ alive, int64_t wstride, int64_t stride, float ymax) {
-  using PV = PassVec<V, X2>;
-  using VT = typename PV::T;
-  constexpr int SW = 32 * V;                     // positions per slice (one warp)
+  constexpr int NW = kPassNW;
+  constexpr int SW = T < 128 ? T : 128;          // positions per unit (4 per lane)
   constexpr int S = T / SW;                      // slices per tile
+  constexpr int LPU = SW / 4;                    // lanes per unit: 8 / 16 / 32
+  constexpr int UPW = 32 / LPU;                  // units per warp (lane segments)
+  constexpr int EPL = 32 / LPU;                  // group entries per lane (slot, bias, row)
+  constexpr int WPS = SW / 32;                   // liveness words per unit
   constexpr int W = T / 32;                      // liveness words per tile
+  constexpr int RPT = kMaxPassRows / (32 * NW);  // input rows per thread
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float *tile_s = reinterpret_cast<float *>(smem_raw);
   unsigned char *rec_s = smem_raw + (size_t)kPassTile * 4;
@@ -614,6 +590,7 @@ __global__ void __launch_bounds__(32 * NW, 3)
   const int tiles = (width + T - 1) / T;
   const int64_t items = (int64_t)P.ncomp * tiles;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int seg = lane / LPU, sll = lane % LPU;  // segment (unit) of the lane, lane in it
   const uint32_t rank = C > 1 ? cluster_rank() : 0u;
   const int64_t cid = C > 1 ? (int64_t)cluster_id_x() : (int64_t)blockIdx.x;
   const int64_t ncl = C > 1 ? (int64_t)nclusters_x() : (int64_t)gridDim.x;
@@ -624,12 +601,16 @@ __global__ void __launch_bounds__(32 * NW, 3)
   }
   for (int q = tid; q < kMaxPassLayers * W; q += blockDim.x) aw[q] = 0u;
   __syncthreads();
-  // rin <= 128 <= blockDim.x: thread r owns input row r of an item
-  int nrow = 0, ncnt = 0;
+  // thread tid owns input rows tid + 128 q of an item
+  int nrow[RPT], ncnt = 0;
   auto fetch_rows = [&](int64_t it) {
     const int64_t cb = (it / tiles) * C + rank;
     ncnt = __ldg(P.in_count + cb);
-    nrow = tid < P.rin ? __ldg(P.in_rows + cb * P.rin + tid) : 0;
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+      const int r = tid + q * 32 * NW;
+      nrow[q] = r < P.rin ? __ldg(P.in_rows + cb * P.rin + r) : 0;
+    }
   };
   auto issue_load = [&](int64_t it) {
     const int64_t c = it / tiles;
@@ -639,16 +620,17 @@ __global__ void __launch_bounds__(32 * NW, 3)
       mbar_expect_tx_arrive(bar, (uint32_t)ncnt * T * 4 + (uint32_t)P.rec_bytes);
       bulk_g2s(rec_s, P.rec + cb * P.rec_bytes, P.rec_bytes, bar);
     }
-    if (tid < ncnt)
-      bulk_g2s(tile_s + (size_t)tid * T, Yin + (int64_t)nrow * stride + (int64_t)tile * T, T * 4, bar);
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+      const int r = tid + q * 32 * NW;
+      if (r < ncnt)
+        bulk_g2s(tile_s + (size_t)r * T, Yin + (int64_t)nrow[q] * stride + (int64_t)tile * T, T * 4, bar);
+    }
   };
   auto release = [&]() {                         // every reader of every tile is done
     if (C > 1) cluster_sync();
     else __syncthreads();
   };
-  // the last layer releases the tiles before its HBM stores when every warp owns
-  // at most one (group, slice) unit of it
-  const bool early = P.layers[P.m - 1].NG * S <= NW;
   if (cid < items) {
     fetch_rows(cid);
     issue_load(cid);
@@ -664,89 +646,119 @@ __global__ void __launch_bounds__(32 * NW, 3)
     for (int j = 0; j < P.m; ++j) {
       const PassLayerDev PL = P.layers[j];
       const bool last = j == P.m - 1;
+      const bool remote = C > 1 && last;         // sources anywhere in the cluster
       const float wu = PL.wu;
+      const bool ubias = PL.off_bias < 0;
       const int units = PL.NG * S;
       const uint16_t *kg_s = reinterpret_cast<const uint16_t *>(rec_s + PL.off_kg);
       const uint16_t *src_s = reinterpret_cast<const uint16_t *>(rec_s + PL.off_src);
-      const float *bias_s = reinterpret_cast<const float *>(rec_s + PL.off_bias);
-      if (C > 1 && last) cluster_sync();         // every CTA's tile is at boundary m-1
-      for (int u0 = 0; u0 < (last && early ? NW : units); u0 += NW) {
-        const int u = u0 + warp;
-        const bool active = u < units;
-        int G = 0, K = 0, sl = 0, gi = 0;
-        if (active) {
+      const float *bias_s = reinterpret_cast<const float *>(rec_s + (ubias ? 0 : PL.off_bias));
+      const int32_t *orow_s = reinterpret_cast<const int32_t *>(rec_s + (last ? PL.off_orow : 0));
+      // the last layer releases the tiles before its HBM stores when every warp
+      // owns at most one unit per segment (one round)
+      const bool early = last && units <= NW * UPW;
+      if (remote) cluster_sync();                // every CTA's tile is at boundary m-1
+      for (int u0 = 0; u0 < units; u0 += NW * UPW) {
+        const int u = u0 + warp * UPW + seg;
+        int K = 0, G = 0, gi = 0, sl = 0;
+        if (u < units) {
           gi = u / S;
           sl = u - gi * S;
           const uint32_t kg = kg_s[gi];
           K = kg & 0xffu;
           G = kg >> 8;
         }
-        const int pofs = sl * SW + lane * V;
-        const float mybias = (active && lane < G) ? bias_s[gi * 32 + lane] : 0.f;
-        int mysrc = 0;                           // local slot offset (floats)
-        uint32_t myaddr = 0;                     // C > 1, last layer: row base in its owner CTA
-        if (active && lane < K) {
-          const uint32_t code = src_s[gi * 32 + lane];
-          if (C > 1 && last)
-            myaddr = cluster_map(tile_u32 + (code & 0xffu) * (T * 4), code >> 8);
-          else
-            mysrc = (int)(code & 0xffu) * T;
-        }
-        float *myrow = nullptr;
-        if (last)                                // lane v: member v's output row base
-          myrow = Yout + (int64_t)tile * T + sl * SW +
-                  ((active && lane < G)
-                       ? (int64_t)reinterpret_cast<const int32_t *>(rec_s + PL.off_orow)[gi * 32 + lane] * stride
-                       : 0);
-        float acc[V];
+        const int pofs = sl * SW + sll * 4;      // this lane's 4 positions in the tile
+        // entry e = r * LPU + sll of the group: source slot (a term past K points
+        // at source 0 with weight 0: fmaf(x, 0, acc) == acc for finite x, acc != -0)
+        uint32_t soff[EPL];                      // float offset in the tile / cluster address
+        float bia[EPL];
+        int32_t orw[EPL];
 #pragma unroll
-        for (int e = 0; e < V; ++e) acc[e] = 0.f;
-        if (G > 0) {
-          if (C > 1 && last) {
-#pragma unroll 8
-            for (int t = 0; t < K; ++t)
-              PV::acc(PV::ld_cluster(__shfl_sync(FULL, myaddr, t) + (uint32_t)(pofs * 4)), wu, acc);
+        for (int r = 0; r < EPL; ++r) {
+          const int e = r * LPU + sll;
+          const uint32_t code = K > 0 ? src_s[gi * 32 + (e < K ? e : 0)] : 0u;
+          soff[r] = remote ? cluster_map(tile_u32 + (code & 0x3ffu) * (T * 4), code >> 10)
+                           : (code & 0x3ffu) * T;
+          bia[r] = (!ubias && e < G) ? bias_s[gi * 32 + e] : 0.f;
+          orw[r] = (last && e < G) ? orow_s[gi * 32 + e] : 0;
+        }
+        const int kmax = __reduce_max_sync(FULL, K);
+        const bool fullk = __all_sync(FULL, K == kmax || K == 0);
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+        // the canonical chain: terms in ascending source order.  Fast path (every
+        // unit of the warp has kmax == 32 terms): no per-term conditions, so the
+        // loads (DSMEM: ~200 cycles) issue back to back ahead of their FMAs.
+        if (kmax == 32 && fullk) {
+          if (remote) {
+#pragma unroll
+            for (int r = 0; r < EPL; ++r)
+#pragma unroll
+              for (int l = 0; l < LPU; ++l)
+                acc4<X2>(acc, ld_cluster_f4(__shfl_sync(FULL, soff[r], l, LPU) + (uint32_t)(pofs * 4)), wu);
           } else {
-#pragma unroll 8
-            for (int t = 0; t < K; ++t)
-              PV::acc(*reinterpret_cast<const VT *>(tile_s + __shfl_sync(FULL, mysrc, t) + pofs), wu, acc);
+#pragma unroll
+            for (int r = 0; r < EPL; ++r)
+#pragma unroll
+              for (int l = 0; l < LPU; ++l)
+                acc4<X2>(acc, *reinterpret_cast<const float4 *>(tile_s + __shfl_sync(FULL, soff[r], l, LPU) + pofs),
+                         wu);
+          }
+        } else {
+#pragma unroll
+          for (int r = 0; r < EPL; ++r) {
+            if (r * LPU >= kmax) break;
+#pragma unroll 4
+            for (int l = 0; l < LPU; ++l) {
+              const int t = r * LPU + l;
+              const uint32_t so = __shfl_sync(FULL, soff[r], l, LPU);
+              if (t < kmax) {
+                const float w = t < K ? wu : 0.f;
+                if (remote) acc4<X2>(acc, ld_cluster_f4(so + (uint32_t)(pofs * 4)), w);
+                else acc4<X2>(acc, *reinterpret_cast<const float4 *>(tile_s + so + pofs), w);
+              }
+            }
           }
         }
-        if (last && early) {
+        if (early) {
           // generic-proxy tile reads/writes before the next item's TMA writes
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           release();
           if (next < items) issue_load(next);
           issued = true;
         }
-        if (G == 0) continue;
-        uint32_t o[V];                           // per member, between the stores
+        const int gmax = __reduce_max_sync(FULL, G);
+        uint32_t o = 0u;
+        // members: uniform bias => every member of the group has the same value
+        float4 yu = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (ubias && G > 0) yu = out4<X2>(acc, PL.bu, ymax, o);
+        float *obase = Yout + (int64_t)tile * T + pofs;
 #pragma unroll
-        for (int e = 0; e < V; ++e) o[e] = 0u;
-        if (last) {
-          for (int v = 0; v < G; ++v) {
-            float *row = reinterpret_cast<float *>(__shfl_sync(FULL, reinterpret_cast<uintptr_t>(myrow), v));
-            const VT y = PV::out(acc, __shfl_sync(FULL, mybias, v), ymax, o);
-            *reinterpret_cast<VT *>(row + lane * V) = y;
-          }
-        } else {
-          for (int v = 0; v < G; ++v) {          // member v overwrites source slot v (in place)
-            const int off = __shfl_sync(FULL, mysrc, v);
-            const VT y = PV::out(acc, __shfl_sync(FULL, mybias, v), ymax, o);
-            *reinterpret_cast<VT *>(tile_s + off + pofs) = y;
+        for (int r = 0; r < EPL; ++r) {
+          if (r * LPU >= gmax) break;
+#pragma unroll 8
+          for (int l = 0; l < LPU; ++l) {
+            const int v = r * LPU + l;           // member v (owns source slot v when in place)
+            const int32_t dst = last ? __shfl_sync(FULL, orw[r], l, LPU)
+                                     : (int32_t)__shfl_sync(FULL, soff[r], l, LPU);
+            const float bv = ubias ? 0.f : __shfl_sync(FULL, bia[r], l, LPU);
+            if (v < G) {
+              const float4 y = ubias ? yu : out4<X2>(acc, bv, ymax, o);
+              if (last) *reinterpret_cast<float4 *>(obase + (int64_t)dst * stride) = y;
+              else *reinterpret_cast<float4 *>(tile_s + dst + pofs) = y;
+            }
           }
         }
-        const uint32_t am = PV::bits(o);
-        // liveness: lane L holds positions sl*SW + L*V + e; word sl*V + q of the
-        // tile has bit b = position q*32 + b of the slice -> lane (q*32+b)/V, e = b%V
-        uint32_t bal[V];
+        // liveness: lane sll of a segment holds positions sl*SW + 4 sll + e; word
+        // w of the unit has bit b = position 32 w + b -> lane (32 w + b) / 4, e = b % 4
+        uint32_t bal[4];
 #pragma unroll
-        for (int e = 0; e < V; ++e) bal[e] = __ballot_sync(FULL, (am >> e) & 1u);
-        if (lane < V) {
+        for (int e = 0; e < 4; ++e) bal[e] = __ballot_sync(FULL, (o >> e) & 1u);
+        if (sll < WPS && G > 0) {
           uint32_t word = 0;
 #pragma unroll
-          for (int b = 0; b < 32; ++b) word |= ((bal[b % V] >> (lane * (32 / V) + b / V)) & 1u) << b;
-          if (word) atomicOr(&aw[j * W + sl * V + lane], word);
+          for (int b = 0; b < 32; ++b) word |= ((bal[b & 3] >> (seg * LPU + sll * 8 + (b >> 2))) & 1u) << b;
+          if (word) atomicOr(&aw[j * W + sl * WPS + sll], word);
         }
       }
       __syncthreads();                           // the next layer reads slots other warps wrote
@@ -1012,30 +1024,20 @@ void configure_kernels() {
         b.ctas <= 4)
       g_bulk = b;
   }
-#define X(TT, VV, NN, CC, XX) \
-  cudaFuncSetAttribute(k_pass<TT, VV, NN, CC, XX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPassSmem);
+#define X(TT, CC, XX) \
+  cudaFuncSetAttribute(k_pass<TT, CC, XX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPassSmem);
   SDNN_PASS_VARIANTS(X)
 #undef X
 }
 
-// pass-kernel shape: V positions per lane and NW warps (default V = 4: 4 warps
-// of float4 lanes; SDNN_PASS_V = 2: 8 warps of float2 lanes)
-static int pass_v() {
-  static const int v = [] {
-    const char *e = getenv("SDNN_PASS_V");
-    return (e && atoi(e) == 2) ? 2 : 4;
-  }();
-  return v;
-}
-
 // clusters of C CTAs that can be co-resident
-template <int T, int V, int NW, int C, bool X2>
+template <int T, int C, bool X2>
 static int pass_clusters(int sms) {
   static int cached = 0;
   if (cached) return cached;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(C * sms * 3);
-  cfg.blockDim = dim3(32 * NW);
+  cfg.blockDim = dim3(32 * kPassNW);
   cfg.dynamicSmemBytes = kPassSmem;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
@@ -1045,7 +1047,7 @@ static int pass_clusters(int sms) {
   cfg.attrs = at;
   cfg.numAttrs = 1;
   int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, k_pass<T, V, NW, C, X2>, &cfg) != cudaSuccess || n <= 0) {
+  if (cudaOccupancyMaxActiveClusters(&n, k_pass<T, C, X2>, &cfg) != cudaSuccess || n <= 0) {
     cudaGetLastError();
     n = sms * 3 / C / 2;                         // conservative
   }
@@ -1053,17 +1055,17 @@ static int pass_clusters(int sms) {
   return n;
 }
 
-template <int T, int V, int NW, int C, bool X2>
+template <int T, int C, bool X2>
 static void launch_pass_t(const LaunchCfg &c, const Workspace &w, const DevPass &P, uint32_t *alive,
                           float ymax, cudaStream_t s) {
   if (C == 1) {
-    k_pass<T, V, NW, 1, X2><<<c.sms * 3, 32 * NW, kPassSmem, s>>>(P, w.st, w.Y[0], w.Y[1], alive, w.words,
-                                                              w.stride, ymax);
+    k_pass<T, 1, X2><<<c.sms * 3, 32 * kPassNW, kPassSmem, s>>>(P, w.st, w.Y[0], w.Y[1], alive, w.words,
+                                                            w.stride, ymax);
     return;
   }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(C * pass_clusters<T, V, NW, C, X2>(c.sms));
-  cfg.blockDim = dim3(32 * NW);
+  cfg.gridDim = dim3(C * pass_clusters<T, C, X2>(c.sms));
+  cfg.blockDim = dim3(32 * kPassNW);
   cfg.dynamicSmemBytes = kPassSmem;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
@@ -1073,7 +1075,7 @@ static void launch_pass_t(const LaunchCfg &c, const Workspace &w, const DevPass 
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, k_pass<T, V, NW, C, X2>, P, (const LayerState *)w.st, w.Y[0], w.Y[1], alive,
+  cudaLaunchKernelEx(&cfg, k_pass<T, C, X2>, P, (const LayerState *)w.st, w.Y[0], w.Y[1], alive,
                      (int64_t)w.words, (int64_t)w.stride, ymax);
 }
 
@@ -1130,27 +1132,20 @@ void launch_layer(const LaunchCfg &c, const Workspace &w, const DevLayer &L, int
 
 void launch_pass(const LaunchCfg &c, const Workspace &w, const DevPass &P, uint32_t *alive,
                  float ymax, cudaStream_t s) {
-  static const int x2_c1 = [] {                  // SDNN_PASS_X2=1: packed path for C = 1 too
+  static const bool x2_c1 = [] {                 // SDNN_PASS_X2=1: packed path for C = 1 too
     const char *e = getenv("SDNN_PASS_X2");
-    return e ? atoi(e) : 0;
+    return e && atoi(e) != 0;
   }();
-  const bool v4 = pass_v() == 4;
-  if (P.C == 4) {
-    if (v4) launch_pass_t<128, 4, 4, 4, true>(c, w, P, alive, ymax, s);
-    else launch_pass_t<128, 2, 8, 4, true>(c, w, P, alive, ymax, s);
-  } else if (P.C == 2) {
-    if (v4) launch_pass_t<128, 4, 4, 2, true>(c, w, P, alive, ymax, s);
-    else launch_pass_t<128, 2, 8, 2, true>(c, w, P, alive, ymax, s);
-  } else if (P.T == 512) {
-    if (v4) launch_pass_t<512, 4, 4, 1, false>(c, w, P, alive, ymax, s);
-    else launch_pass_t<512, 2, 8, 1, true>(c, w, P, alive, ymax, s);
-  } else if (P.T == 256) {
-    if (v4) launch_pass_t<256, 4, 4, 1, false>(c, w, P, alive, ymax, s);
-    else launch_pass_t<256, 2, 8, 1, true>(c, w, P, alive, ymax, s);
-  } else {
-    if (!v4) launch_pass_t<128, 2, 8, 1, true>(c, w, P, alive, ymax, s);
-    else if (x2_c1) launch_pass_t<128, 4, 4, 1, true>(c, w, P, alive, ymax, s);
-    else launch_pass_t<128, 4, 4, 1, false>(c, w, P, alive, ymax, s);
+  const bool x2 = P.C > 1 || x2_c1;
+  switch (P.C * 1024 + P.T + (x2 ? 4096 * 4 : 0)) {
+#define X(TT, CC, XX)                                        \
+  case CC * 1024 + TT + (XX ? 4096 * 4 : 0):                 \
+    launch_pass_t<TT, CC, XX>(c, w, P, alive, ymax, s);      \
+    return;
+    SDNN_PASS_VARIANTS(X)
+#undef X
+    default:
+      break;                                     // make_plan rejects other shapes (pass_variant)
   }
 }
 

@@ -101,7 +101,10 @@ struct LayerState {
 // canonical ascending-source fmaf sequence.
 // ---------------------------------------------------------------------------
 constexpr int kMaxPassLayers = 16;
-constexpr int kMaxPassRows = 128;      // slots per CTA (one 64 KB tile of >= 128 positions)
+constexpr int kMaxPassRows = 512;      // slots per CTA (one 64 KB tile of >= 32 positions)
+constexpr int kDefaultPassRows = 512;  // default component cap
+constexpr int kDefaultCtaRows = 512;   // default slots per CTA (pass_cta_rows())
+int pass_cta_rows();
 constexpr int kMaxPassCluster = 4;     // CTAs per component (thread-block cluster, DSMEM)
 
 struct Step {
@@ -114,13 +117,16 @@ constexpr int32_t kResidentStep = -2;  // layers [a, L) in the SMEM-resident ker
 // every layer but the last allows in-place slots (exclusive sources,
 // G_g <= K_g), the sub-components of all layers but the last fit one CTA
 // (kMaxPassRows slots) and every component's sub-components pack into
-// cap / kMaxPassRows CTAs (cap <= kMaxPassRows * kMaxPassCluster)
+// cap / kMaxPassRows CTAs (cap <= kMaxPassRows * kMaxPassCluster); tile
+// T = 16384 / (rows per CTA rounded up to a power of two), 32 <= T <= 512
 std::vector<Step> plan_steps(const std::vector<const PackedLayer *> &layers, int32_t n, int cap,
-                             int max_m);
+                             int max_m, int a_begin = 0);
 
 struct PassHostLayer {
   int32_t NG = 0;                      // group slots per component (max over components)
   float wu = 0.f;
+  bool bias_uniform = false;           // every member's bias is bu (no bias array in the record)
+  float bu = 0.f;
   int32_t off_kg = 0, off_src = 0, off_bias = 0, off_orow = -1;  // record byte offsets
   std::vector<uint16_t> src;           // [ncomp][NG][32] smem slots of the sources
   std::vector<float> bias;             // [ncomp][NG][32] bias of each member
@@ -134,24 +140,26 @@ struct PassHost {
   std::vector<int32_t> in_count;       // [ncomp]
   std::vector<PassHostLayer> layers;   // [m]
   // per-component metadata record (one bulk copy next to the tile):
-  //   for each layer j: kg[NG_j] u16 (K | G << 8) padded to 16 B, src[NG_j][32] u16,
-  //   bias[NG_j][32] f32; last layer: orow[NG][32] i32
+  //   for each layer j: kg[NG_j] u16 (K | G << 8) padded to 16 B, src[NG_j][32] u16
+  //   slot codes (bin << 10 | slot), bias[NG_j][32] f32 unless the layer's biases
+  //   are uniform over the pass; last layer: orow[NG][32] i32
   int32_t rec_bytes = 0;
   std::vector<unsigned char> rec;      // [ncomp][rec_bytes]
 };
 constexpr int kPassRecMax = 8192;      // record bytes per component (3 CTAs per SM)
 void build_pass(const std::vector<const PackedLayer *> &layers, int32_t n, const Step &s,
                 int tile_floats, PassHost &out);
-// plan_steps, build every fused pass, and split (in halves) any pass whose
-// record exceeds kPassRecMax; `built[i]` is the PassHost of steps[i] (m > 1)
+// plan_steps, build every fused pass; a pass whose record exceeds kPassRecMax
+// drops its last layer and the rest is planned again; `built[i]` is the
+// PassHost of steps[i] (m > 1)
 std::vector<Step> plan_passes(const std::vector<const PackedLayer *> &layers, int32_t n, int cap,
                               int max_m, int tile_floats, int threads,
                               std::vector<PassHost> *built);
 
 struct PassLayerDev {
   int32_t off_kg, off_src, off_bias, off_orow;   // byte offsets in the component record
-  int32_t NG;
-  float wu;
+  int32_t NG;                                    // off_bias < 0: every bias is bu
+  float wu, bu;
 };
 struct DevPass {
   int32_t a, m, ncomp, rin, R, T, rec_bytes;
@@ -222,6 +230,7 @@ void launch_layer(const LaunchCfg &c, const Workspace &w, const DevLayer &L, int
                   uint32_t *alive, float ymax, cudaStream_t s, uint32_t *sat = nullptr);
 bool layer_tracks_saturation(const LaunchCfg &c, const DevLayer &L);
 int pass_tile_floats();        // smem floats per component tile (tile T = this / R)
+bool pass_variant(int T, int C);   // a k_pass instance exists for tile T and cluster size C
 // a fused pass: reads st[P.a], liveness of layer a+j to alive + j*words
 void launch_pass(const LaunchCfg &c, const Workspace &w, const DevPass &P, uint32_t *alive,
                  float ymax, cudaStream_t s);

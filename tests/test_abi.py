@@ -178,8 +178,8 @@ def test_plan_steps_rn_and_rr(sd):
     """Fused multi-layer passes: in a RadiX-Net layer every group is a dense
     32x32 block varying one 5-bit field of the neuron id, so the connected
     components over layers a..b span 2^|union of their fields' bits| neurons.
-    A pass keeps all layers but the last in one CTA (sub-components of <= 128
-    slots) and lets the last layer read across a cluster of cap/128 CTAs; the
+    A pass keeps all layers but the last in one CTA (sub-components of <= 512
+    slots) and lets the last layer read across a cluster of cap/512 CTAs; the
     planner extends every pass while that holds (greedy, maximal).
     Random-regular layers have one giant component and are never fused."""
     rn = list(g.iter_layers(g.rn_spec(1024, 24)))
@@ -193,22 +193,22 @@ def test_plan_steps_rn_and_rr(sd):
 
     def feasible(a, m, cap):
         sub, full = comp(a, m - 1), comp(a, m)
-        cta = min(cap, 128)
-        return sub <= cta and -(-full // (cta // sub * sub)) <= max(1, cap // 128)
+        cta = min(cap, 512)
+        return sub <= cta and -(-full // (cta // sub * sub)) <= max(1, cap // 512)
 
     default = sd.sdnn_plan_steps(1024, rn)                         # fusion on by default
     assert default == sd.sdnn_plan_steps(1024, rn, fuse_rows=512)
-    assert sd.sdnn_plan_steps(1024, rn, fuse_rows=4096) == default   # clamped to 512
-    for cap in (128, 256, 512):
+    assert sd.sdnn_plan_steps(1024, rn, fuse_rows=4096) == sd.sdnn_plan_steps(1024, rn, fuse_rows=2048)
+    for cap in (128, 256, 512, 1024, 2048):
         plan = sd.sdnn_plan_steps(1024, rn, fuse_rows=cap)
         assert sum(plan) == 24 and max(plan) > 1
         a = 0
         for m in plan:                      # every pass fits, and is maximal (greedy)
             assert m == 1 or feasible(a, m, cap)
-            if a + m < 24 and m < 8:
+            if a + m < 24 and m < 8 and cap <= 512:   # larger caps: the 8 KB record may end a pass first
                 assert not feasible(a, m + 1, cap)
             a += m
-    assert max(default) == 3                # 3-layer passes need the 4-CTA cluster
+    assert max(default) == 5                # 512-row components in one CTA: 9 of the 10 id bits
     assert max(sd.sdnn_plan_steps(1024, rn, fuse_rows=128)) == 2
     assert sd.sdnn_plan_steps(1024, rn, fuse_rows=0) == [1] * 24
     assert sd.sdnn_plan_steps(1024, rn, fuse_rows=64) == [1] * 24    # 2 layers need 128 rows
@@ -221,6 +221,7 @@ def test_plan_steps_rn_and_rr(sd):
     big = [g.gen_layer(g.rn_spec(65536, 12), l, fmt="ell") for l in range(12)]
     assert sd.sdnn_plan_steps(65536, big, fmt="ell") == [3, 3, 3, 3]
     assert sd.sdnn_plan_steps(65536, big, fmt="ell", fuse_rows=128) == [2] * 6
+    assert sd.sdnn_plan_steps(65536, big, fmt="ell", fuse_rows=2048) == [4, 2, 4, 2]   # 4-CTA clusters; field wrap after 6
 
 
 def identity_layer(n):
@@ -234,12 +235,13 @@ def identity_layer(n):
 def test_plan_splits_oversized_records(sd):
     """A pass's per-component metadata record must fit kPassRecMax (8 KB):
     [identity, rn0, rn1] forms 128-row components (plan [3] by the component cap
-    alone) but the identity layer has 128 singleton groups per component (~25 KB
-    of record), so the pass is split in halves -> [1, 2]."""
+    alone) but the identity layer has 128 singleton groups per component (~8.4 KB
+    of record with the uniform bias stored once), so the pass drops its last
+    layer and the rest is planned again -> [2, 1]."""
     n = 1024
     rn = [g.gen_layer(g.rn_spec(n, 2), l) for l in range(2)]
     assert sd.sdnn_plan_steps(n, rn) == [2]
-    assert sd.sdnn_plan_steps(n, [identity_layer(n)] + rn) == [1, 2]
+    assert sd.sdnn_plan_steps(n, [identity_layer(n)] + rn) == [2, 1]
     # two layers [identity, rn0]: 32-row components, 32 singletons (~6.5 KB) fit
     assert sd.sdnn_plan_steps(n, [identity_layer(n)] + rn, fuse_layers=2) == [2, 1]
 

@@ -131,12 +131,14 @@ def test_smem_resident_ka(sd):
 
 @pytest.mark.parametrize("fuse_rows,fuse_layers", [(0, -1), (128, -1), (256, -1),
                                                    (256, 2), (256, 16), (512, -1), (512, 3),
-                                                   (512, 16)])
+                                                   (512, 16), (1024, -1), (1024, 16),
+                                                   (2048, -1), (2048, 4)])
 def test_fused_passes_rn(sd, fuse_rows, fuse_layers):
-    """Multi-layer passes (model decomposition): single-CTA passes (cap 128)
-    and 2- / 4-CTA cluster passes whose last layer reads through distributed
-    shared memory (cap 256 / 512), pass lengths 2..16, compaction between
-    passes, ragged batch."""
+    """Multi-layer passes (model decomposition): single-CTA passes (cap <= 512:
+    tiles of 128 / 64 / 32 positions for 128- / 256- / 512-row components) and
+    2- / 4-CTA cluster passes whose last layer reads through distributed shared
+    memory (cap 1024 / 2048), pass lengths 2..16, compaction between passes,
+    ragged batch."""
     n, L, B = 1024, 40, 700
     spec = g.rn_spec(n, L)
     layers = list(g.iter_layers(spec))
@@ -161,6 +163,25 @@ def test_fused_t64_and_irregular_components(sd):
         cg, Yg, st = run_gpu(sd, n, layers, rp, idx, val, fuse_rows=cap)
         assert st["fused_layers"] > 0
         assert_parity(cg, Yg, cats, Y)
+
+
+@pytest.mark.parametrize("cap", [128, 512, 2048])
+def test_fused_nonuniform_bias(sd, cap):
+    """Per-neuron biases (record carries a bias per member) next to uniform
+    ones (stored once): RN structure with seeded biases in [-0.6, -0.2] on
+    every other layer, binary and real-valued inputs."""
+    import dataclasses
+    n, L = 1024, 20
+    layers = list(g.iter_layers(g.rn_spec(n, L)))
+    rng = np.random.default_rng(77)
+    layers = [dataclasses.replace(la, bias=rng.uniform(-0.6, -0.2, n).astype(np.float32)) if l % 2 else la
+              for l, la in enumerate(layers)]
+    rp, idx = g.ms_inputs(n, 517, seed=8)
+    cats, Y, prof = oracle.infer(n, layers, rp, idx, None, profile=True)
+    cg, Yg, st = run_gpu(sd, n, layers, rp, idx, None, fuse_rows=cap, flags=sd.SDNN_F_NO_RESIDENT)
+    assert st["fused_layers"] > 0
+    assert_parity(cg, Yg, cats, Y)
+    assert st["live_rows"] == prof
 
 
 def test_fused_ka_long_passes(sd):

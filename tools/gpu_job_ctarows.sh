@@ -1,0 +1,8 @@
+# cluster-size study: 128 / 256 / 512 slots per CTA (C = 4 / 2 / 1 for 512-row components)
+cd $GRAFT_REPO_ROOT
+for r in 128 256; do SDNN_PASS_CTA_ROWS=$r timeout 900 python -m pytest tests -m gpu -q -x -k "fused or c1_full or stream" > gpurun_out/cr_tests_$r.log 2>&1; echo "rows=$r $(tail -1 gpurun_out/cr_tests_$r.log)"; done
+for r in 128 256 512; do
+  SDNN_PASS_CTA_ROWS=$r timeout 900 python bench.py --config c4 --no-cpu-baseline --e2e-steps 1 > gpurun_out/cr_bench_$r.json 2> gpurun_out/cr_bench_$r.err
+  echo "rows=$r $(tail -1 gpurun_out/cr_bench_$r.json | python -c "import json,sys;d=json.loads(sys.stdin.read());print(round(d['ms_per_step'],1),'%.3e'%d['value'],d['roofline']['frac'],d['fuse'])")"; done
+SDNN_PASS_CTA_ROWS=256 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c4_cr256.csv python bench.py --oneshot --steps 1 --warmup 0 > /dev/null 2>&1
+python tools/ncu_summary.py launches gpurun_out/launches_c4_cr256.csv 2>&1 | head -8
