@@ -111,7 +111,7 @@ typedef struct sdnn_opts {
                           across a thread-block cluster of up to fuse_rows / 512
                           CTAs (distributed shared memory), so a component has
                           <= fuse_rows neurons (<= 2048, larger values are
-                          clamped; <= 512: single-CTA passes; 0 = off; -1 = 512) */
+                          clamped; <= 512: single-CTA passes; 0 = off; -1 = 1024) */
   int32_t fuse_layers; /* at most this many layers per pass (<= 16; -1 = 8)           */
   int32_t resident_from; /* N <= 4096: layers [resident_from, L) run in one kernel that
                           keeps each CTA's batch tile resident in shared memory

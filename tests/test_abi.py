@@ -197,7 +197,7 @@ def test_plan_steps_rn_and_rr(sd):
         return sub <= cta and -(-full // (cta // sub * sub)) <= max(1, cap // 512)
 
     default = sd.sdnn_plan_steps(1024, rn)                         # fusion on by default
-    assert default == sd.sdnn_plan_steps(1024, rn, fuse_rows=512)
+    assert default == sd.sdnn_plan_steps(1024, rn, fuse_rows=1024)
     assert sd.sdnn_plan_steps(1024, rn, fuse_rows=4096) == sd.sdnn_plan_steps(1024, rn, fuse_rows=2048)
     for cap in (128, 256, 512, 1024, 2048):
         plan = sd.sdnn_plan_steps(1024, rn, fuse_rows=cap)
@@ -208,7 +208,7 @@ def test_plan_steps_rn_and_rr(sd):
             if a + m < 24 and m < 8 and cap <= 512:   # larger caps: the 8 KB record may end a pass first
                 assert not feasible(a, m + 1, cap)
             a += m
-    assert max(default) == 5                # 512-row components in one CTA: 9 of the 10 id bits
+    assert max(sd.sdnn_plan_steps(1024, rn, fuse_rows=512)) == 5   # 512-row components: 9 of 10 id bits
     assert max(sd.sdnn_plan_steps(1024, rn, fuse_rows=128)) == 2
     assert sd.sdnn_plan_steps(1024, rn, fuse_rows=0) == [1] * 24
     assert sd.sdnn_plan_steps(1024, rn, fuse_rows=64) == [1] * 24    # 2 layers need 128 rows
@@ -219,7 +219,7 @@ def test_plan_steps_rn_and_rr(sd):
     assert sd.sdnn_plan_steps(1024, ka, fuse_layers=16) == [16, 4]
     assert max(sd.sdnn_plan_steps(1024, ka, fuse_layers=2)) == 2
     big = [g.gen_layer(g.rn_spec(65536, 12), l, fmt="ell") for l in range(12)]
-    assert sd.sdnn_plan_steps(65536, big, fmt="ell") == [3, 3, 3, 3]
+    assert sd.sdnn_plan_steps(65536, big, fmt="ell", fuse_rows=512) == [3, 3, 3, 3]
     assert sd.sdnn_plan_steps(65536, big, fmt="ell", fuse_rows=128) == [2] * 6
     assert sd.sdnn_plan_steps(65536, big, fmt="ell", fuse_rows=2048) == [4, 2, 4, 2]   # 4-CTA clusters; field wrap after 6
 

@@ -33,6 +33,16 @@ def main():
         with sd.Net.from_layers(256, lays, fmt="ell", fuse_rows=cap) as net:
             c, Y = net.infer(rp, idx, None, want_y=True)
         assert np.array_equal(c, ref[0]) and np.array_equal(Y, ref[1])
+    spec2 = g.rn_spec(1024, 8)                       # 512-row single-CTA and 2-/4-CTA cluster passes
+    lays2 = list(g.iter_layers(spec2))
+    rp2, idx2 = g.ms_inputs(1024, 200)
+    ref2 = None
+    for cap in (0, 512, 1024, 2048):
+        with sd.Net.from_layers(1024, lays2, fmt="ell", fuse_rows=cap, flags=sd.SDNN_F_NO_RESIDENT) as net:
+            c, Y = net.infer(rp2, idx2, None, want_y=True)
+        if ref2 is None:
+            ref2 = (c, Y)
+        assert np.array_equal(c, ref2[0]) and np.array_equal(Y, ref2[1])
     for rf in (0, 3):                                # SMEM-resident tail (P = 32 at N = 256)
         with sd.Net.from_layers(256, lays, fmt="ell", resident_from=rf) as net:
             c, Y = net.infer(rp, idx, None, want_y=True)
