@@ -512,3 +512,59 @@ def test_full_size_c2(sd):
 @pytest.mark.slow
 def test_full_size_c4(sd):
     _full_size(sd, 65536, 1920, 24)
+
+
+def ragged_block_layers(n, L, w, seed, sb=64, shift=0.0, bmin=1):
+    """Block-diagonal layers inside super-blocks of `sb` neurons: every layer
+    splits each super-block into dense blocks of 1..32 neurons (K = G = block
+    size, sources a seeded permutation of the block's input neurons), so fused
+    passes see groups of different K and G side by side in one warp; odd
+    layers carry per-neuron biases, even ones a uniform bias."""
+    rng = np.random.default_rng(seed)
+    layers = []
+    for l in range(L):
+        ks, js = [], []
+        for s0 in range(0, n, sb):
+            outs = s0 + rng.permutation(sb)
+            ins = s0 + rng.permutation(sb)
+            p = 0
+            while p < sb:
+                sz = int(min(sb - p, rng.integers(bmin, 33)))
+                for j in outs[p:p + sz]:
+                    for k in ins[p:p + sz]:
+                        ks.append(k)
+                        js.append(j)
+                p += sz
+        ks, js = np.array(ks, np.int64), np.array(js, np.int64)
+        o = np.lexsort((js, ks))
+        ks, js = ks[o], js[o]
+        rowptr = np.zeros(n + 1, np.int64)
+        np.add.at(rowptr, ks + 1, 1)
+        rowptr = np.cumsum(rowptr)
+        kmax = int(np.bincount(js, minlength=n).max())
+        ell = np.full((n, kmax), -1, np.int32)
+        fill = np.zeros(n, np.int64)
+        for k, j in zip(ks, js):
+            ell[j, fill[j]] = k
+            fill[j] += 1
+        bias = (rng.uniform(-0.3 + shift, shift, n) if l % 2 else np.full(n, -0.1 + shift)).astype(np.float32)
+        layers.append(g.Layer(rowptr, js.astype(np.int32), None, ell, None, float(w), bias))
+    return layers
+
+
+@pytest.mark.parametrize("sb,bmin,shift", [(64, 1, -0.8), (128, 1, -0.5), (512, 24, -0.7)])
+def test_fused_ragged_groups(sd, sb, bmin, shift):
+    """Fused passes whose groups differ in K and G inside one warp (the padded
+    zero-weight chain path, partial member loops, several unit rounds per
+    layer, late tile release), per-neuron and uniform biases, real-valued
+    inputs; components of sb rows -> tiles of 256 / 128 / 32 positions.
+    Bit-exact against the oracle."""
+    n, L = 1024, 12
+    layers = ragged_block_layers(n, L, 0.125, seed=3, sb=sb, shift=shift, bmin=bmin)
+    rp, idx, val = g.random_inputs(n, 389, seed=21, density=0.3, lo=0.0, hi=2.0)
+    cats, Y, prof = oracle.infer(n, layers, rp, idx, val, profile=True)
+    assert 0 < len(np.flatnonzero(cats)) < 389
+    cg, Yg, st = run_gpu(sd, n, layers, rp, idx, val, flags=sd.SDNN_F_NO_RESIDENT)
+    assert st["fused_layers"] >= L // 2
+    assert_parity(cg, Yg, cats, Y)
+    assert st["live_rows"] == prof
