@@ -116,8 +116,9 @@ typedef struct sdnn_opts {
   int32_t resident_from; /* N <= 4096: layers [resident_from, L) run in one kernel that
                           keeps each CTA's batch tile resident in shared memory
                           (earlier layers stream with dead-row compaction);
-                          -1 = 24 when L > 32 (else off); >= L or SDNN_F_NO_RESIDENT
-                          = off                                                      */
+                          -1 = 24 when L > 32 and N <= 1024 (else off: from 2048
+                          neurons the fused passes are faster, C2 4096x480: 19.2
+                          vs 20.3 ms); >= L or SDNN_F_NO_RESIDENT = off           */
   int32_t stream_slots; /* weight streaming (the paper streams weight
                           partitions because "preloading ... is impossible",
                           PAPER.md:2560-2569).  0 = every packed layer and pass
@@ -187,7 +188,9 @@ typedef struct sdnn_stats {
   int32_t struct_size;        /* caller sets sizeof(sdnn_stats) (versioning)            */
   int32_t neurons, layers;
   int32_t path;               /* bit 0: fused multi-layer passes used; bit 1: the
-                                 SMEM-resident kernel runs the last layers              */
+                                 SMEM-resident kernel runs the last layers; bit 2:
+                                 position-blocked activations (every step a fused
+                                 pass; SDNN_YBLOCK=0 in the environment disables)     */
   int32_t grouped_layers;     /* layers packed with >1 column per source-list group    */
   int32_t max_group;          /* largest group size (columns sharing a source list)    */
   int32_t max_k;              /* largest column nnz over all layers                    */

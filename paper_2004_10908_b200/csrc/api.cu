@@ -92,6 +92,8 @@ struct sdnn_net {
   int32_t fused_layers = 0;
   int32_t resident_layers = 0;
   ResLayerDev *d_res = nullptr;        // device table for the resident step (pass_arena)
+  int32_t yblk = 0;                    // plan: position-blocked activations (Workspace::yblk)
+  const int32_t *d_sig0 = nullptr;     // plan: input storage order (pass_arena)
   std::vector<uint8_t> sat_suffix;     // f2: layers [l, L) all saturation-preserving
   // f3 weight streaming (opts.stream_slots > 0): every step's weight block in one
   // pinned host buffer, copied into a ring of device slots during the chain
@@ -360,7 +362,7 @@ sdnn_status make_plan(sdnn_net *net) {
   std::vector<std::vector<unsigned char>> blobs;
   std::vector<ResLayerDev> rl;
   if (!(net->opts.flags & (SDNN_F_NO_RESIDENT | SDNN_F_SATURATE)) && !weight_streaming(net) &&
-      resident_positions(net->n) > 0) {
+      resident_positions(net->n) > 0 && (net->opts.resident_from >= 0 || net->n <= kResidentDefaultMaxN)) {
     int a0 = net->opts.resident_from >= 0 ? net->opts.resident_from : (net->L > 32 ? 24 : net->L);
     a0 = std::min(a0, net->L);
     bool ok = a0 < net->L;
@@ -373,6 +375,11 @@ sdnn_status make_plan(sdnn_net *net) {
   for (int l = 0; l < net->L; ++l) lp[l] = &net->host[l];
   std::vector<const PackedLayer *> head(lp.begin(), lp.begin() + ar);
   std::vector<PassHost> ph;
+  const char *eyb = getenv("SDNN_YBLOCK");
+  const bool want_yblk = (eyb ? atoi(eyb) != 0 : kYBlockDefault) && !weight_streaming(net) && !sat &&
+                         ar == net->L;
+  // (merging small components into full 512-row CTAs for the blocked layout was
+  // measured no faster on C4: 2080 vs 2069 ms/step)
   net->steps = plan_passes(head, net->n, cap, maxm, pass_tile_floats(), nthreads_default(), &ph);
   net->pass_arena.release();
   free_stream(net);
@@ -388,6 +395,51 @@ sdnn_status make_plan(sdnn_net *net) {
     if (bytes) CK(cudaMemcpy(*d, h, bytes, cudaMemcpyHostToDevice));
     return SDNN_OK;
   };
+  // Position-blocked activations (SDNN_YBLOCK; only when every step is a fused
+  // pass): at the input boundary of each pass the neurons get a storage order
+  // in which every (component, CTA) row list is consecutive, so a tile's
+  // 32-position blocks are single contiguous runs; the final boundary keeps
+  // the identity order.  in_rows and the last layer's output rows are
+  // rewritten to storage rows; the input scatter uses sig0.
+  bool yblk = want_yblk && net->L > 0 && !net->steps.empty();
+  for (const Step &S : net->steps) yblk = yblk && S.m > 1;
+  std::vector<int32_t> sig0;
+  if (yblk) {
+    const int n = net->n;
+    const size_t ns = net->steps.size();
+    std::vector<std::vector<int32_t>> sig(ns);
+    for (size_t q = 0; q < ns; ++q) {
+      const PassHost &H = ph[q];
+      std::vector<int32_t> &sq = sig[q];
+      sq.assign(n, -1);
+      int32_t next = 0;
+      for (int64_t cb = 0; cb < (int64_t)H.ncomp * H.C; ++cb)
+        for (int i = 0; i < H.in_count[cb]; ++i) sq[H.in_rows[cb * H.rin + i]] = next++;
+      for (int j = 0; j < n; ++j)
+        if (sq[j] < 0) sq[j] = next++;
+    }
+    for (size_t q = 0; q < ns; ++q) {
+      PassHost &H = ph[q];
+      for (auto &r : H.in_rows)
+        if (r >= 0) r = sig[q][r];
+      if (q + 1 < ns) {
+        const PassHostLayer &HL = H.layers[H.m - 1];
+        for (int64_t cb = 0; cb < (int64_t)H.ncomp * H.C; ++cb) {
+          int32_t *orow = reinterpret_cast<int32_t *>(H.rec.data() + cb * H.rec_bytes + HL.off_orow);
+          for (int k = 0; k < HL.NG * 32; ++k) orow[k] = sig[q + 1][orow[k]];
+        }
+      }
+    }
+    sig0 = std::move(sig[0]);
+  }
+  net->yblk = yblk ? net->n : 0;
+  net->d_sig0 = nullptr;
+  if (yblk) {
+    void *d;
+    sdnn_status st2 = up(sig0.data(), sig0.size() * 4, &d);
+    if (st2) return st2;
+    net->d_sig0 = (const int32_t *)d;
+  }
   for (size_t q = 0; q < net->steps.size(); ++q) {
     if (net->steps[q].m == 1) continue;
     PassHost &H = ph[q];
@@ -403,6 +455,7 @@ sdnn_status make_plan(sdnn_net *net) {
     D.T = H.T;
     D.C = H.C;
     D.rec_bytes = H.rec_bytes;
+    D.yblk = net->yblk;
     if (!streaming) {                            // else: pointers into the slot ring
       void *p1, *p2, *p3;
       sdnn_status st;
@@ -567,6 +620,9 @@ sdnn_status infer_device_impl(sdnn_net *net, const int64_t *d_rowptr, const int3
   if (net->nset.load() != net->L) return fail(SDNN_E_STATE, "not every layer has been set");
   sdnn_status st = ensure_ws(net, batch);
   if (st) return st;
+  if (net->L > 0 && (st = make_plan(net))) return st;   // the layout of Y is a plan property
+  net->ws.yblk = net->L > 0 ? net->yblk : 0;
+  net->ws.sig0 = net->L > 0 ? net->d_sig0 : nullptr;
   const bool compact = compact_enabled(net);
   launch_densify(net->cfg, net->ws, net->n, batch, d_rowptr, d_idx, d_val, compact, s);
   int64_t launches = 4;
@@ -1023,7 +1079,7 @@ sdnn_status sdnn_stats_get(const sdnn_net *cnet, sdnn_stats *out, int64_t *live_
   s.struct_size = sizeof(sdnn_stats);
   s.neurons = net->n;
   s.layers = net->L;
-  s.path = (net->fused_layers > 0 ? 1 : 0) | (net->resident_layers > 0 ? 2 : 0);
+  s.path = (net->fused_layers > 0 ? 1 : 0) | (net->resident_layers > 0 ? 2 : 0) | (net->yblk > 0 ? 4 : 0);
   s.steps = (int32_t)net->steps.size();
   s.fused_layers = net->fused_layers;
   s.resident_layers = net->resident_layers;

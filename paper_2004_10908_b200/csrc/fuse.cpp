@@ -223,6 +223,13 @@ void build_pass(const std::vector<const PackedLayer *> &layers, int32_t n, const
     }
   }
   const int cta_rows = pass_cta_rows();
+  std::vector<int32_t> prev_group;               // group of each neuron in layer a-1
+  if (s.a > 0) {
+    const PackedLayer &pp = *layers[s.a - 1];
+    prev_group.assign(n, -1);
+    for (int32_t g = 0; g < pp.ngroups; ++g)
+      for (int u = 0; u < pp.gg[g]; ++u) prev_group[pp.col[(size_t)g * pp.gmax + u]] = g;
+  }
   std::vector<std::vector<std::vector<int32_t>>> bins(ncomp);   // [comp][bin] rows
   int C = 1, R = 1;
   for (int c = 0; c < ncomp; ++c) {
@@ -239,7 +246,18 @@ void build_pass(const std::vector<const PackedLayer *> &layers, int32_t n, const
       if (!placed) bins[c].push_back(sv);
     }
     for (auto &b : bins[c]) {
-      std::sort(b.begin(), b.end());              // slots in ascending neuron id
+      // slot order: rows written by the same group of the previous layer
+      // (layer a-1, the last layer of the previous pass) next to each other,
+      // then ascending neuron id.  Any order is correct; with position-blocked
+      // activations (make_plan) slots are consecutive storage rows, so a writer
+      // group's member stores become runs of consecutive rows.
+      if (prev_group.empty()) {
+        std::sort(b.begin(), b.end());
+      } else {
+        std::sort(b.begin(), b.end(), [&](int32_t x, int32_t y) {
+          return prev_group[x] != prev_group[y] ? prev_group[x] < prev_group[y] : x < y;
+        });
+      }
       R = std::max<int>(R, (int)b.size());
     }
     C = std::max<int>(C, (int)bins[c].size());

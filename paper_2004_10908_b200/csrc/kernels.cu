@@ -445,10 +445,16 @@ __global__ void __launch_bounds__(1024) k_scan_input(const uint32_t *inmask, int
 }
 
 // warp per input row: scatter its stored values into its (compacted) column
+// element (storage row r, position p) of an activation buffer
+__device__ __forceinline__ int64_t yix(int64_t r, int64_t p, int64_t stride, int32_t yblk) {
+  return yblk ? ((p >> 5) * yblk + r) * 32 + (p & 31) : r * stride + p;
+}
+
 __global__ void k_scatter(int64_t batch, const int64_t *__restrict__ rowptr,
                           const int32_t *__restrict__ idx, const float *__restrict__ val,
                           const uint32_t *__restrict__ inmask, const int32_t *__restrict__ wpre,
-                          float *Y0, int32_t *rid0, int64_t stride) {
+                          float *Y0, int32_t *rid0, int64_t stride, int32_t yblk,
+                          const int32_t *__restrict__ sig0) {
   const int lane = threadIdx.x & 31;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < batch; i += nw) {
@@ -457,7 +463,7 @@ __global__ void k_scatter(int64_t batch, const int64_t *__restrict__ rowptr,
     const int64_t pos = wpre[i >> 5] + __popc(word & ((1u << (i & 31)) - 1u));
     if (lane == 0) rid0[pos] = (int32_t)i;
     for (int64_t e = rowptr[i] + lane; e < rowptr[i + 1]; e += 32)
-      Y0[(int64_t)idx[e] * stride + pos] = val ? val[e] : 1.0f;
+      Y0[yix(sig0 ? sig0[idx[e]] : idx[e], pos, stride, yblk)] = val ? val[e] : 1.0f;
   }
 }
 
@@ -603,8 +609,16 @@ __global__ void __launch_bounds__(32 * kPassNW, 3)
   const int64_t cid = C > 1 ? (int64_t)cluster_id_x() : (int64_t)blockIdx.x;
   const int64_t ncl = C > 1 ? (int64_t)nclusters_x() : (int64_t)gridDim.x;
   const uint32_t tile_u32 = smem_u32(tile_s);
+  // position-blocked activations: a CTA's rows are consecutive storage rows, so
+  // each 32-position block of its tile is ONE contiguous run of ncnt*128 B,
+  // copied by one cp.async.bulk into the tile laid out [T/32][rin][32]
+  const int32_t R = P.yblk;
+  const bool blk = R > 0;
+  const bool ldg = kLdgsts && !blk;
+  const int rin = P.rin;
+  const int sm = blk ? 32 : T;                   // tile floats per slot step
   if (tid == 0) {
-    mbar_init(bar, kLdgsts ? 32 * NW + 1 : 1);   // LDGSTS: one noinc arrival per thread
+    mbar_init(bar, ldg ? 32 * NW + 1 : 1);       // LDGSTS: one noinc arrival per thread
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int q = tid; q < kMaxPassLayers * W; q += blockDim.x) aw[q] = 0u;
@@ -625,10 +639,16 @@ __global__ void __launch_bounds__(32 * kPassNW, 3)
     const int tile = (int)(it - c * tiles);
     const int64_t cb = c * C + rank;
     if (tid == 0) {
-      mbar_expect_tx_arrive(bar, (kLdgsts ? 0u : (uint32_t)ncnt * T * 4) + (uint32_t)P.rec_bytes);
+      mbar_expect_tx_arrive(bar, (ldg ? 0u : (uint32_t)ncnt * T * 4) + (uint32_t)P.rec_bytes);
       bulk_g2s(rec_s, P.rec + cb * P.rec_bytes, P.rec_bytes, bar);
+      if (blk && ncnt > 0)                       // nrow[0] = the first storage row
+#pragma unroll
+        for (int q = 0; q < T / 32; ++q)
+          bulk_g2s(tile_s + q * rin * 32, Yin + (((int64_t)tile * (T / 32) + q) * R + nrow[0]) * 32,
+                   (uint32_t)ncnt * 128u, bar);
     }
-    if (kLdgsts) {
+    if (blk) {
+    } else if (kLdgsts) {
       // warp w copies rows q*128 + 32w + j; lane = (row j % RPI, chunk)
       const int ch = lane % CPR;
       const float *src0 = Yin + (int64_t)tile * T + ch * 4;
@@ -695,6 +715,7 @@ __global__ void __launch_bounds__(32 * kPassNW, 3)
           G = kg >> 8;
         }
         const int pofs = sl * SW + sll * 4;      // this lane's 4 positions in the tile
+        const int pa = blk ? ((pofs >> 5) * rin * 32 + (pofs & 31)) : pofs;   // their smem offset
         // entry e = r * LPU + sll of the group: source slot (a term past K points
         // at source 0 with weight 0: fmaf(x, 0, acc) == acc for finite x, acc != -0)
         uint32_t soff[EPL];                      // float offset in the tile / cluster address
@@ -704,8 +725,8 @@ __global__ void __launch_bounds__(32 * kPassNW, 3)
         for (int r = 0; r < EPL; ++r) {
           const int e = r * LPU + sll;
           const uint32_t code = K > 0 ? src_s[gi * 32 + (e < K ? e : 0)] : 0u;
-          soff[r] = remote ? cluster_map(tile_u32 + (code & 0x3ffu) * (T * 4), code >> 10)
-                           : (code & 0x3ffu) * T;
+          soff[r] = remote ? cluster_map(tile_u32 + (code & 0x3ffu) * (sm * 4), code >> 10)
+                           : (code & 0x3ffu) * sm;
           bia[r] = (!ubias && e < G) ? bias_s[gi * 32 + e] : 0.f;
           orw[r] = (last && e < G) ? orow_s[gi * 32 + e] : 0;
         }
@@ -721,13 +742,13 @@ __global__ void __launch_bounds__(32 * kPassNW, 3)
             for (int r = 0; r < EPL; ++r)
 #pragma unroll
               for (int l = 0; l < LPU; ++l)
-                acc4<X2>(acc, ld_cluster_f4(__shfl_sync(FULL, soff[r], l, LPU) + (uint32_t)(pofs * 4)), wu);
+                acc4<X2>(acc, ld_cluster_f4(__shfl_sync(FULL, soff[r], l, LPU) + (uint32_t)(pa * 4)), wu);
           } else {
 #pragma unroll
             for (int r = 0; r < EPL; ++r)
 #pragma unroll
               for (int l = 0; l < LPU; ++l)
-                acc4<X2>(acc, *reinterpret_cast<const float4 *>(tile_s + __shfl_sync(FULL, soff[r], l, LPU) + pofs),
+                acc4<X2>(acc, *reinterpret_cast<const float4 *>(tile_s + __shfl_sync(FULL, soff[r], l, LPU) + pa),
                          wu);
           }
         } else {
@@ -740,8 +761,8 @@ __global__ void __launch_bounds__(32 * kPassNW, 3)
               const uint32_t so = __shfl_sync(FULL, soff[r], l, LPU);
               if (t < kmax) {
                 const float w = t < K ? wu : 0.f;
-                if (remote) acc4<X2>(acc, ld_cluster_f4(so + (uint32_t)(pofs * 4)), w);
-                else acc4<X2>(acc, *reinterpret_cast<const float4 *>(tile_s + so + pofs), w);
+                if (remote) acc4<X2>(acc, ld_cluster_f4(so + (uint32_t)(pa * 4)), w);
+                else acc4<X2>(acc, *reinterpret_cast<const float4 *>(tile_s + so + pa), w);
               }
             }
           }
@@ -758,7 +779,9 @@ __global__ void __launch_bounds__(32 * kPassNW, 3)
         // members: uniform bias => every member of the group has the same value
         float4 yu = make_float4(0.f, 0.f, 0.f, 0.f);
         if (ubias && G > 0) yu = out4<X2>(acc, PL.bu, ymax, o);
-        float *obase = Yout + (int64_t)tile * T + pofs;
+        float *obase = blk ? Yout + ((int64_t)tile * (T / 32) + (pofs >> 5)) * R * 32 + (pofs & 31)
+                           : Yout + (int64_t)tile * T + pofs;
+        const int64_t rowmul = blk ? 32 : stride;
 #pragma unroll
         for (int r = 0; r < EPL; ++r) {
           if (r * LPU >= gmax) break;
@@ -770,8 +793,8 @@ __global__ void __launch_bounds__(32 * kPassNW, 3)
             const float bv = ubias ? 0.f : __shfl_sync(FULL, bia[r], l, LPU);
             if (v < G) {
               const float4 y = ubias ? yu : out4<X2>(acc, bv, ymax, o);
-              if (last) *reinterpret_cast<float4 *>(obase + (int64_t)dst * stride) = y;
-              else *reinterpret_cast<float4 *>(tile_s + dst + pofs) = y;
+              if (last) *reinterpret_cast<float4 *>(obase + (int64_t)dst * rowmul) = y;
+              else *reinterpret_cast<float4 *>(tile_s + dst + pa) = y;
             }
           }
         }
@@ -781,9 +804,16 @@ __global__ void __launch_bounds__(32 * kPassNW, 3)
 #pragma unroll
         for (int e = 0; e < 4; ++e) bal[e] = __ballot_sync(FULL, (o >> e) & 1u);
         if (sll < WPS && G > 0) {
-          uint32_t word = 0;
-#pragma unroll
-          for (int b = 0; b < 32; ++b) word |= ((bal[b & 3] >> (seg * LPU + sll * 8 + (b >> 2))) & 1u) << b;
+          // the 8 lanes of word sll give 4 bits each: spread each ballot byte so
+          // lane bit l lands on bit 4 l, then interleave the four e planes
+          auto spread8 = [](uint32_t x) {
+            x = (x | (x << 12)) & 0x000F000Fu;
+            x = (x | (x << 6)) & 0x03030303u;
+            return (x | (x << 3)) & 0x11111111u;
+          };
+          const int sh = seg * LPU + sll * 8;
+          const uint32_t word = spread8((bal[0] >> sh) & 0xffu) | (spread8((bal[1] >> sh) & 0xffu) << 1) |
+                                (spread8((bal[2] >> sh) & 0xffu) << 2) | (spread8((bal[3] >> sh) & 0xffu) << 3);
           if (word) atomicOr(&aw[j * W + sl * WPS + sll], word);
         }
       }
@@ -895,7 +925,8 @@ __global__ void __launch_bounds__(1024) k_scan_step(LayerState *st, int a, int m
 // Move the live batch columns of the step's output into the free buffer.
 __global__ void k_compact(const LayerState *__restrict__ st, int a, int m, float *Ya, float *Yb,
                           int32_t *ridA, int32_t *ridB, const uint32_t *__restrict__ alive,
-                          const int32_t *__restrict__ wpre, int32_t n, int64_t stride) {
+                          const int32_t *__restrict__ wpre, int32_t n, int64_t stride,
+                          int32_t yblk) {
   const LayerState N1 = st[a + m];
   if (!N1.compacted) return;
   const LayerState S = st[a];
@@ -914,7 +945,7 @@ __global__ void k_compact(const LayerState *__restrict__ st, int a, int m, float
     const int64_t to = wpre[q] + __popc(bits & ((1u << lane) - 1u));
     const int64_t from = q * 32 + lane;
     if (k < n)
-      dst[k * stride + to] = src[k * stride + from];
+      dst[yix(k, to, stride, yblk)] = src[yix(k, from, stride, yblk)];
     else
       rdst[to] = rsrc[from];
   }
@@ -1001,7 +1032,7 @@ __global__ void k_yout_retired(const uint32_t *__restrict__ retired, int64_t bat
 // Y_L (neuron-major, positions) -> row-major [batch][n] (rows not present are 0)
 __global__ void k_yout(const LayerState *__restrict__ st, int a, int final_out,
                        const float *Ya, const float *Yb, const int32_t *ridA,
-                       const int32_t *ridB, int32_t n, int64_t stride, float *yout) {
+                       const int32_t *ridB, int32_t n, int64_t stride, int32_t yblk, float *yout) {
   const LayerState S = st[a];
   const int bufsel = final_out ? 1 - S.in : S.in;
   const float *Y = bufsel ? Yb : Ya;
@@ -1010,7 +1041,7 @@ __global__ void k_yout(const LayerState *__restrict__ st, int a, int final_out,
   for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < total;
        it += (int64_t)gridDim.x * blockDim.x) {
     const int64_t j = it / S.width, p = it - j * S.width;
-    yout[(int64_t)rid[p] * n + j] = Y[j * stride + p];
+    yout[(int64_t)rid[p] * n + j] = Y[yix(j, p, stride, yblk)];
   }
 }
 
@@ -1124,7 +1155,7 @@ void launch_densify(const LaunchCfg &c, const Workspace &w, int32_t n, int64_t b
   }
   if (batch > 0)
     k_scatter<<<c.sms * 8, 256, 0, s>>>(batch, rowptr, idx, val, w.inmask, w.wpre, w.Y[0],
-                                        w.rid[0], w.stride);
+                                        w.rid[0], w.stride, w.yblk, w.sig0);
 }
 
 void launch_zero_layers_alive(const Workspace &w, int64_t batch, const int64_t *rowptr,
@@ -1200,7 +1231,7 @@ void launch_yout_retired(const Workspace &w, int32_t n, int64_t batch, float yma
 void launch_compact_copy(const LaunchCfg &c, const Workspace &w, int32_t a, int32_t m,
                          const uint32_t *alive_last, int32_t n, cudaStream_t s) {
   k_compact<<<c.copy_blocks, 256, 0, s>>>(w.st, a, m, w.Y[0], w.Y[1], w.rid[0], w.rid[1],
-                                          alive_last, w.wpre, n, w.stride);
+                                          alive_last, w.wpre, n, w.stride, w.yblk);
 }
 
 void launch_readout(const Workspace &w, int32_t a, const uint32_t *alive_last,
@@ -1214,7 +1245,7 @@ void launch_yout(const Workspace &w, int32_t a, bool final_out, int32_t n, int64
                  float *d_yout, cudaStream_t s) {
   cudaMemsetAsync(d_yout, 0, sizeof(float) * (size_t)n * (size_t)batch, s);
   k_yout<<<148 * 4, 256, 0, s>>>(w.st, a, final_out ? 1 : 0, w.Y[0], w.Y[1], w.rid[0], w.rid[1],
-                                 n, w.stride, d_yout);
+                                 n, w.stride, w.yblk, d_yout);
 }
 
 }  // namespace sdnn

@@ -104,6 +104,7 @@ constexpr int kMaxPassLayers = 16;
 constexpr int kMaxPassRows = 512;      // slots per CTA (one 64 KB tile of >= 32 positions)
 constexpr int kDefaultPassRows = 1024; // default component cap (C4: 2324 ms vs 2435 at 512, 2652 at 2048)
 constexpr int kDefaultCtaRows = 512;   // default slots per CTA (pass_cta_rows())
+constexpr bool kYBlockDefault = true;  // position-blocked activations (SDNN_YBLOCK=0 disables)
 int pass_cta_rows();
 constexpr int kMaxPassCluster = 4;     // CTAs per component (thread-block cluster, DSMEM)
 
@@ -164,6 +165,8 @@ struct PassLayerDev {
 struct DevPass {
   int32_t a, m, ncomp, rin, R, T, rec_bytes;
   int32_t C;                           // cluster size: in_rows/in_count/rec indexed [comp * C + rank]
+  int32_t yblk;                        // 0: Y is [rows][stride]; R > 0: Y is [stride/32][R][32] and
+                                       // every (comp, rank)'s rows are R-consecutive storage rows
   const int32_t *in_rows, *in_count;
   const unsigned char *rec;            // [ncomp][rec_bytes]
   PassLayerDev layers[kMaxPassLayers]; // by value: the kernel parameter carries them
@@ -179,6 +182,7 @@ struct ResLayerDev {
   int32_t off_col, off_bias, off_counts;
 };
 int resident_positions(int n);         // batch positions per CTA (0 = not eligible)
+constexpr int kResidentDefaultMaxN = 1024;  // resident tail by default only up to this width
 int resident_max_blob();
 bool build_resident_blob(const PackedLayer &p, std::vector<unsigned char> &blob, ResLayerDev &d);
 void configure_resident();
@@ -204,6 +208,11 @@ struct Workspace {
   int32_t *nretired = nullptr;
   uint32_t *orig = nullptr;
   int64_t stride = 0;                 // row stride (capacity in batch columns)
+  // position-blocked activations (plan property, see make_plan): yblk = storage
+  // rows R, element (row r, position p) at ((p / 32) * R + r) * 32 + p % 32;
+  // sig0[neuron] = storage row of an input neuron (NULL: identity)
+  int32_t yblk = 0;
+  const int32_t *sig0 = nullptr;
   int64_t words = 0;                  // stride / 32
   uint32_t *alive_set(int s) const { return alive[s & 1]; }
   uint32_t *alive_row(int s, int j) const { return alive[s & 1] + (int64_t)j * words; }
