@@ -913,9 +913,12 @@ sdnn_status sdnn_infer(sdnn_net *net, const int64_t *y0_rowptr, const int32_t *y
   if (st) return st;
   const int64_t nnz = y0_rowptr[batch];
   if (nnz > 0 && !y0_idx) return fail(SDNN_E_ARG, "y0_idx is NULL");
+  // rowptr must be sane before its last entry sizes the copies below; the full
+  // validation runs on the host while the (page-locked) input is in flight
   if (!(net->opts.flags & SDNN_F_TRUST_INPUT)) {
-    st = validate_y0(net->n, y0_rowptr, y0_idx, y0_val, batch);
-    if (st) return st;
+    if (y0_rowptr[0] != 0) return fail(SDNN_E_FORMAT, "y0_rowptr[0] != 0");
+    for (int64_t i = 0; i < batch; ++i)
+      if (y0_rowptr[i + 1] < y0_rowptr[i]) return fail(SDNN_E_FORMAT, "y0_rowptr not non-decreasing");
   }
   cudaStream_t s = net->opts.stream ? (cudaStream_t)net->opts.stream : net->own;
   // device input buffers (grow-only)
@@ -964,7 +967,12 @@ sdnn_status sdnn_infer(sdnn_net *net, const int64_t *y0_rowptr, const int32_t *y
       for (size_t off = 0; off < p.bytes; off += kChunk) {
         const size_t b = std::min(kChunk, p.bytes - off);
         if (used[slot]) CK(cudaEventSynchronize(ev[slot]));
-        std::memcpy(stage + slot * kChunk, (const char *)p.h + off, b);
+        {                                          // pageable -> pinned on several host threads
+          char *dst = stage + slot * kChunk;
+          const char *src = (const char *)p.h + off;
+          parallel_for((int64_t)b, std::min(nthreads_default(), 8),
+                       [&](int64_t x, int64_t y) { std::memcpy(dst + x, src + x, (size_t)(y - x)); });
+        }
         CK(cudaMemcpyAsync((char *)p.d + off, stage + slot * kChunk, b, cudaMemcpyHostToDevice, s));
         CK(cudaEventRecord(ev[slot], s));
         used[slot] = true;
@@ -973,6 +981,13 @@ sdnn_status sdnn_infer(sdnn_net *net, const int64_t *y0_rowptr, const int32_t *y
     }
     cudaEventDestroy(ev[0]);
     cudaEventDestroy(ev[1]);
+  }
+  if (!(net->opts.flags & SDNN_F_TRUST_INPUT)) {
+    st = validate_y0(net->n, y0_rowptr, y0_idx, y0_val, batch);
+    if (st) {
+      cudaStreamSynchronize(s);                  // no DMA may still read the caller's buffers
+      return st;
+    }
   }
   st = infer_device_impl(net, net->d_rowptr, net->d_idx, y0_val ? net->d_val : nullptr, batch,
                          nullptr, nullptr, s);
