@@ -151,7 +151,7 @@ sdnn_status check_opts(const sdnn_opts *o, sdnn_opts &out) {
   out = sdnn_opts{-1, 0u, 32.f, nullptr, -1, -1, -1, 0};
   if (o) out = *o;
   if (out.stream_slots < 0 || out.stream_slots > 64) return fail(SDNN_E_ARG, "stream_slots must be in [0, 64]");
-  if (out.fuse_rows > pass_cta_rows() * kMaxPassCluster) out.fuse_rows = pass_cta_rows() * kMaxPassCluster;
+  if (out.fuse_rows > kMaxPassRows * kMaxPassCluster) out.fuse_rows = kMaxPassRows * kMaxPassCluster;
   if (out.fuse_layers > kMaxPassLayers) return fail(SDNN_E_ARG, "fuse_layers > 16");
   if (!(out.ymax > 0.f) || !std::isfinite(out.ymax)) return fail(SDNN_E_ARG, "ymax must be finite and > 0");
   return SDNN_OK;
@@ -347,12 +347,15 @@ sdnn_status build_stream_blobs(sdnn_net *net, const std::vector<PassHost> &ph) {
 
 // Plan the steps (fused passes where the component cap allows) and upload the
 // pass descriptors.  Create-time work, redone only when layers change.
+// position-blocked activations wanted (default on; SDNN_YBLOCK=0 disables)
+bool yblock_wanted() {
+  const char *e = getenv("SDNN_YBLOCK");
+  return e ? atoi(e) != 0 : kYBlockDefault;
+}
+
 sdnn_status make_plan(sdnn_net *net) {
   if (!net->plan_dirty) return SDNN_OK;
   const bool sat = net->opts.flags & SDNN_F_SATURATE;
-  const int cap = sat ? 0 : std::min(net->opts.fuse_rows < 0 ? kDefaultPassRows
-                                                              : net->opts.fuse_rows,
-                                     pass_cta_rows() * kMaxPassCluster);
   net->sat_suffix.assign(net->L + 1, 1);
   for (int l = net->L - 1; l >= 0; --l)
     net->sat_suffix[l] = net->sat_suffix[l + 1] && saturation_preserving(net->host[l], net->opts.ymax);
@@ -375,12 +378,15 @@ sdnn_status make_plan(sdnn_net *net) {
   for (int l = 0; l < net->L; ++l) lp[l] = &net->host[l];
   std::vector<const PackedLayer *> head(lp.begin(), lp.begin() + ar);
   std::vector<PassHost> ph;
-  const char *eyb = getenv("SDNN_YBLOCK");
-  const bool want_yblk = (eyb ? atoi(eyb) != 0 : kYBlockDefault) && !weight_streaming(net) && !sat &&
-                         ar == net->L;
+  const bool want_yblk = yblock_wanted() && !weight_streaming(net) && !sat && ar == net->L;
+  // position-blocked plans put up to 1024 rows in a CTA (16-position tiles);
   // (merging small components into full 512-row CTAs for the blocked layout was
   // measured no faster on C4: 2080 vs 2069 ms/step)
-  net->steps = plan_passes(head, net->n, cap, maxm, pass_tile_floats(), nthreads_default(), &ph);
+  const int cta = pass_cta_rows(want_yblk);
+  const int cap = sat ? 0 : std::min(net->opts.fuse_rows < 0 ? kDefaultPassRows : net->opts.fuse_rows,
+                                     cta * kMaxPassCluster);
+  net->steps = plan_passes(head, net->n, cap, maxm, pass_tile_floats(), nthreads_default(), &ph, cta,
+                           want_yblk);
   net->pass_arena.release();
   free_stream(net);
   net->passes.clear();
@@ -402,7 +408,7 @@ sdnn_status make_plan(sdnn_net *net) {
   // the identity order.  in_rows and the last layer's output rows are
   // rewritten to storage rows; the input scatter uses sig0.
   bool yblk = want_yblk && net->L > 0 && !net->steps.empty();
-  for (const Step &S : net->steps) yblk = yblk && S.m > 1;
+  for (size_t q = 0; q < ph.size(); ++q) yblk = yblk && ph[q].m > 0;   // every step a pass
   std::vector<int32_t> sig0;
   if (yblk) {
     const int n = net->n;
@@ -425,8 +431,8 @@ sdnn_status make_plan(sdnn_net *net) {
       if (q + 1 < ns) {
         const PassHostLayer &HL = H.layers[H.m - 1];
         for (int64_t cb = 0; cb < (int64_t)H.ncomp * H.C; ++cb) {
-          int32_t *orow = reinterpret_cast<int32_t *>(H.rec.data() + cb * H.rec_bytes + HL.off_orow);
-          for (int k = 0; k < HL.NG * 32; ++k) orow[k] = sig[q + 1][orow[k]];
+          uint16_t *orow = reinterpret_cast<uint16_t *>(H.rec.data() + cb * H.rec_bytes + HL.off_orow);
+          for (int k = 0; k < HL.NG * 32; ++k) orow[k] = (uint16_t)sig[q + 1][orow[k]];
         }
       }
     }
@@ -441,7 +447,7 @@ sdnn_status make_plan(sdnn_net *net) {
     net->d_sig0 = (const int32_t *)d;
   }
   for (size_t q = 0; q < net->steps.size(); ++q) {
-    if (net->steps[q].m == 1) continue;
+    if (ph[q].m == 0) continue;                  // a plain layer step
     PassHost &H = ph[q];
     if (!pass_variant(H.T, H.C))
       return fail(SDNN_E_UNSUPPORTED, "no fused-pass kernel for tile " + std::to_string(H.T) + " x cluster " +
@@ -546,9 +552,9 @@ void enqueue_chain(sdnn_net *net, bool compact, cudaStream_t s, int64_t *launche
     const DevLayer &dl = streaming ? net->step_dl[si] : net->dl[S.a];
     const bool sat = (net->opts.flags & SDNN_F_SATURATE) && S.m == 1 &&
                      layer_tracks_saturation(net->cfg, dl);
-    if (S.m == 1)
+    if (S.pass < 0)
       launch_layer(net->cfg, w, dl, S.a, w.alive_row(si, 0), ymax, s, sat ? w.sat[si & 1] : nullptr);
-    else
+    else                                          // a fused pass (m >= 1)
       launch_pass(net->cfg, w, net->passes[S.pass], w.alive_set(si), ymax, s);
     if (prof) cudaEventRecordWithFlags(net->ev_after[S.a], s, evflags);
     if (streaming) {                              // slot si mod S is free again
@@ -1075,12 +1081,13 @@ sdnn_status sdnn_plan_steps(int32_t neurons, int32_t layers, const sdnn_layer *W
   }
   std::vector<const PackedLayer *> lp(layers);
   for (int l = 0; l < layers; ++l) lp[l] = &host[l];
+  // as make_plan, without the resident tail (a plan of fused passes and layers)
+  const int cta = pass_cta_rows(yblock_wanted() && !(o.flags & SDNN_F_SATURATE) && o.stream_slots == 0);
   const int cap = (o.flags & SDNN_F_SATURATE)
                       ? 0
-                      : std::min(o.fuse_rows < 0 ? kDefaultPassRows : o.fuse_rows,
-                                 pass_cta_rows() * kMaxPassCluster);
+                      : std::min(o.fuse_rows < 0 ? kDefaultPassRows : o.fuse_rows, cta * kMaxPassCluster);
   const int maxm = o.fuse_layers < 0 ? 8 : o.fuse_layers;
-  const std::vector<Step> steps = plan_passes(lp, neurons, cap, maxm, pass_tile_floats(), 1, nullptr);
+  const std::vector<Step> steps = plan_passes(lp, neurons, cap, maxm, pass_tile_floats(), 1, nullptr, cta);
   for (size_t i = 0; i < steps.size(); ++i) step_len[i] = steps[i].m;
   *nsteps = (int32_t)steps.size();
   return SDNN_OK;

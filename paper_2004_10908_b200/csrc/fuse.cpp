@@ -130,16 +130,18 @@ int bins_needed(UF &full, UF &sub, int32_t n, int cap_cta, std::vector<int32_t> 
 
 }  // namespace
 
-// slots per CTA of a fused pass (128 / 256 / 512; SDNN_PASS_CTA_ROWS overrides
-// the default for A/B runs): a component larger than this spreads over a
-// cluster of up to kMaxPassCluster CTAs
-int pass_cta_rows() {
-  static const int r = [] {
+// slots per CTA of a fused pass: 512 (row-major activations: 32-position
+// tiles of 128 B row segments) or 1024 (position-blocked activations, where a
+// CTA's rows are consecutive storage rows and 16-position tiles stay cheap);
+// SDNN_PASS_CTA_ROWS = 128 / 256 / 512 / 1024 overrides for A/B runs.  A
+// component larger than this spreads over a cluster of up to kMaxPassCluster CTAs
+int pass_cta_rows(bool blocked) {
+  static const int env = [] {
     const char *e = getenv("SDNN_PASS_CTA_ROWS");
-    const int v = e ? atoi(e) : kDefaultCtaRows;
-    return (v == 128 || v == 256 || v == 512) ? v : kDefaultCtaRows;
+    const int v = e ? atoi(e) : 0;
+    return (v == 128 || v == 256 || v == 512 || v == 1024) ? v : 0;
   }();
-  return r;
+  return env ? env : (blocked ? kMaxPassRows : kDefaultCtaRows);
 }
 
 // A pass [a, a+m) keeps every layer but the last inside one CTA: the
@@ -148,11 +150,10 @@ int pass_cta_rows() {
 // sub-components of a full component are bin-packed into at most
 // cap / pass_cta_rows() CTAs (cap <= pass_cta_rows(): one CTA of cap slots).
 std::vector<Step> plan_steps(const std::vector<const PackedLayer *> &layers, int32_t n, int cap,
-                             int max_m, int a_begin) {
+                             int max_m, int cta_rows, int a_begin) {
   std::vector<Step> steps;
   const int L = (int)layers.size();
   max_m = std::max(1, std::min(max_m, kMaxPassLayers));
-  const int cta_rows = pass_cta_rows();
   cap = std::min(cap, cta_rows * kMaxPassCluster);
   const int cap_cta = std::min(cap, cta_rows);
   const int max_bins = std::max(1, cap / cta_rows);
@@ -189,7 +190,7 @@ std::vector<Step> plan_steps(const std::vector<const PackedLayer *> &layers, int
 }
 
 void build_pass(const std::vector<const PackedLayer *> &layers, int32_t n, const Step &s,
-                int tile_floats, PassHost &out) {
+                int tile_floats, int cta_rows, PassHost &out) {
   const int m = s.m;
   UF full, sub;
   full.init((int64_t)(m + 1) * n);
@@ -222,7 +223,6 @@ void build_pass(const std::vector<const PackedLayer *> &layers, int32_t n, const
       subs[c][sub_idx[sr]].push_back(i);
     }
   }
-  const int cta_rows = pass_cta_rows();
   std::vector<int32_t> prev_group;               // group of each neuron in layer a-1
   if (s.a > 0) {
     const PackedLayer &pp = *layers[s.a - 1];
@@ -275,7 +275,7 @@ void build_pass(const std::vector<const PackedLayer *> &layers, int32_t n, const
   out.rin = R;
   int Rp = 32;                                    // one tile of tile_floats per CTA
   while (Rp < R) Rp <<= 1;
-  out.T = std::max(32, std::min(512, tile_floats / Rp));
+  out.T = std::max(16, std::min(512, tile_floats / Rp));
   out.in_rows.assign((size_t)ncomp * C * R, -1);
   out.in_count.assign((size_t)ncomp * C, 0);
   for (int c = 0; c < ncomp; ++c)
@@ -312,7 +312,7 @@ void build_pass(const std::vector<const PackedLayer *> &layers, int32_t n, const
     H.bias.assign(units * NG * 32, 0.f);
     H.k.assign(units * NG, 0);
     H.g.assign(units * NG, 0);
-    if (last) H.orow.assign(units * NG * 32, 0);
+    if (last) H.orow.assign(units * NG * 32, 0);      // u16: N <= 65536
     const int64_t in0 = (int64_t)b * n, out0 = (int64_t)(b + 1) * n;
     for (size_t cb = 0; cb < units; ++cb)
       for (size_t q = 0; q < groups[cb].size(); ++q) {
@@ -332,7 +332,7 @@ void build_pass(const std::vector<const PackedLayer *> &layers, int32_t n, const
           const int32_t j = p.col[(size_t)g * p.gmax + u];
           H.bias[rec * 32 + u] = p.bias[j];
           if (last)
-            H.orow[rec * 32 + u] = j;
+            H.orow[rec * 32 + u] = (uint16_t)j;
           else                             // member u overwrites the slot of source u
             slot[out0 + j] = code[u];
         }
@@ -373,7 +373,7 @@ void build_pass(const std::vector<const PackedLayer *> &layers, int32_t n, const
     }
     if (b == m - 1) {
       H.off_orow = off;
-      off += H.NG * 128;
+      off += H.NG * 64;
     }
   }
   out.rec_bytes = off;
@@ -390,28 +390,32 @@ void build_pass(const std::vector<const PackedLayer *> &layers, int32_t n, const
       }
       std::memcpy(r + H.off_src, H.src.data() + g0 * 32, (size_t)H.NG * 64);
       if (H.off_bias >= 0) std::memcpy(r + H.off_bias, H.bias.data() + g0 * 32, (size_t)H.NG * 128);
-      if (H.off_orow >= 0) std::memcpy(r + H.off_orow, H.orow.data() + g0 * 32, (size_t)H.NG * 128);
+      if (H.off_orow >= 0) std::memcpy(r + H.off_orow, H.orow.data() + g0 * 32, (size_t)H.NG * 64);
     }
   }
 }
 
 std::vector<Step> plan_passes(const std::vector<const PackedLayer *> &layers, int32_t n, int cap,
                               int max_m, int tile_floats, int threads,
-                              std::vector<PassHost> *built) {
-  std::vector<Step> steps = plan_steps(layers, n, cap, max_m, 0);
+                              std::vector<PassHost> *built, int cta_rows, bool single_passes) {
+  std::vector<Step> steps = plan_steps(layers, n, cap, max_m, cta_rows, 0);
   std::vector<PassHost> ph(steps.size());
   std::vector<char> done(steps.size(), 0);
+  // single_passes: a lone fusable layer also runs as a (one-layer) pass
+  auto is_pass = [&](const Step &x) {
+    return x.m > 1 || (single_passes && cap > 0 && fusable(*layers[x.a]));
+  };
   for (;;) {
     std::vector<int> todo;
     for (int i = 0; i < (int)steps.size(); ++i)
-      if (steps[i].m > 1 && !done[i]) todo.push_back(i);
+      if (is_pass(steps[i]) && !done[i]) todo.push_back(i);
     std::atomic<int> next{0};
     std::vector<std::thread> th;
     const int nt = std::max(1, std::min<int>(threads, (int)todo.size()));
     for (int t = 0; t < nt && !todo.empty(); ++t)
       th.emplace_back([&] {
         for (int q = next++; q < (int)todo.size(); q = next++)
-          build_pass(layers, n, steps[todo[q]], tile_floats, ph[todo[q]]);
+          build_pass(layers, n, steps[todo[q]], tile_floats, cta_rows, ph[todo[q]]);
       });
     for (auto &x : th) x.join();
     for (int i : todo) done[i] = 1;
@@ -420,6 +424,8 @@ std::vector<Step> plan_passes(const std::vector<const PackedLayer *> &layers, in
     int bad = -1;
     for (int i = 0; i < (int)steps.size() && bad < 0; ++i)
       if (steps[i].m > 1 && ph[i].rec_bytes > kPassRecMax) bad = i;
+    for (int i = 0; i < (int)steps.size(); ++i)   // a one-layer record that does not fit: plain layer
+      if (steps[i].m == 1 && ph[i].rec_bytes > kPassRecMax) ph[i] = PassHost();
     if (bad < 0) break;
     Step &S = steps[bad];
     S.m -= 1;
@@ -427,9 +433,9 @@ std::vector<Step> plan_passes(const std::vector<const PackedLayer *> &layers, in
     steps.resize(bad + 1);
     ph.resize(bad + 1);
     done.resize(bad + 1);
-    done[bad] = S.m == 1;
+    done[bad] = 0;
     ph[bad] = PassHost();
-    for (const Step &x : plan_steps(layers, n, cap, max_m, resume)) {
+    for (const Step &x : plan_steps(layers, n, cap, max_m, cta_rows, resume)) {
       steps.push_back(x);
       ph.emplace_back();
       done.push_back(0);

@@ -520,7 +520,7 @@ int pass_tile_floats() { return kPassTile; }
 // (packed FFMA2/FADD2) is the cluster default; SDNN_PASS_X2=1 selects it for
 // single-CTA passes too.
 #define SDNN_PASS_VARIANTS(X)                                                                    \
-  X(32, 1, false) X(64, 1, false) X(128, 1, false) X(256, 1, false) X(512, 1, false)           \
+  X(16, 1, false) X(16, 1, true) X(16, 2, true) X(32, 1, false) X(64, 1, false) X(128, 1, false) X(256, 1, false) X(512, 1, false)           \
   X(32, 1, true) X(64, 1, true) X(128, 1, true) X(256, 1, true) X(512, 1, true) X(32, 2, true) \
   X(32, 4, true) X(64, 2, true) X(64, 4, true) X(128, 2, true) X(128, 4, true)
 
@@ -581,7 +581,7 @@ __global__ void __launch_bounds__(32 * kPassNW, 3)
   constexpr int UPW = 32 / LPU;                  // units per warp (lane segments)
   constexpr int EPL = 32 / LPU;                  // group entries per lane (slot, bias, row)
   constexpr int WPS = SW / 32;                   // liveness words per unit
-  constexpr int W = T / 32;                      // liveness words per tile
+  constexpr int W = T >= 32 ? T / 32 : 1;        // liveness words per tile (T = 16: half a word)
   constexpr int RPT = kMaxPassRows / (32 * NW);  // input rows per thread
   // tiles of <= 64 positions: rows arrive as 16-B cp.async (LDGSTS) chunks, a
   // warp instruction covering RPI whole rows (one cp.async.bulk per row would
@@ -614,9 +614,10 @@ __global__ void __launch_bounds__(32 * kPassNW, 3)
   // copied by one cp.async.bulk into the tile laid out [T/32][rin][32]
   const int32_t R = P.yblk;
   const bool blk = R > 0;
-  const bool ldg = kLdgsts && !blk;
+  const bool bt = blk && T >= 32;               // blocked tile: smem [T/32][rin][32]
+  const bool ldg = kLdgsts && (!blk || T < 32);   // (T = 16 blocked: half-block LDGSTS rows)
   const int rin = P.rin;
-  const int sm = blk ? 32 : T;                   // tile floats per slot step
+  const int sm = bt ? 32 : T;                    // tile floats per slot step
   if (tid == 0) {
     mbar_init(bar, ldg ? 32 * NW + 1 : 1);       // LDGSTS: one noinc arrival per thread
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -628,6 +629,10 @@ __global__ void __launch_bounds__(32 * kPassNW, 3)
   auto fetch_rows = [&](int64_t it) {
     const int64_t cb = (it / tiles) * C + rank;
     ncnt = __ldg(P.in_count + cb);
+    if (blk) {                                   // consecutive storage rows: the first one
+      nrow[0] = __ldg(P.in_rows + cb * P.rin);
+      return;
+    }
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
       const int r = tid + q * 32 * NW;
@@ -641,13 +646,19 @@ __global__ void __launch_bounds__(32 * kPassNW, 3)
     if (tid == 0) {
       mbar_expect_tx_arrive(bar, (ldg ? 0u : (uint32_t)ncnt * T * 4) + (uint32_t)P.rec_bytes);
       bulk_g2s(rec_s, P.rec + cb * P.rec_bytes, P.rec_bytes, bar);
-      if (blk && ncnt > 0)                       // nrow[0] = the first storage row
+      if (bt && ncnt > 0)                        // nrow[0] = the first storage row
 #pragma unroll
-        for (int q = 0; q < T / 32; ++q)
+        for (int q = 0; q < (T >= 32 ? T / 32 : 0); ++q)
           bulk_g2s(tile_s + q * rin * 32, Yin + (((int64_t)tile * (T / 32) + q) * R + nrow[0]) * 32,
                    (uint32_t)ncnt * 128u, bar);
     }
-    if (blk) {
+    if (bt) {
+    } else if (blk) {
+      // T = 16: 64 B of each consecutive 128 B block row (block tile/2, half tile%2)
+      const float *src0 = Yin + ((int64_t)(tile >> 1) * R + nrow[0]) * 32 + (tile & 1) * 16;
+      for (int x = tid; x < ncnt * 4; x += 32 * NW)
+        cp_async16(tile_s + (size_t)x * 4, src0 + (int64_t)(x >> 2) * 32 + (x & 3) * 4);
+      cp_async_arrive(bar);
     } else if (kLdgsts) {
       // warp w copies rows q*128 + 32w + j; lane = (row j % RPI, chunk)
       const int ch = lane % CPR;
@@ -699,7 +710,7 @@ __global__ void __launch_bounds__(32 * kPassNW, 3)
       const uint16_t *kg_s = reinterpret_cast<const uint16_t *>(rec_s + PL.off_kg);
       const uint16_t *src_s = reinterpret_cast<const uint16_t *>(rec_s + PL.off_src);
       const float *bias_s = reinterpret_cast<const float *>(rec_s + (ubias ? 0 : PL.off_bias));
-      const int32_t *orow_s = reinterpret_cast<const int32_t *>(rec_s + (last ? PL.off_orow : 0));
+      const uint16_t *orow_s = reinterpret_cast<const uint16_t *>(rec_s + (last ? PL.off_orow : 0));
       // the last layer releases the tiles before its HBM stores when every warp
       // owns at most one unit per segment (one round)
       const bool early = last && units <= NW * UPW;
@@ -715,7 +726,7 @@ __global__ void __launch_bounds__(32 * kPassNW, 3)
           G = kg >> 8;
         }
         const int pofs = sl * SW + sll * 4;      // this lane's 4 positions in the tile
-        const int pa = blk ? ((pofs >> 5) * rin * 32 + (pofs & 31)) : pofs;   // their smem offset
+        const int pa = bt ? ((pofs >> 5) * rin * 32 + (pofs & 31)) : pofs;   // their smem offset
         // entry e = r * LPU + sll of the group: source slot (a term past K points
         // at source 0 with weight 0: fmaf(x, 0, acc) == acc for finite x, acc != -0)
         uint32_t soff[EPL];                      // float offset in the tile / cluster address
@@ -779,7 +790,7 @@ __global__ void __launch_bounds__(32 * kPassNW, 3)
         // members: uniform bias => every member of the group has the same value
         float4 yu = make_float4(0.f, 0.f, 0.f, 0.f);
         if (ubias && G > 0) yu = out4<X2>(acc, PL.bu, ymax, o);
-        float *obase = blk ? Yout + ((int64_t)tile * (T / 32) + (pofs >> 5)) * R * 32 + (pofs & 31)
+        float *obase = blk ? Yout + (((int64_t)tile * T + pofs) >> 5) * R * 32 + (((int64_t)tile * T + pofs) & 31)
                            : Yout + (int64_t)tile * T + pofs;
         const int64_t rowmul = blk ? 32 : stride;
 #pragma unroll
@@ -816,6 +827,16 @@ __global__ void __launch_bounds__(32 * kPassNW, 3)
                                 (spread8((bal[2] >> sh) & 0xffu) << 2) | (spread8((bal[3] >> sh) & 0xffu) << 3);
           if (word) atomicOr(&aw[j * W + sl * WPS + sll], word);
         }
+        if (WPS == 0 && sll == 0 && G > 0) {   // T = 16: the unit is the tile's 16 positions
+          auto spread4 = [](uint32_t x) {
+            x = (x | (x << 6)) & 0x0303u;
+            return (x | (x << 3)) & 0x1111u;
+          };
+          const int sh = seg * LPU;
+          const uint32_t hw = spread4((bal[0] >> sh) & 0xfu) | (spread4((bal[1] >> sh) & 0xfu) << 1) |
+                              (spread4((bal[2] >> sh) & 0xfu) << 2) | (spread4((bal[3] >> sh) & 0xfu) << 3);
+          if (hw) atomicOr(&aw[j * W], hw);
+        }
       }
       __syncthreads();                           // the next layer reads slots other warps wrote
     }
@@ -826,7 +847,7 @@ __global__ void __launch_bounds__(32 * kPassNW, 3)
         const int64_t base = (int64_t)tile * T + tid * 32;
         if (base >= width) word = 0u;
         else if (width - base < 32) word &= (1u << (width - base)) - 1u;
-        if (word) atomicOr(&alive[j * wstride + (base >> 5)], word);
+        if (word) atomicOr(&alive[j * wstride + (base >> 5)], word << (base & 31));
       }
     }
     if (!issued) {

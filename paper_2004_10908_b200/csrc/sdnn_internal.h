@@ -101,11 +101,11 @@ struct LayerState {
 // canonical ascending-source fmaf sequence.
 // ---------------------------------------------------------------------------
 constexpr int kMaxPassLayers = 16;
-constexpr int kMaxPassRows = 512;      // slots per CTA (one 64 KB tile of >= 32 positions)
+constexpr int kMaxPassRows = 1024;     // slots per CTA (one 64 KB tile of >= 16 positions)
 constexpr int kDefaultPassRows = 1024; // default component cap (C4: 2324 ms vs 2435 at 512, 2652 at 2048)
-constexpr int kDefaultCtaRows = 512;   // default slots per CTA (pass_cta_rows())
+constexpr int kDefaultCtaRows = 512;   // slots per CTA with row-major activations
 constexpr bool kYBlockDefault = true;  // position-blocked activations (SDNN_YBLOCK=0 disables)
-int pass_cta_rows();
+int pass_cta_rows(bool blocked);
 constexpr int kMaxPassCluster = 4;     // CTAs per component (thread-block cluster, DSMEM)
 
 struct Step {
@@ -121,7 +121,7 @@ constexpr int32_t kResidentStep = -2;  // layers [a, L) in the SMEM-resident ker
 // cap / kMaxPassRows CTAs (cap <= kMaxPassRows * kMaxPassCluster); tile
 // T = 16384 / (rows per CTA rounded up to a power of two), 32 <= T <= 512
 std::vector<Step> plan_steps(const std::vector<const PackedLayer *> &layers, int32_t n, int cap,
-                             int max_m, int a_begin = 0);
+                             int max_m, int cta_rows, int a_begin = 0);
 
 struct PassHostLayer {
   int32_t NG = 0;                      // group slots per component (max over components)
@@ -131,7 +131,7 @@ struct PassHostLayer {
   int32_t off_kg = 0, off_src = 0, off_bias = 0, off_orow = -1;  // record byte offsets
   std::vector<uint16_t> src;           // [ncomp][NG][32] smem slots of the sources
   std::vector<float> bias;             // [ncomp][NG][32] bias of each member
-  std::vector<int32_t> orow;           // last layer only: [ncomp][NG][32] global output rows
+  std::vector<uint16_t> orow;          // last layer only: [ncomp][NG][32] output rows (N <= 65536)
   std::vector<uint8_t> k, g;           // [ncomp][NG] sources / members (0 = empty slot)
 };
 struct PassHost {
@@ -143,19 +143,19 @@ struct PassHost {
   // per-component metadata record (one bulk copy next to the tile):
   //   for each layer j: kg[NG_j] u16 (K | G << 8) padded to 16 B, src[NG_j][32] u16
   //   slot codes (bin << 10 | slot), bias[NG_j][32] f32 unless the layer's biases
-  //   are uniform over the pass; last layer: orow[NG][32] i32
+  //   are uniform over the pass; last layer: orow[NG][32] u16
   int32_t rec_bytes = 0;
   std::vector<unsigned char> rec;      // [ncomp][rec_bytes]
 };
-constexpr int kPassRecMax = 8192;      // record bytes per component (3 CTAs per SM)
+constexpr int kPassRecMax = 10224;     // record bytes per component (3 CTAs per SM: 3 x 75 KB)
 void build_pass(const std::vector<const PackedLayer *> &layers, int32_t n, const Step &s,
-                int tile_floats, PassHost &out);
+                int tile_floats, int cta_rows, PassHost &out);
 // plan_steps, build every fused pass; a pass whose record exceeds kPassRecMax
 // drops its last layer and the rest is planned again; `built[i]` is the
-// PassHost of steps[i] (m > 1)
+// PassHost of steps[i] (m > 1, or m == 1 with single_passes; else m == 0)
 std::vector<Step> plan_passes(const std::vector<const PackedLayer *> &layers, int32_t n, int cap,
                               int max_m, int tile_floats, int threads,
-                              std::vector<PassHost> *built);
+                              std::vector<PassHost> *built, int cta_rows, bool single_passes = false);
 
 struct PassLayerDev {
   int32_t off_kg, off_src, off_bias, off_orow;   // byte offsets in the component record

@@ -174,14 +174,16 @@ def test_product_path_never_touches_oracle():
                 assert "sdnn_oracle" not in txt and "liboracle" not in txt, p
 
 
-def test_plan_steps_rn_and_rr(sd):
+def test_plan_steps_rn_and_rr(sd, monkeypatch):
     """Fused multi-layer passes: in a RadiX-Net layer every group is a dense
     32x32 block varying one 5-bit field of the neuron id, so the connected
     components over layers a..b span 2^|union of their fields' bits| neurons.
     A pass keeps all layers but the last in one CTA (sub-components of <= 512
     slots) and lets the last layer read across a cluster of cap/512 CTAs; the
     planner extends every pass while that holds (greedy, maximal).
-    Random-regular layers have one giant component and are never fused."""
+    Random-regular layers have one giant component and are never fused.
+    (Row-major activations: 512 slots per CTA; see the blocked variant below.)"""
+    monkeypatch.setenv("SDNN_YBLOCK", "0")
     rn = list(g.iter_layers(g.rn_spec(1024, 24)))
     fields = [g.rn_field(1024, l) for l in range(24)]
 
@@ -224,6 +226,31 @@ def test_plan_steps_rn_and_rr(sd):
     assert sd.sdnn_plan_steps(65536, big, fmt="ell", fuse_rows=2048) == [4, 2, 4, 2]   # 4-CTA clusters; field wrap after 6
 
 
+def test_plan_steps_blocked_layout(sd, monkeypatch):
+    """With position-blocked activations (the default) a CTA holds up to 1024
+    slots (16-position tiles), so the default cap 1024 needs no cluster: every
+    pass is feasible for one CTA and maximal, except where its metadata
+    record (<= 10224 B) ends it first."""
+    monkeypatch.setenv("SDNN_YBLOCK", "1")
+    fields = [g.rn_field(65536, l) for l in range(24)]
+    big = [g.gen_layer(g.rn_spec(65536, 24), l, fmt="ell") for l in range(24)]
+
+    def comp(a, m):
+        bits = set()
+        for p in fields[a:a + m]:
+            bits |= set(range(p, p + 5))
+        return 2 ** len(bits)
+
+    plan = sd.sdnn_plan_steps(65536, big, fmt="ell")
+    assert sum(plan) == 24 and max(plan) == 3   # (a lone layer runs as a one-layer pass)
+    a = 0
+    for m in plan:
+        assert comp(a, m) <= 1024
+        a += m
+    monkeypatch.setenv("SDNN_YBLOCK", "0")
+    assert sum(sd.sdnn_plan_steps(65536, big, fmt="ell")) == 24
+
+
 def identity_layer(n):
     """W = I, uniform 1, bias 0: Y -> min(max(Y, 0), 32) (the identity on Y in [0, 32])."""
     from types import SimpleNamespace
@@ -232,18 +259,20 @@ def identity_layer(n):
                            ell=np.arange(n, dtype=np.int32).reshape(n, 1), ell_val=None)
 
 
-def test_plan_splits_oversized_records(sd):
-    """A pass's per-component metadata record must fit kPassRecMax (8 KB):
-    [identity, rn0, rn1] forms 128-row components (plan [3] by the component cap
-    alone) but the identity layer has 128 singleton groups per component (~8.4 KB
-    of record with the uniform bias stored once), so the pass drops its last
-    layer and the rest is planned again -> [2, 1]."""
+def test_plan_splits_oversized_records(sd, monkeypatch):
+    """A pass's per-component metadata record must fit kPassRecMax (10224 B):
+    [identity, identity, rn0, rn1] forms 128-row components (plan [4] by the
+    component cap alone) but each identity layer has 128 singleton groups per
+    component (~8.4 KB of record each), so the pass drops its last layer (32-row
+    components, ~4.4 KB) and the rest is planned again -> [3, 1];
+    [identity, rn0, rn1] (~9.2 KB) still fits."""
     n = 1024
     rn = [g.gen_layer(g.rn_spec(n, 2), l) for l in range(2)]
+    ident = identity_layer(n)
     assert sd.sdnn_plan_steps(n, rn) == [2]
-    assert sd.sdnn_plan_steps(n, [identity_layer(n)] + rn) == [2, 1]
-    # two layers [identity, rn0]: 32-row components, 32 singletons (~6.5 KB) fit
-    assert sd.sdnn_plan_steps(n, [identity_layer(n)] + rn, fuse_layers=2) == [2, 1]
+    assert sd.sdnn_plan_steps(n, [ident] + rn) == [3]
+    assert sd.sdnn_plan_steps(n, [ident, ident] + rn) == [3, 1]
+    assert sd.sdnn_plan_steps(n, [ident] + rn, fuse_layers=2) == [2, 1]
 
 
 def test_plan_steps_not_in_place_not_fused(sd):
