@@ -35,6 +35,10 @@ CONFIGS = {
     "c3": (16384, 1920, 60000),
     "c4": (65536, 1920, 60000),
 }
+# configs[4]: the width/depth sweep for roofline and scaling curves (tools/sweep.sh)
+for _n in (1024, 4096, 16384, 65536):
+    for _l in (120, 480, 1920):
+        CONFIGS[f"s{_n}x{_l}"] = (_n, _l, 60000)
 METRIC = "edges/sec (inputs×nnz/time) for 65536-neuron×1920-layer net at 1/2/4/8 B200"
 UNIT = "edges/s"
 
