@@ -109,6 +109,12 @@ def lib_flags(sd, names):
     return f
 
 
+def net_spec(g, args, n, L):
+    """The network family: RN (headline, RadiX-Net-shaped) or RR (random
+    32-regular: no two columns share a source list, the general gather path)."""
+    return g.rn_spec(n, L) if args.net == "rn" else g.rr_spec(n, L)
+
+
 def kernel_name(net):
     st = net.stats()
     return "k_layer_bulk" if st.get("fused_layers", 0) == 0 else "k_pass+k_layer_bulk"
@@ -132,7 +138,7 @@ def run_reference(args):
     import oracle
     import sdnngen as g
     n, L, B = CONFIGS[args.config]
-    spec = g.rn_spec(n, L)
+    spec = net_spec(g, args, n, L)
     rp, idx = make_inputs(n, B, 0)
     cores = oracle.default_threads()
     rows_per_step = args.ref_rows or max(1, cores)
@@ -157,8 +163,8 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic",
-        "config": {"workload": f"rn{n}x{L}-ms", "neurons": n, "layers": L,
-                   "inputs_sampled_per_step": rows_per_step, "inputs_full": B},
+        "config": {"workload": f"{args.net}{n}x{L}-ms{B}", "neurons": n, "layers": L,
+                   "nnz_per_column": 32, "inputs_sampled_per_step": rows_per_step, "inputs_full": B},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
                          "sample": f"{rows_per_step} random rows of the {B}-input batch per step, "
                                    f"all {L} layers (oracle/sdnn_oracle.c, {cores} threads)"},
@@ -200,7 +206,7 @@ def run_gpu(args):
             dist.init_process_group(backend)
     from paper_2004_10908_b200 import dist as sdist
     n, L, B = CONFIGS[args.config]
-    spec = g.rn_spec(n, L)
+    spec = net_spec(g, args, n, L)
     t0 = time.time()
     net = sd.Net.from_spec(spec, fmt="ell", threads=args.load_threads, device=local,
                            flags=sd.SDNN_F_PROFILE | lib_flags(sd, args.flags),
@@ -329,10 +335,12 @@ def run_gpu(args):
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak" if args.scaling != "strong" else "strong", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"rn{n}x{L}-ms{B}", "neurons": n, "layers": L,
+            "config": {"workload": f"{args.net}{n}x{L}-ms{B}", "neurons": n, "layers": L,
                        "nnz_per_column": 32, "inputs_per_gpu": batch,
                        "global_batch": batch * ws if args.scaling != "strong" else B,
-                       "network": "RadiX-Net-shaped (sdnngen.rn_spec), w=1/16, b=%g" % spec.bias,
+                       "network": ("RadiX-Net-shaped (sdnngen.rn_spec)" if args.net == "rn" else
+                                   "random 32-regular, no shared source sets (sdnngen.rr_spec)")
+                                  + ", w=1/16, b=%g" % spec.bias,
                        "inputs": "binary MNIST-shaped strokes (sdnngen.ms_inputs)",
                        "parallelism": f"dp{ws}" if ws > 1 else "single",
                        "l2": "inputs larger than L2 (Y = %.1f GB per GPU)" % (4.0 * n * batch / 1e9)},
@@ -366,7 +374,7 @@ def run_oneshot(args):
     import paper_2004_10908_b200 as sd
     import sdnngen as g
     n, L, B = CONFIGS[args.config]
-    net = sd.Net.from_spec(g.rn_spec(n, L), fmt="ell", threads=args.load_threads, device=0,
+    net = sd.Net.from_spec(net_spec(g, args, n, L), fmt="ell", threads=args.load_threads, device=0,
                            flags=lib_flags(sd, args.flags), fuse_rows=args.fuse_rows,
                            fuse_layers=args.fuse_layers, stream_slots=args.stream_slots)
     rp, idx = make_inputs(n, B, 0)
@@ -387,6 +395,8 @@ def main():
     ap.add_argument("--impl", default="sdnn", choices=["sdnn", "reference"])
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--net", default="rn", choices=["rn", "rr"],
+                    help="network family: rn = RadiX-Net-shaped (headline), rr = random 32-regular")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
