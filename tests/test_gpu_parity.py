@@ -510,8 +510,14 @@ def test_full_size_c2(sd):
 
 
 @pytest.mark.slow
+def test_full_size_c3(sd):
+    _full_size(sd, 16384, 1920, 48)
+
+
+@pytest.mark.slow
 def test_full_size_c4(sd):
-    _full_size(sd, 65536, 1920, 24)
+    cats, st = _full_size(sd, 65536, 1920, 24)
+    assert st["path"] & 4                      # the benchmarked (position-blocked) layout
 
 
 def ragged_block_layers(n, L, w, seed, sb=64, shift=0.0, bmin=1):
