@@ -105,13 +105,15 @@ typedef struct sdnn_opts {
   int32_t fuse_rows;   /* multi-layer passes ("model decomposition"):
                           consecutive uniform layers run as one pass over the
                           connected components of their union.  All layers but the
-                          last stay inside one CTA (sub-components of <= 512
+                          last stay inside one CTA (sub-components of <= R
                           neurons, updated in place in a 64 KB shared-memory tile
-                          of 16384/rows batch positions); the last layer reads
-                          across a thread-block cluster of up to fuse_rows / 512
-                          CTAs (distributed shared memory), so a component has
-                          <= fuse_rows neurons (<= 2048, larger values are
-                          clamped; <= 512: single-CTA passes; 0 = off; -1 = 1024) */
+                          of 16384/rows batch positions; R = 1024 with
+                          position-blocked activations, see stats.path bit 2,
+                          else 512); the last layer reads across a thread-block
+                          cluster of up to fuse_rows / R CTAs (distributed shared
+                          memory), so a component has <= fuse_rows neurons
+                          (<= 4 R, larger values are clamped; <= R: single-CTA
+                          passes; 0 = off; -1 = 1024)                             */
   int32_t fuse_layers; /* at most this many layers per pass (<= 16; -1 = 8)           */
   int32_t resident_from; /* N <= 4096: layers [resident_from, L) run in one kernel that
                           keeps each CTA's batch tile resident in shared memory
