@@ -184,6 +184,7 @@ def test_plan_steps_rn_and_rr(sd, monkeypatch):
     Random-regular layers have one giant component and are never fused.
     (Row-major activations: 512 slots per CTA; see the blocked variant below.)"""
     monkeypatch.setenv("SDNN_YBLOCK", "0")
+    monkeypatch.setenv("SDNN_PLAN", "greedy")        # maximality is the greedy cover's property
     rn = list(g.iter_layers(g.rn_spec(1024, 24)))
     fields = [g.rn_field(1024, l) for l in range(24)]
 
@@ -224,6 +225,38 @@ def test_plan_steps_rn_and_rr(sd, monkeypatch):
     assert sd.sdnn_plan_steps(65536, big, fmt="ell", fuse_rows=512) == [3, 3, 3, 3]
     assert sd.sdnn_plan_steps(65536, big, fmt="ell", fuse_rows=128) == [2] * 6
     assert sd.sdnn_plan_steps(65536, big, fmt="ell", fuse_rows=2048) == [4, 2, 4, 2]   # 4-CTA clusters; field wrap after 6
+
+
+@pytest.mark.parametrize("plan", ["cost", "greedy"])
+def test_plan_steps_cost_cover(sd, monkeypatch, plan):
+    """The default cost-weighted cover and the greedy one both tile the layers
+    with feasible passes (component cap 1024, one CTA with blocked activations);
+    the cost cover never pays more than the greedy one under its own model
+    (1 per pass, +0.3 for components above 512 rows)."""
+    monkeypatch.setenv("SDNN_YBLOCK", "1")
+    L = 72
+    fields = [g.rn_field(65536, l) for l in range(L)]
+    big = [g.gen_layer(g.rn_spec(65536, L), l, fmt="ell") for l in range(L)]
+
+    def comp(a, m):
+        bits = set()
+        for p in fields[a:a + m]:
+            bits |= set(range(p, p + 5))
+        return 2 ** len(bits)
+
+    def cost(plan_):
+        a, c = 0, 0.0
+        for m in plan_:
+            assert comp(a, m) <= 1024 or m == 1
+            c += 1.0 + (0.3 if m > 1 and comp(a, m) > 512 else 0.0)
+            a += m
+        assert a == L
+        return c
+
+    monkeypatch.setenv("SDNN_PLAN", plan)
+    mine = cost(sd.sdnn_plan_steps(65536, big, fmt="ell"))
+    monkeypatch.setenv("SDNN_PLAN", "greedy")
+    assert mine <= cost(sd.sdnn_plan_steps(65536, big, fmt="ell")) + 1e-9
 
 
 def test_plan_steps_blocked_layout(sd, monkeypatch):
