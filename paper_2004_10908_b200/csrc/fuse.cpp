@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cmath>
 #include <atomic>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
@@ -257,12 +258,17 @@ static std::vector<Step> plan_steps_cost(const std::vector<const PackedLayer *> 
       });
     for (auto &x : th) x.join();
   }
+  // SDNN_PLAN_COST="big,small": penalties for >512-row components and for
+  // 2-layer passes of <= 256 rows (A/B knobs; defaults 0.3, 0)
+  double big = 0.3, small = 0.0;
+  if (const char *e = getenv("SDNN_PLAN_COST")) sscanf(e, "%lf,%lf", &big, &small);
   std::vector<double> best(L + 1, 0.0);
   std::vector<int> choice(L + 1, 1);
   for (int a = L - 1; a >= a_begin; --a) {
     best[a] = 1e300;
     for (int k = std::min(mm[a], L - a); k >= 1; --k) {
-      const double c = 1.0 + (k > 1 && rows[a][k] > 512 ? 0.3 : 0.0) + best[a + k];
+      const double c = 1.0 + (k > 1 && rows[a][k] > 512 ? big : 0.0) +
+                       (k == 2 && rows[a][k] <= 256 ? small : 0.0) + best[a + k];
       if (c < best[a] - 1e-9) {
         best[a] = c;
         choice[a] = k;
