@@ -185,6 +185,21 @@ sdnn_status sdnn_infer_device(sdnn_net *net, const int64_t *d_rowptr, const int3
                               const float *d_val, int64_t batch, uint32_t *d_alive,
                               float *d_y_out, void *stream);
 
+/* Final activations Y_L of SELECTED input rows of the last inference, without
+ * materialising the whole [batch x neurons] matrix (15.7 GB at 65536 neurons x
+ * 60,000 inputs): the golden-reference check of PAPER.md:2570 on sampled rows.
+ *   d_rows  [nrows] int32 DEVICE array of original (0-based) row ids, any
+ *           order, repeats allowed; an id outside [0, last batch) yields zeros;
+ *   d_y     [nrows * neurons] fp32 DEVICE, row-major: row q receives Y_L of
+ *           input row d_rows[q] (all zeros for a row that died or was empty,
+ *           all YMAX for a row retired as saturated under SDNN_F_SATURATE).
+ * Asynchronous on `stream` (cudaStream_t; NULL = legacy default stream); it
+ * must be ordered after the inference it reads (same stream, or after the
+ * synchronous sdnn_infer returned) and before the next inference on the
+ * handle.  Returns SDNN_E_STATE before the first inference. */
+sdnn_status sdnn_gather_rows(sdnn_net *net, const int32_t *d_rows, int64_t nrows, float *d_y,
+                             void *stream);
+
 /* Statistics of the handle and of its last completed inference. */
 typedef struct sdnn_stats {
   int32_t struct_size;        /* caller sets sizeof(sdnn_stats) (versioning)            */

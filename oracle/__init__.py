@@ -153,7 +153,7 @@ def infer_spec_rows(spec, rowptr, idx, val=None, rows=None, ymax: float = 32.0,
     o = Oracle(spec.n, rowptr, idx, val)
     prof = [] if profile else None
     for l in range(spec.L):
-        lay = sdnngen.gen_layer(spec, l, fmt="csr")
+        lay = sdnngen.gen_layer(spec, l, fmt="csr" if spec.wdist == "uniform" else "both")
         o.apply(lay, ymax=ymax, nthreads=nthreads)
         if profile:
             prof.append(o.live_rows())

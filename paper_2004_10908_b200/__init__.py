@@ -34,7 +34,7 @@ SDNN_F_SATURATE = 256
 EXPORTS = ["sdnn_create", "sdnn_create_empty", "sdnn_set_layer", "sdnn_infer",
            "sdnn_infer_device", "sdnn_stats_get", "sdnn_validate_layer", "sdnn_destroy",
            "sdnn_last_error", "sdnn_abi_version", "sdnn_layer_times", "sdnn_plan_steps",
-           "sdnn_step_plan"]
+           "sdnn_step_plan", "sdnn_gather_rows"]
 
 
 class SdnnError(RuntimeError):
@@ -99,6 +99,7 @@ def lib() -> ctypes.CDLL:
         L.sdnn_layer_times.argtypes = [V, V]
         L.sdnn_plan_steps.argtypes = [I32, I32, P(sdnn_layer), V, P(sdnn_opts), V, P(I32)]
         L.sdnn_step_plan.argtypes = [V, V, P(I32)]
+        L.sdnn_gather_rows.argtypes = [V, V, I64, V, V]
         L.sdnn_destroy.argtypes = [V]
         L.sdnn_destroy.restype = None
         L.sdnn_last_error.argtypes = []
@@ -106,7 +107,7 @@ def lib() -> ctypes.CDLL:
         L.sdnn_abi_version.restype = I32
         for name in ["sdnn_create", "sdnn_create_empty", "sdnn_set_layer", "sdnn_infer",
                      "sdnn_infer_device", "sdnn_stats_get", "sdnn_validate_layer",
-                     "sdnn_layer_times", "sdnn_plan_steps", "sdnn_step_plan"]:
+                     "sdnn_layer_times", "sdnn_plan_steps", "sdnn_step_plan", "sdnn_gather_rows"]:
             getattr(L, name).restype = I32
         _LIB = L
     return _LIB
@@ -313,6 +314,27 @@ class Net:
                           alive_t.data_ptr() if alive_t.numel() else None,
                           None if y_t is None else y_t.data_ptr(), s.cuda_stream)
         return alive_t
+
+    def gather_rows_torch(self, rows_t, y_t=None, stream=None):
+        """Y_L of the given original rows (int32 CUDA tensor) of the last
+        inference, via sdnn_gather_rows; returns a [len(rows), n] fp32 tensor."""
+        import torch
+        if y_t is None:
+            y_t = torch.empty((rows_t.numel(), self.n), dtype=torch.float32, device=rows_t.device)
+        s = stream if stream is not None else torch.cuda.current_stream(rows_t.device)
+        _check(lib().sdnn_gather_rows(self.h, rows_t.data_ptr() if rows_t.numel() else None,
+                                      int(rows_t.numel()), y_t.data_ptr() if y_t.numel() else None,
+                                      s.cuda_stream))
+        return y_t
+
+    def gather_rows(self, rows):
+        """Host convenience: Y_L rows (numpy) of the given original row ids."""
+        import torch
+        dev = torch.device("cuda", torch.cuda.current_device())
+        rows_t = torch.from_numpy(np.ascontiguousarray(rows, np.int32)).to(dev)
+        y = self.gather_rows_torch(rows_t)
+        torch.cuda.synchronize(dev)
+        return y.cpu().numpy()
 
     def stats(self):
         return sdnn_stats_get(self.h, self.L)

@@ -74,6 +74,8 @@ struct sdnn_net {
   std::vector<DevLayer> dl;
   std::vector<PackedLayer> host;   // host copy of every packed layer (pass planning)
   std::vector<uint8_t> set;        // layer loaded?
+  std::vector<void *> lblock;      // per layer: its arena block (reused on re-set)
+  std::vector<size_t> lbytes;
   std::vector<uint8_t> bias_nonpos;
   std::vector<int64_t> nnz;
   std::atomic<int> nset{0};
@@ -382,11 +384,24 @@ sdnn_status make_plan(sdnn_net *net) {
   // position-blocked plans put up to 1024 rows in a CTA (16-position tiles);
   // (merging small components into full 512-row CTAs for the blocked layout was
   // measured no faster on C4: 2080 vs 2069 ms/step)
-  const int cta = pass_cta_rows(want_yblk);
-  const int cap = sat ? 0 : std::min(net->opts.fuse_rows < 0 ? kDefaultPassRows : net->opts.fuse_rows,
-                                     cta * kMaxPassCluster);
-  net->steps = plan_passes(head, net->n, cap, maxm, pass_tile_floats(), nthreads_default(), &ph, cta,
-                           want_yblk);
+  auto plan_for = [&](bool blocked) {
+    const int cta = pass_cta_rows(blocked);
+    const int cap = sat ? 0 : std::min(net->opts.fuse_rows < 0 ? kDefaultPassRows : net->opts.fuse_rows,
+                                       cta * kMaxPassCluster);
+    net->steps = plan_passes(head, net->n, cap, maxm, pass_tile_floats(), nthreads_default(), &ph, cta,
+                             blocked);
+  };
+  plan_for(want_yblk);
+  if (want_yblk) {
+    // the blocked layout needs every step to be a fused pass; otherwise plan
+    // again for row-major activations (<= 512 rows per CTA, no one-layer passes)
+    bool all = net->L > 0 && !net->steps.empty();
+    for (size_t q = 0; q < ph.size(); ++q) all = all && ph[q].m > 0;
+    if (!all) {
+      ph.clear();
+      plan_for(false);
+    }
+  }
   net->pass_arena.release();
   free_stream(net);
   net->passes.clear();
@@ -761,6 +776,8 @@ sdnn_status sdnn_create_empty(int32_t neurons, int32_t layers, const sdnn_opts *
   net->dl.resize(layers);
   net->host.resize(layers);
   net->set.assign(layers, 0);
+  net->lblock.assign(layers, nullptr);
+  net->lbytes.assign(layers, 0);
   net->bias_nonpos.assign(layers, 1);
   net->nnz.assign(layers, 0);
   net->last_live.assign(std::max(layers, 1), 0);
@@ -802,28 +819,51 @@ sdnn_status sdnn_set_layer(sdnn_net *net, int32_t l, const sdnn_layer *W, const 
   std::string msg;
   const int rc = pack_layer(net->n, in, bias_l, !(net->opts.flags & SDNN_F_NO_GROUPS), p, msg);
   if (rc) return fail(rc, "layer " + std::to_string(l) + ": " + msg);
-  // upload: one arena block per layer
+  // upload: one arena block per layer, reused when the layer is set again and
+  // the new packing fits (a larger one takes a fresh block; the old one is
+  // returned only at destroy)
   const size_t G = p.ngroups;
   const size_t b_src = sizeof(uint16_t) * p.src.size(), b_col = sizeof(int32_t) * p.col.size();
   const size_t b_gk = sizeof(int32_t) * G, b_val = sizeof(float) * p.val.size();
   const size_t b_bias = sizeof(float) * net->n;
-  auto up = [&](const void *h, size_t bytes, void **d) -> sdnn_status {
-    if (bytes == 0) { *d = nullptr; return SDNN_OK; }
-    cudaError_t e = net->arena.alloc(bytes, d);
-    if (e != cudaSuccess) {
-      cudaGetLastError();
-      return fail(SDNN_E_NOMEM, "device allocation for layer " + std::to_string(l) + " failed");
-    }
-    CK(cudaMemcpy(*d, h, bytes, cudaMemcpyHostToDevice));
-    return SDNN_OK;
-  };
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  const size_t total = al(b_src) + al(b_col) + 2 * al(b_gk) + al(b_val) + al(b_bias);
   DevLayer d{};
   void *ps = nullptr, *pc = nullptr, *pk = nullptr, *pg = nullptr, *pv = nullptr, *pb = nullptr;
-  if (!weight_streaming(net) &&                   // f3: the blocks stay on the host
-      ((st = up(p.src.data(), b_src, &ps)) || (st = up(p.col.data(), b_col, &pc)) ||
-       (st = up(p.gk.data(), b_gk, &pk)) || (st = up(p.gg.data(), b_gk, &pg)) ||
-       (st = up(p.val.data(), b_val, &pv)) || (st = up(p.bias.data(), b_bias, &pb))))
-    return st;
+  if (!weight_streaming(net)) {                   // f3: the blocks stay on the host
+    char *blk = nullptr;
+    {
+      std::lock_guard<std::mutex> g(net->stat_mu);
+      if (net->set[l] && net->lbytes[l] >= total) {
+        blk = (char *)net->lblock[l];
+        CK(cudaDeviceSynchronize());              // no inference may still read the old layer
+      }
+    }
+    if (!blk) {
+      void *v = nullptr;
+      if (net->arena.alloc(total, &v) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(SDNN_E_NOMEM, "device allocation for layer " + std::to_string(l) + " failed");
+      }
+      blk = (char *)v;
+    }
+    size_t off = 0;
+    auto up = [&](const void *h, size_t bytes, void **dp) -> sdnn_status {
+      *dp = bytes ? blk + off : nullptr;
+      if (bytes) CK(cudaMemcpy(*dp, h, bytes, cudaMemcpyHostToDevice));
+      off += al(bytes);
+      return SDNN_OK;
+    };
+    if ((st = up(p.src.data(), b_src, &ps)) || (st = up(p.col.data(), b_col, &pc)) ||
+        (st = up(p.gk.data(), b_gk, &pk)) || (st = up(p.gg.data(), b_gk, &pg)) ||
+        (st = up(p.val.data(), b_val, &pv)) || (st = up(p.bias.data(), b_bias, &pb)))
+      return st;
+    std::lock_guard<std::mutex> g(net->stat_mu);
+    if (!(net->set[l] && net->lblock[l] == blk)) {
+      net->lblock[l] = blk;
+      net->lbytes[l] = total;
+    }
+  }
   d.src = (const uint16_t *)ps;
   d.col = (const int32_t *)pc;
   d.gk = (const int32_t *)pk;
@@ -1013,6 +1053,24 @@ sdnn_status sdnn_infer(sdnn_net *net, const int64_t *y0_rowptr, const int32_t *y
   }
   *n_categories = ncat;
   net->last_ncat = ncat;
+  return SDNN_OK;
+}
+
+sdnn_status sdnn_gather_rows(sdnn_net *net, const int32_t *d_rows, int64_t nrows, float *d_y,
+                             void *stream) {
+  if (!net) return fail(SDNN_E_ARG, "net is NULL");
+  if (nrows < 0) return fail(SDNN_E_ARG, "nrows < 0");
+  if (nrows > 0 && (!d_rows || !d_y)) return fail(SDNN_E_ARG, "NULL argument");
+  if (net->ws_cap < 0 || (net->L > 0 && net->plan_dirty)) return fail(SDNN_E_STATE, "no inference yet");
+  sdnn_status st = set_device(net);
+  if (st) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (net->L == 0)
+    launch_gather_rows(net->ws, 0, false, net->n, net->opts.ymax, d_rows, nrows, net->last_batch, d_y, s);
+  else
+    launch_gather_rows(net->ws, net->steps.back().a, true, net->n, net->opts.ymax, d_rows, nrows,
+                       net->last_batch, d_y, s);
+  CK(cudaGetLastError());
   return SDNN_OK;
 }
 

@@ -368,11 +368,20 @@ void build_pass(const std::vector<const PackedLayer *> &layers, int32_t n, const
     }
     C = std::max<int>(C, (int)bins[c].size());
   }
+  // a component that needs more CTAs than a cluster holds is not buildable:
+  // leave `out` empty (m = 0) and let plan_passes fall back (one-layer steps
+  // run as plain layers, longer passes lose their last layer)
+  out = PassHost();
+  if (C > kMaxPassCluster) return;
   if (C > 1) C = C <= 2 ? 2 : 4;                  // cluster sizes 2 / 4
+  {
+    int Rp = 32;
+    while (Rp < R) Rp <<= 1;
+    if (!pass_variant(std::max(16, std::min(512, tile_floats / Rp)), C)) return;   // no kernel instance
+  }
   // slot code of a boundary node: (bin << 8) | slot within the bin
   std::vector<int32_t> slot((size_t)(m + 1) * n, -1);
   std::vector<int32_t> bin_of_sub((size_t)(m + 1) * n, 0);
-  out = PassHost();
   out.a = s.a;
   out.m = m;
   out.ncomp = ncomp;
@@ -529,7 +538,7 @@ std::vector<Step> plan_passes(const std::vector<const PackedLayer *> &layers, in
     // layers after it are planned again (any prefix of a pass is a pass)
     int bad = -1;
     for (int i = 0; i < (int)steps.size() && bad < 0; ++i)
-      if (steps[i].m > 1 && ph[i].rec_bytes > kPassRecMax) bad = i;
+      if (steps[i].m > 1 && (ph[i].m == 0 || ph[i].rec_bytes > kPassRecMax)) bad = i;
     for (int i = 0; i < (int)steps.size(); ++i)   // a one-layer record that does not fit: plain layer
       if (steps[i].m == 1 && ph[i].rec_bytes > kPassRecMax) ph[i] = PassHost();
     if (bad < 0) break;

@@ -1018,9 +1018,7 @@ __global__ void __launch_bounds__(1024) k_list_bits(const uint32_t *__restrict__
                                                     const uint32_t *__restrict__ retired,
                                                     int64_t words, int32_t *wpre, int32_t *cats,
                                                     int32_t *ncat, uint32_t *d_alive_out) {
-  __shared__ int dummy;
-  (void)dummy;
-  // merge (in place into a scratch copy is not needed: OR on the fly)
+  // merge the two bitmasks on the fly
   const int64_t per = (words + blockDim.x - 1) / blockDim.x;
   const int64_t w0 = min(words, (int64_t)threadIdx.x * per), w1 = min(words, w0 + per);
   int64_t sum = 0;
@@ -1063,6 +1061,43 @@ __global__ void k_yout(const LayerState *__restrict__ st, int a, int final_out,
        it += (int64_t)gridDim.x * blockDim.x) {
     const int64_t j = it / S.width, p = it - j * S.width;
     yout[(int64_t)rid[p] * n + j] = Y[yix(j, p, stride, yblk)];
+  }
+}
+
+// Y_L of selected ORIGINAL rows (sampled-row parity at full size): one CTA per
+// requested row; its position is found by binary search in the final row-id
+// map (ascending: densify and compaction are stable); a row without a position
+// (dropped as empty or dead) is all zeros, a retired row (f2) all YMAX.
+__global__ void __launch_bounds__(256) k_gather_rows(const LayerState *__restrict__ st, int a, int final_out,
+                                                     const float *Ya, const float *Yb, const int32_t *ridA,
+                                                     const int32_t *ridB, int32_t n, int64_t stride,
+                                                     int32_t yblk, const uint32_t *__restrict__ retired,
+                                                     float ymax, const int32_t *__restrict__ rows,
+                                                     int64_t nrows, int64_t batch, float *out) {
+  __shared__ int64_t s_pos;
+  const LayerState S = st[a];
+  const float *Y = (final_out ? 1 - S.in : S.in) ? Yb : Ya;
+  const int32_t *rid = S.rid ? ridB : ridA;
+  for (int64_t q = blockIdx.x; q < nrows; q += gridDim.x) {
+    const int32_t row = rows[q];
+    if (threadIdx.x == 0) {
+      int64_t lo = 0, hi = S.width;                  // first position with rid >= row
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (rid[mid] < row) lo = mid + 1;
+        else hi = mid;
+      }
+      int64_t p = (lo < S.width && rid[lo] == row) ? lo : -1;
+      if (row < 0 || row >= batch) p = -1;         // out of range: zeros
+      else if (retired && ((retired[row >> 5] >> (row & 31)) & 1u)) p = -2;
+      s_pos = p;
+    }
+    __syncthreads();
+    const int64_t p = s_pos;
+    float *o = out + q * (int64_t)n;
+    for (int32_t j = threadIdx.x; j < n; j += blockDim.x)
+      o[j] = p >= 0 ? Y[yix(j, p, stride, yblk)] : (p == -2 ? ymax : 0.f);
+    __syncthreads();
   }
 }
 
@@ -1260,6 +1295,14 @@ void launch_readout(const Workspace &w, int32_t a, const uint32_t *alive_last,
   if (d_alive_out) cudaMemsetAsync(d_alive_out, 0, sizeof(uint32_t) * (size_t)((batch + 31) / 32), s);
   k_readout<<<1, 1024, 0, s>>>(w.st, a, alive_last, w.rid[0], w.rid[1], w.wpre, w.cats, w.ncat,
                                d_alive_out);
+}
+
+void launch_gather_rows(const Workspace &w, int32_t a, bool final_out, int32_t n, float ymax,
+                        const int32_t *d_rows, int64_t nrows, int64_t batch, float *d_y, cudaStream_t s) {
+  if (nrows <= 0) return;
+  k_gather_rows<<<(int)std::min<int64_t>(nrows, 148 * 8), 256, 0, s>>>(
+      w.st, a, final_out ? 1 : 0, w.Y[0], w.Y[1], w.rid[0], w.rid[1], n, w.stride, w.yblk,
+      w.sat[0] ? w.retired : nullptr, ymax, d_rows, nrows, batch, d_y);
 }
 
 void launch_yout(const Workspace &w, int32_t a, bool final_out, int32_t n, int64_t batch,

@@ -262,6 +262,9 @@ void launch_readout(const Workspace &w, int32_t a, const uint32_t *alive_last,
 // Y_L: final_out = the output buffer of the step entered with st[a] (L > 0), else Y_0
 void launch_yout(const Workspace &w, int32_t a, bool final_out, int32_t n, int64_t batch,
                  float *d_yout, cudaStream_t s);
+// Y_L rows of the given original row ids (same buffer selection as launch_yout)
+void launch_gather_rows(const Workspace &w, int32_t a, bool final_out, int32_t n, float ymax,
+                        const int32_t *d_rows, int64_t nrows, int64_t batch, float *d_y, cudaStream_t s);
 void launch_resident(const Workspace &w, const ResLayerDev *layers, int a, int L, int n,
                      uint32_t *alive_final, bool compact, float ymax, cudaStream_t s);
 

@@ -60,7 +60,7 @@ import numpy as np
 
 __all__ = [
     "K", "W_VALUE", "bias_value", "net_seed", "input_seed", "NetSpec", "Layer",
-    "rn_spec", "rr_spec", "ka_spec", "random_spec", "gen_layer", "iter_layers",
+    "rn_spec", "rr_spec", "rw_spec", "rw_bias", "ka_spec", "random_spec", "gen_layer", "iter_layers",
     "ms_inputs", "ka_inputs", "random_inputs", "structure_hash", "csr_from_dense",
     "dense_from_csr", "ka_group_counts",
 ]
@@ -126,6 +126,25 @@ def rn_spec(n: int, L: int, seed: Optional[int] = None, **kw) -> NetSpec:
     assert n >= 32 and n & (n - 1) == 0, "RN needs a power-of-two width >= 32"
     return NetSpec("rn", n, L, net_seed(n, L) if seed is None else seed,
                    kw.pop("bias", bias_value(n)), **kw)
+
+
+# RW (general weights): the RN structure with one seeded value per slot drawn
+# from U(-0.05, 0.15) (mean 0.05 < 1/16); the per-width biases below keep
+# 29-45 % of the MS inputs alive through the whole network (measured with the
+# oracle on sampled rows, reading R-W4)
+_RW_BIAS = {1024: -0.125, 4096: -0.15, 16384: -0.175, 65536: -0.225}
+
+
+def rw_bias(n: int) -> float:
+    if n in _RW_BIAS:
+        return _RW_BIAS[n]
+    lg = np.log2(n) / 2.0 - 5.0
+    return float(np.clip(-0.125 - 0.025 * lg, -0.225, -0.125))
+
+
+def rw_spec(n: int, L: int, seed: Optional[int] = None, **kw) -> NetSpec:
+    """RN structure with per-slot random weights (the general-weight path)."""
+    return rn_spec(n, L, seed=seed, wdist="random", bias=kw.pop("bias", rw_bias(n)), **kw)
 
 
 def rr_spec(n: int, L: int, seed: Optional[int] = None, **kw) -> NetSpec:

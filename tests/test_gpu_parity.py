@@ -485,39 +485,78 @@ def test_row_independence_on_gpu(sd, c1):
 # full 60000-input batch on the GPU, checked on sampled rows the oracle
 # computes one by one (row independence, I4), sentinel rows included.
 # ---------------------------------------------------------------------------
-def _full_size(sd, n, L, nsample):
-    spec = g.rn_spec(n, L)
-    rp, idx = g.ms_inputs(n, 60000)
-    with sd.Net.from_spec(spec, fmt="ell", threads=8) as net:
+def _full_size(sd, spec, nsample, batch=60000, flags=0):
+    """The full batch on the GPU (default options = the benchmarked launch
+    configuration), then on `nsample` random rows plus the sentinel rows:
+    categories bit-exact AND final activations Y_L bit-exact and within the
+    north_star tolerance, the rows gathered on the device (sdnn_gather_rows)
+    so no [batch x N] host copy is needed."""
+    n, L = spec.n, spec.L
+    rp, idx = g.ms_inputs(n, batch)
+    with sd.Net.from_spec(spec, fmt="ell", threads=8, flags=flags) as net:
         cats, _ = net.infer(rp, idx, None)
         st = net.stats()
-    r = np.random.default_rng(n)
-    rows = np.unique(np.concatenate([r.choice(60000, nsample, replace=False),
-                                     [998, 999, 1998, 1999, 59998, 59999]]))
-    oc, _, _, _ = oracle.infer_spec_rows(spec, rp, idx, None, rows)
+        r = np.random.default_rng(n ^ L)
+        sent = [i for i in (998, 999, 1998, 1999, batch - 2, batch - 1) if i < batch]
+        rows = np.unique(np.concatenate([r.choice(batch, nsample, replace=False), sent])).astype(np.int32)
+        Yg = net.gather_rows(rows)
+        Yg2 = net.gather_rows(rows[::-1].copy())[::-1]                # any order
+    oc, oY, _, _ = oracle.infer_spec_rows(spec, rp, idx, None, rows)
     got = np.isin(rows, cats)
     assert np.array_equal(got, oc), rows[got != oc]
-    assert got[np.isin(rows, [999, 1999, 59999])].all()           # all-ones sentinels
-    assert not got[np.isin(rows, [998, 1998, 59998])].any()       # empty sentinels
+    np.testing.assert_allclose(Yg, oY, rtol=RTOL, atol=ATOL)
+    assert np.array_equal(Yg.view(np.uint32), oY.view(np.uint32))
+    assert np.array_equal(Yg2, Yg)
+    assert np.array_equal((Yg > 0).any(1), got)
+    if spec.wdist == "uniform":
+        assert got[np.isin(rows, [999, 1999, batch - 1])].all()   # all-ones sentinels
+    assert not got[np.isin(rows, [998, 1998, batch - 2])].any()   # empty sentinels
     # survivor profile sanity: non-increasing, final == number of categories
     live = st["live_rows"]
     assert all(a >= b for a, b in zip(live, live[1:])) and live[-1] == cats.size
-    return cats, st
+    return cats, st, oY
 
 
 def test_full_size_c2(sd):
-    _full_size(sd, 4096, 480, 200)
+    _full_size(sd, g.rn_spec(4096, 480), 200)
 
 
 @pytest.mark.slow
 def test_full_size_c3(sd):
-    _full_size(sd, 16384, 1920, 48)
+    _full_size(sd, g.rn_spec(16384, 1920), 96)
 
 
 @pytest.mark.slow
 def test_full_size_c4(sd):
-    cats, st = _full_size(sd, 65536, 1920, 24)
+    cats, st, oY = _full_size(sd, g.rn_spec(65536, 1920), 64)
     assert st["path"] & 4                      # the benchmarked (position-blocked) layout
+    assert st["steps"] < 1920                  # fused passes (the cost-cover plan)
+
+
+@pytest.mark.slow
+def test_full_size_per_slot_weights_c3_width(sd):
+    """General weights (one fp32 value per slot, RN structure, bias chosen so
+    ~45 % of the rows survive) at C3 width on the full 60,000-input batch."""
+    cats, st, oY = _full_size(sd, g.rw_spec(16384, 480), 64)
+    assert st["fused_layers"] == 0 or st["max_group"] == 32
+    assert 0.2 * 60000 < cats.size < 0.7 * 60000
+    assert (oY > 0).any() and ((oY > 0) & (oY < 32)).any()      # unsaturated values are compared too
+
+
+def test_gather_rows_edge_cases(sd, c1):
+    """Rows out of range and dead rows gather as zeros; repeated rows; before
+    any inference the call is refused."""
+    spec, layers, rp, idx, cats, Y, prof = c1
+    with sd.Net.from_layers(1024, layers, fmt="ell") as net:
+        with pytest.raises(sd.SdnnError) as e:
+            net.gather_rows(np.array([0], np.int32))
+        assert e.value.status == sd.SDNN_E_STATE
+        net.infer(rp, idx, None)
+        rows = np.array([0, 5, 5, -1, 1000, 999, 998, 3], np.int32)
+        Yg = net.gather_rows(rows)
+    for q, r in enumerate(rows):
+        want = Y[r] if 0 <= r < 1000 else np.zeros(1024, np.float32)
+        assert np.array_equal(Yg[q].view(np.uint32), want.view(np.uint32))
 
 
 def ragged_block_layers(n, L, w, seed, sb=64, shift=0.0, bmin=1):

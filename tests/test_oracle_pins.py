@@ -265,3 +265,49 @@ def test_zero_layers_and_empty_batch():
     assert cats.tolist() == [True, False, False]           # only positive entries count
     cats, Y, _ = oracle.infer(n, [], np.zeros(1, np.int64), np.zeros(0, np.int32), None)
     assert cats.size == 0 and Y.shape == (0, n)
+
+
+# ------------------------------------------------ survivor profile (live rows)
+# oracle_live_rows counts rows with at least one nonzero entry; the GPU tests
+# compare the library's per-layer survivor profile against it, so it is pinned
+# here on its own: a hand-counted matrix and the KA closed form per layer.
+
+def test_live_rows_hand_count():
+    """Rows (n = 4): empty | explicit +0.0 | -0.0 | denormal 2^-149 | -3 |
+    all 32 | +0.5 in the last column | +0.0 and -0.0 together.  By hand: rows
+    3, 4, 5, 6 are nonzero (a -0.0 entry is zero), so the count is 4."""
+    tiny = float.fromhex("0x1p-149")
+    rows = [[], [(1, 0.0)], [(2, -0.0)], [(0, tiny)], [(3, -3.0)],
+            [(0, 32.0), (1, 32.0), (2, 32.0), (3, 32.0)], [(3, 0.5)], [(0, 0.0), (3, -0.0)]]
+    rp = np.zeros(len(rows) + 1, np.int64)
+    rp[1:] = np.cumsum([len(r) for r in rows])
+    idx = np.array([k for r in rows for k, _ in r], np.int32)
+    val = np.array([v for r in rows for _, v in r], np.float32)
+    o = oracle.Oracle(4, rp, idx, val)
+    assert o.live_rows() == 4
+    cats = o.categories()                     # categories need a POSITIVE entry (reading A7)
+    assert cats.tolist() == [False, False, False, True, False, True, True, False]
+
+
+@pytest.mark.parametrize("n,L,seed", [(1024, 20, 11), (2048, 17, 5)])
+def test_live_rows_ka_profile(n, L, seed):
+    """KA closed form per layer: after layer l a row is live iff one of its
+    groups has a nonzero scalar trajectory value at l (groups are independent
+    and uniform after layer 0)."""
+    spec = g.ka_spec(n, L)
+    rp, idx, cnt = g.ka_inputs(n, 300, seed=seed)
+    _, _, prof = oracle.infer(n, g.iter_layers(spec), rp, idx, None, nthreads=2, profile=True)
+    traj = np.stack([ka_scalar_trajectory(c, spec.bias, L) for c in range(33)])   # [count, layer]
+    want = [int((traj[cnt, l] > 0).any(1).sum()) for l in range(L)]
+    assert prof == want
+    assert want[0] > want[-1] > 0
+
+
+def test_live_rows_hand_nets(hand_nets):
+    """The last entry of the profile of every golden hand net equals the number
+    of nonzero rows of its hand-derived Y_L."""
+    for net in hand_nets.values():
+        o = oracle.Oracle(net.n, net.y0_rowptr, net.y0_idx, net.y0_val)
+        for lay in net.layers:
+            o.layer(lay["rowptr"], lay["colidx"], lay["val"], 0.0, lay["bias"], ymax=net.ymax)
+        assert o.live_rows() == int((net.expected_Y != 0).any(1).sum()), net.name
