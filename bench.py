@@ -11,8 +11,12 @@ CSR, run every layer (one captured CUDA Graph), read out the categories and,
 for N > 1, all-gather the category bitmasks over NCCL.  Inputs are resident in
 HBM when the timed region starts (`value`); `e2e` repeats the measurement
 through the host-buffer call sdnn_infer (H2D of Y0 + D2H of the categories
-inside the timed region).  Multi-GPU is weak scaling: every rank infers its
-own 60,000-input batch against a replica of the weights.
+inside the timed region).  Multi-GPU (torchrun, N > 1) is strong scaling by
+default, BASELINE configs[3]: the one 60,000-input batch is split into
+word-aligned contiguous row slices, every rank infers its slice against its
+replica of the weights, the category bitmasks are all-gathered over NCCL and
+decoded on the device; --scaling weak gives every rank
+its own 60,000-input batch.
 """
 import argparse
 import json
@@ -213,7 +217,8 @@ def run_gpu(args):
                            fuse_rows=args.fuse_rows, fuse_layers=args.fuse_layers,
                            stream_slots=args.stream_slots)
     t_load = time.time() - t0
-    if args.scaling == "strong" and ws > 1:
+    strong = args.scaling == "strong"
+    if strong:
         # one global batch, contiguous word-aligned slices (dist.partition)
         rp, idx = make_inputs(n, B, 0)
         lo, hi = sdist.partition(B, ws, rank)
@@ -230,10 +235,20 @@ def run_gpu(args):
     alive_view = alive[: (batch + 31) // 32]
     stream = torch.cuda.current_stream(dev)
 
-    def step():
+    gB = B if strong else batch * ws                  # rows of the global bitmask
+    gev = []                                          # (before, after) the collective, per timed step
+
+    def step(timed=False):
         net.infer_torch(rp_t, idx_t, None, alive_t=alive_view, stream=stream)
         if ws > 1:
-            sdist.gather_bitmask(alive)          # the single collective (NCCL all-gather)
+            if timed:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+            allw = sdist.gather_bitmask(alive)          # the single collective (NCCL all-gather)
+            if timed:
+                e1.record(stream)
+                gev.append((e0, e1))
+            sdist.decode_device(allw, gB, stream)      # global ascending ids, on the device
 
     for _ in range(args.warmup):
         step()
@@ -245,7 +260,7 @@ def run_gpu(args):
         torch.cuda.synchronize(dev)
         ev0.record(stream)
         for _ in range(args.steps):
-            step()
+            step(timed=True)
         ev1.record(stream)
         torch.cuda.synchronize(dev)
     if ws > 1:
@@ -253,13 +268,23 @@ def run_gpu(args):
     ms = ev0.elapsed_time(ev1) / args.steps
     st = net.stats()
     layer_ms = net.layer_times()                     # per-layer kernel durations, last step
+    multi = None
     if ws > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        gms = sum(a.elapsed_time(b) for a, b in gev) / max(1, len(gev))
+        got = [None] * ws
+        dist.all_gather_object(got, [ms, gms])
+        allt = np.array(got, np.float64).reshape(ws, 2)
+        per_rank = allt[:, 0].tolist()
+        ms = float(allt[:, 0].max())
+        multi = {"per_rank_ms": per_rank, "imbalance_max_over_mean": ms / float(np.mean(per_rank)),
+                 "allgather_ms_per_step": float(allt[:, 1].max()),
+                 "rows_per_rank": [int(min(B, (r + 1) * sdist.chunk_rows(B, ws)) - min(B, r * sdist.chunk_rows(B, ws)))
+                                   for r in range(ws)] if strong else [batch] * ws,
+                 "collective": "torch.distributed.all_gather_into_tensor (NCCL) of ceil(rows/32) "
+                               "uint32 bitmask words per rank, then k_bitmask_ids on every rank"}
     total_nnz = st["total_nnz"]
     edges_rank = batch * total_nnz
-    value = edges_rank * ws / (ms * 1e-3) if args.scaling != "strong" else B * total_nnz / (ms * 1e-3)
+    value = edges_rank * ws / (ms * 1e-3) if not strong else B * total_nnz / (ms * 1e-3)
 
     # ---- roofline of the dominant kernels (the layer steps) ---------------------
     # A step (one kernel) runs m layers: k_layer_bulk (m = 1) or a fused pass
@@ -302,26 +327,34 @@ def run_gpu(args):
     # ---- e2e through the public host-buffer call --------------------------------
     e2e = None
     if not args.no_e2e:
+        # pinned host copies of this rank's rows; every step copies them in
         rp_h = torch.from_numpy(rp).pin_memory().numpy()
         idx_h = torch.from_numpy(idx).pin_memory().numpy()
-        for _ in range(1):
-            cats, _ = net.infer(rp_h, idx_h, None)
+        if ws == 1:
+            call = lambda: net.infer(rp_h, idx_h, None)[0]           # noqa: E731
+            what = "sdnn_infer (host CSR in, host categories out)"
+        else:
+            part = sdist.Partitioned(net, gB, device=dev)            # weak: gB = batch * ws
+            call = lambda: part(rp_h, idx_h)                          # noqa: E731
+            what = ("paper_2004_10908_b200.dist.Partitioned: pinned host slice -> H2D -> "
+                    "sdnn_infer_device -> NCCL all-gather -> k_bitmask_ids -> D2H of the ids")
+        cats = call()
         times = []
         for _ in range(args.e2e_steps):
             if ws > 1:
                 dist.barrier()
             t1 = time.perf_counter()
-            cats, _ = net.infer(rp_h, idx_h, None)
+            cats = call()
             times.append(time.perf_counter() - t1)
         te = float(np.mean(times))
         if ws > 1:
             t = torch.tensor([te], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             te = float(t.item())
-        e2e = {"value": edges_rank * ws / te, "unit": UNIT,
-               "h2d_bytes_per_step": int(rp_h.nbytes + idx_h.nbytes),
-               "d2h_bytes_per_step": int(4 + 4 * cats.size), "ms_per_step": te * 1e3,
-               "call": "sdnn_infer (host CSR in, host categories out)"}
+        e2e = {"value": (edges_rank * ws if not strong else B * total_nnz) / te, "unit": UNIT,
+               "h2d_bytes_per_step": int(rp_h.nbytes + idx_h.nbytes) * ws,
+               "d2h_bytes_per_step": int(4 + 4 * cats.size) * ws, "ms_per_step": te * 1e3,
+               "call": what}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -333,11 +366,11 @@ def run_gpu(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak" if args.scaling != "strong" else "strong", "vs_baseline": None,
+            "scaling": "strong" if strong else "weak", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
             "config": {"workload": f"{args.net}{n}x{L}-ms{B}", "neurons": n, "layers": L,
                        "nnz_per_column": 32, "inputs_per_gpu": batch,
-                       "global_batch": batch * ws if args.scaling != "strong" else B,
+                       "global_batch": batch * ws if not strong else B,
                        "network": ("RadiX-Net-shaped (sdnngen.rn_spec)" if args.net == "rn" else
                                    "random 32-regular, no shared source sets (sdnngen.rr_spec)")
                                   + ", w=1/16, b=%g" % spec.bias,
@@ -354,6 +387,7 @@ def run_gpu(args):
                           sorted(set([0, 1, 2, 4, 8, 16, 32, 64, L // 2, L - 1])) if i < L},
                           "categories": int(live[-1]) if live else None,
                           "category_fraction": (live[-1] / batch) if live and batch else None},
+            "multi_gpu": multi,
             "load_seconds": t_load,
             "flags": args.flags or None,
             "fuse": {"rows": args.fuse_rows, "layers": args.fuse_layers,
@@ -394,7 +428,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="sdnn", choices=["sdnn", "reference"])
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
+                    help="N > 1: strong = the one 60,000-input batch split across ranks "
+                         "(BASELINE configs[3], default); weak = every rank its own batch")
     ap.add_argument("--net", default="rn", choices=["rn", "rr"],
                     help="network family: rn = RadiX-Net-shaped (headline), rr = random 32-regular")
     ap.add_argument("--e2e-steps", type=int, default=3)

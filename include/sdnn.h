@@ -200,6 +200,19 @@ sdnn_status sdnn_infer_device(sdnn_net *net, const int64_t *d_rowptr, const int3
 sdnn_status sdnn_gather_rows(sdnn_net *net, const int32_t *d_rows, int64_t nrows, float *d_y,
                              void *stream);
 
+/* Multi-GPU readout (no handle needed): decode a global category bitmask --
+ * e.g. the NCCL all-gather of every rank's d_alive words, rows partitioned in
+ * word-aligned contiguous slices (paper_2004_10908_b200/dist.py; the per-GPU
+ * cudaFlows of PAPER.md:2566-2569 followed by one gather of the categories,
+ * north_star) -- into the ascending 0-based category ids.
+ *   d_words  [ceil(batch/32)] uint32 DEVICE: bit i%32 of word i/32 = row i
+ *            (bits at and beyond `batch` are ignored);
+ *   d_ids    [batch] int32 DEVICE capacity: receives the ascending ids;
+ *   d_n      [1] int32 DEVICE: receives their count.
+ * Asynchronous on `stream` (cudaStream_t; NULL = legacy default stream). */
+sdnn_status sdnn_bitmask_to_ids(const uint32_t *d_words, int64_t batch, int32_t *d_ids,
+                                int32_t *d_n, void *stream);
+
 /* Statistics of the handle and of its last completed inference. */
 typedef struct sdnn_stats {
   int32_t struct_size;        /* caller sets sizeof(sdnn_stats) (versioning)            */

@@ -34,7 +34,7 @@ SDNN_F_SATURATE = 256
 EXPORTS = ["sdnn_create", "sdnn_create_empty", "sdnn_set_layer", "sdnn_infer",
            "sdnn_infer_device", "sdnn_stats_get", "sdnn_validate_layer", "sdnn_destroy",
            "sdnn_last_error", "sdnn_abi_version", "sdnn_layer_times", "sdnn_plan_steps",
-           "sdnn_step_plan", "sdnn_gather_rows"]
+           "sdnn_step_plan", "sdnn_gather_rows", "sdnn_bitmask_to_ids"]
 
 
 class SdnnError(RuntimeError):
@@ -100,6 +100,7 @@ def lib() -> ctypes.CDLL:
         L.sdnn_plan_steps.argtypes = [I32, I32, P(sdnn_layer), V, P(sdnn_opts), V, P(I32)]
         L.sdnn_step_plan.argtypes = [V, V, P(I32)]
         L.sdnn_gather_rows.argtypes = [V, V, I64, V, V]
+        L.sdnn_bitmask_to_ids.argtypes = [V, I64, V, V, V]
         L.sdnn_destroy.argtypes = [V]
         L.sdnn_destroy.restype = None
         L.sdnn_last_error.argtypes = []
@@ -107,7 +108,8 @@ def lib() -> ctypes.CDLL:
         L.sdnn_abi_version.restype = I32
         for name in ["sdnn_create", "sdnn_create_empty", "sdnn_set_layer", "sdnn_infer",
                      "sdnn_infer_device", "sdnn_stats_get", "sdnn_validate_layer",
-                     "sdnn_layer_times", "sdnn_plan_steps", "sdnn_step_plan", "sdnn_gather_rows"]:
+                     "sdnn_layer_times", "sdnn_plan_steps", "sdnn_step_plan", "sdnn_gather_rows",
+                     "sdnn_bitmask_to_ids"]:
             getattr(L, name).restype = I32
         _LIB = L
     return _LIB
@@ -368,6 +370,20 @@ class Net:
 
     def __exit__(self, *a):
         self.close()
+
+
+def bitmask_to_ids_torch(words_t, batch: int, stream=None):
+    """Device decode of a global category bitmask (sdnn_bitmask_to_ids): returns
+    (ids int32 CUDA tensor [batch] capacity, count int32 CUDA tensor [1]); the
+    first count entries are the ascending category ids."""
+    import torch
+    dev = words_t.device
+    ids = torch.empty(max(int(batch), 1), dtype=torch.int32, device=dev)
+    cnt = torch.zeros(1, dtype=torch.int32, device=dev)
+    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    _check(lib().sdnn_bitmask_to_ids(words_t.data_ptr() if batch > 0 else None, int(batch),
+                                     ids.data_ptr(), cnt.data_ptr(), s.cuda_stream))
+    return ids, cnt
 
 
 def bitmask_to_ids(words: np.ndarray, batch: int) -> np.ndarray:

@@ -355,6 +355,15 @@ bool yblock_wanted() {
   return e ? atoi(e) != 0 : kYBlockDefault;
 }
 
+// fused-pass item order (SDNN_PASS_ORDER=comp|tile; A/B knob)
+int pass_order() {
+  static const int v = [] {
+    const char *e = getenv("SDNN_PASS_ORDER");
+    return (e && std::strcmp(e, "tile") == 0) ? 1 : 0;
+  }();
+  return v;
+}
+
 sdnn_status make_plan(sdnn_net *net) {
   if (!net->plan_dirty) return SDNN_OK;
   const bool sat = net->opts.flags & SDNN_F_SATURATE;
@@ -477,6 +486,7 @@ sdnn_status make_plan(sdnn_net *net) {
     D.C = H.C;
     D.rec_bytes = H.rec_bytes;
     D.yblk = net->yblk;
+    D.order = pass_order();
     if (!streaming) {                            // else: pointers into the slot ring
       void *p1, *p2, *p3;
       sdnn_status st;
@@ -1053,6 +1063,16 @@ sdnn_status sdnn_infer(sdnn_net *net, const int64_t *y0_rowptr, const int32_t *y
   }
   *n_categories = ncat;
   net->last_ncat = ncat;
+  return SDNN_OK;
+}
+
+sdnn_status sdnn_bitmask_to_ids(const uint32_t *d_words, int64_t batch, int32_t *d_ids, int32_t *d_n,
+                                void *stream) {
+  if (batch < 0 || batch > (int64_t(1) << 30)) return fail(SDNN_E_ARG, "batch out of range");
+  if (!d_n || (batch > 0 && (!d_words || !d_ids))) return fail(SDNN_E_ARG, "NULL argument");
+  launch_bitmask_ids(d_words, batch, d_ids, d_n, (cudaStream_t)stream);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(SDNN_E_CUDA, std::string("k_bitmask_ids: ") + cudaGetErrorString(e));
   return SDNN_OK;
 }
 

@@ -603,6 +603,13 @@ __global__ void __launch_bounds__(32 * kPassNW, 3)
   float *__restrict__ Yout = Sx.in ? Ya : Yb;
   const int tiles = (width + T - 1) / T;
   const int64_t items = (int64_t)P.ncomp * tiles;
+  // item -> (component, tile): component-major (consecutive CTAs take
+  // consecutive tiles of one component) or tile-major (consecutive CTAs take
+  // the same tile of consecutive components, so the CTAs in flight together
+  // read and write whole position blocks of the activation buffers)
+  const bool tmaj = P.order != 0;
+  auto item_comp = [&](int64_t it) -> int64_t { return tmaj ? it % P.ncomp : it / tiles; };
+  auto item_tile = [&](int64_t it) -> int { return (int)(tmaj ? it / P.ncomp : it % tiles); };
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int seg = lane / LPU, sll = lane % LPU;  // segment (unit) of the lane, lane in it
   const uint32_t rank = C > 1 ? cluster_rank() : 0u;
@@ -627,7 +634,7 @@ __global__ void __launch_bounds__(32 * kPassNW, 3)
   // thread tid owns input rows tid + 128 q of an item (row id in nrow[q])
   int nrow[RPT], ncnt = 0;
   auto fetch_rows = [&](int64_t it) {
-    const int64_t cb = (it / tiles) * C + rank;
+    const int64_t cb = item_comp(it) * C + rank;
     ncnt = __ldg(P.in_count + cb);
     if (blk) {                                   // consecutive storage rows: the first one
       nrow[0] = __ldg(P.in_rows + cb * P.rin);
@@ -640,8 +647,8 @@ __global__ void __launch_bounds__(32 * kPassNW, 3)
     }
   };
   auto issue_load = [&](int64_t it) {
-    const int64_t c = it / tiles;
-    const int tile = (int)(it - c * tiles);
+    const int64_t c = item_comp(it);
+    const int tile = item_tile(it);
     const int64_t cb = c * C + rank;
     if (tid == 0) {
       mbar_expect_tx_arrive(bar, (ldg ? 0u : (uint32_t)ncnt * T * 4) + (uint32_t)P.rec_bytes);
@@ -694,8 +701,8 @@ __global__ void __launch_bounds__(32 * kPassNW, 3)
   }
   uint32_t ph = 0;
   for (int64_t it = cid; it < items; it += ncl, ph ^= 1u) {
-    const int64_t c = it / tiles;
-    const int tile = (int)(it - c * tiles);
+    const int64_t c = item_comp(it);
+    const int tile = item_tile(it);
     const int64_t next = it + ncl;
     if (next < items) fetch_rows(next);          // in flight while this item computes
     bool issued = false;
@@ -1036,6 +1043,38 @@ __global__ void __launch_bounds__(1024) k_list_bits(const uint32_t *__restrict__
   }
   (void)wpre;
   if (threadIdx.x == 0) *ncat = (int32_t)total;
+}
+
+// Multi-GPU readout: the all-gathered global bitmask -> ascending row ids
+// (single CTA: popcount scan over the words, then each thread lists its run)
+__global__ void __launch_bounds__(1024) k_bitmask_ids(const uint32_t *__restrict__ words, int64_t batch,
+                                                      int32_t *ids, int32_t *nids) {
+  const int64_t nw = (batch + 31) >> 5;
+  const int64_t per = (nw + blockDim.x - 1) / blockDim.x;
+  const int64_t w0 = min(nw, (int64_t)threadIdx.x * per), w1 = min(nw, w0 + per);
+  auto word = [&](int64_t q) {
+    uint32_t b = words[q];
+    const int64_t base = q * 32;
+    if (batch - base < 32) b &= (1u << (batch - base)) - 1u;     // bits past the batch
+    return b;
+  };
+  int64_t sum = 0;
+  for (int64_t q = w0; q < w1; ++q) sum += __popc(word(q));
+  int64_t total;
+  int64_t run = block_exclusive_scan(sum, &total);
+  for (int64_t q = w0; q < w1; ++q) {
+    uint32_t bits = word(q);
+    while (bits) {
+      const int b = __ffs(bits) - 1;
+      bits &= bits - 1;
+      ids[run++] = (int32_t)(q * 32 + b);
+    }
+  }
+  if (threadIdx.x == 0) *nids = (int32_t)total;
+}
+
+void launch_bitmask_ids(const uint32_t *d_words, int64_t batch, int32_t *d_ids, int32_t *d_n, cudaStream_t s) {
+  k_bitmask_ids<<<1, 1024, 0, s>>>(d_words, batch, d_ids, d_n);
 }
 
 // f2: rows retired as saturated are all-YMAX in Y_L

@@ -167,6 +167,7 @@ struct DevPass {
   int32_t C;                           // cluster size: in_rows/in_count/rec indexed [comp * C + rank]
   int32_t yblk;                        // 0: Y is [rows][stride]; R > 0: Y is [stride/32][R][32] and
                                        // every (comp, rank)'s rows are R-consecutive storage rows
+  int32_t order;                       // item order: 0 component-major, 1 tile-major
   const int32_t *in_rows, *in_count;
   const unsigned char *rec;            // [ncomp][rec_bytes]
   PassLayerDev layers[kMaxPassLayers]; // by value: the kernel parameter carries them
@@ -262,6 +263,8 @@ void launch_readout(const Workspace &w, int32_t a, const uint32_t *alive_last,
 // Y_L: final_out = the output buffer of the step entered with st[a] (L > 0), else Y_0
 void launch_yout(const Workspace &w, int32_t a, bool final_out, int32_t n, int64_t batch,
                  float *d_yout, cudaStream_t s);
+// global category bitmask (batch bits) -> ascending ids, count in *d_n
+void launch_bitmask_ids(const uint32_t *d_words, int64_t batch, int32_t *d_ids, int32_t *d_n, cudaStream_t s);
 // Y_L rows of the given original row ids (same buffer selection as launch_yout)
 void launch_gather_rows(const Workspace &w, int32_t a, bool final_out, int32_t n, float ymax,
                         const int32_t *d_rows, int64_t nrows, int64_t batch, float *d_y, cudaStream_t s);

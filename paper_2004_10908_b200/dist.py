@@ -61,21 +61,71 @@ def gather_bitmask(local_words, group=None):
 
 
 def decode(words, batch: int) -> np.ndarray:
-    """Global bitmask words -> ascending category ids (< batch)."""
+    """Host decode of global bitmask words -> ascending category ids (< batch);
+    the CPU/gloo path (the GPU path decodes on the device, decode_device)."""
     w = np.ascontiguousarray(np.asarray(words)).view(np.uint32)
     bits = np.unpackbits(w.view(np.uint8), bitorder="little")[:batch]
     return np.flatnonzero(bits).astype(np.int32)
 
 
+def decode_device(words_t, batch: int, stream=None):
+    """Device decode (sdnn_bitmask_to_ids kernel): (ids tensor, count tensor)."""
+    from paper_2004_10908_b200 import bitmask_to_ids_torch
+    return bitmask_to_ids_torch(words_t, batch, stream)
+
+
+class Partitioned:
+    """Strong-scaling inference of one global batch over the process group:
+    this rank owns the contiguous word-aligned slice partition(B, P, rank) of
+    the rows, infers it on its GPU against its replica of the weights
+    (sdnn_infer_device), then the bitmask words are all-gathered over NCCL and
+    decoded on the device into the ascending global category ids.  Inputs
+    arrive from (pinned) host memory each call (the end-to-end path); the
+    staging tensors are allocated once."""
+
+    def __init__(self, net, batch: int, group=None, device=None):
+        import torch
+        import torch.distributed as dist
+        self.net, self.batch, self.group = net, int(batch), group
+        self.ws, self.rank = dist.get_world_size(group), dist.get_rank(group)
+        self.lo, self.hi = partition(self.batch, self.ws, self.rank)
+        self.dev = device or torch.device("cuda", torch.cuda.current_device())
+        self.words = torch.zeros(words_per_rank(self.batch, self.ws), dtype=torch.int32, device=self.dev)
+        self._rp = self._ix = None
+
+    def slice(self, rowptr, idx):
+        return slice_csr(rowptr, idx, None, self.lo, self.hi)[:2]
+
+    def __call__(self, rp_local, idx_local, stream=None):
+        """rp_local/idx_local: this rank's slice (host numpy, ideally pinned).
+        Returns the global ascending category ids (numpy) on every rank."""
+        import torch
+        s = stream if stream is not None else torch.cuda.current_stream(self.dev)
+        if self._rp is None or self._rp.numel() < rp_local.size or self._ix.numel() < max(1, idx_local.size):
+            self._rp = torch.empty(rp_local.size, dtype=torch.int64, device=self.dev)
+            self._ix = torch.empty(max(1, idx_local.size), dtype=torch.int32, device=self.dev)
+        with torch.cuda.stream(s):
+            rp_t = self._rp[:rp_local.size]
+            ix_t = self._ix[:max(1, idx_local.size)]
+            rp_t.copy_(torch.from_numpy(rp_local), non_blocking=True)
+            if idx_local.size:
+                ix_t[:idx_local.size].copy_(torch.from_numpy(idx_local), non_blocking=True)
+            self.words.zero_()
+            if self.hi > self.lo:
+                self.net.infer_torch(rp_t, ix_t, None, alive_t=self.words[: (self.hi - self.lo + 31) // 32],
+                                     stream=s)
+            allw = gather_bitmask(self.words, self.group)
+            ids, cnt = decode_device(allw, self.batch, s)
+            n = int(cnt.item())                                  # D2H: the count, then the ids
+            return ids[:n].cpu().numpy()
+
+
 def infer_partitioned(net, rowptr: np.ndarray, idx: np.ndarray, val: Optional[np.ndarray],
                       group=None, device=None):
-    """Strong-scaling inference of one global batch: this rank infers its
-    contiguous slice on its GPU (sdnn_infer_device), then the bitmasks are
-    all-gathered (NCCL) and decoded.  Every rank returns the same ascending
-    global category ids."""
+    """Strong-scaling inference of one global batch (see Partitioned); every
+    rank returns the same ascending global category ids."""
     import torch
-    import torch.distributed as dist
-    ws, rank = dist.get_world_size(group), dist.get_rank(group)
+    ws, rank = dist_world(group)
     batch = rowptr.size - 1
     lo, hi = partition(batch, ws, rank)
     rp, ix, vv = slice_csr(rowptr, idx, val, lo, hi)
@@ -87,4 +137,10 @@ def infer_partitioned(net, rowptr: np.ndarray, idx: np.ndarray, val: Optional[np
         vv_t = None if vv is None else torch.from_numpy(np.ascontiguousarray(vv)).to(dev)
         net.infer_torch(rp_t, ix_t, vv_t, alive_t=words[: (hi - lo + 31) // 32])
     allw = gather_bitmask(words, group)
-    return decode(allw.cpu().numpy(), batch)
+    ids, cnt = decode_device(allw, batch)
+    return ids[:int(cnt.item())].cpu().numpy()
+
+
+def dist_world(group=None):
+    import torch.distributed as dist
+    return dist.get_world_size(group), dist.get_rank(group)
