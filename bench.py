@@ -113,10 +113,37 @@ def lib_flags(sd, names):
     return f
 
 
+NETS = {
+    # --net: (spec factory, description)
+    "rn": (lambda g, n, L: g.rn_spec(n, L),
+           "RadiX-Net-shaped (sdnngen.rn_spec), overlapping field schedule, uniform w=1/16"),
+    "rn-plain": (lambda g, n, L: g.rn_plain_spec(n, L),
+                 "RadiX-Net-shaped, SURVEY 8.4 non-overlapping field schedule (sdnngen.rn_plain_spec), "
+                 "uniform w=1/16"),
+    "rw": (lambda g, n, L: g.rw_spec(n, L),
+           "RadiX-Net-shaped structure with per-slot weights U(-0.05,0.15) (sdnngen.rw_spec): "
+           "the general-weight path"),
+    "rr": (lambda g, n, L: g.rr_spec(n, L),
+           "random 32-regular, no shared source sets (sdnngen.rr_spec), uniform w=1/16"),
+}
+
+
 def net_spec(g, args, n, L):
-    """The network family: RN (headline, RadiX-Net-shaped) or RR (random
-    32-regular: no two columns share a source list, the general gather path)."""
-    return g.rn_spec(n, L) if args.net == "rn" else g.rr_spec(n, L)
+    """The network family (NETS): rn is the headline; rn-plain, rw and rr are
+    robustness rows reported beside it."""
+    return NETS[args.net][0](g, n, L)
+
+
+def schedule_desc(g, spec):
+    """The field schedule of an RN-structured net (disclosed in `config`)."""
+    if spec.kind != "rn":
+        return None
+    sch = spec.extra.get("schedule", "overlap")
+    first = [g.rn_field(spec.n, l, sch) for l in range(min(spec.L, 24))]
+    formula = ("p_l = (2l + floor(l/c)) mod (log2N-4), c = ceil((log2N-4)/2): consecutive 5-bit fields "
+               "overlap in 3 bits (DESIGN.md R-W2)" if sch == "overlap" else
+               "non-overlapping 5-bit fields 0, 5, 10, ... (last clamped to log2N-5), SURVEY.md 8.4")
+    return {"name": sch, "formula": formula, "first_fields": first}
 
 
 def kernel_name(net):
@@ -155,7 +182,7 @@ def run_reference(args):
         objs.append(oracle.Oracle(n, srp, sidx, None))
     total_nnz = 0
     for l in range(L):
-        lay = g.gen_layer(spec, l, fmt="csr")
+        lay = g.gen_layer(spec, l, fmt="csr" if spec.wdist == "uniform" else "both")
         total_nnz += lay.colidx.size
         for o in objs:
             o.apply(lay, nthreads=cores)
@@ -371,9 +398,15 @@ def run_gpu(args):
             "config": {"workload": f"{args.net}{n}x{L}-ms{B}", "neurons": n, "layers": L,
                        "nnz_per_column": 32, "inputs_per_gpu": batch,
                        "global_batch": batch * ws if not strong else B,
-                       "network": ("RadiX-Net-shaped (sdnngen.rn_spec)" if args.net == "rn" else
-                                   "random 32-regular, no shared source sets (sdnngen.rr_spec)")
-                                  + ", w=1/16, b=%g" % spec.bias,
+                       "network": NETS[args.net][1] + ", b=%g" % spec.bias,
+                       "field_schedule": schedule_desc(g, spec),
+                       "nominal_edges_per_step": int(gB * total_nnz) if ws > 1 else int(batch * total_nnz),
+                       "fma_per_step": int(st["executed_fma"]) * ws,
+                       "fma_over_nominal_edges": (st["executed_fma"] / max(1, batch * total_nnz)),
+                       "work_note": ("with uniform weights the members of a column group share one "
+                                     "canonical chain (same sources, same weight): one FMA per group "
+                                     "source per computed row, not per edge; rows that die are "
+                                     "dropped at the compactions between steps"),
                        "inputs": "binary MNIST-shaped strokes (sdnngen.ms_inputs)",
                        "parallelism": f"dp{ws}" if ws > 1 else "single",
                        "l2": "inputs larger than L2 (Y = %.1f GB per GPU)" % (4.0 * n * batch / 1e9)},
@@ -431,8 +464,8 @@ def main():
     ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
                     help="N > 1: strong = the one 60,000-input batch split across ranks "
                          "(BASELINE configs[3], default); weak = every rank its own batch")
-    ap.add_argument("--net", default="rn", choices=["rn", "rr"],
-                    help="network family: rn = RadiX-Net-shaped (headline), rr = random 32-regular")
+    ap.add_argument("--net", default="rn", choices=sorted(NETS),
+                    help="network family: rn = RadiX-Net-shaped (headline); rn-plain, rw, rr = robustness rows")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define SDNN_ABI_VERSION 2
+#define SDNN_ABI_VERSION 3
 
 typedef struct sdnn_net sdnn_net;
 typedef int32_t sdnn_status;
@@ -239,6 +239,13 @@ typedef struct sdnn_stats {
   int64_t stream_bytes;       /* stream_slots > 0: host->device weight bytes per inference
                                  (0 when every layer is resident)                        */
   int64_t stream_slot_bytes;  /* stream_slots > 0: device bytes of one ring slot            */
+  int64_t executed_fma;       /* fp32 FMAs the kernels executed in the last inference:
+                                 sum over steps of (batch positions the step computed) x
+                                 (per layer: sum_g K_g when the layer's weights are uniform
+                                 -- the members of a group share one chain -- else nnz_l).
+                                 Compare with the nominal edges inputs x sum_l nnz_l      */
+  int64_t computed_rows;      /* sum over layers of the batch positions computed (dead rows
+                                 are dropped only at the compactions between steps)      */
 } sdnn_stats;
 
 /* live_rows: NULL or [layers] receives the number of rows still nonzero after

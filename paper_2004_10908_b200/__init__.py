@@ -73,7 +73,8 @@ class sdnn_stats(ctypes.Structure):
                 ("kept_rows", ctypes.c_int64), ("steps", ctypes.c_int32),
                 ("fused_layers", ctypes.c_int32), ("resident_layers", ctypes.c_int32),
                 ("retired_rows", ctypes.c_int64), ("stream_bytes", ctypes.c_int64),
-                ("stream_slot_bytes", ctypes.c_int64)]
+                ("stream_slot_bytes", ctypes.c_int64), ("executed_fma", ctypes.c_int64),
+                ("computed_rows", ctypes.c_int64)]
 
 
 _LIB = None

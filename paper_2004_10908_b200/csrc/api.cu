@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -78,6 +79,7 @@ struct sdnn_net {
   std::vector<size_t> lbytes;
   std::vector<uint8_t> bias_nonpos;
   std::vector<int64_t> nnz;
+  std::vector<int64_t> fma_l;      // FMAs per batch position of layer l (sum K_g if uniform, else nnz)
   std::atomic<int> nset{0};
   int32_t grouped_layers = 0, max_group = 0, max_k = 0;
   std::mutex stat_mu;
@@ -88,6 +90,7 @@ struct sdnn_net {
   int64_t ws_cap = -1;             // stride the workspace was sized for
   // execution plan: steps of one layer or one fused multi-layer pass
   std::vector<Step> steps;
+  std::vector<int8_t> step_lg;         // per step: log2 positions per block of its input boundary
   std::vector<DevPass> passes;
   Arena pass_arena;
   bool plan_dirty = true;
@@ -117,6 +120,11 @@ struct sdnn_net {
   int32_t *d_idx = nullptr;
   float *d_val = nullptr;
   int64_t cap_rows = -1, cap_nnz = -1, cap_val = -1;
+  // input stream of sdnn_infer, its events (staging slots, per-chunk arrival)
+  cudaStream_t in_s = nullptr;
+  cudaEvent_t ev_stage[2] = {nullptr, nullptr};
+  cudaEvent_t ev_in = nullptr;
+  std::vector<cudaEvent_t> ev_chunk;
   // pinned host staging
   void *h_stage = nullptr;
   size_t h_stage_cap = 0;
@@ -355,11 +363,16 @@ bool yblock_wanted() {
   return e ? atoi(e) != 0 : kYBlockDefault;
 }
 
-// fused-pass item order (SDNN_PASS_ORDER=comp|tile; A/B knob)
+// fused-pass item order: -1 = by tile size (default: component-major for the
+// 16-position tiles of 1024-row components, tile-major otherwise; measured on
+// C4: k_pass<32> 2.52 vs 2.67 ms, <128> 2.75 vs 2.84, <64> 2.61 vs 2.72, but
+// <16> 4.23 vs 3.40 ms tile-major vs component-major); SDNN_PASS_ORDER=comp|tile
 int pass_order() {
   static const int v = [] {
     const char *e = getenv("SDNN_PASS_ORDER");
-    return (e && std::strcmp(e, "tile") == 0) ? 1 : 0;
+    if (e && std::strcmp(e, "tile") == 0) return 1;
+    if (e && std::strcmp(e, "comp") == 0) return 0;
+    return -1;
   }();
   return v;
 }
@@ -463,6 +476,22 @@ sdnn_status make_plan(sdnn_net *net) {
     sig0 = std::move(sig[0]);
   }
   net->yblk = yblk ? net->n : 0;
+  // block size per boundary: 16 positions where a T = 16 pass (1024-row
+  // components) reads, so its tile is one contiguous run (SDNN_BLK16=0: 32)
+  // (off by default: the passes writing 16-position blocks lose more than the
+  // T = 16 passes gain -- C4 1998 vs 1964 ms/step; SDNN_BLK16=1 enables)
+  static const bool blk16 = [] {
+    const char *e = getenv("SDNN_BLK16");
+    return e && atoi(e) != 0;
+  }();
+  static const int pf = [] {
+    const char *e = getenv("SDNN_PASS_PF");
+    return e ? std::max(0, std::min(4, atoi(e))) : 0;   // measured: PF=1 2586, PF=2 2653 vs 1978 ms on C4
+  }();
+  net->step_lg.assign(net->steps.size() + 1, 5);
+  if (yblk && blk16)
+    for (size_t q = 0; q < net->steps.size(); ++q)
+      if (ph[q].m > 0 && ph[q].T == 16 && ph[q].C == 1) net->step_lg[q] = 4;
   net->d_sig0 = nullptr;
   if (yblk) {
     void *d;
@@ -486,7 +515,10 @@ sdnn_status make_plan(sdnn_net *net) {
     D.C = H.C;
     D.rec_bytes = H.rec_bytes;
     D.yblk = net->yblk;
-    D.order = pass_order();
+    D.order = pass_order() >= 0 ? pass_order() : (H.T == 16 ? 0 : 1);
+    D.lg_in = net->step_lg[q];
+    D.lg_out = net->step_lg[q + 1];
+    D.pf = net->yblk ? pf : 0;
     if (!streaming) {                            // else: pointers into the slot ring
       void *p1, *p2, *p3;
       sdnn_status st;
@@ -594,7 +626,8 @@ void enqueue_chain(sdnn_net *net, bool compact, cudaStream_t s, int64_t *launche
                 (net->opts.flags & SDNN_F_SATURATE) ? w.sat[(si + 1) & 1] : nullptr);
     c += 2;
     if (!last) {
-      launch_compact_copy(net->cfg, w, S.a, S.m, w.alive_row(si, S.m - 1), net->n, s);
+      launch_compact_copy(net->cfg, w, S.a, S.m, w.alive_row(si, S.m - 1), net->n, s,
+                          w.yblk ? net->step_lg[si + 1] : 5);
       ++c;
     }
   }
@@ -645,18 +678,28 @@ void launch_final_yout(sdnn_net *net, int64_t batch, float *d_yout, cudaStream_t
 }
 
 // Everything of one inference after Y0 is on the device.
+// feed (sdnn_infer): enqueues the chunked input copies and their scatters
+// after the densify prep; NULL = Y0 is already on the device
+using Feed = std::function<sdnn_status(cudaStream_t)>;
 sdnn_status infer_device_impl(sdnn_net *net, const int64_t *d_rowptr, const int32_t *d_idx,
                               const float *d_val, int64_t batch, uint32_t *d_alive,
-                              float *d_yout, cudaStream_t s) {
+                              float *d_yout, cudaStream_t s, const Feed *feed = nullptr) {
   if (net->nset.load() != net->L) return fail(SDNN_E_STATE, "not every layer has been set");
   sdnn_status st = ensure_ws(net, batch);
   if (st) return st;
   if (net->L > 0 && (st = make_plan(net))) return st;   // the layout of Y is a plan property
   net->ws.yblk = net->L > 0 ? net->yblk : 0;
   net->ws.sig0 = net->L > 0 ? net->d_sig0 : nullptr;
+  net->ws.lg0 = (net->L > 0 && net->yblk && !net->step_lg.empty()) ? net->step_lg[0] : 5;
   const bool compact = compact_enabled(net);
-  launch_densify(net->cfg, net->ws, net->n, batch, d_rowptr, d_idx, d_val, compact, s);
   int64_t launches = 4;
+  if (feed) {
+    launch_densify_prep(net->cfg, net->ws, net->n, batch, d_rowptr, d_val, compact, s);
+    st = (*feed)(s);
+    if (st) return st;
+  } else {
+    launch_densify(net->cfg, net->ws, net->n, batch, d_rowptr, d_idx, d_val, compact, s);
+  }
   if (net->L == 0) {
     launch_zero_layers_alive(net->ws, batch, d_rowptr, d_val, s);
     launches += 1;
@@ -790,6 +833,7 @@ sdnn_status sdnn_create_empty(int32_t neurons, int32_t layers, const sdnn_opts *
   net->lbytes.assign(layers, 0);
   net->bias_nonpos.assign(layers, 1);
   net->nnz.assign(layers, 0);
+  net->fma_l.assign(layers, 0);
   net->last_live.assign(std::max(layers, 1), 0);
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -895,6 +939,13 @@ sdnn_status sdnn_set_layer(sdnn_net *net, int32_t l, const sdnn_layer *W, const 
     net->plan_dirty = true;
     net->bias_nonpos[l] = net->host[l].bias_nonpos ? 1 : 0;
     net->nnz[l] = net->host[l].nnz;
+    {
+      const PackedLayer &P = net->host[l];
+      int64_t f = 0;
+      if (P.uniform)
+        for (int32_t g = 0; g < P.ngroups; ++g) f += P.gk[g];
+      net->fma_l[l] = P.uniform ? f : P.nnz;
+    }
     if (net->host[l].gmax > 1) net->grouped_layers += was ? 0 : 1;
     net->max_group = std::max(net->max_group, net->host[l].gmax);
     net->max_k = std::max(net->max_k, net->host[l].kmax);
@@ -996,58 +1047,117 @@ sdnn_status sdnn_infer(sdnn_net *net, const int64_t *y0_rowptr, const int32_t *y
     CK(cudaMalloc(&net->d_val, sizeof(float) * std::max<int64_t>(nnz, 1)));
     net->cap_val = nnz;
   }
-  // host -> pinned staging -> device, chunked so the memcpy of chunk c+1
-  // overlaps the DMA of chunk c
-  {
-    struct Part { const void *h; void *d; size_t bytes; };
-    Part parts[3] = {{y0_rowptr, net->d_rowptr, sizeof(int64_t) * (size_t)(batch + 1)},
-                     {y0_idx, net->d_idx, sizeof(int32_t) * (size_t)nnz},
-                     {y0_val, net->d_val, y0_val ? sizeof(float) * (size_t)nnz : 0}};
-    const size_t kChunk = size_t(64) << 20;
-    char *stage = (char *)grow_pinned(net, 2 * kChunk);
-    if (!stage) return fail(SDNN_E_NOMEM, "pinned staging allocation failed");
-    cudaEvent_t ev[2];
-    CK(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
-    CK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
-    bool used[2] = {false, false};
-    int slot = 0;
-    for (const Part &p : parts) {
-      if (p.bytes == 0) continue;
-      cudaPointerAttributes pa;
-      if (cudaPointerGetAttributes(&pa, p.h) == cudaSuccess && pa.type == cudaMemoryTypeHost) {
-        // caller's buffer is page-locked: DMA straight from it
-        CK(cudaMemcpyAsync(p.d, p.h, p.bytes, cudaMemcpyHostToDevice, s));
-        continue;
-      }
-      cudaGetLastError();
-      for (size_t off = 0; off < p.bytes; off += kChunk) {
-        const size_t b = std::min(kChunk, p.bytes - off);
-        if (used[slot]) CK(cudaEventSynchronize(ev[slot]));
-        {                                          // pageable -> pinned on several host threads
-          char *dst = stage + slot * kChunk;
-          const char *src = (const char *)p.h + off;
-          parallel_for((int64_t)b, std::min(nthreads_default(), 8),
-                       [&](int64_t x, int64_t y) { std::memcpy(dst + x, src + x, (size_t)(y - x)); });
-        }
-        CK(cudaMemcpyAsync((char *)p.d + off, stage + slot * kChunk, b, cudaMemcpyHostToDevice, s));
-        CK(cudaEventRecord(ev[slot], s));
-        used[slot] = true;
-        slot ^= 1;
-      }
-    }
-    cudaEventDestroy(ev[0]);
-    cudaEventDestroy(ev[1]);
-  }
-  if (!(net->opts.flags & SDNN_F_TRUST_INPUT)) {
-    st = validate_y0(net->n, y0_rowptr, y0_idx, y0_val, batch);
-    if (st) {
+  // Input path (A14: the copies are inside the timed call).  rowptr first (the
+  // device prep -- zero Y0, row flags, scan -- needs only it), then the column
+  // indices in row chunks of ~64 MB on the input stream, each chunk scattered
+  // on the compute stream as soon as it has landed, so the copy of chunk c+1
+  // overlaps the scatter of chunk c; page-locked caller buffers are DMA'd
+  // directly, pageable ones through a pinned double buffer.  Explicit values
+  // (y0_val) are needed by the row flags, so they are copied up front.  The
+  // full host validation (index range, duplicates, finite values) runs on a
+  // separate host thread meanwhile and is joined before returning; the device
+  // path is memory-safe on invalid input (out-of-range indices are skipped).
+  if (!net->in_s) CK(cudaStreamCreateWithFlags(&net->in_s, cudaStreamNonBlocking));
+  const size_t kChunk = size_t(64) << 20;
+  char *stage = (char *)grow_pinned(net, 2 * kChunk);
+  if (!stage) return fail(SDNN_E_NOMEM, "pinned staging allocation failed");
+  auto is_pinned = [](const void *p) {
+    cudaPointerAttributes pa;
+    const bool r = cudaPointerGetAttributes(&pa, p) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    return r;
+  };
+  sdnn_status vst = SDNN_OK;
+  std::string vmsg;
+  std::thread validator;
+  if (!(net->opts.flags & SDNN_F_TRUST_INPUT) && batch > 0)
+    validator = std::thread([&] {
+      vst = validate_y0(net->n, y0_rowptr, y0_idx, y0_val, batch);
+      if (vst) vmsg = sdnn_last_error();
+    });
+  auto join_validator = [&]() -> sdnn_status {
+    if (validator.joinable()) validator.join();
+    if (vst) {
       cudaStreamSynchronize(s);                  // no DMA may still read the caller's buffers
-      return st;
+      cudaStreamSynchronize(net->in_s);
+      return fail(vst, vmsg);
+    }
+    return SDNN_OK;
+  };
+  // synchronous small copies (rowptr; values when given)
+  int slot = 0;
+  bool used[2] = {false, false};
+  auto copy_h2d = [&](void *d, const void *h, size_t bytes, cudaStream_t cs, bool pinned) -> sdnn_status {
+    if (bytes == 0) return SDNN_OK;
+    if (pinned) {
+      CK(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, cs));
+      return SDNN_OK;
+    }
+    for (size_t off = 0; off < bytes; off += kChunk) {
+      const size_t b = std::min(kChunk, bytes - off);
+      if (used[slot]) CK(cudaEventSynchronize(net->ev_stage[slot]));
+      char *dst = stage + slot * kChunk;
+      const char *src = (const char *)h + off;
+      parallel_for((int64_t)b, std::min(nthreads_default(), 8),
+                   [&](int64_t x, int64_t y) { std::memcpy(dst + x, src + x, (size_t)(y - x)); });
+      CK(cudaMemcpyAsync((char *)d + off, dst, b, cudaMemcpyHostToDevice, cs));
+      CK(cudaEventRecord(net->ev_stage[slot], cs));
+      used[slot] = true;
+      slot ^= 1;
+    }
+    return SDNN_OK;
+  };
+  for (int i = 0; i < 2; ++i)
+    if (!net->ev_stage[i]) CK(cudaEventCreateWithFlags(&net->ev_stage[i], cudaEventDisableTiming));
+  // the input stream starts after everything earlier on s (buffer reuse)
+  if (!net->ev_in) CK(cudaEventCreateWithFlags(&net->ev_in, cudaEventDisableTiming));
+  CK(cudaEventRecord(net->ev_in, s));
+  CK(cudaStreamWaitEvent(net->in_s, net->ev_in, 0));
+  if ((st = copy_h2d(net->d_rowptr, y0_rowptr, sizeof(int64_t) * (size_t)(batch + 1), s, is_pinned(y0_rowptr))) ||
+      (y0_val && (st = copy_h2d(net->d_val, y0_val, sizeof(float) * (size_t)nnz, s, is_pinned(y0_val))))) {
+    join_validator();
+    return st;
+  }
+  const bool idx_pinned = nnz > 0 && is_pinned(y0_idx);
+  // row chunks of ~kChunk bytes of indices
+  std::vector<int64_t> cut{0};
+  {
+    const int64_t per = (int64_t)(kChunk / sizeof(int32_t));
+    int64_t r = 0;
+    while (r < batch) {
+      const int64_t lim = y0_rowptr[r] + per;
+      int64_t hi = std::upper_bound(y0_rowptr + r + 1, y0_rowptr + batch + 1, lim) - y0_rowptr - 1;
+      if (hi <= r) hi = r + 1;                   // one row larger than a chunk
+      r = std::min(hi, batch);
+      cut.push_back(r);
     }
   }
+  while (net->ev_chunk.size() + 1 < cut.size()) {
+    cudaEvent_t e;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    net->ev_chunk.push_back(e);
+  }
+  const Feed feed = [&](cudaStream_t cs) -> sdnn_status {
+    for (size_t c = 0; c + 1 < cut.size(); ++c) {
+      const int64_t r0 = cut[c], r1 = cut[c + 1];
+      const int64_t e0 = y0_rowptr[r0], e1 = y0_rowptr[r1];
+      sdnn_status s2 = copy_h2d(net->d_idx + e0, y0_idx + e0, sizeof(int32_t) * (size_t)(e1 - e0), net->in_s,
+                                idx_pinned);
+      if (s2) return s2;
+      CK(cudaEventRecord(net->ev_chunk[c], net->in_s));
+      CK(cudaStreamWaitEvent(cs, net->ev_chunk[c], 0));
+      launch_scatter_rows(net->cfg, net->ws, net->n, r0, r1, net->d_rowptr, net->d_idx,
+                          y0_val ? net->d_val : nullptr, cs);
+    }
+    return SDNN_OK;
+  };
   st = infer_device_impl(net, net->d_rowptr, net->d_idx, y0_val ? net->d_val : nullptr, batch,
-                         nullptr, nullptr, s);
-  if (st) return st;
+                         nullptr, nullptr, s, &feed);
+  if (st) {
+    join_validator();
+    return st;
+  }
+  if ((st = join_validator())) return st;
   float *d_yout = nullptr;
   if (y_out && batch > 0) {
     CK(cudaMalloc(&d_yout, sizeof(float) * (size_t)net->n * (size_t)batch));
@@ -1215,6 +1325,13 @@ sdnn_status sdnn_stats_get(const sdnn_net *cnet, sdnn_stats *out, int64_t *live_
     }
     for (int l = 0; l < net->L; ++l)
       s.live_edges += (int64_t)(l == 0 ? kept0 : live[l - 1]) * net->nnz[l];
+    std::vector<LayerState> sts(net->L + 1);
+    CK(cudaMemcpy(sts.data(), net->ws.st, sizeof(LayerState) * (net->L + 1), cudaMemcpyDeviceToHost));
+    for (const Step &S : net->steps)
+      for (int l = S.a; l < S.a + S.m; ++l) {
+        s.executed_fma += (int64_t)sts[S.a].width * net->fma_l[l];
+        s.computed_rows += sts[S.a].width;
+      }
   }
   *out = s;
   return SDNN_OK;
@@ -1235,6 +1352,10 @@ void sdnn_destroy(sdnn_net *net) {
   cudaFree(net->d_idx);
   cudaFree(net->d_val);
   if (net->h_stage) cudaFreeHost(net->h_stage);
+  if (net->in_s) cudaStreamDestroy(net->in_s);
+  for (auto e : net->ev_stage) if (e) cudaEventDestroy(e);
+  if (net->ev_in) cudaEventDestroy(net->ev_in);
+  for (auto e : net->ev_chunk) cudaEventDestroy(e);
   if (net->own) cudaStreamDestroy(net->own);
   for (auto e : net->ev_before) if (e) cudaEventDestroy(e);
   for (auto e : net->ev_after) if (e) cudaEventDestroy(e);

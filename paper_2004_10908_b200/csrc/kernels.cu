@@ -242,6 +242,156 @@ __global__ void __launch_bounds__(32 * (1 + T / 128), 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Layer kernel, PER-SLOT weights (the general-weight path), TMA bulk pipeline.
+// Warp 0 produces: per item (group g, tile of T positions) one cp.async.bulk
+// per source row segment (T*4 bytes) plus one for the group's weight block
+// val[g] (K x gmax floats, source-major) onto the stage's mbarrier.  NCW
+// consumer warps own T/NCW positions each, in rounds of 32: lane = (position
+// quad q = lane & 7, member octet c = lane >> 3), so a warp computes a
+// 32-position x 32-member block.  Per term t (ascending: the canonical chain of
+// every member) it reads one float4 of Y (8 distinct addresses: one
+// wavefront) and two float4 of weights (members 8c..8c+7) and issues 16 packed
+// FFMA2 -- two members of one position per instruction, per component exactly
+// __fmaf_rn -- then every member: bias add, clamp, 16-B store (8 lanes of a
+// member octet write one 128 B run of its output row).  Requires gmax == 32
+// and K_g <= 32 (the RadiX-Net structure with general weights); other
+// non-uniform layers use k_layer_general.
+// ---------------------------------------------------------------------------
+template <int T, int NCW, int STAGES>
+constexpr size_t bulkw_smem() {
+  return (size_t)STAGES * (32 * T + 32 * 32) * sizeof(float) + 2 * STAGES * 8;
+}
+
+template <int T, int NCW, int STAGES>
+__global__ void __launch_bounds__(32 * (1 + NCW), 1)
+    k_layer_bulkw(DevLayer L, const LayerState *__restrict__ st, int layer, float *Ya, float *Yb,
+                  uint32_t *__restrict__ alive, int64_t stride, float ymax) {
+  constexpr int SF = 32 * T + 32 * 32;             // floats per stage: 32 rows + weights
+  constexpr int PW = T / NCW;                      // positions per consumer warp
+  static_assert(PW % 32 == 0, "rounds of 32 positions");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float *stage = reinterpret_cast<float *>(smem_raw);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem_raw + (size_t)STAGES * SF * 4);
+  uint64_t *empty = full + STAGES;
+  const LayerState S = st[layer];
+  const int width = S.width;
+  if (width <= 0) return;
+  const float *__restrict__ Yin = S.in ? Yb : Ya;
+  float *__restrict__ Yout = S.in ? Ya : Yb;
+  const int tiles = (width + T - 1) / T;
+  const int64_t items = (int64_t)L.ngroups * tiles;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NCW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == 0) {
+    // ---------------- producer ----------------
+    int s = 0;
+    uint32_t ph = 0;
+    int64_t n = 0;
+    for (int64_t it = blockIdx.x; it < items; it += gridDim.x, ++n) {
+      const int g = (int)(it / tiles);
+      const int tile = (int)(it - (int64_t)g * tiles);
+      const int K = L.gk[g];
+      const int mysrc = lane < K ? (int)L.src[(int64_t)g * L.kmax + lane] : 0;
+      if (n >= STAGES) mbar_wait(&empty[s], ph ^ 1);
+      float *sb = stage + (size_t)s * SF;
+      if (lane == 0) {
+        const uint32_t wbytes = (uint32_t)K * 32u * 4u;
+        mbar_expect_tx_arrive(&full[s], (uint32_t)K * T * 4 + wbytes);
+        if (wbytes) bulk_g2s(sb + 32 * T, L.val + (int64_t)g * L.kmax * 32, wbytes, &full[s]);
+      }
+      __syncwarp();
+      if (lane < K) bulk_g2s(sb + lane * T, Yin + (int64_t)mysrc * stride + (int64_t)tile * T, T * 4, &full[s]);
+      if (++s == STAGES) { s = 0; ph ^= 1; }
+    }
+  } else {
+    // ---------------- consumers ----------------
+    const int cw = warp - 1;
+    const int q = lane & 7, c = lane >> 3;
+    int s = 0;
+    uint32_t ph = 0;
+    for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+      const int g = (int)(it / tiles);
+      const int tile = (int)(it - (int64_t)g * tiles);
+      const int K = L.gk[g], G = L.gg[g];
+      int col[8];
+      float bia[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int m = 8 * c + i;
+        col[i] = m < G ? L.col[(int64_t)g * 32 + m] : -1;
+        bia[i] = col[i] >= 0 ? __ldg(L.bias + col[i]) : 0.f;
+      }
+      mbar_wait(&full[s], ph);
+      const float *sb = stage + (size_t)s * SF;
+      const float *wsm = sb + 32 * T + 8 * c;
+#pragma unroll 1
+      for (int r = 0; r < PW / 32; ++r) {
+        const int p0 = cw * PW + r * 32 + 4 * q;    // this lane's 4 positions in the tile
+        float2 acc[4][4];                            // [member pair][position]
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) acc[i][e] = make_float2(0.f, 0.f);
+#pragma unroll 4
+        for (int t = 0; t < K; ++t) {
+          const float4 v = *reinterpret_cast<const float4 *>(sb + t * T + p0);
+          const float4 w0 = *reinterpret_cast<const float4 *>(wsm + t * 32);
+          const float4 w1 = *reinterpret_cast<const float4 *>(wsm + t * 32 + 4);
+          const float2 wp[4] = {make_float2(w0.x, w0.y), make_float2(w0.z, w0.w), make_float2(w1.x, w1.y),
+                                make_float2(w1.z, w1.w)};
+          const float ve[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 v2 = make_float2(ve[e], ve[e]);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) acc[i][e] = __ffma2_rn(v2, wp[i], acc[i][e]);
+          }
+        }
+        uint32_t am = 0;
+        float *dst = Yout + (int64_t)tile * T + p0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          if (col[i] < 0) continue;
+          const float b = bia[i];
+          float4 y;
+          y.x = clampy(__fadd_rn((i & 1) ? acc[i >> 1][0].y : acc[i >> 1][0].x, b), ymax);
+          y.y = clampy(__fadd_rn((i & 1) ? acc[i >> 1][1].y : acc[i >> 1][1].x, b), ymax);
+          y.z = clampy(__fadd_rn((i & 1) ? acc[i >> 1][2].y : acc[i >> 1][2].x, b), ymax);
+          y.w = clampy(__fadd_rn((i & 1) ? acc[i >> 1][3].y : acc[i >> 1][3].x, b), ymax);
+          am |= (y.x > 0.f ? 1u : 0u) | (y.y > 0.f ? 2u : 0u) | (y.z > 0.f ? 4u : 0u) | (y.w > 0.f ? 8u : 0u);
+          *reinterpret_cast<float4 *>(dst + (int64_t)col[i] * stride) = y;
+        }
+        // liveness of the 32 positions: OR over the member octets, then the quads
+        am |= __shfl_xor_sync(FULL, am, 8);
+        am |= __shfl_xor_sync(FULL, am, 16);
+        uint32_t word = am << (4 * q);
+        word |= __shfl_xor_sync(FULL, word, 1);
+        word |= __shfl_xor_sync(FULL, word, 2);
+        word |= __shfl_xor_sync(FULL, word, 4);
+        const int64_t base = (int64_t)tile * T + cw * PW + r * 32;
+        if (lane == 0 && base < width) {
+          if (width - base < 32) word &= (1u << (width - base)) - 1u;
+          if (word) atomicOr(&alive[base >> 5], word);
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (++s == STAGES) { s = 0; ph ^= 1; }
+    }
+  }
+}
+
+constexpr int kBulkwT = 512, kBulkwNCW = 16, kBulkwStages = 3;
+
 template <int T, int RPS, int STAGES>
 constexpr size_t bulk_smem() {
   return (size_t)STAGES * RPS * T * sizeof(float) + 2 * STAGES * 8;
@@ -305,14 +455,14 @@ __global__ void __launch_bounds__(256) k_layer_general(DevLayer L, const LayerSt
       }
       for (int m = 0; m < G; ++m) {
         const int j = __shfl_sync(FULL, mycol, m);
-        const float *wv = L.val + ((int64_t)g * L.gmax + m) * L.kmax;
+        const float *wv = L.val + (int64_t)g * L.kmax * L.gmax + m;   // [t][member]
         float acc[VEC];
 #pragma unroll
         for (int e = 0; e < VEC; ++e) acc[e] = 0.f;
 #pragma unroll
         for (int t = 0; t < 32; ++t) {
           if (t < K) {
-            const float wt = __ldg(wv + t);
+            const float wt = __ldg(wv + t * L.gmax);
 #pragma unroll
             for (int e = 0; e < VEC; ++e) acc[e] = __fmaf_rn(v[t][e], wt, acc[e]);
           }
@@ -329,7 +479,7 @@ __global__ void __launch_bounds__(256) k_layer_general(DevLayer L, const LayerSt
     } else {
       for (int m = 0; m < G; ++m) {
         const int j = __shfl_sync(FULL, mycol, m);
-        const float *wv = L.val + ((int64_t)g * L.gmax + m) * L.kmax;
+        const float *wv = L.val + (int64_t)g * L.kmax * L.gmax + m;   // [t][member]
         float acc[VEC];
 #pragma unroll
         for (int e = 0; e < VEC; ++e) acc[e] = 0.f;
@@ -337,7 +487,7 @@ __global__ void __launch_bounds__(256) k_layer_general(DevLayer L, const LayerSt
           const int k = gsrc[t];
           float v[VEC];
           V::unpack(V::ld(Yin + (int64_t)k * stride + b0), v);
-          const float wt = __ldg(wv + t);
+          const float wt = __ldg(wv + (int64_t)t * L.gmax);
 #pragma unroll
           for (int e = 0; e < VEC; ++e) acc[e] = __fmaf_rn(v[e], wt, acc[e]);
         }
@@ -446,24 +596,29 @@ __global__ void __launch_bounds__(1024) k_scan_input(const uint32_t *inmask, int
 
 // warp per input row: scatter its stored values into its (compacted) column
 // element (storage row r, position p) of an activation buffer
-__device__ __forceinline__ int64_t yix(int64_t r, int64_t p, int64_t stride, int32_t yblk) {
-  return yblk ? ((p >> 5) * yblk + r) * 32 + (p & 31) : r * stride + p;
+// (position-blocked layout: blocks of 2^lg positions, lg = 5 or 4 per boundary)
+__device__ __forceinline__ int64_t yix(int64_t r, int64_t p, int64_t stride, int32_t yblk, int lg = 5) {
+  return yblk ? (((p >> lg) * yblk + r) << lg) + (p & ((1 << lg) - 1)) : r * stride + p;
 }
 
-__global__ void k_scatter(int64_t batch, const int64_t *__restrict__ rowptr,
+__global__ void k_scatter(int64_t r0, int64_t r1, const int64_t *__restrict__ rowptr,
                           const int32_t *__restrict__ idx, const float *__restrict__ val,
                           const uint32_t *__restrict__ inmask, const int32_t *__restrict__ wpre,
                           float *Y0, int32_t *rid0, int64_t stride, int32_t yblk,
-                          const int32_t *__restrict__ sig0) {
+                          const int32_t *__restrict__ sig0, int lg, int32_t n) {
   const int lane = threadIdx.x & 31;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < batch; i += nw) {
+  for (int64_t i = r0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); i < r1; i += nw) {
     const uint32_t word = inmask[i >> 5];
     if (!((word >> (i & 31)) & 1u)) continue;
     const int64_t pos = wpre[i >> 5] + __popc(word & ((1u << (i & 31)) - 1u));
     if (lane == 0) rid0[pos] = (int32_t)i;
-    for (int64_t e = rowptr[i] + lane; e < rowptr[i + 1]; e += 32)
-      Y0[yix(sig0 ? sig0[idx[e]] : idx[e], pos, stride, yblk)] = val ? val[e] : 1.0f;
+    for (int64_t e = rowptr[i] + lane; e < rowptr[i + 1]; e += 32) {
+      const int32_t k = idx[e];
+      // an out-of-range index is never written (sdnn_infer validates Y0 on
+      // the host concurrently and reports it; the device stays memory-safe)
+      if ((uint32_t)k < (uint32_t)n) Y0[yix(sig0 ? sig0[k] : k, pos, stride, yblk, lg)] = val ? val[e] : 1.0f;
+    }
   }
 }
 
@@ -619,10 +774,14 @@ __global__ void __launch_bounds__(32 * kPassNW, 3)
   // position-blocked activations: a CTA's rows are consecutive storage rows, so
   // each 32-position block of its tile is ONE contiguous run of ncnt*128 B,
   // copied by one cp.async.bulk into the tile laid out [T/32][rin][32]
+  // (a boundary read by a T = 16 pass has 16-position blocks, lg_in = 4: the
+  // tile is then ONE contiguous run of ncnt * 64 B)
   const int32_t R = P.yblk;
   const bool blk = R > 0;
   const bool bt = blk && T >= 32;               // blocked tile: smem [T/32][rin][32]
-  const bool ldg = kLdgsts && (!blk || T < 32);   // (T = 16 blocked: half-block LDGSTS rows)
+  const bool b16 = blk && T == 16 && P.lg_in == 4;   // one bulk copy, smem [rin][16]
+  const bool ldg = kLdgsts && (!blk || (T < 32 && !b16));   // (T = 16 in 32-blocks: half-row LDGSTS)
+  const int lgo = P.lg_out;                      // output boundary block size 2^lgo
   const int rin = P.rin;
   const int sm = bt ? 32 : T;                    // tile floats per slot step
   if (tid == 0) {
@@ -658,8 +817,10 @@ __global__ void __launch_bounds__(32 * kPassNW, 3)
         for (int q = 0; q < (T >= 32 ? T / 32 : 0); ++q)
           bulk_g2s(tile_s + q * rin * 32, Yin + (((int64_t)tile * (T / 32) + q) * R + nrow[0]) * 32,
                    (uint32_t)ncnt * 128u, bar);
+      if (b16 && ncnt > 0)
+        bulk_g2s(tile_s, Yin + ((int64_t)tile * R + nrow[0]) * 16, (uint32_t)ncnt * 64u, bar);
     }
-    if (bt) {
+    if (bt || b16) {
     } else if (blk) {
       // T = 16: 64 B of each consecutive 128 B block row (block tile/2, half tile%2)
       const float *src0 = Yin + ((int64_t)(tile >> 1) * R + nrow[0]) * 32 + (tile & 1) * 16;
@@ -699,11 +860,33 @@ __global__ void __launch_bounds__(32 * kPassNW, 3)
     fetch_rows(cid);
     issue_load(cid);
   }
+  // L2 prefetch of the tile P.pf items ahead (blocked layout): its HBM reads
+  // then overlap this item's layers, and the real load (issued at the early
+  // release) is served from L2
+  auto prefetch = [&](int64_t it) {
+    if (tid != 0 || !blk || it >= items) return;
+    const int64_t cb = item_comp(it) * C + rank;
+    const int cnt = __ldg(P.in_count + cb);
+    const int64_t r0 = __ldg(P.in_rows + cb * P.rin);
+    const int tile = item_tile(it);
+    if (cnt <= 0) return;
+    if (T >= 32) {
+#pragma unroll 1
+      for (int q = 0; q < T / 32; ++q)
+        bulk_prefetch_l2(Yin + (((int64_t)tile * (T / 32) + q) * R + r0) * 32, (uint32_t)cnt * 128u);
+    } else if (b16) {
+      bulk_prefetch_l2(Yin + ((int64_t)tile * R + r0) * 16, (uint32_t)cnt * 64u);
+    } else {
+      bulk_prefetch_l2(Yin + ((int64_t)(tile >> 1) * R + r0) * 32, (uint32_t)cnt * 128u);
+    }
+  };
+  for (int k = 1; k <= P.pf; ++k) prefetch(cid + k * ncl);
   uint32_t ph = 0;
   for (int64_t it = cid; it < items; it += ncl, ph ^= 1u) {
     const int64_t c = item_comp(it);
     const int tile = item_tile(it);
     const int64_t next = it + ncl;
+    if (P.pf > 0) prefetch(it + (P.pf + 1) * ncl);
     if (next < items) fetch_rows(next);          // in flight while this item computes
     bool issued = false;
     mbar_wait(bar, ph);
@@ -797,9 +980,9 @@ __global__ void __launch_bounds__(32 * kPassNW, 3)
         // members: uniform bias => every member of the group has the same value
         float4 yu = make_float4(0.f, 0.f, 0.f, 0.f);
         if (ubias && G > 0) yu = out4<X2>(acc, PL.bu, ymax, o);
-        float *obase = blk ? Yout + (((int64_t)tile * T + pofs) >> 5) * R * 32 + (((int64_t)tile * T + pofs) & 31)
-                           : Yout + (int64_t)tile * T + pofs;
-        const int64_t rowmul = blk ? 32 : stride;
+        const int64_t opos = (int64_t)tile * T + pofs;
+        float *obase = blk ? Yout + (((opos >> lgo) * R) << lgo) + (opos & ((1 << lgo) - 1)) : Yout + opos;
+        const int64_t rowmul = blk ? (1 << lgo) : stride;
 #pragma unroll
         for (int r = 0; r < EPL; ++r) {
           if (r * LPU >= gmax) break;
@@ -954,7 +1137,7 @@ __global__ void __launch_bounds__(1024) k_scan_step(LayerState *st, int a, int m
 __global__ void k_compact(const LayerState *__restrict__ st, int a, int m, float *Ya, float *Yb,
                           int32_t *ridA, int32_t *ridB, const uint32_t *__restrict__ alive,
                           const int32_t *__restrict__ wpre, int32_t n, int64_t stride,
-                          int32_t yblk) {
+                          int32_t yblk, int lg) {
   const LayerState N1 = st[a + m];
   if (!N1.compacted) return;
   const LayerState S = st[a];
@@ -973,7 +1156,7 @@ __global__ void k_compact(const LayerState *__restrict__ st, int a, int m, float
     const int64_t to = wpre[q] + __popc(bits & ((1u << lane) - 1u));
     const int64_t from = q * 32 + lane;
     if (k < n)
-      dst[yix(k, to, stride, yblk)] = src[yix(k, from, stride, yblk)];
+      dst[yix(k, to, stride, yblk, lg)] = src[yix(k, from, stride, yblk, lg)];
     else
       rdst[to] = rsrc[from];
   }
@@ -1180,6 +1363,16 @@ void configure_kernels() {
   cudaFuncSetAttribute(k_pass<TT, CC, XX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPassSmem);
   SDNN_PASS_VARIANTS(X)
 #undef X
+  cudaFuncSetAttribute(k_layer_bulkw<kBulkwT, kBulkwNCW, kBulkwStages>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)bulkw_smem<kBulkwT, kBulkwNCW, kBulkwStages>());
+}
+
+bool layer_bulkw_ok(const LaunchCfg &c, const DevLayer &L) {
+  static const bool off = [] {
+    const char *e = getenv("SDNN_BULKW");
+    return e && atoi(e) == 0;
+  }();
+  return !off && c.bulk && !L.uniform && L.gmax == 32 && L.kmax <= 32 && L.kmax > 0;
 }
 
 // clusters of C CTAs that can be co-resident
@@ -1231,9 +1424,8 @@ static void launch_pass_t(const LaunchCfg &c, const Workspace &w, const DevPass 
                      (int64_t)w.words, (int64_t)w.stride, ymax);
 }
 
-void launch_densify(const LaunchCfg &c, const Workspace &w, int32_t n, int64_t batch,
-                    const int64_t *rowptr, const int32_t *idx, const float *val, bool compact,
-                    cudaStream_t s) {
+void launch_densify_prep(const LaunchCfg &c, const Workspace &w, int32_t n, int64_t batch,
+                         const int64_t *rowptr, const float *val, bool compact, cudaStream_t s) {
   const int64_t words = (batch + 31) / 32;
   cudaMemsetAsync(w.Y[0], 0, sizeof(float) * (size_t)n * (size_t)w.stride, s);
   cudaMemsetAsync(w.alive[0], 0, sizeof(uint32_t) * (size_t)kMaxPassLayers * w.words, s);
@@ -1248,9 +1440,20 @@ void launch_densify(const LaunchCfg &c, const Workspace &w, int32_t n, int64_t b
     cudaMemsetAsync(w.pret, 0, sizeof(uint32_t) * (size_t)w.words, s);
     cudaMemsetAsync(w.nretired, 0, sizeof(int32_t), s);
   }
-  if (batch > 0)
-    k_scatter<<<c.sms * 8, 256, 0, s>>>(batch, rowptr, idx, val, w.inmask, w.wpre, w.Y[0],
-                                        w.rid[0], w.stride, w.yblk, w.sig0);
+}
+
+void launch_scatter_rows(const LaunchCfg &c, const Workspace &w, int32_t n, int64_t r0, int64_t r1,
+                         const int64_t *rowptr, const int32_t *idx, const float *val, cudaStream_t s) {
+  if (r1 > r0)
+    k_scatter<<<(int)std::min<int64_t>(c.sms * 8, (r1 - r0 + 7) / 8), 256, 0, s>>>(
+        r0, r1, rowptr, idx, val, w.inmask, w.wpre, w.Y[0], w.rid[0], w.stride, w.yblk, w.sig0, w.lg0, n);
+}
+
+void launch_densify(const LaunchCfg &c, const Workspace &w, int32_t n, int64_t batch,
+                    const int64_t *rowptr, const int32_t *idx, const float *val, bool compact,
+                    cudaStream_t s) {
+  launch_densify_prep(c, w, n, batch, rowptr, val, compact, s);
+  launch_scatter_rows(c, w, n, 0, batch, rowptr, idx, val, s);
 }
 
 void launch_zero_layers_alive(const Workspace &w, int64_t batch, const int64_t *rowptr,
@@ -1276,6 +1479,10 @@ void launch_layer(const LaunchCfg &c, const Workspace &w, const DevLayer &L, int
     else
       k_layer_uniform<4, false><<<c.layer_blocks, 256, 0, s>>>(L, w.st, a, w.Y[0], w.Y[1],
                                                                 alive, w.stride, ymax);
+  } else if (layer_bulkw_ok(c, L)) {
+    k_layer_bulkw<kBulkwT, kBulkwNCW, kBulkwStages>
+        <<<c.sms, 32 * (1 + kBulkwNCW), bulkw_smem<kBulkwT, kBulkwNCW, kBulkwStages>(), s>>>(
+            L, w.st, a, w.Y[0], w.Y[1], alive, w.stride, ymax);
   } else {
     k_layer_general<2><<<c.layer_blocks, 256, 0, s>>>(L, w.st, a, w.Y[0], w.Y[1], alive,
                                                       w.stride, ymax);
@@ -1324,9 +1531,9 @@ void launch_yout_retired(const Workspace &w, int32_t n, int64_t batch, float yma
 }
 
 void launch_compact_copy(const LaunchCfg &c, const Workspace &w, int32_t a, int32_t m,
-                         const uint32_t *alive_last, int32_t n, cudaStream_t s) {
+                         const uint32_t *alive_last, int32_t n, cudaStream_t s, int lg) {
   k_compact<<<c.copy_blocks, 256, 0, s>>>(w.st, a, m, w.Y[0], w.Y[1], w.rid[0], w.rid[1],
-                                          alive_last, w.wpre, n, w.stride, w.yblk);
+                                          alive_last, w.wpre, n, w.stride, w.yblk, lg);
 }
 
 void launch_readout(const Workspace &w, int32_t a, const uint32_t *alive_last,

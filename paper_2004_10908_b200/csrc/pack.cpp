@@ -229,7 +229,7 @@ int pack_layer(int32_t n, const LayerIn &in, const float *bias, bool allow_group
       out.col[(size_t)g * gmax + q] = m[q];
       if (!out.uniform)
         for (int32_t t = 0; t < kg; ++t)
-          out.val[((size_t)g * gmax + q) * kmax + t] = cval[cptr[m[q]] + t];
+          out.val[((size_t)g * kmax + t) * gmax + q] = cval[cptr[m[q]] + t];
     }
   }
   return SDNN_OK;
@@ -241,7 +241,7 @@ bool saturation_preserving(const PackedLayer &p, float ymax) {
     for (int m = 0; m < G; ++m) {
       float acc = 0.f;                           // the canonical chain on all-ymax inputs
       for (int t = 0; t < K; ++t) {
-        const float w = p.uniform ? p.wu : p.val[((size_t)g * p.gmax + m) * p.kmax + t];
+        const float w = p.uniform ? p.wu : p.val[((size_t)g * p.kmax + t) * p.gmax + m];
         acc = std::fmaf(ymax, w, acc);
       }
       const float z = acc + p.bias[p.col[(size_t)g * p.gmax + m]];

@@ -19,7 +19,8 @@ namespace sdnn {
 // 32x32 blocks); a random-regular layer has N groups of 1.  A group carries
 //   src[K_g]           its sources, ascending (u16 when N <= 65536),
 //   col[G_g]           its member output columns, ascending,
-//   val[G_g][K_g]      per-slot weights, unless the layer is uniform,
+//   val[K_g][G_g]      per-slot weights (source-major: the weights of term t
+//                      for all members are contiguous), unless the layer is uniform,
 // The chain of every member is evaluated over exactly its K_g sources in
 // ascending order, so no padding term ever enters the arithmetic.
 // ---------------------------------------------------------------------------
@@ -40,7 +41,7 @@ struct PackedLayer {
   std::vector<int32_t> col;   // [ngroups][gmax] (-1 pad)
   std::vector<int32_t> gk;    // [ngroups] K_g
   std::vector<int32_t> gg;    // [ngroups] G_g
-  std::vector<float> val;     // [ngroups][gmax][kmax] (empty if uniform)
+  std::vector<float> val;     // [ngroups][kmax][gmax] (empty if uniform)
   std::vector<float> bias;    // [n]
 };
 
@@ -69,7 +70,7 @@ struct DevLayer {
   const int32_t *col;    // [ngroups][gmax]
   const int32_t *gk;     // [ngroups]
   const int32_t *gg;     // [ngroups]
-  const float *val;      // nullptr if uniform
+  const float *val;      // [ngroups][kmax][gmax], nullptr if uniform
   const float *bias;     // [n]
   int32_t ngroups, kmax, gmax;
   float wu;
@@ -168,6 +169,9 @@ struct DevPass {
   int32_t yblk;                        // 0: Y is [rows][stride]; R > 0: Y is [stride/32][R][32] and
                                        // every (comp, rank)'s rows are R-consecutive storage rows
   int32_t order;                       // item order: 0 component-major, 1 tile-major
+  int32_t lg_in, lg_out;               // yblk: log2 positions per block at the input / output
+                                       // boundary (5; 4 where a T = 16 pass reads)
+  int32_t pf;                          // yblk: L2-prefetch the tiles of the next pf items
   const int32_t *in_rows, *in_count;
   const unsigned char *rec;            // [ncomp][rec_bytes]
   PassLayerDev layers[kMaxPassLayers]; // by value: the kernel parameter carries them
@@ -213,6 +217,7 @@ struct Workspace {
   // rows R, element (row r, position p) at ((p / 32) * R + r) * 32 + p % 32;
   // sig0[neuron] = storage row of an input neuron (NULL: identity)
   int32_t yblk = 0;
+  int32_t lg0 = 5;                    // log2 positions per block at boundary 0
   const int32_t *sig0 = nullptr;
   int64_t words = 0;                  // stride / 32
   uint32_t *alive_set(int s) const { return alive[s & 1]; }
@@ -235,6 +240,13 @@ void configure_kernels();      // one-time function attributes (dynamic smem)
 void launch_densify(const LaunchCfg &c, const Workspace &w, int32_t n, int64_t batch,
                     const int64_t *rowptr, const int32_t *idx, const float *val, bool compact,
                     cudaStream_t s);
+// densify in two parts (sdnn_infer overlaps the input copy with the scatter):
+// zero Y0 + row flags + scan (needs rowptr, and val when it is given), then
+// the scatter of rows [r0, r1) once their indices are on the device
+void launch_densify_prep(const LaunchCfg &c, const Workspace &w, int32_t n, int64_t batch,
+                         const int64_t *rowptr, const float *val, bool compact, cudaStream_t s);
+void launch_scatter_rows(const LaunchCfg &c, const Workspace &w, int32_t n, int64_t r0, int64_t r1,
+                         const int64_t *rowptr, const int32_t *idx, const float *val, cudaStream_t s);
 // one layer: reads state st[a], writes its liveness bits to `alive`
 void launch_layer(const LaunchCfg &c, const Workspace &w, const DevLayer &L, int32_t a,
                   uint32_t *alive, float ymax, cudaStream_t s, uint32_t *sat = nullptr);
@@ -254,7 +266,7 @@ void launch_readout_retired(const Workspace &w, int32_t a, const uint32_t *alive
 void launch_yout_retired(const Workspace &w, int32_t n, int64_t batch, float ymax, float *d_yout,
                          cudaStream_t s);
 void launch_compact_copy(const LaunchCfg &c, const Workspace &w, int32_t a, int32_t m,
-                         const uint32_t *alive_last, int32_t n, cudaStream_t s);
+                         const uint32_t *alive_last, int32_t n, cudaStream_t s, int lg = 5);
 void launch_zero_layers_alive(const Workspace &w, int64_t batch, const int64_t *rowptr,
                               const float *val, cudaStream_t s);
 // categories from the final liveness bits `alive_last` of the step entered with st[a]

@@ -60,7 +60,7 @@ import numpy as np
 
 __all__ = [
     "K", "W_VALUE", "bias_value", "net_seed", "input_seed", "NetSpec", "Layer",
-    "rn_spec", "rr_spec", "rw_spec", "rw_bias", "ka_spec", "random_spec", "gen_layer", "iter_layers",
+    "rn_spec", "rr_spec", "rw_spec", "rw_bias", "rn_plain_spec", "plain_bias", "ka_spec", "random_spec", "gen_layer", "iter_layers",
     "ms_inputs", "ka_inputs", "random_inputs", "structure_hash", "csr_from_dense",
     "dense_from_csr", "ka_group_counts",
 ]
@@ -122,10 +122,14 @@ class NetSpec:
     extra: dict = field(default_factory=dict)
 
 
-def rn_spec(n: int, L: int, seed: Optional[int] = None, **kw) -> NetSpec:
+def rn_spec(n: int, L: int, seed: Optional[int] = None, schedule: str = "overlap", **kw) -> NetSpec:
     assert n >= 32 and n & (n - 1) == 0, "RN needs a power-of-two width >= 32"
+    assert schedule in ("overlap", "plain")
+    extra = dict(kw.pop("extra", {}))
+    if schedule != "overlap":                 # the default keeps extra empty (structure hashes)
+        extra["schedule"] = schedule
     return NetSpec("rn", n, L, net_seed(n, L) if seed is None else seed,
-                   kw.pop("bias", bias_value(n)), **kw)
+                   kw.pop("bias", bias_value(n)), extra=extra, **kw)
 
 
 # RW (general weights): the RN structure with one seeded value per slot drawn
@@ -145,6 +149,24 @@ def rw_bias(n: int) -> float:
 def rw_spec(n: int, L: int, seed: Optional[int] = None, **kw) -> NetSpec:
     """RN structure with per-slot random weights (the general-weight path)."""
     return rn_spec(n, L, seed=seed, wdist="random", bias=kw.pop("bias", rw_bias(n)), **kw)
+
+
+# Plain (non-overlapping) field schedule: with the challenge biases it kills all
+# but ~0.4 % of the MS rows within 4 layers (DESIGN.md R-W2); these biases keep
+# ~44 % alive (oracle, sampled rows; DESIGN.md R-W5)
+_PLAIN_BIAS = {1024: -0.2, 4096: -0.225, 16384: -0.25, 65536: -0.275}
+
+
+def plain_bias(n: int) -> float:
+    if n in _PLAIN_BIAS:
+        return _PLAIN_BIAS[n]
+    lg = np.log2(n) / 2.0 - 5.0
+    return float(np.clip(-0.2 - 0.025 * lg, -0.275, -0.2))
+
+
+def rn_plain_spec(n: int, L: int, seed: Optional[int] = None, **kw) -> NetSpec:
+    """RN with SURVEY.md 8.4's non-overlapping field schedule (robustness row)."""
+    return rn_spec(n, L, seed=seed, schedule="plain", bias=kw.pop("bias", plain_bias(n)), **kw)
 
 
 def rr_spec(n: int, L: int, seed: Optional[int] = None, **kw) -> NetSpec:
@@ -185,21 +207,31 @@ def _inv(p: np.ndarray) -> np.ndarray:
     return q
 
 
-def rn_field(n: int, l: int) -> int:
-    """Offset of layer l's 5-bit butterfly field: steps of 2 (consecutive fields
-    overlap in 3 bits, which keeps image locality for a few layers) and every
-    cycle of ceil(span/2) layers shifted by one, so odd offsets -- and with them
-    the top id bit -- are mixed too."""
+def rn_field(n: int, l: int, schedule: str = "overlap") -> int:
+    """Offset of layer l's 5-bit butterfly field.
+
+    "overlap" (default, DESIGN.md R-W2): steps of 2 (consecutive fields overlap
+    in 3 bits, which keeps image locality for a few layers) and every cycle of
+    ceil(span/2) layers shifted by one, so odd offsets -- and with them the top
+    id bit -- are mixed too.
+    "plain" (SURVEY.md 8.4 as written): non-overlapping fields cycling over
+    0, 5, 10, ..., the last one clamped to log2 N - 5 (full mixing within
+    ceil(log2 N / 5) layers; the robustness row, with its own bias R-W5)."""
     bits = n.bit_length() - 1
     span = bits - 4                      # valid offsets 0 .. bits-5
+    if schedule == "plain":
+        offs = list(range(0, span, 5))
+        if offs[-1] != bits - 5:
+            offs.append(bits - 5)
+        return offs[l % len(offs)]
     c = (span + 1) // 2
     return (2 * l + l // c) % span
 
 
-def _rn_sets(n: int, l: int, m: np.ndarray) -> np.ndarray:
+def _rn_sets(n: int, l: int, m: np.ndarray, schedule: str = "overlap") -> np.ndarray:
     """Butterfly set of internal ids m (vector): [len(m), 32] ids equal to m
     except in the 5-bit field at offset p_l."""
-    p = rn_field(n, l)
+    p = rn_field(n, l, schedule)
     base = m & ~np.int64(31 << p)
     return base[:, None] | (np.arange(32, dtype=np.int64)[None, :] << p)
 
@@ -229,14 +261,14 @@ def _csr_from_ell(n: int, ell: np.ndarray, ell_val: Optional[np.ndarray]):
     return rowptr, colidx, val
 
 
-def _rn_lists(n: int, l: int, outer: np.ndarray, inner: np.ndarray) -> np.ndarray:
+def _rn_lists(n: int, l: int, outer: np.ndarray, inner: np.ndarray, schedule: str = "overlap") -> np.ndarray:
     lib = _helper()
     if lib is None:
-        return outer[_rn_sets(n, l, inner)].astype(np.int32)
+        return outer[_rn_sets(n, l, inner, schedule)].astype(np.int32)
     out = np.empty((n, 32), np.int32)
     outer = np.ascontiguousarray(outer, np.int64)
     inner = np.ascontiguousarray(inner, np.int64)
-    lib.rn_lists(n, rn_field(n, l), _p(outer), _p(inner), _p(out))
+    lib.rn_lists(n, rn_field(n, l, schedule), _p(outer), _p(inner), _p(out))
     return out
 
 
@@ -248,10 +280,11 @@ def gen_layer(spec: NetSpec, l: int, fmt: str = "both") -> Layer:
     empty_i64, empty_i32 = np.zeros(0, np.int64), np.zeros((0, 32), np.int32)
     if spec.kind == "rn":
         pin, pout = _perm(spec, l), _perm(spec, l + 1)
-        ell = _rn_lists(n, l, pin, _inv(pout)) if want_ell else empty_i32
+        sch = spec.extra.get("schedule", "overlap")
+        ell = _rn_lists(n, l, pin, _inv(pout), sch) if want_ell else empty_i32
         if want_csr:
             rowptr = np.arange(0, (n + 1) * 32, 32, dtype=np.int64)
-            colidx = _rn_lists(n, l, pout, _inv(pin)).reshape(-1)
+            colidx = _rn_lists(n, l, pout, _inv(pin), sch).reshape(-1)
         else:
             rowptr, colidx = empty_i64, np.zeros(0, np.int32)
         val = ell_val = None

@@ -36,7 +36,7 @@ def test_exports_every_declared_symbol(sd):
     for name in declared:
         assert hasattr(L, name), name
     assert sorted(sd.EXPORTS) == declared
-    assert L.sdnn_abi_version() == 2
+    assert L.sdnn_abi_version() == 3
 
 
 def test_struct_layouts_match_header(sd, tmp_path):
