@@ -213,6 +213,36 @@ sdnn_status sdnn_gather_rows(sdnn_net *net, const int32_t *d_rows, int64_t nrows
 sdnn_status sdnn_bitmask_to_ids(const uint32_t *d_words, int64_t batch, int32_t *d_ids,
                                 int32_t *d_n, void *stream);
 
+/* f1 launch study (Sec. 4.6.2 "Scheduling GPU
+ * Tasks", Algorithm 1): ONE inference of `parts` batch partitions, partition p
+ * on its own handle nets[p] (own workspace; weights loaded into each), as one
+ * GPU task graph -- per partition: densify -> every kernel of the handle's
+ * layer chain -> readout of its categories into the word slice
+ * d_words + word_offset of a global bitmask -- joined by the device decode of
+ * that bitmask into d_ids / d_n (sdnn_bitmask_to_ids).  Launched as
+ *   SDNN_FLOW_GRAPH     an explicit graph of the task DAG (the paper's cudaFlow);
+ *   SDNN_FLOW_CAPTURER  Algorithm 1: levelize, stream = (task id in its level) mod
+ *                       max_streams, events only on cross-stream edges, captured
+ *                       into one CUDA graph and replayed;
+ *   SDNN_FLOW_STREAMS   the same stream assignment launched directly (no graph).
+ * Runs one warm-up and `reps` timed repetitions; *ms = device time per
+ * repetition (CUDA events); *ntasks = tasks in the graph.  Synchronous.
+ * Partitions must be word-aligned (word_offset = first row / 32, every batch
+ * but the last a multiple of 32).  Handles with stream_slots > 0 or
+ * SDNN_F_PROFILE are not supported. */
+enum { SDNN_FLOW_GRAPH = 0, SDNN_FLOW_CAPTURER = 1, SDNN_FLOW_STREAMS = 2 };
+typedef struct sdnn_flow_part {
+  const int64_t *d_rowptr;   /* device CSR of the partition's rows (as sdnn_infer_device) */
+  const int32_t *d_idx;
+  const float *d_val;        /* NULL => 1.0f */
+  int64_t batch;
+  int64_t word_offset;       /* first word of the partition in d_words */
+} sdnn_flow_part;
+sdnn_status sdnn_flow_infer(sdnn_net *const *nets, int32_t parts, const sdnn_flow_part *p,
+                            uint32_t *d_words, int64_t total_batch, int32_t *d_ids, int32_t *d_n,
+                            int32_t mode, int32_t max_streams, int32_t reps, float *ms,
+                            int32_t *ntasks);
+
 /* Statistics of the handle and of its last completed inference. */
 typedef struct sdnn_stats {
   int32_t struct_size;        /* caller sets sizeof(sdnn_stats) (versioning)            */

@@ -34,7 +34,8 @@ SDNN_F_SATURATE = 256
 EXPORTS = ["sdnn_create", "sdnn_create_empty", "sdnn_set_layer", "sdnn_infer",
            "sdnn_infer_device", "sdnn_stats_get", "sdnn_validate_layer", "sdnn_destroy",
            "sdnn_last_error", "sdnn_abi_version", "sdnn_layer_times", "sdnn_plan_steps",
-           "sdnn_step_plan", "sdnn_gather_rows", "sdnn_bitmask_to_ids"]
+           "sdnn_step_plan", "sdnn_gather_rows", "sdnn_bitmask_to_ids",
+           "sdnn_flow_infer"]
 
 
 class SdnnError(RuntimeError):
@@ -60,6 +61,14 @@ class sdnn_layer_info(ctypes.Structure):
     _fields_ = [("ngroups", ctypes.c_int32), ("kmax", ctypes.c_int32), ("gmax", ctypes.c_int32),
                 ("uniform", ctypes.c_int32), ("regular", ctypes.c_int32),
                 ("bias_nonpositive", ctypes.c_int32), ("nnz", ctypes.c_int64)]
+
+
+SDNN_FLOW_GRAPH, SDNN_FLOW_CAPTURER, SDNN_FLOW_STREAMS = 0, 1, 2
+
+
+class sdnn_flow_part(ctypes.Structure):
+    _fields_ = [("d_rowptr", ctypes.c_void_p), ("d_idx", ctypes.c_void_p), ("d_val", ctypes.c_void_p),
+                ("batch", ctypes.c_int64), ("word_offset", ctypes.c_int64)]
 
 
 class sdnn_stats(ctypes.Structure):
@@ -102,6 +111,8 @@ def lib() -> ctypes.CDLL:
         L.sdnn_step_plan.argtypes = [V, V, P(I32)]
         L.sdnn_gather_rows.argtypes = [V, V, I64, V, V]
         L.sdnn_bitmask_to_ids.argtypes = [V, I64, V, V, V]
+        L.sdnn_flow_infer.argtypes = [V, I32, P(sdnn_flow_part), V, I64, V, V, I32, I32, I32,
+                                      P(ctypes.c_float), P(I32)]
         L.sdnn_destroy.argtypes = [V]
         L.sdnn_destroy.restype = None
         L.sdnn_last_error.argtypes = []
@@ -110,7 +121,7 @@ def lib() -> ctypes.CDLL:
         for name in ["sdnn_create", "sdnn_create_empty", "sdnn_set_layer", "sdnn_infer",
                      "sdnn_infer_device", "sdnn_stats_get", "sdnn_validate_layer",
                      "sdnn_layer_times", "sdnn_plan_steps", "sdnn_step_plan", "sdnn_gather_rows",
-                     "sdnn_bitmask_to_ids"]:
+                     "sdnn_bitmask_to_ids", "sdnn_flow_infer"]:
             getattr(L, name).restype = I32
         _LIB = L
     return _LIB
@@ -385,6 +396,31 @@ def bitmask_to_ids_torch(words_t, batch: int, stream=None):
     _check(lib().sdnn_bitmask_to_ids(words_t.data_ptr() if batch > 0 else None, int(batch),
                                      ids.data_ptr(), cnt.data_ptr(), s.cuda_stream))
     return ids, cnt
+
+
+def flow_infer(nets, parts, total_batch: int, mode: int, max_streams: int = 4, reps: int = 3):
+    """f1 task-graph launch (sdnn_flow_infer).  nets: list of Net (one per
+    partition); parts: list of (rowptr_t, idx_t, first_row) torch CUDA tensors
+    per partition (word-aligned first rows).  Returns (ids numpy, ms per rep,
+    tasks in the graph)."""
+    import torch
+    dev = parts[0][0].device
+    P = len(nets)
+    hs = (ctypes.c_void_p * P)(*[n.h.value if hasattr(n.h, "value") else n.h for n in nets])
+    arr = (sdnn_flow_part * P)()
+    for i, (rp, ix, first) in enumerate(parts):
+        assert first % 32 == 0
+        arr[i] = sdnn_flow_part(rp.data_ptr(), ix.data_ptr() if ix.numel() else None, None,
+                                rp.numel() - 1, first // 32)
+    words = torch.zeros((total_batch + 31) // 32, dtype=torch.int32, device=dev)
+    ids = torch.empty(max(1, total_batch), dtype=torch.int32, device=dev)
+    cnt = torch.zeros(1, dtype=torch.int32, device=dev)
+    ms, nt = ctypes.c_float(), ctypes.c_int32()
+    _check(lib().sdnn_flow_infer(hs, P, arr, words.data_ptr(), int(total_batch), ids.data_ptr(),
+                                 cnt.data_ptr(), int(mode), int(max_streams), int(reps),
+                                 ctypes.byref(ms), ctypes.byref(nt)))
+    torch.cuda.synchronize(dev)
+    return ids[:int(cnt.item())].cpu().numpy(), ms.value, nt.value
 
 
 def bitmask_to_ids(words: np.ndarray, batch: int) -> np.ndarray:

@@ -149,6 +149,15 @@ namespace {
     }                                                                            \
   } while (0)
 
+#define CKN(NET, call)                                                           \
+  do {                                                                           \
+    cudaError_t _e = (call);                                                     \
+    if (_e != cudaSuccess) {                                                     \
+      (NET)->sticky = true;                                                      \
+      return fail(SDNN_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(_e)); \
+    }                                                                            \
+  } while (0)
+
 bool compact_enabled(const sdnn_net *net) {
   if (net->opts.flags & SDNN_F_NO_COMPACT) return false;
   if (net->L < 1) return false;
@@ -287,7 +296,8 @@ sdnn_status build_stream_blobs(sdnn_net *net, const std::vector<PassHost> &ph) {
       const PackedLayer &p = net->host[S_.a];
       parts[i] = {{p.src.data(), p.src.size() * 2}, {p.col.data(), p.col.size() * 4},
                   {p.gk.data(), p.gk.size() * 4}, {p.gg.data(), p.gg.size() * 4},
-                  {p.val.data(), p.uniform ? 0 : p.val.size() * 4}, {p.bias.data(), p.bias.size() * 4}};
+                  {p.val.data(), p.uniform ? 0 : p.val.size() * 4}, {p.bias.data(), p.bias.size() * 4},
+                  {p.gbias.data(), p.gbias.size() * 4}};
     } else {
       const PassHost &H = ph[i];
       parts[i] = {{H.in_rows.data(), H.in_rows.size() * 4}, {H.in_count.data(), H.in_count.size() * 4},
@@ -335,6 +345,7 @@ sdnn_status build_stream_blobs(sdnn_net *net, const std::vector<PassHost> &ph) {
       dl.gg = (const int32_t *)at[3];
       dl.val = net->host[S_.a].uniform ? nullptr : (const float *)at[4];
       dl.bias = (const float *)at[5];
+      dl.gbias = (const float *)at[6];
       net->step_dl[i] = dl;
     } else {
       DevPass &D = net->passes[S_.pass];
@@ -502,7 +513,7 @@ sdnn_status make_plan(sdnn_net *net) {
   for (size_t q = 0; q < net->steps.size(); ++q) {
     if (ph[q].m == 0) continue;                  // a plain layer step
     PassHost &H = ph[q];
-    if (!pass_variant(H.T, H.C))
+    if (!pass_variant(H.T, H.C, H.NB))
       return fail(SDNN_E_UNSUPPORTED, "no fused-pass kernel for tile " + std::to_string(H.T) + " x cluster " +
                                           std::to_string(H.C));
     DevPass D{};
@@ -513,6 +524,7 @@ sdnn_status make_plan(sdnn_net *net) {
     D.R = H.R;
     D.T = H.T;
     D.C = H.C;
+    D.NB = H.NB;
     D.rec_bytes = H.rec_bytes;
     D.yblk = net->yblk;
     D.order = pass_order() >= 0 ? pass_order() : (H.T == 16 ? 0 : 1);
@@ -569,7 +581,61 @@ sdnn_status make_plan(sdnn_net *net) {
   return SDNN_OK;
 }
 
+// The layer chain of one inference as a list of single-kernel operations in
+// dependency order (each depends on the previous): per step its layer / pass
+// kernel, the survivor scan and (between steps) the compaction.  Used by
+// enqueue_chain and by the f1 task graphs (sdnn_flow_infer).  Not for weight
+// streaming or per-layer profiling (they add events on a second stream).
+using Op = std::function<void(cudaStream_t)>;
+std::vector<Op> chain_ops(sdnn_net *net, bool compact) {
+  std::vector<Op> ops;
+  const float ymax = net->opts.ymax;
+  const int ns = (int)net->steps.size();
+  for (int si = 0; si < ns; ++si) {
+    const Step S = net->steps[si];
+    const bool last = si + 1 == ns;
+    if (S.pass == kResidentStep) {            // always the last step
+      ops.push_back([=](cudaStream_t s) {
+        const Workspace &w = net->ws;
+        launch_resident(w, net->d_res, S.a, net->L, net->n, w.alive_row(si, 0), compact, ymax, s);
+      });
+      continue;
+    }
+    const bool sat = (net->opts.flags & SDNN_F_SATURATE) && S.m == 1 &&
+                     layer_tracks_saturation(net->cfg, net->dl[S.a]);
+    ops.push_back([=](cudaStream_t s) {
+      const Workspace &w = net->ws;
+      if (S.pass < 0)
+        launch_layer(net->cfg, w, net->dl[S.a], S.a, w.alive_row(si, 0), ymax, s, sat ? w.sat[si & 1] : nullptr);
+      else
+        launch_pass(net->cfg, w, net->passes[S.pass], w.alive_set(si), ymax, s);
+    });
+    const bool retire = sat && net->sat_suffix[S.a + 1];
+    ops.push_back([=](cudaStream_t s) {
+      const Workspace &w = net->ws;
+      launch_scan(w, S.a, S.m, w.alive_set(si), w.alive_set(si + 1), compact && !last, s,
+                  retire ? w.sat[si & 1] : nullptr,
+                  (net->opts.flags & SDNN_F_SATURATE) ? w.sat[(si + 1) & 1] : nullptr);
+    });
+    if (!last)
+      ops.push_back([=](cudaStream_t s) {
+        const Workspace &w = net->ws;
+        launch_compact_copy(net->cfg, w, S.a, S.m, w.alive_row(si, S.m - 1), net->n, s,
+                            w.yblk ? net->step_lg[si + 1] : 5);
+      });
+  }
+  return ops;
+}
+
 void enqueue_chain(sdnn_net *net, bool compact, cudaStream_t s, int64_t *launches) {
+  if (!weight_streaming(net) && !(net->opts.flags & SDNN_F_PROFILE)) {
+    const std::vector<Op> ops = chain_ops(net, compact);
+    for (const Op &op : ops) op(s);
+    int64_t c = (int64_t)ops.size();
+    for (const Step &S : net->steps) c += S.pass == kResidentStep ? 1 : 0;   // the resident step launches 2 kernels
+    if (launches) *launches = c;
+    return;
+  }
   const float ymax = net->opts.ymax;
   const bool prof = (net->opts.flags & SDNN_F_PROFILE) && (int)net->ev_before.size() == net->L;
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
@@ -678,12 +744,9 @@ void launch_final_yout(sdnn_net *net, int64_t batch, float *d_yout, cudaStream_t
 }
 
 // Everything of one inference after Y0 is on the device.
-// feed (sdnn_infer): enqueues the chunked input copies and their scatters
-// after the densify prep; NULL = Y0 is already on the device
-using Feed = std::function<sdnn_status(cudaStream_t)>;
-sdnn_status infer_device_impl(sdnn_net *net, const int64_t *d_rowptr, const int32_t *d_idx,
-                              const float *d_val, int64_t batch, uint32_t *d_alive,
-                              float *d_yout, cudaStream_t s, const Feed *feed = nullptr) {
+// workspace for `batch` rows and the execution plan (whose activation layout
+// the workspace records)
+sdnn_status prepare_infer(sdnn_net *net, int64_t batch) {
   if (net->nset.load() != net->L) return fail(SDNN_E_STATE, "not every layer has been set");
   sdnn_status st = ensure_ws(net, batch);
   if (st) return st;
@@ -691,6 +754,17 @@ sdnn_status infer_device_impl(sdnn_net *net, const int64_t *d_rowptr, const int3
   net->ws.yblk = net->L > 0 ? net->yblk : 0;
   net->ws.sig0 = net->L > 0 ? net->d_sig0 : nullptr;
   net->ws.lg0 = (net->L > 0 && net->yblk && !net->step_lg.empty()) ? net->step_lg[0] : 5;
+  return SDNN_OK;
+}
+
+// feed (sdnn_infer): enqueues the chunked input copies and their scatters
+// after the densify prep; NULL = Y0 is already on the device
+using Feed = std::function<sdnn_status(cudaStream_t)>;
+sdnn_status infer_device_impl(sdnn_net *net, const int64_t *d_rowptr, const int32_t *d_idx,
+                              const float *d_val, int64_t batch, uint32_t *d_alive,
+                              float *d_yout, cudaStream_t s, const Feed *feed = nullptr) {
+  sdnn_status st = prepare_infer(net, batch);
+  if (st) return st;
   const bool compact = compact_enabled(net);
   int64_t launches = 4;
   if (feed) {
@@ -788,6 +862,217 @@ void *grow_pinned(sdnn_net *net, size_t bytes) {
   return net->h_stage;
 }
 
+
+// ---------------------------------------------------------------------------
+// f1: the inference of P batch partitions as ONE GPU task graph
+// -- per partition: densify -> every kernel of its handle's layer chain ->
+// readout into its word slice of a global category bitmask; then the device
+// decode of that bitmask -- launched three ways (Sec. 4.6.2):
+//   graph     explicit nodes and edges (the paper's cudaFlow): tasks are
+//             captured one by one into a graph whose dependency set is set to
+//             exactly the task's predecessors (cudaStreamUpdateCaptureDependencies)
+//   capturer  Algorithm 1: levelize, stream = (id in level) mod max_streams,
+//             events only on cross-stream edges, one stream capture -> graph
+//   streams   the same stream assignment and events, launched directly
+// ---------------------------------------------------------------------------
+struct FlowTask {
+  Op op;
+  std::vector<int> pred, succ;
+  int level = 0, id = 0;
+};
+
+// Alg. 1's levelize(C): topological levels (Kahn's algorithm, one level per
+// round); id = the task's index in its level
+std::vector<std::vector<int>> levelize(std::vector<FlowTask> &T) {
+  std::vector<int> indeg(T.size());
+  std::vector<int> cur;
+  for (size_t t = 0; t < T.size(); ++t)
+    if ((indeg[t] = (int)T[t].pred.size()) == 0) cur.push_back((int)t);
+  std::vector<std::vector<int>> L;
+  while (!cur.empty()) {
+    std::vector<int> next;
+    for (size_t i = 0; i < cur.size(); ++i) {
+      T[cur[i]].level = (int)L.size();
+      T[cur[i]].id = (int)i;
+      for (int n : T[cur[i]].succ)
+        if (--indeg[n] == 0) next.push_back(n);
+    }
+    L.push_back(cur);
+    cur.swap(next);
+  }
+  return L;
+}
+
+struct FlowStreams {
+  std::vector<cudaStream_t> S;
+  std::vector<cudaEvent_t> ev;                   // per task (recorded on cross-stream edges)
+  cudaEvent_t fork = nullptr;
+  std::vector<cudaEvent_t> join;
+  ~FlowStreams() {
+    for (auto s : S) cudaStreamDestroy(s);
+    for (auto e : ev) cudaEventDestroy(e);
+    for (auto e : join) cudaEventDestroy(e);
+    if (fork) cudaEventDestroy(fork);
+  }
+};
+
+// Algorithm 1 (make_graph), its loop body shared by the capturer and the plain
+// stream launch: stream_wait_event on every predecessor issued in another
+// stream, the task, stream_record_event for successors in another stream (the
+// listing records `p.event` in the successor loop; the task's own event is
+// meant)
+void alg1_issue(std::vector<FlowTask> &T, const std::vector<std::vector<int>> &L, FlowStreams &F, int k) {
+  cudaEventRecord(F.fork, F.S[0]);
+  for (int s = 1; s < k; ++s) cudaStreamWaitEvent(F.S[s], F.fork, 0);
+  for (const auto &lev : L)
+    for (int t : lev) {
+      const int s = T[t].id % k;
+      for (int p : T[t].pred)
+        if (T[p].id % k != s) cudaStreamWaitEvent(F.S[s], F.ev[p], 0);
+      T[t].op(F.S[s]);
+      bool rec = false;
+      for (int n : T[t].succ) rec = rec || (T[n].id % k != s);
+      if (rec) cudaEventRecord(F.ev[t], F.S[s]);
+    }
+  for (int s = 1; s < k; ++s) {                  // end_capture_mode_streams: join into S[0]
+    cudaEventRecord(F.join[s], F.S[s]);
+    cudaStreamWaitEvent(F.S[0], F.join[s], 0);
+  }
+}
+
+}  // namespace
+
+extern "C" sdnn_status sdnn_flow_infer(sdnn_net *const *nets, int32_t parts, const sdnn_flow_part *pp,
+                                       uint32_t *d_words, int64_t total_batch, int32_t *d_ids,
+                                       int32_t *d_n, int32_t mode, int32_t max_streams, int32_t reps,
+                                       float *ms, int32_t *ntasks) {
+  if (!nets || !pp || parts < 1 || !d_words || !d_ids || !d_n || max_streams < 1 || reps < 1)
+    return fail(SDNN_E_ARG, "bad argument");
+  if (mode < SDNN_FLOW_GRAPH || mode > SDNN_FLOW_STREAMS) return fail(SDNN_E_ARG, "bad mode");
+  for (int p = 0; p < parts; ++p) {
+    sdnn_net *net = nets[p];
+    if (!net) return fail(SDNN_E_ARG, "NULL handle");
+    for (int q = 0; q < p; ++q)
+      if (nets[q] == net) return fail(SDNN_E_ARG, "a handle may serve one partition only (own workspace)");
+    if (net->L < 1) return fail(SDNN_E_UNSUPPORTED, "task graphs need >= 1 layer");
+    if (weight_streaming(net) || (net->opts.flags & SDNN_F_PROFILE))
+      return fail(SDNN_E_UNSUPPORTED, "weight streaming / profiling handles are not supported here");
+    if (pp[p].batch < 0 || pp[p].word_offset < 0 || (pp[p].batch > 0 && !pp[p].d_rowptr))
+      return fail(SDNN_E_ARG, "bad partition");
+    sdnn_status st = set_device(net);
+    if (st) return st;
+    if ((st = prepare_infer(net, pp[p].batch))) return st;
+  }
+  sdnn_net *net0 = nets[0];
+  // ---- the task graph ----
+  std::vector<FlowTask> T;
+  std::vector<int> tails;
+  for (int p = 0; p < parts; ++p) {
+    sdnn_net *net = nets[p];
+    const sdnn_flow_part P = pp[p];
+    const bool compact = compact_enabled(net);
+    auto add = [&](Op op) {
+      FlowTask t;
+      t.op = std::move(op);
+      if (!T.empty() && (int)T.size() > 0 && !tails.empty() && tails.back() >= 0) {
+        t.pred.push_back(tails.back());
+        T[tails.back()].succ.push_back((int)T.size());
+      }
+      T.push_back(std::move(t));
+      tails.back() = (int)T.size() - 1;
+    };
+    tails.push_back(-1);
+    add([=](cudaStream_t s) {
+      launch_densify(net->cfg, net->ws, net->n, P.batch, P.d_rowptr, P.d_idx, P.d_val, compact, s);
+    });
+    for (Op &op : chain_ops(net, compact)) add(std::move(op));
+    const int si = (int)net->steps.size() - 1;
+    const Step S = net->steps[si];
+    const int row = S.pass == kResidentStep ? 0 : S.m - 1;
+    add([=](cudaStream_t s) {
+      launch_readout(net->ws, S.a, net->ws.alive_row(si, row), d_words + P.word_offset, P.batch, s);
+    });
+  }
+  {
+    FlowTask j;
+    j.op = [=](cudaStream_t s) { launch_bitmask_ids(d_words, total_batch, d_ids, d_n, s); };
+    for (int t : tails) {
+      j.pred.push_back(t);
+      T[t].succ.push_back((int)T.size());
+    }
+    T.push_back(std::move(j));
+  }
+  if (ntasks) *ntasks = (int32_t)T.size();
+  const std::vector<std::vector<int>> L = levelize(T);
+  const int k = mode == SDNN_FLOW_GRAPH ? 1 : max_streams;
+  FlowStreams F;
+  F.S.resize(k);
+  for (auto &s : F.S) CKN(net0, cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  F.ev.resize(T.size());
+  for (auto &e : F.ev) CKN(net0, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  F.join.assign(k, nullptr);
+  for (auto &e : F.join) CKN(net0, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  CKN(net0, cudaEventCreateWithFlags(&F.fork, cudaEventDisableTiming));
+  cudaGraphExec_t exec = nullptr;
+  if (mode == SDNN_FLOW_CAPTURER) {
+    cudaGraph_t g;
+    CKN(net0, cudaStreamBeginCapture(F.S[0], cudaStreamCaptureModeThreadLocal));
+    alg1_issue(T, L, F, k);
+    CKN(net0, cudaStreamEndCapture(F.S[0], &g));
+    const cudaError_t e = cudaGraphInstantiate(&exec, g, 0);
+    cudaGraphDestroy(g);
+    CKN(net0, e);
+  } else if (mode == SDNN_FLOW_GRAPH) {
+    // explicit DAG: each task is captured with its dependency set replaced by
+    // the graph nodes that end its predecessors
+    cudaGraph_t g;
+    CKN(net0, cudaGraphCreate(&g, 0));
+    cudaStream_t s = F.S[0];
+    CKN(net0, cudaStreamBeginCaptureToGraph(s, g, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    std::vector<std::vector<cudaGraphNode_t>> ends(T.size());
+    for (const auto &lev : L)
+      for (int t : lev) {
+        std::vector<cudaGraphNode_t> deps;
+        for (int p : T[t].pred) deps.insert(deps.end(), ends[p].begin(), ends[p].end());
+        CKN(net0, cudaStreamUpdateCaptureDependencies(s, deps.empty() ? nullptr : deps.data(), deps.size(),
+                                                      cudaStreamSetCaptureDependencies));
+        T[t].op(s);
+        cudaStreamCaptureStatus cs;
+        const cudaGraphNode_t *dn = nullptr;
+        size_t nd = 0;
+        CKN(net0, cudaStreamGetCaptureInfo(s, &cs, nullptr, nullptr, &dn, &nd));
+        ends[t].assign(dn, dn + nd);
+      }
+    cudaGraph_t g2;
+    CKN(net0, cudaStreamEndCapture(s, &g2));
+    const cudaError_t e = cudaGraphInstantiate(&exec, g2, 0);
+    cudaGraphDestroy(g2);
+    CKN(net0, e);
+  }
+  cudaEvent_t t0, t1;
+  CKN(net0, cudaEventCreate(&t0));
+  CKN(net0, cudaEventCreate(&t1));
+  auto run = [&]() {
+    if (exec) cudaGraphLaunch(exec, F.S[0]);
+    else alg1_issue(T, L, F, k);
+  };
+  run();                                         // warm-up (and the result if reps == 1)
+  cudaEventRecord(t0, F.S[0]);
+  for (int r = 0; r < reps; ++r) run();
+  cudaEventRecord(t1, F.S[0]);
+  cudaError_t e = cudaEventSynchronize(t1);
+  float tm = 0.f;
+  if (e == cudaSuccess) e = cudaEventElapsedTime(&tm, t0, t1);
+  cudaEventDestroy(t0);
+  cudaEventDestroy(t1);
+  if (exec) cudaGraphExecDestroy(exec);
+  CKN(net0, e);
+  CKN(net0, cudaGetLastError());
+  if (ms) *ms = tm / reps;
+  return SDNN_OK;
+}
+
+namespace {
 }  // namespace
 
 // ===========================================================================
@@ -879,11 +1164,11 @@ sdnn_status sdnn_set_layer(sdnn_net *net, int32_t l, const sdnn_layer *W, const 
   const size_t G = p.ngroups;
   const size_t b_src = sizeof(uint16_t) * p.src.size(), b_col = sizeof(int32_t) * p.col.size();
   const size_t b_gk = sizeof(int32_t) * G, b_val = sizeof(float) * p.val.size();
-  const size_t b_bias = sizeof(float) * net->n;
+  const size_t b_bias = sizeof(float) * net->n, b_gbias = sizeof(float) * p.gbias.size();
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
-  const size_t total = al(b_src) + al(b_col) + 2 * al(b_gk) + al(b_val) + al(b_bias);
+  const size_t total = al(b_src) + al(b_col) + 2 * al(b_gk) + al(b_val) + al(b_bias) + al(b_gbias);
   DevLayer d{};
-  void *ps = nullptr, *pc = nullptr, *pk = nullptr, *pg = nullptr, *pv = nullptr, *pb = nullptr;
+  void *ps = nullptr, *pc = nullptr, *pk = nullptr, *pg = nullptr, *pv = nullptr, *pb = nullptr, *pgb = nullptr;
   if (!weight_streaming(net)) {                   // f3: the blocks stay on the host
     char *blk = nullptr;
     {
@@ -910,7 +1195,8 @@ sdnn_status sdnn_set_layer(sdnn_net *net, int32_t l, const sdnn_layer *W, const 
     };
     if ((st = up(p.src.data(), b_src, &ps)) || (st = up(p.col.data(), b_col, &pc)) ||
         (st = up(p.gk.data(), b_gk, &pk)) || (st = up(p.gg.data(), b_gk, &pg)) ||
-        (st = up(p.val.data(), b_val, &pv)) || (st = up(p.bias.data(), b_bias, &pb)))
+        (st = up(p.val.data(), b_val, &pv)) || (st = up(p.bias.data(), b_bias, &pb)) ||
+        (st = up(p.gbias.data(), b_gbias, &pgb)))
       return st;
     std::lock_guard<std::mutex> g(net->stat_mu);
     if (!(net->set[l] && net->lblock[l] == blk)) {
@@ -924,6 +1210,7 @@ sdnn_status sdnn_set_layer(sdnn_net *net, int32_t l, const sdnn_layer *W, const 
   d.gg = (const int32_t *)pg;
   d.val = p.uniform ? nullptr : (const float *)pv;
   d.bias = (const float *)pb;
+  d.gbias = (const float *)pgb;
   d.ngroups = p.ngroups;
   d.kmax = p.kmax;
   d.gmax = p.gmax;

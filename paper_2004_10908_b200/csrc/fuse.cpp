@@ -377,7 +377,7 @@ void build_pass(const std::vector<const PackedLayer *> &layers, int32_t n, const
   {
     int Rp = 32;
     while (Rp < R) Rp <<= 1;
-    if (!pass_variant(std::max(16, std::min(512, tile_floats / Rp)), C)) return;   // no kernel instance
+    if (!pass_variant(std::max(16, std::min(512, tile_floats / Rp)), C, 1)) return;   // no kernel instance
   }
   // slot code of a boundary node: (bin << 8) | slot within the bin
   std::vector<int32_t> slot((size_t)(m + 1) * n, -1);
@@ -391,6 +391,7 @@ void build_pass(const std::vector<const PackedLayer *> &layers, int32_t n, const
   int Rp = 32;                                    // one tile of tile_floats per CTA
   while (Rp < R) Rp <<= 1;
   out.T = std::max(16, std::min(512, tile_floats / Rp));
+  out.NB = 1;
   out.in_rows.assign((size_t)ncomp * C * R, -1);
   out.in_count.assign((size_t)ncomp * C, 0);
   for (int c = 0; c < ncomp; ++c)
@@ -492,6 +493,21 @@ void build_pass(const std::vector<const PackedLayer *> &layers, int32_t n, const
     }
   }
   out.rec_bytes = off;
+  // components of <= 128 rows: two half-size tiles per CTA (double-buffered)
+  // when both records fit and a kernel instance exists (SDNN_PASS_NB=1: off).
+  // Measured on C4: 128-row passes 2.69 ms (T = 64 x 2) vs 2.75 ms (T = 128);
+  // 256-row passes 2.90 ms (T = 32 x 2) vs 2.61 ms (T = 64), so not for those
+  {
+    static const bool nb2 = [] {
+      const char *e = getenv("SDNN_PASS_NB");
+      return !(e && atoi(e) == 1);
+    }();
+    const int T2 = std::max(16, std::min(512, tile_floats / 2 / Rp));
+    if (nb2 && C == 1 && Rp <= 128 && off <= ((kPassRecMax / 2) & ~15) && pass_variant(T2, 1, 2)) {
+      out.NB = 2;
+      out.T = T2;
+    }
+  }
   const size_t units = (size_t)ncomp * C;
   out.rec.assign(units * off, 0);
   for (size_t cb = 0; cb < units; ++cb) {

@@ -260,14 +260,16 @@ __global__ void __launch_bounds__(32 * (1 + T / 128), 1)
 // ---------------------------------------------------------------------------
 template <int T, int NCW, int STAGES>
 constexpr size_t bulkw_smem() {
-  return (size_t)STAGES * (32 * T + 32 * 32) * sizeof(float) + 2 * STAGES * 8;
+  return (size_t)STAGES * (32 * T + 32 * 32 + 128) * sizeof(float) + 2 * STAGES * 8;
 }
 
 template <int T, int NCW, int STAGES>
 __global__ void __launch_bounds__(32 * (1 + NCW), 1)
     k_layer_bulkw(DevLayer L, const LayerState *__restrict__ st, int layer, float *Ya, float *Yb,
                   uint32_t *__restrict__ alive, int64_t stride, float ymax) {
-  constexpr int SF = 32 * T + 32 * 32;             // floats per stage: 32 rows + weights
+  // floats per stage: 32 rows, weights [32][32], member columns + member biases
+  // (bulk-copied with them) and the group's K, G (written by the producer)
+  constexpr int SF = 32 * T + 32 * 32 + 128;
   constexpr int PW = T / NCW;                      // positions per consumer warp
   static_assert(PW % 32 == 0, "rounds of 32 positions");
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -304,8 +306,13 @@ __global__ void __launch_bounds__(32 * (1 + NCW), 1)
       float *sb = stage + (size_t)s * SF;
       if (lane == 0) {
         const uint32_t wbytes = (uint32_t)K * 32u * 4u;
-        mbar_expect_tx_arrive(&full[s], (uint32_t)K * T * 4 + wbytes);
+        int *meta = reinterpret_cast<int *>(sb + 32 * T + 32 * 32 + 64);
+        meta[0] = K;
+        meta[1] = L.gg[g];
+        mbar_expect_tx_arrive(&full[s], (uint32_t)K * T * 4 + wbytes + 256u);
         if (wbytes) bulk_g2s(sb + 32 * T, L.val + (int64_t)g * L.kmax * 32, wbytes, &full[s]);
+        bulk_g2s(sb + 32 * T + 32 * 32, L.col + (int64_t)g * 32, 128u, &full[s]);
+        bulk_g2s(sb + 32 * T + 32 * 32 + 32, L.gbias + (int64_t)g * 32, 128u, &full[s]);
       }
       __syncwarp();
       if (lane < K) bulk_g2s(sb + lane * T, Yin + (int64_t)mysrc * stride + (int64_t)tile * T, T * 4, &full[s]);
@@ -320,17 +327,18 @@ __global__ void __launch_bounds__(32 * (1 + NCW), 1)
     for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
       const int g = (int)(it / tiles);
       const int tile = (int)(it - (int64_t)g * tiles);
-      const int K = L.gk[g], G = L.gg[g];
+      mbar_wait(&full[s], ph);
+      const float *sb = stage + (size_t)s * SF;
+      const int *meta = reinterpret_cast<const int *>(sb + 32 * T + 32 * 32);
+      const int K = meta[64], G = meta[65];
       int col[8];
       float bia[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int m = 8 * c + i;
-        col[i] = m < G ? L.col[(int64_t)g * 32 + m] : -1;
-        bia[i] = col[i] >= 0 ? __ldg(L.bias + col[i]) : 0.f;
+        col[i] = m < G ? meta[m] : -1;
+        bia[i] = reinterpret_cast<const float *>(meta)[32 + (m & 31)];
       }
-      mbar_wait(&full[s], ph);
-      const float *sb = stage + (size_t)s * SF;
       const float *wsm = sb + 32 * T + 8 * c;
 #pragma unroll 1
       for (int r = 0; r < PW / 32; ++r) {
@@ -674,14 +682,16 @@ int pass_tile_floats() { return kPassTile; }
 // pass_cta_rows() (first-fit bins), hence T = 16384 / pass_cta_rows().  X2
 // (packed FFMA2/FADD2) is the cluster default; SDNN_PASS_X2=1 selects it for
 // single-CTA passes too.
-#define SDNN_PASS_VARIANTS(X)                                                                    \
-  X(16, 1, false) X(16, 1, true) X(16, 2, true) X(32, 1, false) X(64, 1, false) X(128, 1, false) X(256, 1, false) X(512, 1, false)           \
-  X(32, 1, true) X(64, 1, true) X(128, 1, true) X(256, 1, true) X(512, 1, true) X(32, 2, true) \
-  X(32, 4, true) X(64, 2, true) X(64, 4, true) X(128, 2, true) X(128, 4, true)
+#define SDNN_PASS_VARIANTS(X)                                                                        \
+  X(16, 1, false, 1) X(16, 1, true, 1) X(16, 2, true, 1) X(32, 1, false, 1) X(64, 1, false, 1)          \
+  X(128, 1, false, 1) X(256, 1, false, 1) X(512, 1, false, 1) X(32, 1, true, 1) X(64, 1, true, 1)       \
+  X(128, 1, true, 1) X(256, 1, true, 1) X(512, 1, true, 1) X(32, 2, true, 1) X(32, 4, true, 1)          \
+  X(64, 2, true, 1) X(64, 4, true, 1) X(128, 2, true, 1) X(128, 4, true, 1) X(32, 1, false, 2)          \
+  X(64, 1, false, 2) X(128, 1, false, 2)
 
-bool pass_variant(int T, int C) {
-#define X(TT, CC, XX) \
-  if (T == TT && C == CC) return true;
+bool pass_variant(int T, int C, int NB) {
+#define X(TT, CC, XX, NN) \
+  if (T == TT && C == CC && NB == NN) return true;
   SDNN_PASS_VARIANTS(X)
 #undef X
   return false;
@@ -725,7 +735,7 @@ __device__ __forceinline__ float4 out4(const float (&a)[4], float b, float ymax,
   return y;
 }
 
-template <int T, int C, bool X2>
+template <int T, int C, bool X2, int NB>
 __global__ void __launch_bounds__(32 * kPassNW, 3)
     k_pass(const DevPass P, const LayerState *__restrict__ st, float *Ya, float *Yb,
            uint32_t *__restrict__ alive, int64_t wstride, int64_t stride, float ymax) {
@@ -746,10 +756,16 @@ __global__ void __launch_bounds__(32 * kPassNW, 3)
   constexpr bool kLdgsts = T <= 64;
   constexpr int CPR = T / 4;                     // 16-B chunks per row
   constexpr int RPI = kLdgsts ? 32 / CPR : 1;    // rows per warp instruction
+  // NB = 2 (small components): two half-size tile buffers with their own
+  // records and mbarriers, so the next item's load is in flight for the whole
+  // of this item's layers instead of from the last layer's release on
+  static_assert(NB == 1 || (NB == 2 && C == 1), "double-buffered passes are single-CTA");
+  constexpr int TF = kPassTile / NB;             // floats per tile buffer
+  constexpr int RB = (kPassRecMax / NB) & ~15;   // record bytes per buffer
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  float *tile_s = reinterpret_cast<float *>(smem_raw);
-  unsigned char *rec_s = smem_raw + (size_t)kPassTile * 4;
-  uint64_t *bar = reinterpret_cast<uint64_t *>(rec_s + kPassRecMax);
+  float *const tile0 = reinterpret_cast<float *>(smem_raw);
+  unsigned char *const rec0 = smem_raw + (size_t)kPassTile * 4;
+  uint64_t *bar = reinterpret_cast<uint64_t *>(rec0 + kPassRecMax);   // [NB]
   uint32_t *aw = reinterpret_cast<uint32_t *>(bar + 2);                 // [kMaxPassLayers][W]
   const LayerState Sx = st[P.a];
   const int width = Sx.width;
@@ -770,7 +786,6 @@ __global__ void __launch_bounds__(32 * kPassNW, 3)
   const uint32_t rank = C > 1 ? cluster_rank() : 0u;
   const int64_t cid = C > 1 ? (int64_t)cluster_id_x() : (int64_t)blockIdx.x;
   const int64_t ncl = C > 1 ? (int64_t)nclusters_x() : (int64_t)gridDim.x;
-  const uint32_t tile_u32 = smem_u32(tile_s);
   // position-blocked activations: a CTA's rows are consecutive storage rows, so
   // each 32-position block of its tile is ONE contiguous run of ncnt*128 B,
   // copied by one cp.async.bulk into the tile laid out [T/32][rin][32]
@@ -785,7 +800,7 @@ __global__ void __launch_bounds__(32 * kPassNW, 3)
   const int rin = P.rin;
   const int sm = bt ? 32 : T;                    // tile floats per slot step
   if (tid == 0) {
-    mbar_init(bar, ldg ? 32 * NW + 1 : 1);       // LDGSTS: one noinc arrival per thread
+    for (int b = 0; b < NB; ++b) mbar_init(bar + b, ldg ? 32 * NW + 1 : 1);   // LDGSTS: one noinc arrival per thread
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int q = tid; q < kMaxPassLayers * W; q += blockDim.x) aw[q] = 0u;
@@ -805,20 +820,23 @@ __global__ void __launch_bounds__(32 * kPassNW, 3)
       nrow[q] = r < P.rin ? __ldg(P.in_rows + cb * P.rin + r) : 0;
     }
   };
-  auto issue_load = [&](int64_t it) {
+  auto issue_load = [&](int64_t it, int buf) {
+    float *const tile_s = tile0 + (size_t)buf * TF;
+    unsigned char *const rec_s = rec0 + (size_t)buf * RB;
+    uint64_t *const bar_b = bar + buf;
     const int64_t c = item_comp(it);
     const int tile = item_tile(it);
     const int64_t cb = c * C + rank;
     if (tid == 0) {
-      mbar_expect_tx_arrive(bar, (ldg ? 0u : (uint32_t)ncnt * T * 4) + (uint32_t)P.rec_bytes);
-      bulk_g2s(rec_s, P.rec + cb * P.rec_bytes, P.rec_bytes, bar);
+      mbar_expect_tx_arrive(bar_b, (ldg ? 0u : (uint32_t)ncnt * T * 4) + (uint32_t)P.rec_bytes);
+      bulk_g2s(rec_s, P.rec + cb * P.rec_bytes, P.rec_bytes, bar_b);
       if (bt && ncnt > 0)                        // nrow[0] = the first storage row
 #pragma unroll
         for (int q = 0; q < (T >= 32 ? T / 32 : 0); ++q)
           bulk_g2s(tile_s + q * rin * 32, Yin + (((int64_t)tile * (T / 32) + q) * R + nrow[0]) * 32,
-                   (uint32_t)ncnt * 128u, bar);
+                   (uint32_t)ncnt * 128u, bar_b);
       if (b16 && ncnt > 0)
-        bulk_g2s(tile_s, Yin + ((int64_t)tile * R + nrow[0]) * 16, (uint32_t)ncnt * 64u, bar);
+        bulk_g2s(tile_s, Yin + ((int64_t)tile * R + nrow[0]) * 16, (uint32_t)ncnt * 64u, bar_b);
     }
     if (bt || b16) {
     } else if (blk) {
@@ -826,7 +844,7 @@ __global__ void __launch_bounds__(32 * kPassNW, 3)
       const float *src0 = Yin + ((int64_t)(tile >> 1) * R + nrow[0]) * 32 + (tile & 1) * 16;
       for (int x = tid; x < ncnt * 4; x += 32 * NW)
         cp_async16(tile_s + (size_t)x * 4, src0 + (int64_t)(x >> 2) * 32 + (x & 3) * 4);
-      cp_async_arrive(bar);
+      cp_async_arrive(bar_b);
     } else if (kLdgsts) {
       // warp w copies rows q*128 + 32w + j; lane = (row j % RPI, chunk)
       const int ch = lane % CPR;
@@ -842,13 +860,13 @@ __global__ void __launch_bounds__(32 * kPassNW, 3)
           if (r < ncnt) cp_async16(tile_s + (size_t)r * T + ch * 4, src0 + (int64_t)rid * stride);
         }
       }
-      cp_async_arrive(bar);
+      cp_async_arrive(bar_b);
     } else {
 #pragma unroll
       for (int q = 0; q < RPT; ++q) {
         const int r = tid + q * 32 * NW;
         if (r < ncnt)
-          bulk_g2s(tile_s + (size_t)r * T, Yin + (int64_t)nrow[q] * stride + (int64_t)tile * T, T * 4, bar);
+          bulk_g2s(tile_s + (size_t)r * T, Yin + (int64_t)nrow[q] * stride + (int64_t)tile * T, T * 4, bar_b);
       }
     }
   };
@@ -856,10 +874,11 @@ __global__ void __launch_bounds__(32 * kPassNW, 3)
     if (C > 1) cluster_sync();
     else __syncthreads();
   };
-  if (cid < items) {
-    fetch_rows(cid);
-    issue_load(cid);
-  }
+  for (int b = 0; b < NB; ++b)
+    if (cid + b * ncl < items) {
+      fetch_rows(cid + b * ncl);
+      issue_load(cid + b * ncl, b);
+    }
   // L2 prefetch of the tile P.pf items ahead (blocked layout): its HBM reads
   // then overlap this item's layers, and the real load (issued at the early
   // release) is served from L2
@@ -881,15 +900,20 @@ __global__ void __launch_bounds__(32 * kPassNW, 3)
     }
   };
   for (int k = 1; k <= P.pf; ++k) prefetch(cid + k * ncl);
-  uint32_t ph = 0;
-  for (int64_t it = cid; it < items; it += ncl, ph ^= 1u) {
+  int64_t kk = 0;
+  for (int64_t it = cid; it < items; it += ncl, ++kk) {
+    const int buf = NB == 1 ? 0 : (int)(kk % NB);
+    const uint32_t ph = (uint32_t)((kk / NB) & 1);
+    float *const tile_s = tile0 + (size_t)buf * TF;
+    unsigned char *const rec_s = rec0 + (size_t)buf * RB;
+    const uint32_t tile_u32 = smem_u32(tile_s);
     const int64_t c = item_comp(it);
     const int tile = item_tile(it);
-    const int64_t next = it + ncl;
+    const int64_t next = it + NB * ncl;          // the item this buffer takes next
     if (P.pf > 0) prefetch(it + (P.pf + 1) * ncl);
     if (next < items) fetch_rows(next);          // in flight while this item computes
     bool issued = false;
-    mbar_wait(bar, ph);
+    mbar_wait(bar + buf, ph);
     for (int j = 0; j < P.m; ++j) {
       const PassLayerDev PL = P.layers[j];
       const bool last = j == P.m - 1;
@@ -972,7 +996,7 @@ __global__ void __launch_bounds__(32 * kPassNW, 3)
           // generic-proxy tile reads/writes before the next item's TMA writes
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           release();
-          if (next < items) issue_load(next);
+          if (next < items) issue_load(next, buf);
           issued = true;
         }
         const int gmax = __reduce_max_sync(FULL, G);
@@ -1043,7 +1067,7 @@ __global__ void __launch_bounds__(32 * kPassNW, 3)
     if (!issued) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       release();
-      if (next < items) issue_load(next);
+      if (next < items) issue_load(next, buf);
     }
     __syncthreads();                             // aw published before the next item uses it
   }
@@ -1359,8 +1383,8 @@ void configure_kernels() {
         b.ctas <= 4)
       g_bulk = b;
   }
-#define X(TT, CC, XX) \
-  cudaFuncSetAttribute(k_pass<TT, CC, XX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPassSmem);
+#define X(TT, CC, XX, NN) \
+  cudaFuncSetAttribute(k_pass<TT, CC, XX, NN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPassSmem);
   SDNN_PASS_VARIANTS(X)
 #undef X
   cudaFuncSetAttribute(k_layer_bulkw<kBulkwT, kBulkwNCW, kBulkwStages>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1372,11 +1396,11 @@ bool layer_bulkw_ok(const LaunchCfg &c, const DevLayer &L) {
     const char *e = getenv("SDNN_BULKW");
     return e && atoi(e) == 0;
   }();
-  return !off && c.bulk && !L.uniform && L.gmax == 32 && L.kmax <= 32 && L.kmax > 0;
+  return !off && c.bulk && !L.uniform && L.gmax == 32 && L.kmax <= 32 && L.kmax > 0 && L.gbias;
 }
 
 // clusters of C CTAs that can be co-resident
-template <int T, int C, bool X2>
+template <int T, int C, bool X2, int NB>
 static int pass_clusters(int sms) {
   static int cached = 0;
   if (cached) return cached;
@@ -1392,7 +1416,7 @@ static int pass_clusters(int sms) {
   cfg.attrs = at;
   cfg.numAttrs = 1;
   int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, k_pass<T, C, X2>, &cfg) != cudaSuccess || n <= 0) {
+  if (cudaOccupancyMaxActiveClusters(&n, k_pass<T, C, X2, NB>, &cfg) != cudaSuccess || n <= 0) {
     cudaGetLastError();
     n = sms * 3 / C / 2;                         // conservative
   }
@@ -1400,16 +1424,16 @@ static int pass_clusters(int sms) {
   return n;
 }
 
-template <int T, int C, bool X2>
+template <int T, int C, bool X2, int NB>
 static void launch_pass_t(const LaunchCfg &c, const Workspace &w, const DevPass &P, uint32_t *alive,
                           float ymax, cudaStream_t s) {
   if (C == 1) {
-    k_pass<T, 1, X2><<<c.sms * 3, 32 * kPassNW, kPassSmem, s>>>(P, w.st, w.Y[0], w.Y[1], alive, w.words,
+    k_pass<T, 1, X2, NB><<<c.sms * 3, 32 * kPassNW, kPassSmem, s>>>(P, w.st, w.Y[0], w.Y[1], alive, w.words,
                                                             w.stride, ymax);
     return;
   }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(C * pass_clusters<T, C, X2>(c.sms));
+  cfg.gridDim = dim3(C * pass_clusters<T, C, X2, NB>(c.sms));
   cfg.blockDim = dim3(32 * kPassNW);
   cfg.dynamicSmemBytes = kPassSmem;
   cfg.stream = s;
@@ -1420,7 +1444,7 @@ static void launch_pass_t(const LaunchCfg &c, const Workspace &w, const DevPass 
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, k_pass<T, C, X2>, P, (const LayerState *)w.st, w.Y[0], w.Y[1], alive,
+  cudaLaunchKernelEx(&cfg, k_pass<T, C, X2, NB>, P, (const LayerState *)w.st, w.Y[0], w.Y[1], alive,
                      (int64_t)w.words, (int64_t)w.stride, ymax);
 }
 
@@ -1496,10 +1520,10 @@ void launch_pass(const LaunchCfg &c, const Workspace &w, const DevPass &P, uint3
     return e && atoi(e) != 0;
   }();
   const bool x2 = P.C > 1 || x2_c1;
-  switch (P.C * 1024 + P.T + (x2 ? 4096 * 4 : 0)) {
-#define X(TT, CC, XX)                                        \
-  case CC * 1024 + TT + (XX ? 4096 * 4 : 0):                 \
-    launch_pass_t<TT, CC, XX>(c, w, P, alive, ymax, s);      \
+  switch (P.C * 1024 + P.T + (x2 ? 4096 * 4 : 0) + P.NB * 4096 * 8) {
+#define X(TT, CC, XX, NN)                                               \
+  case CC * 1024 + TT + (XX ? 4096 * 4 : 0) + NN * 4096 * 8:            \
+    launch_pass_t<TT, CC, XX, NN>(c, w, P, alive, ymax, s);             \
     return;
     SDNN_PASS_VARIANTS(X)
 #undef X

@@ -232,6 +232,13 @@ int pack_layer(int32_t n, const LayerIn &in, const float *bias, bool allow_group
           out.val[((size_t)g * kmax + t) * gmax + q] = cval[cptr[m[q]] + t];
     }
   }
+  // per-group member biases (contiguous per group: staged by TMA next to the
+  // weights in k_layer_bulkw)
+  if (!out.uniform) {
+    out.gbias.assign((size_t)G * std::max(gmax, 1), 0.f);
+    for (int32_t g = 0; g < G; ++g)
+      for (int32_t q = 0; q < out.gg[g]; ++q) out.gbias[(size_t)g * gmax + q] = bias[out.col[(size_t)g * gmax + q]];
+  }
   return SDNN_OK;
 }
 

@@ -43,6 +43,7 @@ struct PackedLayer {
   std::vector<int32_t> gg;    // [ngroups] G_g
   std::vector<float> val;     // [ngroups][kmax][gmax] (empty if uniform)
   std::vector<float> bias;    // [n]
+  std::vector<float> gbias;   // [ngroups][gmax] bias of each member (non-uniform layers only)
 };
 
 struct LayerIn {              // mirrors sdnn_layer
@@ -72,6 +73,7 @@ struct DevLayer {
   const int32_t *gg;     // [ngroups]
   const float *val;      // [ngroups][kmax][gmax], nullptr if uniform
   const float *bias;     // [n]
+  const float *gbias;    // [ngroups][gmax] member biases (non-uniform layers), else nullptr
   int32_t ngroups, kmax, gmax;
   float wu;
   int32_t uniform;
@@ -138,6 +140,7 @@ struct PassHostLayer {
 struct PassHost {
   int32_t a = 0, m = 0, ncomp = 0, rin = 0, R = 0, T = 0;
   int32_t C = 1;                       // CTAs per component (cluster size; rows/records per [comp][bin])
+  int32_t NB = 1;                      // tile buffers per CTA (2: T for a half tile, double-buffered)
   std::vector<int32_t> in_rows;        // [ncomp][rin]  global neuron ids at boundary a
   std::vector<int32_t> in_count;       // [ncomp]
   std::vector<PassHostLayer> layers;   // [m]
@@ -172,6 +175,7 @@ struct DevPass {
   int32_t lg_in, lg_out;               // yblk: log2 positions per block at the input / output
                                        // boundary (5; 4 where a T = 16 pass reads)
   int32_t pf;                          // yblk: L2-prefetch the tiles of the next pf items
+  int32_t NB;                          // tile buffers per CTA (2: half-size tiles, double-buffered)
   const int32_t *in_rows, *in_count;
   const unsigned char *rec;            // [ncomp][rec_bytes]
   PassLayerDev layers[kMaxPassLayers]; // by value: the kernel parameter carries them
@@ -252,7 +256,7 @@ void launch_layer(const LaunchCfg &c, const Workspace &w, const DevLayer &L, int
                   uint32_t *alive, float ymax, cudaStream_t s, uint32_t *sat = nullptr);
 bool layer_tracks_saturation(const LaunchCfg &c, const DevLayer &L);
 int pass_tile_floats();        // smem floats per component tile (tile T = this / R)
-bool pass_variant(int T, int C);   // a k_pass instance exists for tile T and cluster size C
+bool pass_variant(int T, int C, int NB = 1);   // a k_pass instance exists for tile T, cluster C, NB buffers
 // a fused pass: reads st[P.a], liveness of layer a+j to alive + j*words
 void launch_pass(const LaunchCfg &c, const Workspace &w, const DevPass &P, uint32_t *alive,
                  float ymax, cudaStream_t s);

@@ -1,26 +1,27 @@
-"""f1: launch-path study on B200 -- the paper's only LSDNN
-GPU-side claims are that a cudaFlow (one CUDA graph of the whole GPU task graph)
-beats stream-based execution, 1.5x at one GPU (PAPER.md:2862-2866,
-fig::dnn_cudaflow_overhead), and that the capturer (Algorithm 1)
+"""f1: launch-path study on B200.
+
+The paper's only LSDNN GPU-side claims are that a cudaFlow (one CUDA graph of
+the whole GPU task graph) beats stream-based execution, 1.5x at one GPU
+(PAPER.md:2862-2866), and that the capturer (Algorithm 1)
 with 2-4 streams is about as fast as the cudaFlow.
 
-Same kernels, launched four ways:
-  graph        one inference = one captured CUDA graph (the library default)
-  loop         one inference = a plain stream loop of the same kernels
-               (SDNN_F_NO_GRAPH)
-  streams-k    the batch split into S independent chains (S handles), chains
-               round-robined over k streams, plain launches
-  capturer-k   the same S chains captured into ONE graph with Algorithm 1's
-               stream assignment: levelize (chain c's i-th operation is at
-               level i), stream = id-in-level mod max_streams = c mod k, events
-               only on cross-stream edges (fork/join), then replayed
+The task graph is the library's real one (sdnn_flow_infer): the batch split
+into P partitions, each on its own handle, per partition densify -> every
+kernel of the layer chain -> readout into its slice of the global category
+bitmask, joined by the device decode.  Launched as
+  graph        explicit DAG (the cudaFlow analogue)
+  capturer-k   Algorithm 1 with max_streams = k, captured into one graph
+  streams-k    Algorithm 1's stream assignment launched directly (no graph)
+plus, for reference, the single-handle inference (one captured graph, and the
+same kernels as a plain stream loop, SDNN_F_NO_GRAPH).  Every mode's category
+ids are compared with the single-handle result (the GPU tests compare them
+with the oracle).
 
-Run on the GPU box:  python tools/f1_launch_study.py [c1|c2] [S]
+Run on the GPU box:  python tools/f1_launch_study.py [c1|c2|c3] [P]
 """
 import json
 import os
 import sys
-import time
 
 import numpy as np
 import torch
@@ -33,79 +34,53 @@ from paper_2004_10908_b200 import dist as sdist  # noqa: E402
 CONFIGS = {"c1": (1024, 120, 1000), "c2": (4096, 480, 60000), "c3": (16384, 1920, 60000)}
 
 
-def timed(fn, reps=5, warm=2):
-    for _ in range(warm):
-        fn()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ts = []
-    for _ in range(reps):
-        torch.cuda.synchronize()
-        e0.record()
-        fn()
-        e1.record()
-        torch.cuda.synchronize()
-        ts.append(e0.elapsed_time(e1))
-    return float(np.median(ts))
-
-
 def main():
     cfg = sys.argv[1] if len(sys.argv) > 1 else "c1"
-    S = int(sys.argv[2]) if len(sys.argv) > 2 else 4
+    P = int(sys.argv[2]) if len(sys.argv) > 2 else 4
     n, L, B = CONFIGS[cfg]
+    dev = torch.device("cuda", 0)
     spec = g.rn_spec(n, L)
     rp, idx = g.ms_inputs(n, B)
-    dev = torch.device("cuda", 0)
-    res = {"config": cfg, "chains": S}
-    # the layer chain alone (the resident tail would hide the launch structure)
-    common = dict(fmt="ell", threads=8, flags=sd.SDNN_F_NO_RESIDENT)
     rp_t, idx_t = torch.from_numpy(rp).to(dev), torch.from_numpy(idx).to(dev)
-    for name, flags in (("graph", 0), ("loop", sd.SDNN_F_NO_GRAPH)):
-        net = sd.Net.from_spec(spec, **dict(common, flags=common["flags"] | flags))
-        alive = torch.zeros((B + 31) // 32, dtype=torch.int32, device=dev)
-        res[name] = timed(lambda: net.infer_torch(rp_t, idx_t, None, alive_t=alive))
-        res[name + "_launches"] = net.stats()["launches_per_infer"]
-        net.close()
-    # S independent chains (batch partition) on k streams, and the capturer
+    out = {"config": cfg, "partitions": P}
+    # single handle: one captured graph vs the same kernels as a stream loop
+    ref = None
+    for name, flags in (("single-graph", 0), ("single-loop", sd.SDNN_F_NO_GRAPH)):
+        with sd.Net.from_spec(spec, fmt="ell", flags=flags | sd.SDNN_F_NO_RESIDENT) as net:
+            for _ in range(2):
+                a = net.infer_torch(rp_t, idx_t)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(5):
+                a = net.infer_torch(rp_t, idx_t)
+            e1.record()
+            torch.cuda.synchronize()
+            out[name] = round(e0.elapsed_time(e1) / 5, 3)
+            ids = sd.bitmask_to_ids(a.cpu().numpy(), B)
+            ref = ids if ref is None else ref
+            assert np.array_equal(ids, ref)
+            out[name + "_launches"] = net.stats()["launches_per_infer"]
+    nets = [sd.Net.from_spec(spec, fmt="ell", flags=sd.SDNN_F_NO_RESIDENT) for _ in range(P)]
     parts = []
-    for c in range(S):
-        lo, hi = sdist.partition(B, S, c)
-        p_rp, p_idx, _ = sdist.slice_csr(rp, idx, None, lo, hi)
-        net = sd.Net.from_spec(spec, **dict(common, flags=common["flags"] | sd.SDNN_F_NO_GRAPH))
-        parts.append((net, torch.from_numpy(p_rp).to(dev), torch.from_numpy(np.ascontiguousarray(p_idx)).to(dev),
-                      torch.zeros(max(1, (hi - lo + 31) // 32), dtype=torch.int32, device=dev)))
-    streams = [torch.cuda.Stream(dev) for _ in range(8)]
-
-    def run_k(k):
-        main_s = torch.cuda.current_stream(dev)
-        for s in streams[:k]:
-            s.wait_stream(main_s)
-        for c, (net, a, b_, al) in enumerate(parts):
-            s = streams[c % k]
-            net.infer_torch(a, b_, None, alive_t=al, stream=s)
-        for s in streams[:k]:
-            main_s.wait_stream(s)
-
-    for k in (1, 2, 4):
-        if k <= S:
-            res[f"streams-{k}"] = timed(lambda: run_k(k))
-    for k in (1, 2, 4, 8):
-        run_k(min(k, S))                          # warm: plans + workspaces exist
-        torch.cuda.synchronize()
-        graph = torch.cuda.CUDAGraph()
-        cap = torch.cuda.Stream(dev)
-        with torch.cuda.stream(cap):
-            graph.capture_begin()
-            # Algorithm 1: chain c's operations -> stream (c mod max_streams);
-            # fork/join events are the only cross-stream edges
-            run_k(min(k, S))
-            graph.capture_end()
-        res[f"capturer-{k}"] = timed(lambda: graph.replay())
-        del graph
-    for net, *_ in parts:
-        net.close()
-    res["graph_over_loop"] = res["loop"] / res["graph"]
-    print(json.dumps(res))
+    for r in range(P):
+        lo, hi = sdist.partition(B, P, r)
+        srp, sidx, _ = sdist.slice_csr(rp, idx, None, lo, hi)
+        parts.append((torch.from_numpy(srp).to(dev), torch.from_numpy(np.ascontiguousarray(sidx)).to(dev), lo))
+    ids, ms, nt = sd.flow_infer(nets, parts, B, sd.SDNN_FLOW_GRAPH, 1, reps=5)
+    assert np.array_equal(ids, ref)
+    out["tasks"] = nt
+    out["graph"] = round(ms, 3)
+    for mode, name in ((sd.SDNN_FLOW_CAPTURER, "capturer"), (sd.SDNN_FLOW_STREAMS, "streams")):
+        for k in (1, 2, 4, 8):
+            ids, ms, _ = sd.flow_infer(nets, parts, B, mode, k, reps=5)
+            assert np.array_equal(ids, ref), (name, k)
+            out[f"{name}-{k}"] = round(ms, 3)
+    for x in nets:
+        x.close()
+    out["graph_over_best_streams"] = round(min(out[f"streams-{k}"] for k in (1, 2, 4, 8)) / out["graph"], 3)
+    out["single_graph_over_loop"] = round(out["single-loop"] / out["single-graph"], 3)
+    print(json.dumps(out), flush=True)
 
 
 if __name__ == "__main__":

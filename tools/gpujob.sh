@@ -47,7 +47,7 @@ for R in "$@"; do
               python tools/ncu_summary.py launches gpurun_out/${TAG}_launches_$A.csv 2>&1 | head -12 ;;
     full) timeout 1200 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
             -k "regex:$B" -s "${C:-60}" -c 1 -o gpurun_out/${TAG}_full_${A}_$(echo "$B" | tr -cd 'a-z0-9_') \
-            python bench.py --config $A --oneshot --steps 1 --warmup 0 > gpurun_out/${TAG}_full.log 2>&1
+            python bench.py --config $A --oneshot --steps 1 --warmup 0 ${FULLARGS:-} > gpurun_out/${TAG}_full.log 2>&1
           echo "full $A $B: $(ls gpurun_out/${TAG}_full_${A}_*.ncu-rep 2>/dev/null | tail -1)" ;;
     sanitize) timeout 1200 python tools/sanitize_run.py > gpurun_out/${TAG}_sanitize.log 2>&1
               tail -5 gpurun_out/${TAG}_sanitize.log ;;
