@@ -264,8 +264,24 @@ def run_gpu(args):
 
     gB = B if strong else batch * ws                  # rows of the global bitmask
     gev = []                                          # (before, after) the collective, per timed step
+    # f4: the gather fused into the readout over NVLS multicast when the group
+    # has one (--gather auto), else / with --gather nccl the NCCL all-gather
+    nvg = None
+    if ws > 1 and args.gather != "nccl" and dist.get_backend() == "nccl":
+        try:
+            nvg = sdist.NvlsGather(words * ws, device=dev)
+        except Exception as e:                        # no multicast mapping
+            if args.gather == "nvls":
+                raise
+            print(f"NVLS gather unavailable ({e}); NCCL all-gather", file=sys.stderr)
+    lo_row = sdist.partition(B, ws, rank)[0] if strong else rank * batch
 
     def step(timed=False):
+        if nvg is not None:
+            nv, allw = nvg.params(lo_row // 32)
+            net.infer_torch_nvls(rp_t, idx_t, nv, stream=stream)
+            sdist.decode_device(allw, gB, stream)
+            return
         net.infer_torch(rp_t, idx_t, None, alive_t=alive_view, stream=stream)
         if ws > 1:
             if timed:
@@ -297,14 +313,17 @@ def run_gpu(args):
     layer_ms = net.layer_times()                     # per-layer kernel durations, last step
     multi = None
     if ws > 1:
-        gms = sum(a.elapsed_time(b) for a, b in gev) / max(1, len(gev))
+        gms = sum(a.elapsed_time(b) for a, b in gev) / max(1, len(gev)) if gev else None
         got = [None] * ws
         dist.all_gather_object(got, [ms, gms])
-        allt = np.array(got, np.float64).reshape(ws, 2)
+        allt = np.array([[x if x is not None else np.nan for x in r] for r in got], np.float64).reshape(ws, 2)
         per_rank = allt[:, 0].tolist()
         ms = float(allt[:, 0].max())
         multi = {"per_rank_ms": per_rank, "imbalance_max_over_mean": ms / float(np.mean(per_rank)),
-                 "allgather_ms_per_step": float(allt[:, 1].max()),
+                 "allgather_ms_per_step": (float(np.nanmax(allt[:, 1])) if nvg is None else None),
+                 "gather": ("nvls: readout kernel stores the category words through the multicast "
+                            "mapping (multimem.st) + arrival counter (k_readout_nvls)" if nvg is not None
+                            else "nccl all_gather_into_tensor"),
                  "rows_per_rank": [int(min(B, (r + 1) * sdist.chunk_rows(B, ws)) - min(B, r * sdist.chunk_rows(B, ws)))
                                    for r in range(ws)] if strong else [batch] * ws,
                  "collective": "torch.distributed.all_gather_into_tensor (NCCL) of ceil(rows/32) "
@@ -464,6 +483,9 @@ def main():
     ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
                     help="N > 1: strong = the one 60,000-input batch split across ranks "
                          "(BASELINE configs[3], default); weak = every rank its own batch")
+    ap.add_argument("--gather", default="auto", choices=["auto", "nccl", "nvls"],
+                    help="N > 1: category gather fused into the readout over NVLS (auto: when the "
+                         "group has a multicast mapping) or the NCCL all-gather")
     ap.add_argument("--net", default="rn", choices=sorted(NETS),
                     help="network family: rn = RadiX-Net-shaped (headline); rn-plain, rw, rr = robustness rows")
     ap.add_argument("--e2e-steps", type=int, default=3)

@@ -200,6 +200,37 @@ sdnn_status sdnn_infer_device(sdnn_net *net, const int64_t *d_rowptr, const int3
 sdnn_status sdnn_gather_rows(sdnn_net *net, const int32_t *d_rows, int64_t nrows, float *d_y,
                              void *stream);
 
+/* f4: sdnn_infer_device with the category readout fused with the
+ * cross-GPU gather over NVLink SHARP (NVLS multicast), replacing the separate
+ * NCCL all-gather: the readout kernel builds this rank's words in its slice of
+ * a symmetric bitmask buffer, writes each word through the buffer's
+ * MULTICAST mapping with multimem.st (one store reaches every GPU's copy),
+ * adds 1 to a multicast arrival counter (release) and waits until the local
+ * copy of the counter reaches `target`.  On return of the enqueued work every
+ * GPU's local_words holds the whole global bitmask (decode it with
+ * sdnn_bitmask_to_ids).  The buffers come from the caller (e.g. torch
+ * symmetric memory with NVLS multicast, paper_2004_10908_b200/dist.py
+ * NvlsGather); the ranks' slices are word-aligned (dist.partition).
+ *   local_words  unicast VA of this GPU's copy of the global bitmask
+ *   mc_words     multicast VA of the same buffer
+ *   local_flag / mc_flag  unicast / multicast VA of a uint32 arrival counter that
+ *                every rank increments once per call (never reset)
+ *   word_offset  this rank's first word; target = (calls so far) x world size.
+ * Reuse of a word buffer must alternate (two buffers by call parity): a rank
+ * may start its next call while another still decodes this one.  Needs >= 1
+ * layer; not with SDNN_F_SATURATE.  Asynchronous on `stream`. */
+typedef struct sdnn_nvls {
+  uint32_t *local_words;
+  uint32_t *mc_words;
+  uint32_t *local_flag;
+  uint32_t *mc_flag;
+  int64_t word_offset;
+  uint32_t target;
+} sdnn_nvls;
+sdnn_status sdnn_infer_device_nvls(sdnn_net *net, const int64_t *d_rowptr, const int32_t *d_idx,
+                                   const float *d_val, int64_t batch, const sdnn_nvls *nv,
+                                   void *stream);
+
 /* Multi-GPU readout (no handle needed): decode a global category bitmask --
  * e.g. the NCCL all-gather of every rank's d_alive words, rows partitioned in
  * word-aligned contiguous slices (paper_2004_10908_b200/dist.py; the per-GPU

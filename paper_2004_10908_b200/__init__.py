@@ -35,7 +35,7 @@ EXPORTS = ["sdnn_create", "sdnn_create_empty", "sdnn_set_layer", "sdnn_infer",
            "sdnn_infer_device", "sdnn_stats_get", "sdnn_validate_layer", "sdnn_destroy",
            "sdnn_last_error", "sdnn_abi_version", "sdnn_layer_times", "sdnn_plan_steps",
            "sdnn_step_plan", "sdnn_gather_rows", "sdnn_bitmask_to_ids",
-           "sdnn_flow_infer"]
+           "sdnn_flow_infer", "sdnn_infer_device_nvls"]
 
 
 class SdnnError(RuntimeError):
@@ -69,6 +69,12 @@ SDNN_FLOW_GRAPH, SDNN_FLOW_CAPTURER, SDNN_FLOW_STREAMS = 0, 1, 2
 class sdnn_flow_part(ctypes.Structure):
     _fields_ = [("d_rowptr", ctypes.c_void_p), ("d_idx", ctypes.c_void_p), ("d_val", ctypes.c_void_p),
                 ("batch", ctypes.c_int64), ("word_offset", ctypes.c_int64)]
+
+
+class sdnn_nvls(ctypes.Structure):
+    _fields_ = [("local_words", ctypes.c_void_p), ("mc_words", ctypes.c_void_p),
+                ("local_flag", ctypes.c_void_p), ("mc_flag", ctypes.c_void_p),
+                ("word_offset", ctypes.c_int64), ("target", ctypes.c_uint32)]
 
 
 class sdnn_stats(ctypes.Structure):
@@ -111,6 +117,7 @@ def lib() -> ctypes.CDLL:
         L.sdnn_step_plan.argtypes = [V, V, P(I32)]
         L.sdnn_gather_rows.argtypes = [V, V, I64, V, V]
         L.sdnn_bitmask_to_ids.argtypes = [V, I64, V, V, V]
+        L.sdnn_infer_device_nvls.argtypes = [V, V, V, V, I64, P(sdnn_nvls), V]
         L.sdnn_flow_infer.argtypes = [V, I32, P(sdnn_flow_part), V, I64, V, V, I32, I32, I32,
                                       P(ctypes.c_float), P(I32)]
         L.sdnn_destroy.argtypes = [V]
@@ -121,7 +128,7 @@ def lib() -> ctypes.CDLL:
         for name in ["sdnn_create", "sdnn_create_empty", "sdnn_set_layer", "sdnn_infer",
                      "sdnn_infer_device", "sdnn_stats_get", "sdnn_validate_layer",
                      "sdnn_layer_times", "sdnn_plan_steps", "sdnn_step_plan", "sdnn_gather_rows",
-                     "sdnn_bitmask_to_ids", "sdnn_flow_infer"]:
+                     "sdnn_bitmask_to_ids", "sdnn_flow_infer", "sdnn_infer_device_nvls"]:
             getattr(L, name).restype = I32
         _LIB = L
     return _LIB
@@ -349,6 +356,15 @@ class Net:
         y = self.gather_rows_torch(rows_t)
         torch.cuda.synchronize(dev)
         return y.cpu().numpy()
+
+    def infer_torch_nvls(self, rowptr_t, idx_t, nv: "sdnn_nvls", stream=None):
+        """sdnn_infer_device_nvls: inference + readout fused with the NVLS
+        multicast gather into every GPU's copy of the global bitmask."""
+        import torch
+        batch = rowptr_t.numel() - 1
+        s = stream if stream is not None else torch.cuda.current_stream(rowptr_t.device)
+        _check(lib().sdnn_infer_device_nvls(self.h, rowptr_t.data_ptr(), idx_t.data_ptr() if idx_t.numel() else None,
+                                            None, batch, ctypes.byref(nv), s.cuda_stream))
 
     def stats(self):
         return sdnn_stats_get(self.h, self.L)

@@ -762,7 +762,8 @@ sdnn_status prepare_infer(sdnn_net *net, int64_t batch) {
 using Feed = std::function<sdnn_status(cudaStream_t)>;
 sdnn_status infer_device_impl(sdnn_net *net, const int64_t *d_rowptr, const int32_t *d_idx,
                               const float *d_val, int64_t batch, uint32_t *d_alive,
-                              float *d_yout, cudaStream_t s, const Feed *feed = nullptr) {
+                              float *d_yout, cudaStream_t s, const Feed *feed = nullptr,
+                              const sdnn_nvls *nv = nullptr) {
   sdnn_status st = prepare_infer(net, batch);
   if (st) return st;
   const bool compact = compact_enabled(net);
@@ -782,7 +783,13 @@ sdnn_status infer_device_impl(sdnn_net *net, const int64_t *d_rowptr, const int3
     if (st) return st;
     launches += net->chain_launches;
   }
-  if (net->L == 0) {
+  if (nv) {                                      // f4: fused NVLS gather (L >= 1, checked by the caller)
+    const int si = (int)net->steps.size() - 1;
+    const Step &S = net->steps[si];
+    const int row = S.pass == kResidentStep ? 0 : S.m - 1;
+    launch_readout_nvls(net->ws, S.a, net->ws.alive_row(si, row), batch, nv->local_words + nv->word_offset,
+                        nv->mc_words + nv->word_offset, nv->local_flag, nv->mc_flag, nv->target, s);
+  } else if (net->L == 0) {
     launch_readout(net->ws, 0, net->ws.alive_row(0, 0), d_alive, batch, s);
   } else {
     const int si = (int)net->steps.size() - 1;
@@ -1461,6 +1468,20 @@ sdnn_status sdnn_infer(sdnn_net *net, const int64_t *y0_rowptr, const int32_t *y
   *n_categories = ncat;
   net->last_ncat = ncat;
   return SDNN_OK;
+}
+
+sdnn_status sdnn_infer_device_nvls(sdnn_net *net, const int64_t *d_rowptr, const int32_t *d_idx,
+                                   const float *d_val, int64_t batch, const sdnn_nvls *nv, void *stream) {
+  if (!net || !nv) return fail(SDNN_E_ARG, "NULL argument");
+  if (batch < 0 || batch > (int64_t(1) << 30)) return fail(SDNN_E_ARG, "batch out of range");
+  if (!d_rowptr || !nv->local_words || !nv->mc_words || !nv->local_flag || !nv->mc_flag || nv->word_offset < 0)
+    return fail(SDNN_E_ARG, "NULL argument");
+  if (net->L < 1) return fail(SDNN_E_UNSUPPORTED, "the NVLS readout needs >= 1 layer");
+  if (net->opts.flags & SDNN_F_SATURATE) return fail(SDNN_E_UNSUPPORTED, "NVLS readout with SDNN_F_SATURATE");
+  sdnn_status st = set_device(net);
+  if (st) return st;
+  return infer_device_impl(net, d_rowptr, d_idx, d_val, batch, nullptr, nullptr, (cudaStream_t)stream,
+                           nullptr, nv);
 }
 
 sdnn_status sdnn_bitmask_to_ids(const uint32_t *d_words, int64_t batch, int32_t *d_ids, int32_t *d_n,

@@ -1252,6 +1252,59 @@ __global__ void __launch_bounds__(1024) k_list_bits(const uint32_t *__restrict__
   if (threadIdx.x == 0) *ncat = (int32_t)total;
 }
 
+// f4: readout fused with the cross-GPU gather over NVLink
+// SHARP / NVLS.  The rank's category words are built in its slice of the
+// symmetric bitmask buffer (unicast view), then every word is written with
+// multimem.st through the multicast view -- one store lands in every GPU's
+// copy -- and the CTA announces itself with a release multimem add on an
+// arrival counter; it returns once the counter shows every rank (target =
+// epoch x world), so the local copy then holds the whole global bitmask.
+// Single CTA (like k_readout).
+__global__ void __launch_bounds__(1024) k_readout_nvls(const LayerState *__restrict__ st, int a,
+                                                       const uint32_t *__restrict__ alive,
+                                                       const int32_t *ridA, const int32_t *ridB,
+                                                       int64_t batch, uint32_t *local_words,
+                                                       uint32_t *mc_words, uint32_t *local_flag,
+                                                       uint32_t *mc_flag, uint32_t target) {
+  const LayerState S = st[a];
+  const int64_t words = ((int64_t)S.width + 31) >> 5, out_words = (batch + 31) >> 5;
+  const int32_t *rid = S.rid ? ridB : ridA;
+  for (int64_t q = threadIdx.x; q < out_words; q += blockDim.x) local_words[q] = 0u;
+  __syncthreads();
+  for (int64_t q = threadIdx.x; q < words; q += blockDim.x) {
+    uint32_t bits = alive[q];
+    while (bits) {
+      const int b = __ffs(bits) - 1;
+      bits &= bits - 1;
+      const int32_t id = rid[q * 32 + b];
+      atomicOr(&local_words[id >> 5], 1u << (id & 31));
+    }
+  }
+  __syncthreads();
+  for (int64_t q = threadIdx.x; q < out_words; q += blockDim.x) {
+    const uint32_t v = *((volatile uint32_t *)local_words + q);
+    asm volatile("multimem.st.relaxed.sys.global.b32 [%0], %1;" ::"l"(mc_words + q), "r"(v) : "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    asm volatile("multimem.red.release.sys.global.add.u32 [%0], %1;" ::"l"(mc_flag), "r"(1u) : "memory");
+    uint32_t seen = 0;
+    do {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(seen) : "l"(local_flag) : "memory");
+      if (seen < target) __nanosleep(64);
+    } while (seen < target);
+  }
+  __syncthreads();
+}
+
+void launch_readout_nvls(const Workspace &w, int32_t a, const uint32_t *alive_last, int64_t batch,
+                         uint32_t *local_words, uint32_t *mc_words, uint32_t *local_flag, uint32_t *mc_flag,
+                         uint32_t target, cudaStream_t s) {
+  k_readout_nvls<<<1, 1024, 0, s>>>(w.st, a, alive_last, w.rid[0], w.rid[1], batch, local_words, mc_words,
+                                    local_flag, mc_flag, target);
+}
+
 // Multi-GPU readout: the all-gathered global bitmask -> ascending row ids
 // (single CTA: popcount scan over the words, then each thread lists its run)
 __global__ void __launch_bounds__(1024) k_bitmask_ids(const uint32_t *__restrict__ words, int64_t batch,

@@ -279,6 +279,10 @@ void launch_readout(const Workspace &w, int32_t a, const uint32_t *alive_last,
 // Y_L: final_out = the output buffer of the step entered with st[a] (L > 0), else Y_0
 void launch_yout(const Workspace &w, int32_t a, bool final_out, int32_t n, int64_t batch,
                  float *d_yout, cudaStream_t s);
+// f4: readout into the symmetric bitmask + multimem.st to every GPU + arrival wait
+void launch_readout_nvls(const Workspace &w, int32_t a, const uint32_t *alive_last, int64_t batch,
+                         uint32_t *local_words, uint32_t *mc_words, uint32_t *local_flag, uint32_t *mc_flag,
+                         uint32_t target, cudaStream_t s);
 // global category bitmask (batch bits) -> ascending ids, count in *d_n
 void launch_bitmask_ids(const uint32_t *d_words, int64_t batch, int32_t *d_ids, int32_t *d_n, cudaStream_t s);
 // Y_L rows of the given original row ids (same buffer selection as launch_yout)

@@ -60,6 +60,43 @@ def gather_bitmask(local_words, group=None):
     return torch.cat(parts).to(local_words.device)
 
 
+class NvlsGather:
+    """f4: the category gather fused into the readout kernel over NVLink SHARP
+    (sdnn_infer_device_nvls).  Two word buffers (alternating by call parity)
+    and an arrival counter live in one torch symmetric-memory allocation whose
+    multicast mapping the readout kernel stores through (multimem.st); the
+    all_gather_into_tensor path (gather_bitmask) is the checked equivalent.
+    Raises RuntimeError when the group has no multicast mapping (no NVLS)."""
+
+    def __init__(self, total_words: int, group=None, device=None):
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+        self.group = group or dist.group.WORLD
+        self.ws = dist.get_world_size(self.group)
+        self.dev = device or torch.device("cuda", torch.cuda.current_device())
+        self.nw = int(total_words)
+        self.stride = -(-self.nw // 32) * 32                    # words per buffer (128 B aligned)
+        self.buf = symm.empty(2 * self.stride + 32, dtype=torch.int32, device=self.dev)
+        self.buf.zero_()
+        self.hdl = symm.rendezvous(self.buf, self.group.group_name)
+        if not getattr(self.hdl, "multicast_ptr", 0):
+            raise RuntimeError("no NVLS multicast mapping for this group")
+        self.hdl.barrier()
+        self.calls = 0
+
+    def params(self, word_offset: int):
+        """sdnn_nvls for the next call; returns (struct, the local word tensor it fills)."""
+        from paper_2004_10908_b200 import sdnn_nvls
+        b = self.calls % 2
+        self.calls += 1
+        base, mc = self.buf.data_ptr(), self.hdl.multicast_ptr
+        off, flag = 4 * b * self.stride, 4 * 2 * self.stride
+        nv = sdnn_nvls(base + off, mc + off, base + flag, mc + flag, int(word_offset),
+                       self.calls * self.ws)
+        return nv, self.buf[b * self.stride: b * self.stride + self.nw]
+
+
 def decode(words, batch: int) -> np.ndarray:
     """Host decode of global bitmask words -> ascending category ids (< batch);
     the CPU/gloo path (the GPU path decodes on the device, decode_device)."""
@@ -83,7 +120,7 @@ class Partitioned:
     arrive from (pinned) host memory each call (the end-to-end path); the
     staging tensors are allocated once."""
 
-    def __init__(self, net, batch: int, group=None, device=None):
+    def __init__(self, net, batch: int, group=None, device=None, nvls: Optional[bool] = None):
         import torch
         import torch.distributed as dist
         self.net, self.batch, self.group = net, int(batch), group
@@ -92,6 +129,15 @@ class Partitioned:
         self.dev = device or torch.device("cuda", torch.cuda.current_device())
         self.words = torch.zeros(words_per_rank(self.batch, self.ws), dtype=torch.int32, device=self.dev)
         self._rp = self._ix = None
+        # f4: fused NVLS gather when asked (nvls=True) or, by default, when the
+        # group has a multicast mapping; otherwise the NCCL all-gather
+        self.nvls = None
+        if nvls is not False and dist.get_backend(group) == "nccl":
+            try:
+                self.nvls = NvlsGather(words_per_rank(self.batch, self.ws) * self.ws, group, self.dev)
+            except Exception:
+                if nvls:
+                    raise
 
     def slice(self, rowptr, idx):
         return slice_csr(rowptr, idx, None, self.lo, self.hi)[:2]
@@ -110,11 +156,15 @@ class Partitioned:
             rp_t.copy_(torch.from_numpy(rp_local), non_blocking=True)
             if idx_local.size:
                 ix_t[:idx_local.size].copy_(torch.from_numpy(idx_local), non_blocking=True)
-            self.words.zero_()
-            if self.hi > self.lo:
-                self.net.infer_torch(rp_t, ix_t, None, alive_t=self.words[: (self.hi - self.lo + 31) // 32],
-                                     stream=s)
-            allw = gather_bitmask(self.words, self.group)
+            if self.nvls is not None:
+                nv, allw = self.nvls.params(self.lo // 32)
+                self.net.infer_torch_nvls(rp_t, ix_t, nv, stream=s)
+            else:
+                self.words.zero_()
+                if self.hi > self.lo:
+                    self.net.infer_torch(rp_t, ix_t, None, alive_t=self.words[: (self.hi - self.lo + 31) // 32],
+                                         stream=s)
+                allw = gather_bitmask(self.words, self.group)
             ids, cnt = decode_device(allw, self.batch, s)
             n = int(cnt.item())                                  # D2H: the count, then the ids
             return ids[:n].cpu().numpy()

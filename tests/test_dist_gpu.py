@@ -156,3 +156,58 @@ def test_bench_two_ranks_strong_scaling(tmp_path):
     assert len(m["per_rank_ms"]) == 2 and m["imbalance_max_over_mean"] >= 1.0
     assert m["rows_per_rank"] == [512, 488]
     assert line["e2e"]["value"] > 0
+
+
+def _worker_nvls(port, q):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2004_10908_b200 as sd
+    import sdnngen as g
+    from paper_2004_10908_b200 import dist as sdist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+    try:
+        n, L, B = 1024, 30, 999
+        spec = g.rn_spec(n, L)
+        rp, idx = g.ms_inputs(n, B, seed=5)
+        rp_t, idx_t = torch.from_numpy(rp).to(dev), torch.from_numpy(idx).to(dev)
+        try:
+            nvg = sdist.NvlsGather((B + 31) // 32, device=dev)
+        except Exception as e:                              # no multicast on this box
+            q.put(("skip", repr(e)))
+            return
+        out = []
+        with sd.Net.from_spec(spec, fmt="ell", threads=4, device=0) as net:
+            ref = net.infer_torch(rp_t, idx_t).clone()
+            for _ in range(3):                              # both buffers, counter epochs 1..3
+                nv, allw = nvg.params(0)
+                net.infer_torch_nvls(rp_t, idx_t, nv)
+                ids, cnt = sdist.decode_device(allw, B)
+                torch.cuda.synchronize()
+                out.append(ids[: int(cnt.item())].cpu().numpy().tolist())
+        want = sd.bitmask_to_ids(ref.cpu().numpy(), B).tolist()
+        q.put(("ok", out, want))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_nvls_fused_readout_world1():
+    """f4: the readout kernel that stores the category words through the NVLS
+    multicast mapping (multimem.st) and waits on the arrival counter, with a
+    one-rank NCCL group (the only topology available here): the gathered
+    bitmask must equal the plain readout's, on three consecutive calls."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_worker_nvls, args=(_free_port(), q))
+    p.start()
+    res = q.get(timeout=600)
+    p.join(timeout=120)
+    if res[0] == "skip":
+        pytest.skip("no NVLS multicast mapping: " + res[1])
+    assert p.exitcode == 0
+    _, out, want = res
+    assert 0 < len(want) < 999
+    assert all(o == want for o in out)
