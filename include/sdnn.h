@@ -87,6 +87,10 @@ enum {
                                     (read back with sdnn_layer_times)                    */
   SDNN_F_NO_BULK = 1u << 6,      /* uniform layers: use the register-staged gather kernel
                                     instead of the TMA bulk-copy pipeline                */
+  SDNN_F_SHARE_VALUES = 1u << 9, /* fused passes: a layer with uniform weights and equal
+                                    biases stores one value per column group in shared
+                                    memory instead of one per member (exact; measured
+                                    slower on C4, so opt-in)                             */
   SDNN_F_SATURATE = 1u << 8      /* f2 (reported separately): a row whose
                                     every output equals YMAX before a suffix of layers
                                     that map all-YMAX rows to all-YMAX rows (checked per

@@ -29,7 +29,7 @@ SDNN_E_NOMEM, SDNN_E_CUDA, SDNN_E_STATE = -4, -5, -6
 SDNN_W_CSR, SDNN_W_ELLCOL = 0, 1
 SDNN_F_NO_COMPACT, SDNN_F_NO_GROUPS, SDNN_F_NO_GRAPH = 1, 2, 4
 SDNN_F_NO_RESIDENT, SDNN_F_TRUST_INPUT, SDNN_F_PROFILE, SDNN_F_NO_BULK = 8, 16, 32, 64
-SDNN_F_SATURATE = 256
+SDNN_F_SATURATE, SDNN_F_SHARE_VALUES = 256, 512
 
 EXPORTS = ["sdnn_create", "sdnn_create_empty", "sdnn_set_layer", "sdnn_infer",
            "sdnn_infer_device", "sdnn_stats_get", "sdnn_validate_layer", "sdnn_destroy",

@@ -422,7 +422,7 @@ sdnn_status make_plan(sdnn_net *net) {
     const int cap = sat ? 0 : std::min(net->opts.fuse_rows < 0 ? kDefaultPassRows : net->opts.fuse_rows,
                                        cta * kMaxPassCluster);
     net->steps = plan_passes(head, net->n, cap, maxm, pass_tile_floats(), nthreads_default(), &ph, cta,
-                             blocked);
+                             blocked, (net->opts.flags & SDNN_F_SHARE_VALUES) != 0);
   };
   plan_for(want_yblk);
   if (want_yblk) {
@@ -527,7 +527,9 @@ sdnn_status make_plan(sdnn_net *net) {
     D.NB = H.NB;
     D.rec_bytes = H.rec_bytes;
     D.yblk = net->yblk;
-    D.order = pass_order() >= 0 ? pass_order() : (H.T == 16 ? 0 : 1);
+    // tile-major pays when a pass has many components (C4: 128-512); with few
+    // (C2: 8-32) component-major was measured faster (18.4 vs 18.8 ms)
+    D.order = pass_order() >= 0 ? pass_order() : ((H.T == 16 || H.ncomp < 64) ? 0 : 1);
     D.lg_in = net->step_lg[q];
     D.lg_out = net->step_lg[q + 1];
     D.pf = net->yblk ? pf : 0;
@@ -544,7 +546,8 @@ sdnn_status make_plan(sdnn_net *net) {
     }
     for (int j = 0; j < H.m; ++j) {
       const PassHostLayer &HL = H.layers[j];
-      D.layers[j] = PassLayerDev{HL.off_kg, HL.off_src, HL.off_bias, HL.off_orow, HL.NG, HL.wu, HL.bu};
+      D.layers[j] = PassLayerDev{HL.off_kg, HL.off_src, HL.off_bias, HL.off_orow, HL.NG, HL.wu, HL.bu,
+                                 HL.off_vs};
     }
     net->steps[q].pass = (int32_t)net->passes.size();
     net->passes.push_back(D);

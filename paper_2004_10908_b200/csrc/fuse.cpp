@@ -295,8 +295,16 @@ std::vector<Step> plan_steps(const std::vector<const PackedLayer *> &layers, int
                         : plan_steps_greedy(layers, n, cap, max_m, cta_rows, a_begin);
 }
 
+static void build_pass_impl(const std::vector<const PackedLayer *> &layers, int32_t n, const Step &s,
+                            int tile_floats, int cta_rows, PassHost &out, bool allow_dedup);
+
 void build_pass(const std::vector<const PackedLayer *> &layers, int32_t n, const Step &s,
-                int tile_floats, int cta_rows, PassHost &out) {
+                int tile_floats, int cta_rows, PassHost &out, bool share_values) {
+  build_pass_impl(layers, n, s, tile_floats, cta_rows, out, share_values);
+}
+
+static void build_pass_impl(const std::vector<const PackedLayer *> &layers, int32_t n, const Step &s,
+                            int tile_floats, int cta_rows, PassHost &out, bool allow_dedup) {
   const int m = s.m;
   UF full, sub;
   full.init((int64_t)(m + 1) * n);
@@ -405,6 +413,25 @@ void build_pass(const std::vector<const PackedLayer *> &layers, int32_t n, const
       out.in_count[(size_t)c * C + b] = (int32_t)rows.size();
     }
   out.layers.resize(m);
+  // value sharing (SDNN_F_SHARE_VALUES, opt-in): in a layer with uniform
+  // weights whose member biases are all equal, every member of a group has
+  // bit-identical outputs, so a non-last layer stores the group's value once --
+  // into the slot of its source 0 when only this group reads it, else into a
+  // slot no group of the layer reads -- and the next layer's terms read that
+  // slot.  The chains are unchanged (same operands, same order); only the
+  // shared-memory stores drop by the group size.  Measured on C4: 2021 vs 1945
+  // ms/step (the 1024-row passes slow down: 3.92 vs 3.11 ms), so off by default.
+  const bool dedup_on = allow_dedup;
+  // A layer after a sharing layer reads shared slots, so it cannot overwrite its
+  // sources in place: it must share too (or be the last layer) -- decided from
+  // the back.
+  std::vector<char> dedup(m, 0);
+  for (int b = m - 2; b >= 0 && dedup_on; --b) {
+    const PackedLayer &p = *layers[s.a + b];
+    bool eq = p.uniform && p.gmax > 1;           // (groups of one member gain nothing)
+    for (int32_t j = 1; j < n && eq; ++j) eq = std::memcmp(&p.bias[j], &p.bias[0], 4) == 0;
+    dedup[b] = eq && (b + 1 == m - 1 || dedup[b + 1]);
+  }
   for (int b = 0; b < m; ++b) {
     const PackedLayer &p = *layers[s.a + b];
     const bool last = b == m - 1;
@@ -423,6 +450,7 @@ void build_pass(const std::vector<const PackedLayer *> &layers, int32_t n, const
     PassHostLayer &H = out.layers[b];
     H.NG = NG;
     H.wu = p.wu;
+    H.dedup = dedup[b];
     const size_t units = (size_t)ncomp * C;
     H.src.assign(units * NG * 32, 0);
     H.bias.assign(units * NG * 32, 0.f);
@@ -430,7 +458,14 @@ void build_pass(const std::vector<const PackedLayer *> &layers, int32_t n, const
     H.g.assign(units * NG, 0);
     if (last) H.orow.assign(units * NG * 32, 0);      // u16: N <= 65536
     const int64_t in0 = (int64_t)b * n, out0 = (int64_t)(b + 1) * n;
-    for (size_t cb = 0; cb < units; ++cb)
+    if (!last && dedup[b]) H.vs.assign(units * NG, 0);
+    // the input slots of this layer are exclusive to one group each unless the
+    // previous layer shared values (then several groups read one value slot)
+    const bool excl = b == 0 || !dedup[b - 1];
+    std::vector<char> live;
+    for (size_t cb = 0; cb < units; ++cb) {
+      if (!last && dedup[b] && !excl) live.assign(kMaxPassRows, 0);
+      std::vector<int32_t> code0(groups[cb].size());
       for (size_t q = 0; q < groups[cb].size(); ++q) {
         const int32_t g = groups[cb][q];
         const size_t rec = cb * NG + q;
@@ -443,16 +478,38 @@ void build_pass(const std::vector<const PackedLayer *> &layers, int32_t n, const
         for (int t = 0; t < K; ++t) {
           code[t] = slot[in0 + p.src[(size_t)g * p.kmax + t]];
           H.src[rec * 32 + t] = (uint16_t)(last ? code[t] : (code[t] & 0x3ff));
+          if (!live.empty()) live[code[t] & 0x3ff] = 1;
         }
+        code0[q] = K > 0 ? code[0] : 0;
         for (int u = 0; u < G; ++u) {
           const int32_t j = p.col[(size_t)g * p.gmax + u];
           H.bias[rec * 32 + u] = p.bias[j];
           if (last)
             H.orow[rec * 32 + u] = (uint16_t)j;
-          else                             // member u overwrites the slot of source u
+          else if (!dedup[b])                // member u overwrites the slot of source u
             slot[out0 + j] = code[u];
         }
       }
+      if (last || !dedup[b]) continue;
+      // shared values: one slot per group -- its own source-0 slot when the
+      // inputs are exclusive, else a slot no group of this layer reads
+      int32_t next_free = 0;
+      for (size_t q = 0; q < groups[cb].size(); ++q) {
+        const int32_t g = groups[cb][q];
+        int32_t vcode = code0[q];
+        if (!excl) {
+          while (next_free < R && live[next_free]) ++next_free;
+          if (next_free >= R) {                 // no free slot left: build without sharing
+            build_pass_impl(layers, n, s, tile_floats, cta_rows, out, false);
+            return;
+          }
+          vcode = (code0[q] & ~0x3ff) | next_free;
+          ++next_free;
+        }
+        H.vs[cb * NG + q] = (uint16_t)(vcode & 0x3ff);
+        for (int u = 0; u < p.gg[g]; ++u) slot[out0 + p.col[(size_t)g * p.gmax + u]] = vcode;
+      }
+    }
   }
   // ---- per-(component, bin) records ----
   // a layer whose members all carry the same bias (bitwise) stores it once (bu)
@@ -482,6 +539,11 @@ void build_pass(const std::vector<const PackedLayer *> &layers, int32_t n, const
     off += (H.NG * 2 + 15) / 16 * 16;
     H.off_src = off;
     off += H.NG * 64;
+    H.off_vs = -1;
+    if (!H.vs.empty()) {                          // shared-value slots (dedup), u16 per group
+      H.off_vs = off;
+      off += (H.NG * 2 + 15) / 16 * 16;
+    }
     H.off_bias = -1;
     if (!H.bias_uniform) {
       H.off_bias = off;
@@ -503,7 +565,8 @@ void build_pass(const std::vector<const PackedLayer *> &layers, int32_t n, const
       return !(e && atoi(e) == 1);
     }();
     const int T2 = std::max(16, std::min(512, tile_floats / 2 / Rp));
-    if (nb2 && C == 1 && Rp <= 128 && off <= ((kPassRecMax / 2) & ~15) && pass_variant(T2, 1, 2)) {
+    if (nb2 && C == 1 && Rp <= 128 && ncomp >= 256 && off <= ((kPassRecMax / 2) & ~15) &&
+        pass_variant(T2, 1, 2)) {                 // (C2's 32-component passes: 18.8 vs 18.4 ms without)
       out.NB = 2;
       out.T = T2;
     }
@@ -520,6 +583,7 @@ void build_pass(const std::vector<const PackedLayer *> &layers, int32_t n, const
         std::memcpy(r + H.off_kg + 2 * q, &kg, 2);
       }
       std::memcpy(r + H.off_src, H.src.data() + g0 * 32, (size_t)H.NG * 64);
+      if (H.off_vs >= 0) std::memcpy(r + H.off_vs, H.vs.data() + g0, (size_t)H.NG * 2);
       if (H.off_bias >= 0) std::memcpy(r + H.off_bias, H.bias.data() + g0 * 32, (size_t)H.NG * 128);
       if (H.off_orow >= 0) std::memcpy(r + H.off_orow, H.orow.data() + g0 * 32, (size_t)H.NG * 64);
     }
@@ -528,7 +592,8 @@ void build_pass(const std::vector<const PackedLayer *> &layers, int32_t n, const
 
 std::vector<Step> plan_passes(const std::vector<const PackedLayer *> &layers, int32_t n, int cap,
                               int max_m, int tile_floats, int threads,
-                              std::vector<PassHost> *built, int cta_rows, bool single_passes) {
+                              std::vector<PassHost> *built, int cta_rows, bool single_passes,
+                              bool share_values) {
   std::vector<Step> steps = plan_steps(layers, n, cap, max_m, cta_rows, 0);
   std::vector<PassHost> ph(steps.size());
   std::vector<char> done(steps.size(), 0);
@@ -546,7 +611,7 @@ std::vector<Step> plan_passes(const std::vector<const PackedLayer *> &layers, in
     for (int t = 0; t < nt && !todo.empty(); ++t)
       th.emplace_back([&] {
         for (int q = next++; q < (int)todo.size(); q = next++)
-          build_pass(layers, n, steps[todo[q]], tile_floats, cta_rows, ph[todo[q]]);
+          build_pass(layers, n, steps[todo[q]], tile_floats, cta_rows, ph[todo[q]], share_values);
       });
     for (auto &x : th) x.join();
     for (int i : todo) done[i] = 1;

@@ -1007,6 +1007,14 @@ __global__ void __launch_bounds__(32 * kPassNW, 3)
         const int64_t opos = (int64_t)tile * T + pofs;
         float *obase = blk ? Yout + (((opos >> lgo) * R) << lgo) + (opos & ((1 << lgo) - 1)) : Yout + opos;
         const int64_t rowmul = blk ? (1 << lgo) : stride;
+        if (!last && PL.off_vs >= 0) {
+          // shared value: one store per group into its value slot (the next
+          // layer's terms of every member of this group point there)
+          if (G > 0) {
+            const int32_t dst = reinterpret_cast<const uint16_t *>(rec_s + PL.off_vs)[gi] * sm;
+            *reinterpret_cast<float4 *>(tile_s + dst + pa) = yu;
+          }
+        } else {
 #pragma unroll
         for (int r = 0; r < EPL; ++r) {
           if (r * LPU >= gmax) break;
@@ -1022,6 +1030,7 @@ __global__ void __launch_bounds__(32 * kPassNW, 3)
               else *reinterpret_cast<float4 *>(tile_s + dst + pa) = y;
             }
           }
+        }
         }
         // liveness: lane sll of a segment holds positions sl*SW + 4 sll + e; word
         // w of the unit has bit b = position 32 w + b -> lane (32 w + b) / 4, e = b % 4

@@ -130,6 +130,9 @@ struct PassHostLayer {
   int32_t NG = 0;                      // group slots per component (max over components)
   float wu = 0.f;
   bool bias_uniform = false;           // every member's bias is bu (no bias array in the record)
+  bool dedup = false;                  // members share one value slot (uniform w, equal biases)
+  std::vector<uint16_t> vs;            // dedup: [ncomp][NG] value slot of each group
+  int32_t off_vs = -1;
   float bu = 0.f;
   int32_t off_kg = 0, off_src = 0, off_bias = 0, off_orow = -1;  // record byte offsets
   std::vector<uint16_t> src;           // [ncomp][NG][32] smem slots of the sources
@@ -153,18 +156,21 @@ struct PassHost {
 };
 constexpr int kPassRecMax = 10224;     // record bytes per component (3 CTAs per SM: 3 x 75 KB)
 void build_pass(const std::vector<const PackedLayer *> &layers, int32_t n, const Step &s,
-                int tile_floats, int cta_rows, PassHost &out);
+                int tile_floats, int cta_rows, PassHost &out, bool share_values = false);
 // plan_steps, build every fused pass; a pass whose record exceeds kPassRecMax
 // drops its last layer and the rest is planned again; `built[i]` is the
 // PassHost of steps[i] (m > 1, or m == 1 with single_passes; else m == 0)
 std::vector<Step> plan_passes(const std::vector<const PackedLayer *> &layers, int32_t n, int cap,
                               int max_m, int tile_floats, int threads,
-                              std::vector<PassHost> *built, int cta_rows, bool single_passes = false);
+                              std::vector<PassHost> *built, int cta_rows, bool single_passes = false,
+                              bool share_values = false);
 
 struct PassLayerDev {
   int32_t off_kg, off_src, off_bias, off_orow;   // byte offsets in the component record
   int32_t NG;                                    // off_bias < 0: every bias is bu
   float wu, bu;
+  int32_t off_vs;                                // >= 0: non-last layer stores one value per group
+                                                 // into the slot vs[group] (u16 array at this offset)
 };
 struct DevPass {
   int32_t a, m, ncomp, rin, R, T, rec_bytes;

@@ -144,7 +144,7 @@ def test_fused_passes_rn(sd, fuse_rows, fuse_layers):
     layers = list(g.iter_layers(spec))
     rp, idx = g.ms_inputs(n, B, seed=31)
     cats, Y, prof = oracle.infer(n, layers, rp, idx, None, profile=True)
-    for flags in (0, 4):
+    for flags in (0, 4, 512):                 # default, stream loop, SDNN_F_SHARE_VALUES
         cg, Yg, st = run_gpu(sd, n, layers, rp, idx, None, fmt="ell", flags=flags,
                              fuse_rows=fuse_rows, fuse_layers=fuse_layers)
         assert (st["fused_layers"] > 0) == (fuse_rows > 0)
@@ -184,13 +184,16 @@ def test_fused_nonuniform_bias(sd, cap):
     assert st["live_rows"] == prof
 
 
-def test_fused_ka_long_passes(sd):
+@pytest.mark.parametrize("share", [0, 512])
+def test_fused_ka_long_passes(sd, share):
+    """16-layer passes over KA blocks; with SDNN_F_SHARE_VALUES every layer but
+    the last stores one value per group (free-slot allocation after the first)."""
     from test_oracle_pins import ka_expected
     spec = g.ka_spec(2048, 40)
     layers = list(g.iter_layers(spec))
     rp, idx, cnt = g.ka_inputs(2048, 999, seed=5)
     cg, Yg, st = run_gpu(sd, 2048, layers, rp, idx, None, fmt="ell", fuse_rows=256,
-                         fuse_layers=16, flags=sd.SDNN_F_NO_RESIDENT)
+                         fuse_layers=16, flags=sd.SDNN_F_NO_RESIDENT | share)
     assert st["steps"] == 3 and st["fused_layers"] == 40
     Yx = ka_expected(spec, cnt)
     assert np.array_equal(Yg.view(np.uint32), Yx.view(np.uint32))
