@@ -311,6 +311,8 @@ def run_gpu(args):
     ms = ev0.elapsed_time(ev1) / args.steps
     st = net.stats()
     layer_ms = net.layer_times()                     # per-layer kernel durations, last step
+    if nvg is not None and nvg.timed_out():
+        raise RuntimeError("NVLS gather timed out on this rank: the measurement is invalid")
     multi = None
     if ws > 1:
         gms = sum(a.elapsed_time(b) for a, b in gev) / max(1, len(gev)) if gev else None

@@ -218,7 +218,9 @@ sdnn_status sdnn_gather_rows(sdnn_net *net, const int32_t *d_rows, int64_t nrows
  *   local_words  unicast VA of this GPU's copy of the global bitmask
  *   mc_words     multicast VA of the same buffer
  *   local_flag / mc_flag  unicast / multicast VA of a uint32 arrival counter that
- *                every rank increments once per call (never reset)
+ *                every rank increments once per call (never reset); local_flag[1]
+ *                is set to 1 if a wait gave up after ~4 s (a rank missing: the
+ *                result is then invalid, the GPU is not hung)
  *   word_offset  this rank's first word; target = (calls so far) x world size.
  * Reuse of a word buffer must alternate (two buffers by call parity): a rank
  * may start its next call while another still decodes this one.  Needs >= 1
@@ -234,6 +236,11 @@ typedef struct sdnn_nvls {
 sdnn_status sdnn_infer_device_nvls(sdnn_net *net, const int64_t *d_rowptr, const int32_t *d_idx,
                                    const float *d_val, int64_t batch, const sdnn_nvls *nv,
                                    void *stream);
+
+/* The arrival/wait of sdnn_infer_device_nvls alone (an NVLS barrier; used to
+ * check a multicast mapping once before relying on it): adds 1 through mc_flag,
+ * waits until local_flag reaches target (local_flag[1] = 1 on a ~4 s timeout). */
+sdnn_status sdnn_nvls_barrier(uint32_t *local_flag, uint32_t *mc_flag, uint32_t target, void *stream);
 
 /* Multi-GPU readout (no handle needed): decode a global category bitmask --
  * e.g. the NCCL all-gather of every rank's d_alive words, rows partitioned in

@@ -35,7 +35,7 @@ EXPORTS = ["sdnn_create", "sdnn_create_empty", "sdnn_set_layer", "sdnn_infer",
            "sdnn_infer_device", "sdnn_stats_get", "sdnn_validate_layer", "sdnn_destroy",
            "sdnn_last_error", "sdnn_abi_version", "sdnn_layer_times", "sdnn_plan_steps",
            "sdnn_step_plan", "sdnn_gather_rows", "sdnn_bitmask_to_ids",
-           "sdnn_flow_infer", "sdnn_infer_device_nvls"]
+           "sdnn_flow_infer", "sdnn_infer_device_nvls", "sdnn_nvls_barrier"]
 
 
 class SdnnError(RuntimeError):
@@ -118,6 +118,7 @@ def lib() -> ctypes.CDLL:
         L.sdnn_gather_rows.argtypes = [V, V, I64, V, V]
         L.sdnn_bitmask_to_ids.argtypes = [V, I64, V, V, V]
         L.sdnn_infer_device_nvls.argtypes = [V, V, V, V, I64, P(sdnn_nvls), V]
+        L.sdnn_nvls_barrier.argtypes = [V, V, U32, V]
         L.sdnn_flow_infer.argtypes = [V, I32, P(sdnn_flow_part), V, I64, V, V, I32, I32, I32,
                                       P(ctypes.c_float), P(I32)]
         L.sdnn_destroy.argtypes = [V]
@@ -128,7 +129,8 @@ def lib() -> ctypes.CDLL:
         for name in ["sdnn_create", "sdnn_create_empty", "sdnn_set_layer", "sdnn_infer",
                      "sdnn_infer_device", "sdnn_stats_get", "sdnn_validate_layer",
                      "sdnn_layer_times", "sdnn_plan_steps", "sdnn_step_plan", "sdnn_gather_rows",
-                     "sdnn_bitmask_to_ids", "sdnn_flow_infer", "sdnn_infer_device_nvls"]:
+                     "sdnn_bitmask_to_ids", "sdnn_flow_infer", "sdnn_infer_device_nvls",
+                     "sdnn_nvls_barrier"]:
             getattr(L, name).restype = I32
         _LIB = L
     return _LIB

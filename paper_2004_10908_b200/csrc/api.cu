@@ -1487,6 +1487,14 @@ sdnn_status sdnn_infer_device_nvls(sdnn_net *net, const int64_t *d_rowptr, const
                            nullptr, nv);
 }
 
+sdnn_status sdnn_nvls_barrier(uint32_t *local_flag, uint32_t *mc_flag, uint32_t target, void *stream) {
+  if (!local_flag || !mc_flag) return fail(SDNN_E_ARG, "NULL argument");
+  launch_nvls_barrier(local_flag, mc_flag, target, (cudaStream_t)stream);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(SDNN_E_CUDA, std::string("k_nvls_barrier: ") + cudaGetErrorString(e));
+  return SDNN_OK;
+}
+
 sdnn_status sdnn_bitmask_to_ids(const uint32_t *d_words, int64_t batch, int32_t *d_ids, int32_t *d_n,
                                 void *stream) {
   if (batch < 0 || batch > (int64_t(1) << 30)) return fail(SDNN_E_ARG, "batch out of range");

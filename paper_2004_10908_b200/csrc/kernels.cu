@@ -1269,6 +1269,34 @@ __global__ void __launch_bounds__(1024) k_list_bits(const uint32_t *__restrict__
 // arrival counter; it returns once the counter shows every rank (target =
 // epoch x world), so the local copy then holds the whole global bitmask.
 // Single CTA (like k_readout).
+// arrival on a multicast counter, then wait (acquire) until the local copy
+// reaches target; after ~4 s without progress give up and record the timeout
+// in local_flag[1] (the host checks it) instead of hanging the GPU
+__device__ __forceinline__ void nvls_arrive_wait(uint32_t *local_flag, uint32_t *mc_flag, uint32_t target) {
+  asm volatile("multimem.red.release.sys.global.add.u32 [%0], %1;" ::"l"(mc_flag), "r"(1u) : "memory");
+  uint64_t t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  uint32_t seen = 0;
+  for (;;) {
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(seen) : "l"(local_flag) : "memory");
+    if (seen >= target) break;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 4000000000ull) {
+      atomicExch(local_flag + 1, 1u);
+      break;
+    }
+    __nanosleep(64);
+  }
+}
+
+__global__ void k_nvls_barrier(uint32_t *local_flag, uint32_t *mc_flag, uint32_t target) {
+  if (threadIdx.x == 0) nvls_arrive_wait(local_flag, mc_flag, target);
+}
+
+void launch_nvls_barrier(uint32_t *local_flag, uint32_t *mc_flag, uint32_t target, cudaStream_t s) {
+  k_nvls_barrier<<<1, 32, 0, s>>>(local_flag, mc_flag, target);
+}
+
 __global__ void __launch_bounds__(1024) k_readout_nvls(const LayerState *__restrict__ st, int a,
                                                        const uint32_t *__restrict__ alive,
                                                        const int32_t *ridA, const int32_t *ridB,
@@ -1297,12 +1325,7 @@ __global__ void __launch_bounds__(1024) k_readout_nvls(const LayerState *__restr
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence_system();
-    asm volatile("multimem.red.release.sys.global.add.u32 [%0], %1;" ::"l"(mc_flag), "r"(1u) : "memory");
-    uint32_t seen = 0;
-    do {
-      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(seen) : "l"(local_flag) : "memory");
-      if (seen < target) __nanosleep(64);
-    } while (seen < target);
+    nvls_arrive_wait(local_flag, mc_flag, target);
   }
   __syncthreads();
 }

@@ -289,6 +289,7 @@ void launch_yout(const Workspace &w, int32_t a, bool final_out, int32_t n, int64
 void launch_readout_nvls(const Workspace &w, int32_t a, const uint32_t *alive_last, int64_t batch,
                          uint32_t *local_words, uint32_t *mc_words, uint32_t *local_flag, uint32_t *mc_flag,
                          uint32_t target, cudaStream_t s);
+void launch_nvls_barrier(uint32_t *local_flag, uint32_t *mc_flag, uint32_t target, cudaStream_t s);
 // global category bitmask (batch bits) -> ascending ids, count in *d_n
 void launch_bitmask_ids(const uint32_t *d_words, int64_t batch, int32_t *d_ids, int32_t *d_n, cudaStream_t s);
 // Y_L rows of the given original row ids (same buffer selection as launch_yout)

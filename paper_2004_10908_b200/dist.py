@@ -84,6 +84,23 @@ class NvlsGather:
             raise RuntimeError("no NVLS multicast mapping for this group")
         self.hdl.barrier()
         self.calls = 0
+        # one checked round trip through the multicast counter before relying
+        # on it (the wait gives up after ~4 s rather than hang)
+        import ctypes
+        from paper_2004_10908_b200 import lib, _check
+        base, mc, flag = self.buf.data_ptr(), self.hdl.multicast_ptr, 4 * 2 * self.stride
+        self.calls = 1
+        _check(lib().sdnn_nvls_barrier(ctypes.c_void_p(base + flag), ctypes.c_void_p(mc + flag),
+                                        self.ws, torch.cuda.current_stream(self.dev).cuda_stream))
+        torch.cuda.synchronize(self.dev)
+        ok = torch.tensor([int(self.timed_out() == 0)], dtype=torch.int32, device=self.dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=self.group)
+        if int(ok.item()) != 1:
+            raise RuntimeError("NVLS multicast counter did not reach every rank")
+
+    def timed_out(self) -> int:
+        """1 if a wait on the arrival counter gave up (results invalid)."""
+        return int(self.buf[2 * self.stride + 1].item())
 
     def params(self, word_offset: int):
         """sdnn_nvls for the next call; returns (struct, the local word tensor it fills)."""
@@ -167,6 +184,8 @@ class Partitioned:
                 allw = gather_bitmask(self.words, self.group)
             ids, cnt = decode_device(allw, self.batch, s)
             n = int(cnt.item())                                  # D2H: the count, then the ids
+            if self.nvls is not None and self.nvls.timed_out():
+                raise RuntimeError("NVLS gather: a rank never arrived (result invalid)")
             return ids[:n].cpu().numpy()
 
 
