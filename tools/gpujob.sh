@@ -48,7 +48,13 @@ for R in "$@"; do
     full) timeout 1200 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
             -k "regex:$B" -s "${C:-60}" -c 1 -o gpurun_out/${TAG}_full_${A}_$(echo "$B" | tr -cd 'a-z0-9_') \
             python bench.py --config $A --oneshot --steps 1 --warmup 0 ${FULLARGS:-} > gpurun_out/${TAG}_full.log 2>&1
-          echo "full $A $B: $(ls gpurun_out/${TAG}_full_${A}_*.ncu-rep 2>/dev/null | tail -1)" ;;
+          REP=gpurun_out/${TAG}_full_${A}_$(echo "$B" | tr -cd 'a-z0-9_')
+          # text summaries on the box (gpurun_out/ comes back only if < 64 MiB)
+          ncu -i $REP.ncu-rep --page details > $REP.details.txt 2>/dev/null
+          ncu -i $REP.ncu-rep --page raw --csv > $REP.raw.csv 2>/dev/null
+          ncu -i $REP.ncu-rep --page source --csv --print-source sass > $REP.sass.csv 2>/dev/null
+          [ "${KEEP_REP:-0}" = "1" ] || rm -f $REP.ncu-rep
+          echo "full $A $B: $REP ($(grep -m1 Duration $REP.details.txt | tr -s ' '))" ;;
     sanitize) timeout 1200 python tools/sanitize_run.py > gpurun_out/${TAG}_sanitize.log 2>&1
               tail -5 gpurun_out/${TAG}_sanitize.log ;;
     *) echo "unknown recipe $R" ;;
