@@ -146,9 +146,11 @@ def schedule_desc(g, spec):
     return {"name": sch, "formula": formula, "first_fields": first}
 
 
-def kernel_name(net):
+def kernel_name(net, args=None):
     st = net.stats()
-    return "k_layer_bulk" if st.get("fused_layers", 0) == 0 else "k_pass+k_layer_bulk"
+    if st.get("fused_layers", 0) == 0:
+        return "k_layer_bulkw" if args is not None and args.net == "rw" else "k_layer_bulk"
+    return "k_pass+k_layer_bulk"
 
 
 def make_inputs(n, B, rank):
@@ -349,28 +351,45 @@ def run_gpu(args):
     pk = peaks()
     peak = pk["hbm_gbs"] if pk else 6650.0
     achieved = alg_bytes / kern_s / 1e9 if kern_s > 0 else None
-    traffic, traffic_src = None, None
+    traffic, traffic_src, levels = None, None, None
     try:
-        # dram__bytes_read.sum + dram__bytes_write.sum of one captured launch
-        # (ncu --set full, profiles/layer_traffic.json), expressed per average
-        # launch through its ratio to that launch's algorithmic bytes
+        # dram__bytes_read.sum + dram__bytes_write.sum of one captured launch of
+        # the dominant variant (ncu --set full, profiles/layer_traffic.json),
+        # expressed per average launch through its ratio to that launch's
+        # algorithmic bytes; plus the binding-level utilisations (HBM, L2,
+        # L1/shared, FMA pipe, issue) of the captured kernels of this config
         prof = json.load(open(os.path.join(ROOT, "profiles", "layer_traffic.json")))
-        if prof.get("config") == args.config and prof.get("kernel") == kernel_name(net):
+        if prof.get("config") == args.config and prof.get("kernel") == kernel_name(net, args) and args.net == "rn":
             traffic = prof["dram_over_alg"] * alg_bytes / len(plan)
             traffic_src = prof["source"]
+        key = args.config + ("" if args.net == "rn" else "-" + args.net)
+        if key in prof.get("levels", {}):
+            levels = {x["kernel"].split("(")[0].replace("void ", ""):
+                      {k: (round(x[k], 3) if isinstance(x[k], float) else x[k])
+                       for k in ("duration_ms", "hbm_frac_of_measured", "l2_pct", "l1_pct",
+                                 "smem_wavefront_pct", "smem_bank_conflict_share", "fma_pipe_pct",
+                                 "issue_pct", "warps_active_pct")}
+                      for x in prof["levels"][key]}
     except Exception:
         pass
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": (achieved / peak) if achieved else None, "traffic": traffic,
             "traffic_source": traffic_src,
-            "kernel": f"{kernel_name(net)} ({len(plan)} launches per inference, "
+            "kernel": f"{kernel_name(net, args)} ({len(plan)} launches per inference, "
                       f"{sum(1 for m in plan if m > 1)} fused passes covering "
                       f"{sum(m for m in plan if m > 1)} layers; avg over the last timed "
                       "inference, CUDA events on the launching stream)",
             "peak_source": "MEASURED_PEAKS.json hbm_gbs" if pk else "fallback 6.65 TB/s",
             "kernel_share_of_step": kern_s / (ms * 1e-3),
             "alg_bytes_per_launch": alg_bytes / len(plan),
-            "alg_bytes_per_live_edge": alg_bytes / max(1, st["live_edges"])}
+            "alg_bytes_per_live_edge": alg_bytes / max(1, st["live_edges"]),
+            "levels": levels,
+            "note": ("N <= 1024: the shared-memory-resident kernel runs the last layers (HBM only at "
+                     "entry and exit), so the HBM fraction is not its bound; at C1 (1000 rows = 63 CTAs "
+                     "of 16 positions for 148 SMs) it is latency/occupancy bound, see levels"
+                     if st.get("resident_layers", 0) > 0 else None),
+            "levels_source": "ncu --set full, one launch per kernel (profiles/r02/r02_levels.jsonl; "
+                             "percentages of each unit's peak)" if levels else None}
 
     # ---- e2e through the public host-buffer call --------------------------------
     e2e = None
