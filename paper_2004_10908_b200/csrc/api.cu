@@ -15,6 +15,8 @@
 #include <thread>
 #include <vector>
 
+#include <cudaTypedefs.h>
+
 #include "../../include/sdnn.h"
 #include "sdnn_internal.h"
 
@@ -94,6 +96,9 @@ struct sdnn_net {
   std::vector<DevPass> passes;
   Arena pass_arena;
   bool plan_dirty = true;
+  int64_t plan_gen = 0;                // bumped by every make_plan
+  float *tmap_y[2] = {nullptr, nullptr};   // buffers the pass tensor maps were encoded for
+  int64_t tmap_plan = -1;
   int32_t fused_layers = 0;
   int32_t resident_layers = 0;
   ResLayerDev *d_res = nullptr;        // device table for the resident step (pass_arena)
@@ -581,6 +586,7 @@ sdnn_status make_plan(sdnn_net *net) {
     net->resident_layers = r.m;
   }
   net->plan_dirty = false;
+  ++net->plan_gen;
   return SDNN_OK;
 }
 
@@ -749,6 +755,59 @@ void launch_final_yout(sdnn_net *net, int64_t batch, float *d_yout, cudaStream_t
 // Everything of one inference after Y0 is on the device.
 // workspace for `batch` rows and the execution plan (whose activation layout
 // the workspace records)
+// TMA tensor maps of the two activation buffers for the 16-position passes
+// (position-blocked layout, 32-position blocks): dims {32, N, stride/32},
+// box {16 positions, 256 rows, 1 block}.  Encoded whenever the buffers or the
+// plan change.  Opt-in (SDNN_PASS_TMA16=1): measured on C4 the boxes of 64 B
+// rows are slower than the 16-byte LDGSTS half-row loads (4.25 vs 3.43 ms per
+// 16-position pass, 2027 vs 1939 ms/step).
+sdnn_status encode_tmaps(sdnn_net *net) {
+  static const bool on = [] {
+    const char *e = getenv("SDNN_PASS_TMA16");
+    return e && atoi(e) == 1;
+  }();
+  bool need = false;
+  for (const DevPass &D : net->passes) need = need || (D.T == 16 && D.C == 1 && D.yblk && D.lg_in == 5);
+  if (!on || !need) return SDNN_OK;
+  if (net->tmap_y[0] == net->ws.Y[0] && net->tmap_y[1] == net->ws.Y[1] && net->tmap_plan == net->plan_gen)
+    return SDNN_OK;
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    cudaGetLastError();
+    return (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  }();
+  CUtensorMap maps[2];
+  bool ok = encode != nullptr;
+  for (int i = 0; i < 2 && ok; ++i) {
+    const cuuint64_t dims[3] = {32, (cuuint64_t)net->n, (cuuint64_t)(net->ws.stride / 32)};
+    const cuuint64_t strides[2] = {128, (cuuint64_t)net->n * 128};
+    const cuuint32_t box[3] = {16, 256, 1}, es[3] = {1, 1, 1};
+    ok = encode(&maps[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, net->ws.Y[i], dims, strides, box, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
+  for (DevPass &D : net->passes)
+    if (D.T == 16 && D.C == 1 && D.yblk && D.lg_in == 5) {
+      D.tma16 = ok ? 1 : 0;
+      if (ok) {
+        D.tmap[0] = maps[0];
+        D.tmap[1] = maps[1];
+      }
+    }
+  net->tmap_y[0] = net->ws.Y[0];
+  net->tmap_y[1] = net->ws.Y[1];
+  net->tmap_plan = net->plan_gen;
+  if (net->chain) {                              // pass parameters changed: recapture
+    cudaGraphExecDestroy(net->chain);
+    net->chain = nullptr;
+  }
+  return SDNN_OK;
+}
+
 sdnn_status prepare_infer(sdnn_net *net, int64_t batch) {
   if (net->nset.load() != net->L) return fail(SDNN_E_STATE, "not every layer has been set");
   sdnn_status st = ensure_ws(net, batch);
@@ -757,6 +816,7 @@ sdnn_status prepare_infer(sdnn_net *net, int64_t batch) {
   net->ws.yblk = net->L > 0 ? net->yblk : 0;
   net->ws.sig0 = net->L > 0 ? net->d_sig0 : nullptr;
   net->ws.lg0 = (net->L > 0 && net->yblk && !net->step_lg.empty()) ? net->step_lg[0] : 5;
+  if (net->L > 0 && (st = encode_tmaps(net))) return st;
   return SDNN_OK;
 }
 

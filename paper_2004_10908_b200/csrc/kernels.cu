@@ -737,7 +737,7 @@ __device__ __forceinline__ float4 out4(const float (&a)[4], float b, float ymax,
 
 template <int T, int C, bool X2, int NB>
 __global__ void __launch_bounds__(32 * kPassNW, 3)
-    k_pass(const DevPass P, const LayerState *__restrict__ st, float *Ya, float *Yb,
+    k_pass(const __grid_constant__ DevPass P, const LayerState *__restrict__ st, float *Ya, float *Yb,
            uint32_t *__restrict__ alive, int64_t wstride, int64_t stride, float ymax) {
   constexpr int NW = kPassNW;
   constexpr int SW = T < 128 ? T : 128;          // positions per unit (4 per lane)
@@ -795,7 +795,11 @@ __global__ void __launch_bounds__(32 * kPassNW, 3)
   const bool blk = R > 0;
   const bool bt = blk && T >= 32;               // blocked tile: smem [T/32][rin][32]
   const bool b16 = blk && T == 16 && P.lg_in == 4;   // one bulk copy, smem [rin][16]
-  const bool ldg = kLdgsts && (!blk || (T < 32 && !b16));   // (T = 16 in 32-blocks: half-row LDGSTS)
+  // T = 16 in 32-position blocks: half-block rows by TMA boxes of 256 rows
+  // (tensor map of the input buffer), else 16-byte LDGSTS chunks
+  const bool tma = blk && T == 16 && !b16 && P.tma16;
+  const void *tmap_in = &P.tmap[Sx.in];
+  const bool ldg = kLdgsts && (!blk || (T < 32 && !b16 && !tma));
   const int lgo = P.lg_out;                      // output boundary block size 2^lgo
   const int rin = P.rin;
   const int sm = bt ? 32 : T;                    // tile floats per slot step
@@ -828,7 +832,9 @@ __global__ void __launch_bounds__(32 * kPassNW, 3)
     const int tile = item_tile(it);
     const int64_t cb = c * C + rank;
     if (tid == 0) {
-      mbar_expect_tx_arrive(bar_b, (ldg ? 0u : (uint32_t)ncnt * T * 4) + (uint32_t)P.rec_bytes);
+      // (TMA boxes move whole 256-row boxes: rows past the tensor are zero-filled)
+      const uint32_t tile_bytes = ldg ? 0u : tma ? (uint32_t)((ncnt + 255) >> 8) * 256u * 64u : (uint32_t)ncnt * T * 4;
+      mbar_expect_tx_arrive(bar_b, tile_bytes + (uint32_t)P.rec_bytes);
       bulk_g2s(rec_s, P.rec + cb * P.rec_bytes, P.rec_bytes, bar_b);
       if (bt && ncnt > 0)                        // nrow[0] = the first storage row
 #pragma unroll
@@ -838,7 +844,13 @@ __global__ void __launch_bounds__(32 * kPassNW, 3)
       if (b16 && ncnt > 0)
         bulk_g2s(tile_s, Yin + ((int64_t)tile * R + nrow[0]) * 16, (uint32_t)ncnt * 64u, bar_b);
     }
-    if (bt || b16) {
+    if (tma) {
+      if (tid == 0 && ncnt > 0) {
+        const int nbox = (ncnt + 255) >> 8;
+        for (int q = 0; q < nbox; ++q)
+          tma_load_3d(tile_s + q * 256 * 16, tmap_in, (tile & 1) * 16, nrow[0] + q * 256, tile >> 1, bar_b);
+      }
+    } else if (bt || b16) {
     } else if (blk) {
       // T = 16: 64 B of each consecutive 128 B block row (block tile/2, half tile%2)
       const float *src0 = Yin + ((int64_t)(tile >> 1) * R + nrow[0]) * 32 + (tile & 1) * 16;
@@ -1167,10 +1179,19 @@ __global__ void __launch_bounds__(1024) k_scan_step(LayerState *st, int a, int m
 }
 
 // Move the live batch columns of the step's output into the free buffer.
-__global__ void k_compact(const LayerState *__restrict__ st, int a, int m, float *Ya, float *Yb,
-                          int32_t *ridA, int32_t *ridB, const uint32_t *__restrict__ alive,
-                          const int32_t *__restrict__ wpre, int32_t n, int64_t stride,
-                          int32_t yblk, int lg) {
+// A warp owns one 32-position word q and a slice of the rows: it loads the
+// word's bits and its output offset once, then streams the rows -- each load a
+// whole 128 B line (32 positions of one row), each store the live lanes packed
+// to consecutive output positions -- 8 rows in flight per lane.  In the
+// position-blocked layout the rows of word q are consecutive lines, so a warp
+// walks one contiguous region.  Row n is the row-id vector.
+constexpr int kCompactRowSlices = 8;
+
+__global__ void __launch_bounds__(256) k_compact(const LayerState *__restrict__ st, int a, int m, float *Ya,
+                                                 float *Yb, int32_t *ridA, int32_t *ridB,
+                                                 const uint32_t *__restrict__ alive,
+                                                 const int32_t *__restrict__ wpre, int32_t n, int64_t stride,
+                                                 int32_t yblk, int lg) {
   const LayerState N1 = st[a + m];
   if (!N1.compacted) return;
   const LayerState S = st[a];
@@ -1181,17 +1202,34 @@ __global__ void k_compact(const LayerState *__restrict__ st, int a, int m, float
   const int64_t words = ((int64_t)S.width + 31) >> 5;
   const int lane = threadIdx.x & 31;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t items = (int64_t)(n + 1) * words;   // row n = the row-id vector
+  const int64_t items = words * kCompactRowSlices;
   for (int64_t it = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < items; it += nw) {
-    const int64_t k = it / words, q = it - k * words;
+    const int64_t q = it / kCompactRowSlices;
+    const int slice = (int)(it - q * kCompactRowSlices);
     const uint32_t bits = alive[q];
-    if (!((bits >> lane) & 1u)) continue;
+    if (bits == 0u) continue;
+    const bool live = (bits >> lane) & 1u;
     const int64_t to = wpre[q] + __popc(bits & ((1u << lane) - 1u));
     const int64_t from = q * 32 + lane;
-    if (k < n)
-      dst[yix(k, to, stride, yblk, lg)] = src[yix(k, from, stride, yblk, lg)];
-    else
-      rdst[to] = rsrc[from];
+    const int32_t k0 = (int32_t)((int64_t)(n + 1) * slice / kCompactRowSlices);
+    const int32_t k1 = (int32_t)((int64_t)(n + 1) * (slice + 1) / kCompactRowSlices);
+    int32_t k = k0;
+    for (; k + 8 <= k1 && k + 8 <= n; k += 8) {
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = src[yix(k + u, from, stride, yblk, lg)];
+      if (live)
+#pragma unroll
+        for (int u = 0; u < 8; ++u) dst[yix(k + u, to, stride, yblk, lg)] = v[u];
+    }
+    for (; k < k1; ++k) {
+      if (k < n) {
+        const float v = src[yix(k, from, stride, yblk, lg)];
+        if (live) dst[yix(k, to, stride, yblk, lg)] = v;
+      } else if (live) {
+        rdst[to] = rsrc[from];
+      }
+    }
   }
 }
 
@@ -1600,21 +1638,30 @@ void launch_layer(const LaunchCfg &c, const Workspace &w, const DevLayer &L, int
 
 void launch_pass(const LaunchCfg &c, const Workspace &w, const DevPass &P, uint32_t *alive,
                  float ymax, cudaStream_t s) {
-  static const bool x2_c1 = [] {                 // SDNN_PASS_X2=1: packed path for C = 1 too
+  // SDNN_PASS_X2=1: packed FFMA2 path for single-CTA passes too; =T: only for
+  // tiles of T positions (A/B knob; the default is scalar for C = 1)
+  static const int x2_c1 = [] {
     const char *e = getenv("SDNN_PASS_X2");
-    return e && atoi(e) != 0;
+    return e ? atoi(e) : 0;
   }();
-  const bool x2 = P.C > 1 || x2_c1;
-  switch (P.C * 1024 + P.T + (x2 ? 4096 * 4 : 0) + P.NB * 4096 * 8) {
+  const bool want_x2 = P.NB == 1 && (P.C > 1 || x2_c1 == 1 || (x2_c1 > 1 && x2_c1 == P.T));
+  // (make_plan only plans shapes with an instance, pass_variant; an X2 request
+  // without a packed instance falls back to the scalar one)
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    const bool x2 = want_x2 && attempt == 0;
+    switch (P.C * 1024 + P.T + (x2 ? 4096 * 4 : 0) + P.NB * 4096 * 8) {
 #define X(TT, CC, XX, NN)                                               \
   case CC * 1024 + TT + (XX ? 4096 * 4 : 0) + NN * 4096 * 8:            \
     launch_pass_t<TT, CC, XX, NN>(c, w, P, alive, ymax, s);             \
     return;
-    SDNN_PASS_VARIANTS(X)
+      SDNN_PASS_VARIANTS(X)
 #undef X
-    default:
-      break;                                     // make_plan rejects other shapes (pass_variant)
+      default:
+        break;
+    }
   }
+  fprintf(stderr, "sdnn: no k_pass instance for T=%d C=%d NB=%d\n", P.T, P.C, P.NB);
+  abort();
 }
 
 

@@ -6,6 +6,7 @@
 #include <string>
 #include <vector>
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace sdnn {
@@ -172,7 +173,13 @@ struct PassLayerDev {
   int32_t off_vs;                                // >= 0: non-last layer stores one value per group
                                                  // into the slot vs[group] (u16 array at this offset)
 };
-struct DevPass {
+struct alignas(64) DevPass {
+  // T = 16 passes over position-blocked activations: one TMA tensor map per
+  // activation buffer (dims {32 positions, N rows, stride/32 blocks}, box
+  // {16, 256, 1}), so a tile's half-block rows arrive as <= 4 box copies
+  // instead of 16-byte LDGSTS chunks; tma16 = 0 when not encoded
+  CUtensorMap tmap[2];
+  int32_t tma16;
   int32_t a, m, ncomp, rin, R, T, rec_bytes;
   int32_t C;                           // cluster size: in_rows/in_count/rec indexed [comp * C + rank]
   int32_t yblk;                        // 0: Y is [rows][stride]; R > 0: Y is [stride/32][R][32] and
