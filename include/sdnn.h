@@ -273,6 +273,16 @@ sdnn_status sdnn_bitmask_to_ids(const uint32_t *d_words, int64_t batch, int32_t 
  * but the last a multiple of 32).  Handles with stream_slots > 0 or
  * SDNN_F_PROFILE are not supported. */
 enum { SDNN_FLOW_GRAPH = 0, SDNN_FLOW_CAPTURER = 1, SDNN_FLOW_STREAMS = 2 };
+/* Host-only (no device): Algorithm 1's stream assignment for an arbitrary task
+ * DAG -- the same code sdnn_flow_infer runs.  edges: [nedges] (from, to) pairs
+ * (int32 x 2); level / id / stream: [ntasks] outputs (NULL allowed): level =
+ * topological level (Kahn rounds), id = index inside the level, stream = id mod
+ * max_streams; event_edges: [2 * nedges] capacity or NULL, receives the edges
+ * that cross streams (the stream_record_event / stream_wait_event pairs) in
+ * issue order, *nevents their count.  SDNN_E_FORMAT on a cycle. */
+sdnn_status sdnn_flow_plan(int32_t ntasks, int32_t nedges, const int32_t *edges, int32_t max_streams,
+                           int32_t *level, int32_t *id, int32_t *stream, int32_t *nevents,
+                           int32_t *event_edges);
 typedef struct sdnn_flow_part {
   const int64_t *d_rowptr;   /* device CSR of the partition's rows (as sdnn_infer_device) */
   const int32_t *d_idx;

@@ -35,7 +35,8 @@ EXPORTS = ["sdnn_create", "sdnn_create_empty", "sdnn_set_layer", "sdnn_infer",
            "sdnn_infer_device", "sdnn_stats_get", "sdnn_validate_layer", "sdnn_destroy",
            "sdnn_last_error", "sdnn_abi_version", "sdnn_layer_times", "sdnn_plan_steps",
            "sdnn_step_plan", "sdnn_gather_rows", "sdnn_bitmask_to_ids",
-           "sdnn_flow_infer", "sdnn_infer_device_nvls", "sdnn_nvls_barrier"]
+           "sdnn_flow_infer", "sdnn_infer_device_nvls", "sdnn_nvls_barrier",
+           "sdnn_flow_plan"]
 
 
 class SdnnError(RuntimeError):
@@ -119,6 +120,7 @@ def lib() -> ctypes.CDLL:
         L.sdnn_bitmask_to_ids.argtypes = [V, I64, V, V, V]
         L.sdnn_infer_device_nvls.argtypes = [V, V, V, V, I64, P(sdnn_nvls), V]
         L.sdnn_nvls_barrier.argtypes = [V, V, U32, V]
+        L.sdnn_flow_plan.argtypes = [I32, I32, V, I32, V, V, V, P(I32), V]
         L.sdnn_flow_infer.argtypes = [V, I32, P(sdnn_flow_part), V, I64, V, V, I32, I32, I32,
                                       P(ctypes.c_float), P(I32)]
         L.sdnn_destroy.argtypes = [V]
@@ -130,7 +132,7 @@ def lib() -> ctypes.CDLL:
                      "sdnn_infer_device", "sdnn_stats_get", "sdnn_validate_layer",
                      "sdnn_layer_times", "sdnn_plan_steps", "sdnn_step_plan", "sdnn_gather_rows",
                      "sdnn_bitmask_to_ids", "sdnn_flow_infer", "sdnn_infer_device_nvls",
-                     "sdnn_nvls_barrier"]:
+                     "sdnn_nvls_barrier", "sdnn_flow_plan"]:
             getattr(L, name).restype = I32
         _LIB = L
     return _LIB
@@ -414,6 +416,19 @@ def bitmask_to_ids_torch(words_t, batch: int, stream=None):
     _check(lib().sdnn_bitmask_to_ids(words_t.data_ptr() if batch > 0 else None, int(batch),
                                      ids.data_ptr(), cnt.data_ptr(), s.cuda_stream))
     return ids, cnt
+
+
+def flow_plan(ntasks: int, edges, max_streams: int):
+    """Algorithm 1's stream assignment (sdnn_flow_plan, host only): returns
+    (level, id, stream, cross-stream event edges) for the DAG."""
+    e = np.ascontiguousarray(np.asarray(edges, np.int32).reshape(-1, 2))
+    lv, ids, st = (np.zeros(max(ntasks, 1), np.int32) for _ in range(3))
+    ev = np.zeros(max(2 * len(e), 2), np.int32)
+    ne = ctypes.c_int32()
+    _check(lib().sdnn_flow_plan(int(ntasks), len(e), _p(e) if len(e) else None, int(max_streams), _p(lv),
+                                _p(ids), _p(st), ctypes.byref(ne), _p(ev)))
+    return (lv[:ntasks].tolist(), ids[:ntasks].tolist(), st[:ntasks].tolist(),
+            [tuple(x) for x in ev[:2 * ne.value].reshape(-1, 2).tolist()])
 
 
 def flow_infer(nets, parts, total_batch: int, mode: int, max_streams: int = 4, reps: int = 3):

@@ -1012,6 +1012,44 @@ void alg1_issue(std::vector<FlowTask> &T, const std::vector<std::vector<int>> &L
 
 }  // namespace
 
+extern "C" sdnn_status sdnn_flow_plan(int32_t ntasks, int32_t nedges, const int32_t *edges, int32_t max_streams,
+                                      int32_t *level, int32_t *id, int32_t *stream, int32_t *nevents,
+                                      int32_t *event_edges) {
+  if (ntasks < 0 || nedges < 0 || max_streams < 1 || (nedges > 0 && !edges) || !nevents)
+    return fail(SDNN_E_ARG, "bad argument");
+  std::vector<FlowTask> T(ntasks);
+  for (int e = 0; e < nedges; ++e) {
+    const int u = edges[2 * e], v = edges[2 * e + 1];
+    if (u < 0 || u >= ntasks || v < 0 || v >= ntasks || u == v) return fail(SDNN_E_ARG, "bad edge");
+    T[u].succ.push_back(v);
+    T[v].pred.push_back(u);
+  }
+  const std::vector<std::vector<int>> L = levelize(T);
+  size_t placed = 0;
+  for (const auto &lev : L) placed += lev.size();
+  if ((int)placed != ntasks) return fail(SDNN_E_FORMAT, "the task graph has a cycle");
+  int32_t ne = 0;
+  for (int t = 0; t < ntasks; ++t) {
+    if (level) level[t] = T[t].level;
+    if (id) id[t] = T[t].id;
+    if (stream) stream[t] = T[t].id % max_streams;
+  }
+  // Alg. 1's events: one per edge whose ends sit in different streams, in the
+  // order the algorithm issues them (level by level, successors per task)
+  for (const auto &lev : L)
+    for (int t : lev)
+      for (int n : T[t].succ)
+        if (T[n].id % max_streams != T[t].id % max_streams) {
+          if (event_edges) {
+            event_edges[2 * ne] = t;
+            event_edges[2 * ne + 1] = n;
+          }
+          ++ne;
+        }
+  *nevents = ne;
+  return SDNN_OK;
+}
+
 extern "C" sdnn_status sdnn_flow_infer(sdnn_net *const *nets, int32_t parts, const sdnn_flow_part *pp,
                                        uint32_t *d_words, int64_t total_batch, int32_t *d_ids,
                                        int32_t *d_n, int32_t mode, int32_t max_streams, int32_t reps,

@@ -55,8 +55,11 @@ for R in "$@"; do
           ncu -i $REP.ncu-rep --page source --csv --print-source sass > $REP.sass.csv 2>/dev/null
           [ "${KEEP_REP:-0}" = "1" ] || rm -f $REP.ncu-rep
           echo "full $A $B: $REP ($(grep -m1 Duration $REP.details.txt | tr -s ' '))" ;;
-    sanitize) timeout 1200 python tools/sanitize_run.py > gpurun_out/${TAG}_sanitize.log 2>&1
-              tail -5 gpurun_out/${TAG}_sanitize.log ;;
+    sanitize) for tool in memcheck synccheck racecheck; do
+                timeout 1500 compute-sanitizer --tool $tool python tools/sanitize_run.py \
+                  > gpurun_out/${TAG}_sanitize_$tool.log 2>&1
+                echo "$tool: $(grep -E 'ERROR SUMMARY|RACECHECK SUMMARY|sanitize_run ok' gpurun_out/${TAG}_sanitize_$tool.log | tr '\n' ' ')"
+              done ;;
     *) echo "unknown recipe $R" ;;
   esac
 done

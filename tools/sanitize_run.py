@@ -55,6 +55,34 @@ def main():
     with sd.Net(64, 0) as net:
         c, _ = net.infer(np.array([0, 1, 1], np.int64), np.array([3], np.int32), None)
     out.append(c.size)
+    # round 2: per-slot weights on the TMA pipeline (k_layer_bulkw), Y_L row
+    # gather, device bitmask decode, the f1 task graph (graph / capturer / streams)
+    import torch
+    spec = g.rw_spec(1024, 4)
+    lays = list(g.iter_layers(spec))
+    rp, idx, val = g.random_inputs(1024, 300, seed=7, density=0.3, lo=0.0, hi=2.0)
+    with sd.Net.from_layers(1024, lays, fmt="ell") as net:
+        c, Y = net.infer(rp, idx, val, want_y=True)
+        rows = np.array([0, 5, 299, 17], np.int32)
+        assert np.array_equal(net.gather_rows(rows), Y[rows])
+    out.append(c.size)
+    w = torch.from_numpy(np.random.default_rng(1).integers(0, 2**31, 40, dtype=np.int64).astype(np.int32)).cuda()
+    ids, cnt = sd.bitmask_to_ids_torch(w, 1250)
+    torch.cuda.synchronize()
+    spec = g.rn_spec(1024, 12)
+    lays = list(g.iter_layers(spec))
+    rp, idx = g.ms_inputs(1024, 400, seed=3)
+    nets = [sd.Net.from_layers(1024, lays, fmt="ell") for _ in range(2)]
+    parts = []
+    for r, (lo, hi) in enumerate([(0, 224), (224, 400)]):
+        srp = (rp[lo:hi + 1] - rp[lo]).astype(np.int64)
+        sidx = np.ascontiguousarray(idx[rp[lo]:rp[hi]])
+        parts.append((torch.from_numpy(srp).cuda(), torch.from_numpy(sidx).cuda(), lo))
+    got = [sd.flow_infer(nets, parts, 400, mode, 2, reps=1)[0].tolist()
+           for mode in (sd.SDNN_FLOW_GRAPH, sd.SDNN_FLOW_CAPTURER, sd.SDNN_FLOW_STREAMS)]
+    assert got[0] == got[1] == got[2]
+    for x in nets:
+        x.close()
     print("sanitize_run ok", out)
 
 
