@@ -194,10 +194,11 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f32",
         "data": "synthetic",
         "config": {"workload": f"{args.net}{n}x{L}-ms{B}", "neurons": n, "layers": L,
-                   "nnz_per_column": 32, "inputs_sampled_per_step": rows_per_step, "inputs_full": B},
+                   "nnz_per_column": 32, "inputs_sampled_per_step": rows_per_step, "inputs_full": B,
+                   "global_batch": B},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
                          "sample": f"{rows_per_step} random rows of the {B}-input batch per step, "
                                    f"all {L} layers (oracle/sdnn_oracle.c, {cores} threads)"},
