@@ -552,7 +552,7 @@ sdnn_status make_plan(sdnn_net *net) {
     for (int j = 0; j < H.m; ++j) {
       const PassHostLayer &HL = H.layers[j];
       D.layers[j] = PassLayerDev{HL.off_kg, HL.off_src, HL.off_bias, HL.off_orow, HL.NG, HL.wu, HL.bu,
-                                 HL.off_vs};
+                                 HL.off_vs, HL.vt};
     }
     net->steps[q].pass = (int32_t)net->passes.size();
     net->passes.push_back(D);

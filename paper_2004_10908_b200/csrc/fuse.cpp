@@ -432,6 +432,26 @@ static void build_pass_impl(const std::vector<const PackedLayer *> &layers, int3
     for (int32_t j = 1; j < n && eq; ++j) eq = std::memcmp(&p.bias[j], &p.bias[0], 4) == 0;
     dedup[b] = eq && (b + 1 == m - 1 || dedup[b + 1]);
   }
+  // Value table for the 2-layer passes of 16-position tiles (1024-row
+  // components: two 64 B rows share each 128 B shared-memory line, so two
+  // units of one quarter-warp phase that read rows of equal parity conflict):
+  // when layer 0's members of a group share one value (uniform weights, equal
+  // biases), the group writes that value twice into line q of a value table --
+  // copy 0 in the first 64 B, copy 1 in the second -- once every group has read
+  // its sources; layer 1's terms read line g(t), the unit in the first half of
+  // a phase copy 0 and the one in the second half copy 1, so every phase covers
+  // both bank halves.  SDNN_PASS_VT=0 disables.
+  static const bool vt_env = [] {
+    const char *e = getenv("SDNN_PASS_VT");
+    return !(e && atoi(e) == 0);
+  }();
+  bool vt = false;
+  if (vt_env && m == 2 && C == 1 && out.T == 16) {
+    const PackedLayer &p = *layers[s.a];
+    bool eq = p.uniform && p.gmax > 1;
+    for (int32_t j = 1; j < n && eq; ++j) eq = std::memcmp(&p.bias[j], &p.bias[0], 4) == 0;
+    vt = eq;
+  }
   for (int b = 0; b < m; ++b) {
     const PackedLayer &p = *layers[s.a + b];
     const bool last = b == m - 1;
@@ -451,6 +471,8 @@ static void build_pass_impl(const std::vector<const PackedLayer *> &layers, int3
     H.NG = NG;
     H.wu = p.wu;
     H.dedup = dedup[b];
+    if (vt && b == 0 && 2 * NG > R) vt = false;   // the table must fit the tile
+    H.vt = vt ? (b == 0 ? 1 : 2) : 0;
     const size_t units = (size_t)ncomp * C;
     H.src.assign(units * NG * 32, 0);
     H.bias.assign(units * NG * 32, 0.f);
@@ -486,6 +508,8 @@ static void build_pass_impl(const std::vector<const PackedLayer *> &layers, int3
           H.bias[rec * 32 + u] = p.bias[j];
           if (last)
             H.orow[rec * 32 + u] = (uint16_t)j;
+          else if (vt)                       // value table: line = record index q
+            slot[out0 + j] = (int32_t)q;
           else if (!dedup[b])                // member u overwrites the slot of source u
             slot[out0 + j] = code[u];
         }

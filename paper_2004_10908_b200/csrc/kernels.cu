@@ -940,6 +940,7 @@ __global__ void __launch_bounds__(32 * kPassNW, 3)
       // the last layer releases the tiles before its HBM stores when every warp
       // owns at most one unit per segment (one round)
       const bool early = last && units <= NW * UPW;
+      const bool vtw = PL.vt == 1, vtr = PL.vt == 2;     // value table write / read (fuse.cpp)
       if (remote) cluster_sync();                // every CTA's tile is at boundary m-1
       for (int u0 = 0; u0 < units; u0 += NW * UPW) {
         const int u = u0 + warp * UPW + seg;
@@ -953,6 +954,9 @@ __global__ void __launch_bounds__(32 * kPassNW, 3)
         }
         const int pofs = sl * SW + sll * 4;      // this lane's 4 positions in the tile
         const int pa = bt ? ((pofs >> 5) * rin * 32 + (pofs & 31)) : pofs;   // their smem offset
+        // value-table reads: the unit in the second half of a quarter-warp phase
+        // reads copy 1 (the other 64 B of the line), so a phase spans all banks
+        const int par = vtr ? pa + 16 * (seg & 1) : pa;
         // entry e = r * LPU + sll of the group: source slot (a term past K points
         // at source 0 with weight 0: fmaf(x, 0, acc) == acc for finite x, acc != -0)
         uint32_t soff[EPL];                      // float offset in the tile / cluster address
@@ -963,7 +967,7 @@ __global__ void __launch_bounds__(32 * kPassNW, 3)
           const int e = r * LPU + sll;
           const uint32_t code = K > 0 ? src_s[gi * 32 + (e < K ? e : 0)] : 0u;
           soff[r] = remote ? cluster_map(tile_u32 + (code & 0x3ffu) * (sm * 4), code >> 10)
-                           : (code & 0x3ffu) * sm;
+                           : (code & 0x3ffu) * (vtr ? 32 : sm);
           bia[r] = (!ubias && e < G) ? bias_s[gi * 32 + e] : 0.f;
           orw[r] = (last && e < G) ? orow_s[gi * 32 + e] : 0;
         }
@@ -985,7 +989,7 @@ __global__ void __launch_bounds__(32 * kPassNW, 3)
             for (int r = 0; r < EPL; ++r)
 #pragma unroll
               for (int l = 0; l < LPU; ++l)
-                acc4<X2>(acc, *reinterpret_cast<const float4 *>(tile_s + __shfl_sync(FULL, soff[r], l, LPU) + pa),
+                acc4<X2>(acc, *reinterpret_cast<const float4 *>(tile_s + __shfl_sync(FULL, soff[r], l, LPU) + par),
                          wu);
           }
         } else {
@@ -999,7 +1003,7 @@ __global__ void __launch_bounds__(32 * kPassNW, 3)
               if (t < kmax) {
                 const float w = t < K ? wu : 0.f;
                 if (remote) acc4<X2>(acc, ld_cluster_f4(so + (uint32_t)(pa * 4)), w);
-                else acc4<X2>(acc, *reinterpret_cast<const float4 *>(tile_s + so + pa), w);
+                else acc4<X2>(acc, *reinterpret_cast<const float4 *>(tile_s + so + par), w);
               }
             }
           }
@@ -1019,7 +1023,15 @@ __global__ void __launch_bounds__(32 * kPassNW, 3)
         const int64_t opos = (int64_t)tile * T + pofs;
         float *obase = blk ? Yout + (((opos >> lgo) * R) << lgo) + (opos & ((1 << lgo) - 1)) : Yout + opos;
         const int64_t rowmul = blk ? (1 << lgo) : stride;
-        if (!last && PL.off_vs >= 0) {
+        if (!last && vtw) {
+          // value table: every group has read its sources (the table overwrites
+          // tile rows), then line gi = [copy 0 | copy 1] of the group's value
+          __syncthreads();
+          if (G > 0) {
+            *reinterpret_cast<float4 *>(tile_s + gi * 32 + pa) = yu;
+            *reinterpret_cast<float4 *>(tile_s + gi * 32 + 16 + pa) = yu;
+          }
+        } else if (!last && PL.off_vs >= 0) {
           // shared value: one store per group into its value slot (the next
           // layer's terms of every member of this group point there)
           if (G > 0) {

@@ -134,6 +134,7 @@ struct PassHostLayer {
   bool dedup = false;                  // members share one value slot (uniform w, equal biases)
   std::vector<uint16_t> vs;            // dedup: [ncomp][NG] value slot of each group
   int32_t off_vs = -1;
+  int32_t vt = 0;                      // value table (fuse.cpp): 1 = this layer writes it, 2 = reads it
   float bu = 0.f;
   int32_t off_kg = 0, off_src = 0, off_bias = 0, off_orow = -1;  // record byte offsets
   std::vector<uint16_t> src;           // [ncomp][NG][32] smem slots of the sources
@@ -172,6 +173,8 @@ struct PassLayerDev {
   float wu, bu;
   int32_t off_vs;                                // >= 0: non-last layer stores one value per group
                                                  // into the slot vs[group] (u16 array at this offset)
+  int32_t vt;                                    // value table: 1 = write (two copies per group line),
+                                                 // 2 = read (line = code, copy = phase half)
 };
 struct alignas(64) DevPass {
   // T = 16 passes over position-blocked activations: one TMA tensor map per
