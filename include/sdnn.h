@@ -177,6 +177,24 @@ sdnn_status sdnn_infer(sdnn_net *net, const int64_t *y0_rowptr, const int32_t *y
                        const float *y0_val, int64_t batch, int32_t *categories,
                        int64_t *n_categories, float *y_out);
 
+/* Pipelined host-buffer inference (serving): sdnn_infer_submit does what
+ * sdnn_infer does up to the device work -- host checks, input copy, densify,
+ * layer chain, readout, the copy of the categories into a page-locked result
+ * buffer -- and returns once it is enqueued; sdnn_infer_wait(ticket) blocks
+ * until that inference is complete and returns its categories (and the status
+ * of its host validation).  Up to two submissions may be outstanding on a
+ * handle: the input copy of the next one then overlaps the layers of the
+ * current one.  The caller's input buffers must stay valid and unchanged until
+ * the matching wait returns.  y_out is not available on this path;
+ * sdnn_infer returns SDNN_E_STATE while submissions are outstanding.
+ *   ticket      receives an id for sdnn_infer_wait (waits in submission order
+ *               are not required, but a third submit before a wait returns
+ *               SDNN_E_STATE). */
+sdnn_status sdnn_infer_submit(sdnn_net *net, const int64_t *y0_rowptr, const int32_t *y0_idx,
+                              const float *y0_val, int64_t batch, int64_t *ticket);
+sdnn_status sdnn_infer_wait(sdnn_net *net, int64_t ticket, int32_t *categories,
+                            int64_t *n_categories);
+
 /* Asynchronous inference from DEVICE buffers on `stream` (cudaStream_t; NULL =
  * legacy default stream).  Same Y0 layout as sdnn_infer, all pointers device
  * pointers; Y0 is NOT validated here.

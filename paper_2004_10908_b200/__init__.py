@@ -36,7 +36,7 @@ EXPORTS = ["sdnn_create", "sdnn_create_empty", "sdnn_set_layer", "sdnn_infer",
            "sdnn_last_error", "sdnn_abi_version", "sdnn_layer_times", "sdnn_plan_steps",
            "sdnn_step_plan", "sdnn_gather_rows", "sdnn_bitmask_to_ids",
            "sdnn_flow_infer", "sdnn_infer_device_nvls", "sdnn_nvls_barrier",
-           "sdnn_flow_plan"]
+           "sdnn_flow_plan", "sdnn_infer_submit", "sdnn_infer_wait"]
 
 
 class SdnnError(RuntimeError):
@@ -121,6 +121,8 @@ def lib() -> ctypes.CDLL:
         L.sdnn_infer_device_nvls.argtypes = [V, V, V, V, I64, P(sdnn_nvls), V]
         L.sdnn_nvls_barrier.argtypes = [V, V, U32, V]
         L.sdnn_flow_plan.argtypes = [I32, I32, V, I32, V, V, V, P(I32), V]
+        L.sdnn_infer_submit.argtypes = [V, V, V, V, I64, P(I64)]
+        L.sdnn_infer_wait.argtypes = [V, I64, V, P(I64)]
         L.sdnn_flow_infer.argtypes = [V, I32, P(sdnn_flow_part), V, I64, V, V, I32, I32, I32,
                                       P(ctypes.c_float), P(I32)]
         L.sdnn_destroy.argtypes = [V]
@@ -132,7 +134,8 @@ def lib() -> ctypes.CDLL:
                      "sdnn_infer_device", "sdnn_stats_get", "sdnn_validate_layer",
                      "sdnn_layer_times", "sdnn_plan_steps", "sdnn_step_plan", "sdnn_gather_rows",
                      "sdnn_bitmask_to_ids", "sdnn_flow_infer", "sdnn_infer_device_nvls",
-                     "sdnn_nvls_barrier", "sdnn_flow_plan"]:
+                     "sdnn_nvls_barrier", "sdnn_flow_plan", "sdnn_infer_submit",
+                     "sdnn_infer_wait"]:
             getattr(L, name).restype = I32
         _LIB = L
     return _LIB
@@ -322,6 +325,31 @@ class Net:
 
     def infer(self, rowptr, idx, val=None, want_y=False):
         return sdnn_infer(self.h, rowptr, idx, val, self.n, want_y)
+
+    def infer_submit(self, rowptr, idx, val=None):
+        """sdnn_infer_submit: enqueue a host-buffer inference, return its ticket.
+        The arrays must stay alive and unchanged until infer_wait returns (they
+        are kept referenced by the handle until then)."""
+        rowptr = np.ascontiguousarray(rowptr, np.int64)
+        idx = np.ascontiguousarray(idx, np.int32)
+        val = None if val is None else np.ascontiguousarray(val, np.float32)
+        t = ctypes.c_int64()
+        _check(lib().sdnn_infer_submit(self.h, _p(rowptr), _p(idx), _p(val), rowptr.size - 1, ctypes.byref(t)))
+        if not hasattr(self, "_inflight"):
+            self._inflight = {}
+        self._inflight[t.value] = (rowptr, idx, val)
+        return t.value
+
+    def infer_wait(self, ticket):
+        """sdnn_infer_wait: the ascending category ids of a submitted inference."""
+        rowptr = self._inflight[ticket][0]
+        cats = np.empty(max(rowptr.size - 1, 1), np.int32)
+        n = ctypes.c_int64()
+        try:
+            _check(lib().sdnn_infer_wait(self.h, int(ticket), _p(cats), ctypes.byref(n)))
+        finally:
+            del self._inflight[ticket]
+        return cats[:n.value].copy()
 
     def infer_device(self, d_rowptr, d_idx, d_val, batch, d_alive, d_y_out=None, stream=0):
         sdnn_infer_device(self.h, d_rowptr, d_idx, d_val, batch, d_alive, d_y_out, stream)

@@ -68,6 +68,21 @@ struct Arena {
 
 }  // namespace
 
+// one input slot of the host-buffer inference (api.cu host_enqueue)
+struct HostSlot {
+  int64_t *d_rowptr = nullptr;
+  int32_t *d_idx = nullptr;
+  float *d_val = nullptr;
+  int64_t cap_rows = -1, cap_nnz = -1, cap_val = -1;
+  int32_t *h_res = nullptr;            // pinned: [0] = category count, [1..] = ids
+  int64_t h_res_cap = 0, batch = 0;
+  cudaEvent_t done = nullptr;          // result copied back
+  cudaEvent_t in_free = nullptr;       // the slot's device input buffers consumed
+  std::thread validator;
+  sdnn_status vst = SDNN_OK;
+  std::string vmsg;
+};
+
 struct sdnn_net {
   int32_t n = 0, L = 0;
   sdnn_opts opts{-1, 0u, 32.f, nullptr, -1, -1, -1, 0};
@@ -120,11 +135,11 @@ struct sdnn_net {
   cudaGraphExec_t chain = nullptr;
   bool chain_compact = false;
   int64_t chain_launches = 0;
-  // device staging of Y0 for the host call
-  int64_t *d_rowptr = nullptr;
-  int32_t *d_idx = nullptr;
-  float *d_val = nullptr;
-  int64_t cap_rows = -1, cap_nnz = -1, cap_val = -1;
+  // host-buffer inference: two input slots (sdnn_infer uses slot 0;
+  // sdnn_infer_submit alternates) and the outstanding tickets
+  HostSlot slots[2];
+  int64_t pending[2] = {-1, -1};
+  int64_t next_ticket = 0;
   // input stream of sdnn_infer, its events (staging slots, per-chunk arrival)
   cudaStream_t in_s = nullptr;
   cudaEvent_t ev_stage[2] = {nullptr, nullptr};
@@ -1181,6 +1196,184 @@ extern "C" sdnn_status sdnn_flow_infer(sdnn_net *const *nets, int32_t parts, con
 }
 
 namespace {
+// The host-buffer inference, split so that it can be pipelined
+// (sdnn_infer_submit / sdnn_infer_wait): host_enqueue validates rowptr, starts
+// the full host validation on its own thread, enqueues the chunked input copy
+// (input stream), the densify + layer chain + readout (compute stream) and the
+// copy of the categories into the slot's pinned result buffer; host_finish
+// joins the validation and waits for the result.  Two input slots: the copy of
+// submission k+1 (slot (k+1) & 1) overlaps the layers of submission k, and
+// waits (on the device) until the scatter of submission k-1 has consumed that
+// slot's buffers.
+sdnn_status host_enqueue(sdnn_net *net, int slot_i, const int64_t *y0_rowptr, const int32_t *y0_idx,
+                         const float *y0_val, int64_t batch) {
+  HostSlot &H = net->slots[slot_i];
+  sdnn_status st = SDNN_OK;
+  const int64_t nnz = y0_rowptr[batch];
+  if (nnz > 0 && !y0_idx) return fail(SDNN_E_ARG, "y0_idx is NULL");
+  // rowptr must be sane before its last entry sizes the copies below; the full
+  // validation runs on the host while the (page-locked) input is in flight
+  if (!(net->opts.flags & SDNN_F_TRUST_INPUT)) {
+    if (y0_rowptr[0] != 0) return fail(SDNN_E_FORMAT, "y0_rowptr[0] != 0");
+    for (int64_t i = 0; i < batch; ++i)
+      if (y0_rowptr[i + 1] < y0_rowptr[i]) return fail(SDNN_E_FORMAT, "y0_rowptr not non-decreasing");
+  }
+  cudaStream_t s = net->opts.stream ? (cudaStream_t)net->opts.stream : net->own;
+  if (!net->in_s) CK(cudaStreamCreateWithFlags(&net->in_s, cudaStreamNonBlocking));
+  if (!H.done) CK(cudaEventCreateWithFlags(&H.done, cudaEventDisableTiming));
+  if (!H.in_free) CK(cudaEventCreateWithFlags(&H.in_free, cudaEventDisableTiming));
+  // device input buffers of the slot (grow-only; a growing slot first waits
+  // for its previous use)
+  if (batch + 1 > H.cap_rows || nnz > H.cap_nnz || (y0_val && nnz > H.cap_val)) CK(cudaEventSynchronize(H.in_free));
+  if (batch + 1 > H.cap_rows) {
+    cudaFree(H.d_rowptr);
+    H.d_rowptr = nullptr;
+    CK(cudaMalloc(&H.d_rowptr, sizeof(int64_t) * (batch + 1)));
+    H.cap_rows = batch + 1;
+  }
+  if (nnz > H.cap_nnz) {
+    cudaFree(H.d_idx);
+    H.d_idx = nullptr;
+    CK(cudaMalloc(&H.d_idx, sizeof(int32_t) * std::max<int64_t>(nnz, 1)));
+    H.cap_nnz = nnz;
+  }
+  if (y0_val && nnz > H.cap_val) {
+    cudaFree(H.d_val);
+    H.d_val = nullptr;
+    CK(cudaMalloc(&H.d_val, sizeof(float) * std::max<int64_t>(nnz, 1)));
+    H.cap_val = nnz;
+  }
+  if (batch + 1 > H.h_res_cap) {
+    CK(cudaEventSynchronize(H.done));
+    if (H.h_res) cudaFreeHost(H.h_res);
+    H.h_res = nullptr;
+    H.h_res_cap = 0;
+    CK(cudaHostAlloc((void **)&H.h_res, sizeof(int32_t) * (size_t)(batch + 1), cudaHostAllocDefault));
+    H.h_res_cap = batch + 1;
+  }
+  H.batch = batch;
+  // Input path (A14: the copies are inside the timed call).  rowptr first (the
+  // device prep -- zero Y0, row flags, scan -- needs only it), then the column
+  // indices in row chunks of ~64 MB on the input stream, each chunk scattered
+  // on the compute stream as soon as it has landed, so the copy of chunk c+1
+  // overlaps the scatter of chunk c; page-locked caller buffers are DMA'd
+  // directly, pageable ones through a pinned double buffer.  Explicit values
+  // (y0_val) are needed by the row flags, so they are copied up front.  The
+  // full host validation (index range, duplicates, finite values) runs on a
+  // separate host thread meanwhile and is joined in host_finish; the device
+  // path is memory-safe on invalid input (out-of-range indices are skipped).
+  const size_t kChunk = size_t(64) << 20;
+  char *stage = (char *)grow_pinned(net, 2 * kChunk);
+  if (!stage) return fail(SDNN_E_NOMEM, "pinned staging allocation failed");
+  auto is_pinned = [](const void *p) {
+    cudaPointerAttributes pa;
+    const bool r = cudaPointerGetAttributes(&pa, p) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    return r;
+  };
+  H.vst = SDNN_OK;
+  H.vmsg.clear();
+  if (!(net->opts.flags & SDNN_F_TRUST_INPUT) && batch > 0)
+    H.validator = std::thread([net, &H, y0_rowptr, y0_idx, y0_val, batch] {
+      H.vst = validate_y0(net->n, y0_rowptr, y0_idx, y0_val, batch);
+      if (H.vst) H.vmsg = sdnn_last_error();
+    });
+  auto abort_enqueue = [&](sdnn_status e) -> sdnn_status {
+    if (H.validator.joinable()) H.validator.join();
+    cudaStreamSynchronize(s);                    // no DMA may still read the caller's buffers
+    cudaStreamSynchronize(net->in_s);
+    return e;
+  };
+  int sslot = 0;
+  bool used[2] = {false, false};
+  auto copy_h2d = [&](void *d, const void *h, size_t bytes, cudaStream_t cs, bool pinned) -> sdnn_status {
+    if (bytes == 0) return SDNN_OK;
+    if (pinned) {
+      CK(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, cs));
+      return SDNN_OK;
+    }
+    for (size_t off = 0; off < bytes; off += kChunk) {
+      const size_t b = std::min(kChunk, bytes - off);
+      if (used[sslot]) CK(cudaEventSynchronize(net->ev_stage[sslot]));
+      char *dst = stage + sslot * kChunk;
+      const char *src = (const char *)h + off;
+      parallel_for((int64_t)b, std::min(nthreads_default(), 8),
+                   [&](int64_t x, int64_t y) { std::memcpy(dst + x, src + x, (size_t)(y - x)); });
+      CK(cudaMemcpyAsync((char *)d + off, dst, b, cudaMemcpyHostToDevice, cs));
+      CK(cudaEventRecord(net->ev_stage[sslot], cs));
+      used[sslot] = true;
+      sslot ^= 1;
+    }
+    return SDNN_OK;
+  };
+  for (int i = 0; i < 2; ++i)
+    if (!net->ev_stage[i]) CK(cudaEventCreateWithFlags(&net->ev_stage[i], cudaEventDisableTiming));
+  // this slot's buffers are free once the previous scatter from them is done
+  CK(cudaStreamWaitEvent(net->in_s, H.in_free, 0));
+  if ((st = copy_h2d(H.d_rowptr, y0_rowptr, sizeof(int64_t) * (size_t)(batch + 1), net->in_s,
+                     is_pinned(y0_rowptr))) ||
+      (y0_val && (st = copy_h2d(H.d_val, y0_val, sizeof(float) * (size_t)nnz, net->in_s, is_pinned(y0_val)))))
+    return abort_enqueue(st);
+  if (!net->ev_in) CK(cudaEventCreateWithFlags(&net->ev_in, cudaEventDisableTiming));
+  CK(cudaEventRecord(net->ev_in, net->in_s));
+  CK(cudaStreamWaitEvent(s, net->ev_in, 0));       // rowptr (and values) on the device
+  const bool idx_pinned = nnz > 0 && is_pinned(y0_idx);
+  // row chunks of ~kChunk bytes of indices
+  std::vector<int64_t> cut{0};
+  {
+    const int64_t per = (int64_t)(kChunk / sizeof(int32_t));
+    int64_t r = 0;
+    while (r < batch) {
+      const int64_t lim = y0_rowptr[r] + per;
+      int64_t hi = std::upper_bound(y0_rowptr + r + 1, y0_rowptr + batch + 1, lim) - y0_rowptr - 1;
+      if (hi <= r) hi = r + 1;                   // one row larger than a chunk
+      r = std::min(hi, batch);
+      cut.push_back(r);
+    }
+  }
+  while (net->ev_chunk.size() + 1 < cut.size()) {
+    cudaEvent_t e;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    net->ev_chunk.push_back(e);
+  }
+  const Feed feed = [&](cudaStream_t cs) -> sdnn_status {
+    for (size_t c = 0; c + 1 < cut.size(); ++c) {
+      const int64_t r0 = cut[c], r1 = cut[c + 1];
+      const int64_t e0 = y0_rowptr[r0], e1 = y0_rowptr[r1];
+      sdnn_status s2 = copy_h2d(H.d_idx + e0, y0_idx + e0, sizeof(int32_t) * (size_t)(e1 - e0), net->in_s,
+                                idx_pinned);
+      if (s2) return s2;
+      CK(cudaEventRecord(net->ev_chunk[c], net->in_s));
+      CK(cudaStreamWaitEvent(cs, net->ev_chunk[c], 0));
+      launch_scatter_rows(net->cfg, net->ws, net->n, r0, r1, H.d_rowptr, H.d_idx,
+                          y0_val ? H.d_val : nullptr, cs);
+    }
+    CK(cudaEventRecord(H.in_free, cs));           // the slot's input buffers are consumed
+    return SDNN_OK;
+  };
+  st = infer_device_impl(net, H.d_rowptr, H.d_idx, y0_val ? H.d_val : nullptr, batch, nullptr, nullptr, s,
+                         &feed);
+  if (st) return abort_enqueue(st);
+  // result: [0] = count, [1..] = the ascending ids (the capacity of the batch)
+  CK(cudaMemcpyAsync(H.h_res, net->ws.ncat, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  if (batch > 0)
+    CK(cudaMemcpyAsync(H.h_res + 1, net->ws.cats, sizeof(int32_t) * (size_t)batch, cudaMemcpyDeviceToHost, s));
+  CK(cudaEventRecord(H.done, s));
+  return SDNN_OK;
+}
+
+sdnn_status host_finish(sdnn_net *net, int slot_i, int32_t *categories, int64_t *n_categories) {
+  HostSlot &H = net->slots[slot_i];
+  if (H.validator.joinable()) H.validator.join();
+  CK(cudaEventSynchronize(H.done));
+  if (H.vst) return fail(H.vst, H.vmsg);
+  const int32_t ncat = H.h_res[0];
+  if (ncat > 0) std::memcpy(categories, H.h_res + 1, sizeof(int32_t) * (size_t)ncat);
+  *n_categories = ncat;
+  net->last_ncat = ncat;
+  return SDNN_OK;
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -1413,162 +1606,52 @@ sdnn_status sdnn_infer(sdnn_net *net, const int64_t *y0_rowptr, const int32_t *y
   if (batch > 0 && !categories) return fail(SDNN_E_ARG, "categories is NULL");
   sdnn_status st = set_device(net);
   if (st) return st;
-  const int64_t nnz = y0_rowptr[batch];
-  if (nnz > 0 && !y0_idx) return fail(SDNN_E_ARG, "y0_idx is NULL");
-  // rowptr must be sane before its last entry sizes the copies below; the full
-  // validation runs on the host while the (page-locked) input is in flight
-  if (!(net->opts.flags & SDNN_F_TRUST_INPUT)) {
-    if (y0_rowptr[0] != 0) return fail(SDNN_E_FORMAT, "y0_rowptr[0] != 0");
-    for (int64_t i = 0; i < batch; ++i)
-      if (y0_rowptr[i + 1] < y0_rowptr[i]) return fail(SDNN_E_FORMAT, "y0_rowptr not non-decreasing");
-  }
-  cudaStream_t s = net->opts.stream ? (cudaStream_t)net->opts.stream : net->own;
-  // device input buffers (grow-only)
-  if (batch + 1 > net->cap_rows) {
-    cudaFree(net->d_rowptr);
-    net->d_rowptr = nullptr;
-    CK(cudaMalloc(&net->d_rowptr, sizeof(int64_t) * (batch + 1)));
-    net->cap_rows = batch + 1;
-  }
-  if (nnz > net->cap_nnz) {
-    cudaFree(net->d_idx);
-    net->d_idx = nullptr;
-    CK(cudaMalloc(&net->d_idx, sizeof(int32_t) * std::max<int64_t>(nnz, 1)));
-    net->cap_nnz = nnz;
-  }
-  if (y0_val && nnz > net->cap_val) {
-    cudaFree(net->d_val);
-    net->d_val = nullptr;
-    CK(cudaMalloc(&net->d_val, sizeof(float) * std::max<int64_t>(nnz, 1)));
-    net->cap_val = nnz;
-  }
-  // Input path (A14: the copies are inside the timed call).  rowptr first (the
-  // device prep -- zero Y0, row flags, scan -- needs only it), then the column
-  // indices in row chunks of ~64 MB on the input stream, each chunk scattered
-  // on the compute stream as soon as it has landed, so the copy of chunk c+1
-  // overlaps the scatter of chunk c; page-locked caller buffers are DMA'd
-  // directly, pageable ones through a pinned double buffer.  Explicit values
-  // (y0_val) are needed by the row flags, so they are copied up front.  The
-  // full host validation (index range, duplicates, finite values) runs on a
-  // separate host thread meanwhile and is joined before returning; the device
-  // path is memory-safe on invalid input (out-of-range indices are skipped).
-  if (!net->in_s) CK(cudaStreamCreateWithFlags(&net->in_s, cudaStreamNonBlocking));
-  const size_t kChunk = size_t(64) << 20;
-  char *stage = (char *)grow_pinned(net, 2 * kChunk);
-  if (!stage) return fail(SDNN_E_NOMEM, "pinned staging allocation failed");
-  auto is_pinned = [](const void *p) {
-    cudaPointerAttributes pa;
-    const bool r = cudaPointerGetAttributes(&pa, p) == cudaSuccess && pa.type == cudaMemoryTypeHost;
-    cudaGetLastError();
-    return r;
-  };
-  sdnn_status vst = SDNN_OK;
-  std::string vmsg;
-  std::thread validator;
-  if (!(net->opts.flags & SDNN_F_TRUST_INPUT) && batch > 0)
-    validator = std::thread([&] {
-      vst = validate_y0(net->n, y0_rowptr, y0_idx, y0_val, batch);
-      if (vst) vmsg = sdnn_last_error();
-    });
-  auto join_validator = [&]() -> sdnn_status {
-    if (validator.joinable()) validator.join();
-    if (vst) {
-      cudaStreamSynchronize(s);                  // no DMA may still read the caller's buffers
-      cudaStreamSynchronize(net->in_s);
-      return fail(vst, vmsg);
-    }
-    return SDNN_OK;
-  };
-  // synchronous small copies (rowptr; values when given)
-  int slot = 0;
-  bool used[2] = {false, false};
-  auto copy_h2d = [&](void *d, const void *h, size_t bytes, cudaStream_t cs, bool pinned) -> sdnn_status {
-    if (bytes == 0) return SDNN_OK;
-    if (pinned) {
-      CK(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, cs));
-      return SDNN_OK;
-    }
-    for (size_t off = 0; off < bytes; off += kChunk) {
-      const size_t b = std::min(kChunk, bytes - off);
-      if (used[slot]) CK(cudaEventSynchronize(net->ev_stage[slot]));
-      char *dst = stage + slot * kChunk;
-      const char *src = (const char *)h + off;
-      parallel_for((int64_t)b, std::min(nthreads_default(), 8),
-                   [&](int64_t x, int64_t y) { std::memcpy(dst + x, src + x, (size_t)(y - x)); });
-      CK(cudaMemcpyAsync((char *)d + off, dst, b, cudaMemcpyHostToDevice, cs));
-      CK(cudaEventRecord(net->ev_stage[slot], cs));
-      used[slot] = true;
-      slot ^= 1;
-    }
-    return SDNN_OK;
-  };
-  for (int i = 0; i < 2; ++i)
-    if (!net->ev_stage[i]) CK(cudaEventCreateWithFlags(&net->ev_stage[i], cudaEventDisableTiming));
-  // the input stream starts after everything earlier on s (buffer reuse)
-  if (!net->ev_in) CK(cudaEventCreateWithFlags(&net->ev_in, cudaEventDisableTiming));
-  CK(cudaEventRecord(net->ev_in, s));
-  CK(cudaStreamWaitEvent(net->in_s, net->ev_in, 0));
-  if ((st = copy_h2d(net->d_rowptr, y0_rowptr, sizeof(int64_t) * (size_t)(batch + 1), s, is_pinned(y0_rowptr))) ||
-      (y0_val && (st = copy_h2d(net->d_val, y0_val, sizeof(float) * (size_t)nnz, s, is_pinned(y0_val))))) {
-    join_validator();
-    return st;
-  }
-  const bool idx_pinned = nnz > 0 && is_pinned(y0_idx);
-  // row chunks of ~kChunk bytes of indices
-  std::vector<int64_t> cut{0};
-  {
-    const int64_t per = (int64_t)(kChunk / sizeof(int32_t));
-    int64_t r = 0;
-    while (r < batch) {
-      const int64_t lim = y0_rowptr[r] + per;
-      int64_t hi = std::upper_bound(y0_rowptr + r + 1, y0_rowptr + batch + 1, lim) - y0_rowptr - 1;
-      if (hi <= r) hi = r + 1;                   // one row larger than a chunk
-      r = std::min(hi, batch);
-      cut.push_back(r);
-    }
-  }
-  while (net->ev_chunk.size() + 1 < cut.size()) {
-    cudaEvent_t e;
-    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    net->ev_chunk.push_back(e);
-  }
-  const Feed feed = [&](cudaStream_t cs) -> sdnn_status {
-    for (size_t c = 0; c + 1 < cut.size(); ++c) {
-      const int64_t r0 = cut[c], r1 = cut[c + 1];
-      const int64_t e0 = y0_rowptr[r0], e1 = y0_rowptr[r1];
-      sdnn_status s2 = copy_h2d(net->d_idx + e0, y0_idx + e0, sizeof(int32_t) * (size_t)(e1 - e0), net->in_s,
-                                idx_pinned);
-      if (s2) return s2;
-      CK(cudaEventRecord(net->ev_chunk[c], net->in_s));
-      CK(cudaStreamWaitEvent(cs, net->ev_chunk[c], 0));
-      launch_scatter_rows(net->cfg, net->ws, net->n, r0, r1, net->d_rowptr, net->d_idx,
-                          y0_val ? net->d_val : nullptr, cs);
-    }
-    return SDNN_OK;
-  };
-  st = infer_device_impl(net, net->d_rowptr, net->d_idx, y0_val ? net->d_val : nullptr, batch,
-                         nullptr, nullptr, s, &feed);
-  if (st) {
-    join_validator();
-    return st;
-  }
-  if ((st = join_validator())) return st;
+  if (net->pending[0] >= 0 || net->pending[1] >= 0)
+    return fail(SDNN_E_STATE, "submitted inferences are outstanding (sdnn_infer_wait first)");
+  if ((st = host_enqueue(net, 0, y0_rowptr, y0_idx, y0_val, batch))) return st;
   float *d_yout = nullptr;
+  cudaStream_t s = net->opts.stream ? (cudaStream_t)net->opts.stream : net->own;
   if (y_out && batch > 0) {
     CK(cudaMalloc(&d_yout, sizeof(float) * (size_t)net->n * (size_t)batch));
     launch_final_yout(net, batch, d_yout, s);
   }
-  int32_t ncat = 0;
-  CK(cudaMemcpyAsync(&ncat, net->ws.ncat, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  if (ncat > 0) CK(cudaMemcpy(categories, net->ws.cats, sizeof(int32_t) * ncat, cudaMemcpyDeviceToHost));
+  if ((st = host_finish(net, 0, categories, n_categories))) {
+    cudaFree(d_yout);
+    return st;
+  }
   if (d_yout) {
     CK(cudaMemcpy(y_out, d_yout, sizeof(float) * (size_t)net->n * (size_t)batch, cudaMemcpyDeviceToHost));
     cudaFree(d_yout);
   }
-  *n_categories = ncat;
-  net->last_ncat = ncat;
   return SDNN_OK;
+}
+
+sdnn_status sdnn_infer_submit(sdnn_net *net, const int64_t *y0_rowptr, const int32_t *y0_idx,
+                              const float *y0_val, int64_t batch, int64_t *ticket) {
+  if (!net || !y0_rowptr || !ticket) return fail(SDNN_E_ARG, "NULL argument");
+  if (batch < 0) return fail(SDNN_E_ARG, "batch < 0");
+  if (batch > (int64_t(1) << 30)) return fail(SDNN_E_UNSUPPORTED, "batch > 2^30");
+  sdnn_status st = set_device(net);
+  if (st) return st;
+  const int64_t t = net->next_ticket;
+  const int slot = (int)(t & 1);
+  if (net->pending[slot] >= 0) return fail(SDNN_E_STATE, "two submissions outstanding: sdnn_infer_wait first");
+  if ((st = host_enqueue(net, slot, y0_rowptr, y0_idx, y0_val, batch))) return st;
+  net->pending[slot] = t;
+  net->next_ticket = t + 1;
+  *ticket = t;
+  return SDNN_OK;
+}
+
+sdnn_status sdnn_infer_wait(sdnn_net *net, int64_t ticket, int32_t *categories, int64_t *n_categories) {
+  if (!net || !n_categories) return fail(SDNN_E_ARG, "NULL argument");
+  const int slot = (int)(ticket & 1);
+  if (ticket < 0 || net->pending[slot] != ticket) return fail(SDNN_E_STATE, "unknown or finished ticket");
+  if (net->slots[slot].batch > 0 && !categories) return fail(SDNN_E_ARG, "categories is NULL");
+  sdnn_status st = set_device(net);
+  if (st) return st;
+  net->pending[slot] = -1;
+  return host_finish(net, slot, categories, n_categories);
 }
 
 sdnn_status sdnn_infer_device_nvls(sdnn_net *net, const int64_t *d_rowptr, const int32_t *d_idx,
@@ -1765,9 +1848,15 @@ void sdnn_destroy(sdnn_net *net) {
   if (net->copy_s) cudaStreamDestroy(net->copy_s);
   if (net->ev_fork) cudaEventDestroy(net->ev_fork);
   if (net->ev_join) cudaEventDestroy(net->ev_join);
-  cudaFree(net->d_rowptr);
-  cudaFree(net->d_idx);
-  cudaFree(net->d_val);
+  for (HostSlot &H : net->slots) {
+    if (H.validator.joinable()) H.validator.join();
+    cudaFree(H.d_rowptr);
+    cudaFree(H.d_idx);
+    cudaFree(H.d_val);
+    if (H.h_res) cudaFreeHost(H.h_res);
+    if (H.done) cudaEventDestroy(H.done);
+    if (H.in_free) cudaEventDestroy(H.in_free);
+  }
   if (net->h_stage) cudaFreeHost(net->h_stage);
   if (net->in_s) cudaStreamDestroy(net->in_s);
   for (auto e : net->ev_stage) if (e) cudaEventDestroy(e);

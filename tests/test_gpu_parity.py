@@ -633,3 +633,33 @@ def test_blocked_layout_on_off(sd, monkeypatch, yblk, n, L, B):
     assert bool(st["path"] & 4) == (yblk == "1")     # lone layers run as one-layer passes
     assert_parity(cg, Yg, cats, Y)
     assert st["live_rows"] == prof
+
+
+def test_pipelined_submit_wait(sd, c1):
+    """sdnn_infer_submit / sdnn_infer_wait: two submissions in flight (the
+    second's input copy overlaps the first's layers), each bit-exact against
+    the oracle; a third submission, or sdnn_infer, while two are outstanding is
+    refused; invalid input is reported by the wait."""
+    spec, layers, rp, idx, cats, Y, prof = c1
+    rows = np.arange(0, 1000, 3)
+    srp, sidx, _ = oracle.subset_rows(rp, idx, None, rows)
+    with sd.Net.from_layers(1024, layers, fmt="ell") as net:
+        t0 = net.infer_submit(rp, idx)
+        t1 = net.infer_submit(srp, sidx)
+        with pytest.raises(sd.SdnnError) as e:
+            net.infer_submit(rp, idx)
+        assert e.value.status == sd.SDNN_E_STATE
+        with pytest.raises(sd.SdnnError):
+            net.infer(rp, idx, None)
+        assert np.array_equal(net.infer_wait(t0), np.flatnonzero(cats))
+        t2 = net.infer_submit(rp, idx)                      # slot of t0 again, t1 still in flight
+        assert np.array_equal(net.infer_wait(t1), np.flatnonzero(cats[rows]))
+        assert np.array_equal(net.infer_wait(t2), np.flatnonzero(cats))
+        bad = idx.copy()
+        bad[5] = 5000                                       # out of range: reported, device memory-safe
+        t3 = net.infer_submit(rp, bad)
+        with pytest.raises(sd.SdnnError) as e:
+            net.infer_wait(t3)
+        assert e.value.status == sd.SDNN_E_FORMAT
+        cg, _ = net.infer(rp, idx, None)                    # the handle is still usable
+        assert np.array_equal(cg, np.flatnonzero(cats))
