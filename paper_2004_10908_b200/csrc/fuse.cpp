@@ -296,7 +296,8 @@ std::vector<Step> plan_steps(const std::vector<const PackedLayer *> &layers, int
 }
 
 static void build_pass_impl(const std::vector<const PackedLayer *> &layers, int32_t n, const Step &s,
-                            int tile_floats, int cta_rows, PassHost &out, bool allow_dedup);
+                            int tile_floats, int cta_rows, PassHost &out, bool allow_dedup,
+                            bool allow_vt = true);
 
 void build_pass(const std::vector<const PackedLayer *> &layers, int32_t n, const Step &s,
                 int tile_floats, int cta_rows, PassHost &out, bool share_values) {
@@ -304,7 +305,7 @@ void build_pass(const std::vector<const PackedLayer *> &layers, int32_t n, const
 }
 
 static void build_pass_impl(const std::vector<const PackedLayer *> &layers, int32_t n, const Step &s,
-                            int tile_floats, int cta_rows, PassHost &out, bool allow_dedup) {
+                            int tile_floats, int cta_rows, PassHost &out, bool allow_dedup, bool allow_vt) {
   const int m = s.m;
   UF full, sub;
   full.init((int64_t)(m + 1) * n);
@@ -413,6 +414,33 @@ static void build_pass_impl(const std::vector<const PackedLayer *> &layers, int3
       out.in_count[(size_t)c * C + b] = (int32_t)rows.size();
     }
   out.layers.resize(m);
+  // Value tables for the passes of 16-position tiles (1024-row components: two
+  // 64 B rows share each 128 B shared-memory line, so two units of one
+  // quarter-warp phase that read rows of equal parity conflict): when the
+  // members of a group share one value (uniform weights, equal biases), a
+  // non-last layer b writes it twice into line q of table b & 1 -- copy 0 in
+  // the first 64 B, copy 1 in the second -- once every group has read its
+  // sources; the next layer's terms read line g(t), the unit in the first half
+  // of a phase copy 0 and the one in the second half copy 1, so every phase
+  // covers both bank halves.  Opt-in (SDNN_PASS_VT=1): exact, and it removes
+  // 91 % of the shared stores and a third of the load bank conflicts of these
+  // passes, but the C4 step was measured slower (1977 vs 1934 ms/step; the
+  // sampled pass read 10.4 instead of 7.6 GB from DRAM -- the two CTAs that
+  // share each 128 B line of the half-row loads drift apart).
+  static const bool vt_env = [] {
+    const char *e = getenv("SDNN_PASS_VT");
+    return e && atoi(e) == 1;
+  }();
+  bool vt = false;
+  if (vt_env && allow_vt && m >= 2 && C == 1 && out.T == 16) {
+    vt = true;
+    for (int b = 0; b + 1 < m && vt; ++b) {
+      const PackedLayer &p = *layers[s.a + b];
+      bool eq = p.uniform && p.gmax > 1;
+      for (int32_t j = 1; j < n && eq; ++j) eq = std::memcmp(&p.bias[j], &p.bias[0], 4) == 0;
+      vt = eq;
+    }
+  }
   // value sharing (SDNN_F_SHARE_VALUES, opt-in): in a layer with uniform
   // weights whose member biases are all equal, every member of a group has
   // bit-identical outputs, so a non-last layer stores the group's value once --
@@ -421,7 +449,7 @@ static void build_pass_impl(const std::vector<const PackedLayer *> &layers, int3
   // slot.  The chains are unchanged (same operands, same order); only the
   // shared-memory stores drop by the group size.  Measured on C4: 2021 vs 1945
   // ms/step (the 1024-row passes slow down: 3.92 vs 3.11 ms), so off by default.
-  const bool dedup_on = allow_dedup;
+  const bool dedup_on = allow_dedup && !vt;
   // A layer after a sharing layer reads shared slots, so it cannot overwrite its
   // sources in place: it must share too (or be the last layer) -- decided from
   // the back.
@@ -431,26 +459,6 @@ static void build_pass_impl(const std::vector<const PackedLayer *> &layers, int3
     bool eq = p.uniform && p.gmax > 1;           // (groups of one member gain nothing)
     for (int32_t j = 1; j < n && eq; ++j) eq = std::memcmp(&p.bias[j], &p.bias[0], 4) == 0;
     dedup[b] = eq && (b + 1 == m - 1 || dedup[b + 1]);
-  }
-  // Value table for the 2-layer passes of 16-position tiles (1024-row
-  // components: two 64 B rows share each 128 B shared-memory line, so two
-  // units of one quarter-warp phase that read rows of equal parity conflict):
-  // when layer 0's members of a group share one value (uniform weights, equal
-  // biases), the group writes that value twice into line q of a value table --
-  // copy 0 in the first 64 B, copy 1 in the second -- once every group has read
-  // its sources; layer 1's terms read line g(t), the unit in the first half of
-  // a phase copy 0 and the one in the second half copy 1, so every phase covers
-  // both bank halves.  SDNN_PASS_VT=0 disables.
-  static const bool vt_env = [] {
-    const char *e = getenv("SDNN_PASS_VT");
-    return !(e && atoi(e) == 0);
-  }();
-  bool vt = false;
-  if (vt_env && m == 2 && C == 1 && out.T == 16) {
-    const PackedLayer &p = *layers[s.a];
-    bool eq = p.uniform && p.gmax > 1;
-    for (int32_t j = 1; j < n && eq; ++j) eq = std::memcmp(&p.bias[j], &p.bias[0], 4) == 0;
-    vt = eq;
   }
   for (int b = 0; b < m; ++b) {
     const PackedLayer &p = *layers[s.a + b];
@@ -471,8 +479,13 @@ static void build_pass_impl(const std::vector<const PackedLayer *> &layers, int3
     H.NG = NG;
     H.wu = p.wu;
     H.dedup = dedup[b];
-    if (vt && b == 0 && 2 * NG > R) vt = false;   // the table must fit the tile
-    H.vt = vt ? (b == 0 ? 1 : 2) : 0;
+    if (vt && NG > 32) {                           // one round of units per layer (4 warps x 8 units),
+                                                   // so the table stores follow every read of the tile
+      build_pass_impl(layers, n, s, tile_floats, cta_rows, out, allow_dedup, false);
+      return;
+    }
+    // layer b (non-last) writes table b & 1 (lines 0.. or 256..), layer b > 0 reads table (b-1) & 1
+    H.vt = vt ? ((last ? 0 : 1 | ((b & 1) << 2)) | (b > 0 ? 2 : 0)) : 0;
     const size_t units = (size_t)ncomp * C;
     H.src.assign(units * NG * 32, 0);
     H.bias.assign(units * NG * 32, 0.f);
@@ -508,8 +521,8 @@ static void build_pass_impl(const std::vector<const PackedLayer *> &layers, int3
           H.bias[rec * 32 + u] = p.bias[j];
           if (last)
             H.orow[rec * 32 + u] = (uint16_t)j;
-          else if (vt)                       // value table: line = record index q
-            slot[out0 + j] = (int32_t)q;
+          else if (vt)                       // value table b & 1: line = record index q
+            slot[out0 + j] = (b & 1) * 256 + (int32_t)q;
           else if (!dedup[b])                // member u overwrites the slot of source u
             slot[out0 + j] = code[u];
         }
@@ -524,7 +537,7 @@ static void build_pass_impl(const std::vector<const PackedLayer *> &layers, int3
         if (!excl) {
           while (next_free < R && live[next_free]) ++next_free;
           if (next_free >= R) {                 // no free slot left: build without sharing
-            build_pass_impl(layers, n, s, tile_floats, cta_rows, out, false);
+            build_pass_impl(layers, n, s, tile_floats, cta_rows, out, false, allow_vt);
             return;
           }
           vcode = (code0[q] & ~0x3ff) | next_free;
@@ -579,6 +592,9 @@ static void build_pass_impl(const std::vector<const PackedLayer *> &layers, int3
     }
   }
   out.rec_bytes = off;
+  if (getenv("SDNN_PLAN_DEBUG"))
+    fprintf(stderr, "pass a=%d m=%d R=%d T=%d C=%d ncomp=%d rec=%d vt=%d/%d share=%d\n", s.a, m, R, out.T, C, ncomp,
+            off, out.layers[0].vt, m > 1 ? out.layers[1].vt : -1, (int)allow_dedup);
   // components of <= 128 rows: two half-size tiles per CTA (double-buffered)
   // when both records fit and a kernel instance exists (SDNN_PASS_NB=1: off).
   // Measured on C4: 128-row passes 2.69 ms (T = 64 x 2) vs 2.75 ms (T = 128);

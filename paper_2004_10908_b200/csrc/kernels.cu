@@ -940,7 +940,9 @@ __global__ void __launch_bounds__(32 * kPassNW, 3)
       // the last layer releases the tiles before its HBM stores when every warp
       // owns at most one unit per segment (one round)
       const bool early = last && units <= NW * UPW;
-      const bool vtw = PL.vt == 1, vtr = PL.vt == 2;     // value table write / read (fuse.cpp)
+      // value tables (fuse.cpp): write into table (vt >> 2) & 1, read the other
+      const bool vtw = PL.vt & 1, vtr = PL.vt & 2;
+      const int vtline = ((PL.vt >> 2) & 1) * 256;
       if (remote) cluster_sync();                // every CTA's tile is at boundary m-1
       for (int u0 = 0; u0 < units; u0 += NW * UPW) {
         const int u = u0 + warp * UPW + seg;
@@ -1028,8 +1030,8 @@ __global__ void __launch_bounds__(32 * kPassNW, 3)
           // tile rows), then line gi = [copy 0 | copy 1] of the group's value
           __syncthreads();
           if (G > 0) {
-            *reinterpret_cast<float4 *>(tile_s + gi * 32 + pa) = yu;
-            *reinterpret_cast<float4 *>(tile_s + gi * 32 + 16 + pa) = yu;
+            *reinterpret_cast<float4 *>(tile_s + (vtline + gi) * 32 + pa) = yu;
+            *reinterpret_cast<float4 *>(tile_s + (vtline + gi) * 32 + 16 + pa) = yu;
           }
         } else if (!last && PL.off_vs >= 0) {
           // shared value: one store per group into its value slot (the next
