@@ -663,3 +663,20 @@ def test_pipelined_submit_wait(sd, c1):
         assert e.value.status == sd.SDNN_E_FORMAT
         cg, _ = net.infer(rp, idx, None)                    # the handle is still usable
         assert np.array_equal(cg, np.flatnonzero(cats))
+
+
+@pytest.mark.parametrize("env,flags", [({"SDNN_PASS_VT": "1"}, 0), ({"SDNN_PASS_TMA16": "1"}, 0),
+                                       ({"SDNN_BLK16": "1"}, 0), ({"SDNN_PASS_ORDER": "tile"}, 0),
+                                       ({"SDNN_PASS_NB": "1", "SDNN_PASS_X2": "1"}, 0), ({}, 512)])
+def test_opt_in_knobs(sd, env, flags):
+    """The measured-off alternatives stay exact (each in a fresh process, since
+    the library reads its knobs once): value tables, TMA tensor-map loads and
+    16-position blocks for the 1024-row passes, tile-major order everywhere,
+    single tile buffers with packed FFMA2, shared-value stores."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    out = subprocess.run([sys.executable, os.path.join(here, "_knob_check.py"), str(flags)],
+                         env=dict(os.environ, **env), capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and "OK" in out.stdout, out.stderr[-2000:]
