@@ -1262,7 +1262,11 @@ sdnn_status host_enqueue(sdnn_net *net, int slot_i, const int64_t *y0_rowptr, co
   // full host validation (index range, duplicates, finite values) runs on a
   // separate host thread meanwhile and is joined in host_finish; the device
   // path is memory-safe on invalid input (out-of-range indices are skipped).
-  const size_t kChunk = size_t(64) << 20;
+  static const size_t kChunk = [] {               // SDNN_IN_CHUNK_MB: A/B knob (default 64)
+    const char *e = getenv("SDNN_IN_CHUNK_MB");
+    const long v = e ? atol(e) : 64;
+    return size_t(std::max(1L, std::min(v, 4096L))) << 20;
+  }();
   char *stage = (char *)grow_pinned(net, 2 * kChunk);
   if (!stage) return fail(SDNN_E_NOMEM, "pinned staging allocation failed");
   auto is_pinned = [](const void *p) {
