@@ -609,19 +609,20 @@ __device__ __forceinline__ int64_t yix(int64_t r, int64_t p, int64_t stride, int
   return yblk ? (((p >> lg) * yblk + r) << lg) + (p & ((1 << lg) - 1)) : r * stride + p;
 }
 
-__global__ void k_scatter(int64_t r0, int64_t r1, const int64_t *__restrict__ rowptr,
-                          const int32_t *__restrict__ idx, const float *__restrict__ val,
-                          const uint32_t *__restrict__ inmask, const int32_t *__restrict__ wpre,
-                          float *Y0, int32_t *rid0, int64_t stride, int32_t yblk,
-                          const int32_t *__restrict__ sig0, int lg, int32_t n) {
-  const int lane = threadIdx.x & 31;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t i = r0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); i < r1; i += nw) {
+// one CTA per input row (MNIST-shaped rows hold ~8,500 of 65,536 entries: a
+// warp per row left a long serial tail in every chunk of the e2e input path)
+__global__ void __launch_bounds__(256) k_scatter(int64_t r0, int64_t r1, const int64_t *__restrict__ rowptr,
+                                                 const int32_t *__restrict__ idx, const float *__restrict__ val,
+                                                 const uint32_t *__restrict__ inmask,
+                                                 const int32_t *__restrict__ wpre, float *Y0, int32_t *rid0,
+                                                 int64_t stride, int32_t yblk, const int32_t *__restrict__ sig0,
+                                                 int lg, int32_t n) {
+  for (int64_t i = r0 + blockIdx.x; i < r1; i += gridDim.x) {
     const uint32_t word = inmask[i >> 5];
     if (!((word >> (i & 31)) & 1u)) continue;
     const int64_t pos = wpre[i >> 5] + __popc(word & ((1u << (i & 31)) - 1u));
-    if (lane == 0) rid0[pos] = (int32_t)i;
-    for (int64_t e = rowptr[i] + lane; e < rowptr[i + 1]; e += 32) {
+    if (threadIdx.x == 0) rid0[pos] = (int32_t)i;
+    for (int64_t e = rowptr[i] + threadIdx.x; e < rowptr[i + 1]; e += blockDim.x) {
       const int32_t k = idx[e];
       // an out-of-range index is never written (sdnn_infer validates Y0 on
       // the host concurrently and reports it; the device stays memory-safe)
@@ -1606,7 +1607,7 @@ void launch_densify_prep(const LaunchCfg &c, const Workspace &w, int32_t n, int6
 void launch_scatter_rows(const LaunchCfg &c, const Workspace &w, int32_t n, int64_t r0, int64_t r1,
                          const int64_t *rowptr, const int32_t *idx, const float *val, cudaStream_t s) {
   if (r1 > r0)
-    k_scatter<<<(int)std::min<int64_t>(c.sms * 8, (r1 - r0 + 7) / 8), 256, 0, s>>>(
+    k_scatter<<<(int)std::min<int64_t>(c.sms * 8, r1 - r0), 256, 0, s>>>(
         r0, r1, rowptr, idx, val, w.inmask, w.wpre, w.Y[0], w.rid[0], w.stride, w.yblk, w.sig0, w.lg0, n);
 }
 

@@ -537,6 +537,14 @@ def test_full_size_c4(sd):
 
 
 @pytest.mark.slow
+def test_full_size_plain_schedule_c3(sd):
+    """SURVEY 8.4's non-overlapping field schedule (R-W5) at C3 size: a
+    different pass structure (2-layer passes of 1024-row components)."""
+    cats, st, oY = _full_size(sd, g.rn_plain_spec(16384, 1920), 64)
+    assert st["fused_layers"] == 1920 and 0.2 * 60000 < cats.size < 0.7 * 60000
+
+
+@pytest.mark.slow
 def test_full_size_per_slot_weights_c3_width(sd):
     """General weights (one fp32 value per slot, RN structure, bias chosen so
     ~45 % of the rows survive) at C3 width on the full 60,000-input batch."""
