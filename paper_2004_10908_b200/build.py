@@ -14,7 +14,7 @@ ROOT = os.path.dirname(HERE)
 # loads the same SDNN_LIB path
 SO = os.environ.get("SDNN_LIB") or os.path.join(HERE, "libsdnn.so")
 EXTRA = os.environ.get("SDNN_NVCC_FLAGS", "").split()
-SOURCES = ["api.cu", "kernels.cu", "resident.cu", "pack.cpp", "fuse.cpp"]
+SOURCES = ["api.cu", "kernels.cu", "pass_wide.cu", "resident.cu", "pack.cpp", "fuse.cpp"]
 HEADERS = ["sdnn_internal.h", "device_util.cuh", os.path.join("..", "..", "include", "sdnn.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2,-pthread",

@@ -88,6 +88,9 @@ struct sdnn_net {
   sdnn_opts opts{-1, 0u, 32.f, nullptr, -1, -1, -1, 0};
   int device = 0;
   cudaStream_t own = nullptr;
+  // a pageable cudaMemcpy may return before its DMA lands, and the streams are
+  // non-blocking: the first inference after an upload synchronises the device
+  std::atomic<bool> uploads_pending{false};
   Arena arena;
   std::vector<DevLayer> dl;
   std::vector<PackedLayer> host;   // host copy of every packed layer (pass planning)
@@ -467,6 +470,7 @@ sdnn_status make_plan(sdnn_net *net) {
       return fail(SDNN_E_NOMEM, "device allocation for pass descriptors failed");
     }
     if (bytes) CK(cudaMemcpy(*d, h, bytes, cudaMemcpyHostToDevice));
+    net->uploads_pending = true;
     return SDNN_OK;
   };
   // Position-blocked activations (SDNN_YBLOCK; only when every step is a fused
@@ -545,7 +549,11 @@ sdnn_status make_plan(sdnn_net *net) {
     D.T = H.T;
     D.C = H.C;
     D.NB = H.NB;
+    D.NW = H.NW;
+    D.S = H.S;
     D.rec_bytes = H.rec_bytes;
+    if ((H.NB == 3 || H.NW > 0) && !net->yblk)
+      return fail(SDNN_E_UNSUPPORTED, "a position-blocked pass kernel was planned for row-major activations");
     D.yblk = net->yblk;
     // tile-major pays when a pass has many components (C4: 128-512); with few
     // (C2: 8-32) component-major was measured faster (18.4 vs 18.8 ms)
@@ -563,6 +571,11 @@ sdnn_status make_plan(sdnn_net *net) {
       D.in_rows = (const int32_t *)p1;
       D.in_count = (const int32_t *)p2;
       D.rec = (const unsigned char *)p3;
+      if (H.NB == 3) {
+        void *p4;
+        if ((st = up(H.split.data(), H.split.size() * 4, &p4))) return st;
+        D.split = (const int32_t *)p4;
+      }
     }
     for (int j = 0; j < H.m; ++j) {
       const PassHostLayer &HL = H.layers[j];
@@ -832,6 +845,7 @@ sdnn_status prepare_infer(sdnn_net *net, int64_t batch) {
   net->ws.sig0 = net->L > 0 ? net->d_sig0 : nullptr;
   net->ws.lg0 = (net->L > 0 && net->yblk && !net->step_lg.empty()) ? net->step_lg[0] : 5;
   if (net->L > 0 && (st = encode_tmaps(net))) return st;
+  if (net->uploads_pending.exchange(false)) CK(cudaDeviceSynchronize());
   return SDNN_OK;
 }
 
@@ -1289,7 +1303,6 @@ sdnn_status host_enqueue(sdnn_net *net, int slot_i, const int64_t *y0_rowptr, co
     return e;
   };
   int sslot = 0;
-  bool used[2] = {false, false};
   auto copy_h2d = [&](void *d, const void *h, size_t bytes, cudaStream_t cs, bool pinned) -> sdnn_status {
     if (bytes == 0) return SDNN_OK;
     if (pinned) {
@@ -1298,14 +1311,15 @@ sdnn_status host_enqueue(sdnn_net *net, int slot_i, const int64_t *y0_rowptr, co
     }
     for (size_t off = 0; off < bytes; off += kChunk) {
       const size_t b = std::min(kChunk, bytes - off);
-      if (used[sslot]) CK(cudaEventSynchronize(net->ev_stage[sslot]));
+      // (also across calls: a pipelined submission may still be copying from
+      // this staging slot; an event never recorded counts as complete)
+      CK(cudaEventSynchronize(net->ev_stage[sslot]));
       char *dst = stage + sslot * kChunk;
       const char *src = (const char *)h + off;
       parallel_for((int64_t)b, std::min(nthreads_default(), 8),
                    [&](int64_t x, int64_t y) { std::memcpy(dst + x, src + x, (size_t)(y - x)); });
       CK(cudaMemcpyAsync((char *)d + off, dst, b, cudaMemcpyHostToDevice, cs));
       CK(cudaEventRecord(net->ev_stage[sslot], cs));
-      used[sslot] = true;
       sslot ^= 1;
     }
     return SDNN_OK;
@@ -1495,6 +1509,7 @@ sdnn_status sdnn_set_layer(sdnn_net *net, int32_t l, const sdnn_layer *W, const 
     auto up = [&](const void *h, size_t bytes, void **dp) -> sdnn_status {
       *dp = bytes ? blk + off : nullptr;
       if (bytes) CK(cudaMemcpy(*dp, h, bytes, cudaMemcpyHostToDevice));
+      net->uploads_pending = true;
       off += al(bytes);
       return SDNN_OK;
     };
@@ -1624,7 +1639,10 @@ sdnn_status sdnn_infer(sdnn_net *net, const int64_t *y0_rowptr, const int32_t *y
     return st;
   }
   if (d_yout) {
-    CK(cudaMemcpy(y_out, d_yout, sizeof(float) * (size_t)net->n * (size_t)batch, cudaMemcpyDeviceToHost));
+    // on the compute stream, after k_yout (H.done was recorded before it, and
+    // a legacy-stream copy does not wait for a non-blocking stream)
+    CK(cudaMemcpyAsync(y_out, d_yout, sizeof(float) * (size_t)net->n * (size_t)batch, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
     cudaFree(d_yout);
   }
   return SDNN_OK;

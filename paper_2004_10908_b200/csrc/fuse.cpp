@@ -9,12 +9,14 @@
 // component has at most `cap` nodes on every boundary; the greedy planner
 // extends a pass layer by layer while that holds.
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
+#include <string>
 #include <thread>
 
 #include "sdnn_internal.h"
@@ -401,6 +403,200 @@ static void build_pass_impl(const std::vector<const PackedLayer *> &layers, int3
   while (Rp < R) Rp <<= 1;
   out.T = std::max(16, std::min(512, tile_floats / Rp));
   out.NB = 1;
+  // 513-1024 rows in one CTA (position-blocked plans): 32-position tiles in
+  // rotating halves, one CTA per SM (pass_wide.cu) instead of 16-position tiles
+  if (pass_wide_enabled() && C == 1 && Rp == 1024 && cta_rows >= 1024) {
+    out.T = 32;
+    out.NB = 3;
+  }
+  // <= 512 rows (SDNN_PASS_T32=1: <= 256) in the blocked layout: CTAs of
+  // ceil(rows / 128) warps with S 32-position tiles (k_pass_t32)
+  if (out.NB == 1 && C == 1 && cta_rows >= 1024 && pass_t32_mode() > 0 && Rp <= (pass_t32_mode() >= 2 ? 512 : 256)) {
+    out.T = 32;
+    out.NW = Rp <= 128 ? 1 : Rp <= 256 ? 2 : 4;
+    out.S = pass_t32_stages(out.NW);
+    if (!pass_t32_variant(out.NW, out.S)) out.NW = 0;
+  }
+  if (out.NB == 3) {                              // half 0 = the first 512 slots
+    out.split.assign(ncomp, 0);
+    for (int c = 0; c < ncomp; ++c) out.split[c] = std::min<int>(512, (int)bins[c][0].size());
+  }
+  // Bank-parity slot order for 16-position tiles (k_pass<16>: 64 B rows, two
+  // per 128 B shared-memory line).  A quarter-warp phase of k_pass<16> holds the
+  // units of groups 2i and 2i+1 (record order) at the same term t: their rows
+  // src_2i[t] and src_2i+1[t] conflict when their slots have equal parity, and
+  // so do the in-place member stores (member v goes to the slot of source v).
+  // Any slot order and any member -> source-slot assignment within a group is
+  // correct, so the planner chooses them: at boundary 0 the parity of a row is
+  // its slot position's; at boundary j >= 1 a member takes the parity of the
+  // source slot of its group (layer j-1) it is assigned to.  Per boundary, each
+  // read pair (x, y) wants opposite parities, each writer (the slot order /
+  // layer j-1 group) has a fixed number of even slots, and, when layer j writes
+  // in place, each group of layer j wants half of its slots even (so the next
+  // boundary stays solvable): an orientation problem, solved by local search
+  // (an Eulerian orientation satisfies the writer counts alone).  On C4 it cuts
+  // the equal-parity read pairs of these passes from ~50 % to < 1 %, but the
+  // passes read 18.4 instead of 14.6 GB from DRAM and the step slowed down
+  // (2000 vs 1929 ms/step with SDNN_PASS_WIDE=0), so it is opt-in
+  // (SDNN_PASS_PARITY=1).  member_at[b][g * gmax + v] = member written into the
+  // slot of source v of group g of layer b.
+  std::vector<std::vector<int32_t>> member_at(m);
+  static const bool parity_env = [] {            // opt-in (measured slower, see below)
+    const char *e = getenv("SDNN_PASS_PARITY");
+    return e && atoi(e) == 1;
+  }();
+  static const bool vt_env0 = [] {
+    const char *e = getenv("SDNN_PASS_VT");
+    return e && atoi(e) == 1;
+  }();
+  if (parity_env && out.T == 16 && C == 1 && out.NB == 1 && !allow_dedup && !vt_env0) {
+    for (int b = 0; b + 1 < m; ++b) {
+      const PackedLayer &p = *layers[s.a + b];
+      member_at[b].assign(p.col.begin(), p.col.end());
+    }
+    // groups of each layer per component, ascending (the record order)
+    std::vector<std::vector<std::vector<int32_t>>> cg(m, std::vector<std::vector<int32_t>>(ncomp));
+    for (int b = 0; b < m; ++b) {
+      const PackedLayer &p = *layers[s.a + b];
+      for (int32_t g = 0; g < p.ngroups; ++g) {
+        const int32_t c = comp_of_root[full.find((int32_t)((int64_t)(b + 1) * n + p.col[(size_t)g * p.gmax]))];
+        if (c >= 0) cg[b][c].push_back(g);
+      }
+    }
+    std::vector<int8_t> parP(n, 0), par(n, 0);   // parities at boundaries b-1 and b (this component)
+    std::vector<int32_t> wof(n, -1);             // writer index of a node
+    std::vector<int32_t> eidx(n, -1);            // edge of a node
+    uint64_t rng = 0x9E3779B97F4A7C15ull ^ (uint64_t)s.a;
+    auto rnd = [&]() {
+      rng ^= rng << 13;
+      rng ^= rng >> 7;
+      rng ^= rng << 17;
+      return rng;
+    };
+    for (int c = 0; c < ncomp; ++c) {
+      std::vector<int32_t> &rows0 = bins[c][0];
+      for (int b = 0; b < m; ++b) {
+        const PackedLayer &p = *layers[s.a + b];
+        const auto &G = cg[b][c];
+        // nodes of boundary b with their writer: b = 0 the slot order (writer 0),
+        // else the layer b-1 group that has them as a member
+        std::vector<int32_t> nodes;
+        std::vector<int32_t> cap;                  // even slots per writer
+        std::vector<std::vector<int32_t>> wsrc;    // b >= 1: source-slot parities per writer
+        if (b == 0) {
+          nodes = rows0;
+          cap.push_back(((int)nodes.size() + 1) / 2);
+          for (int32_t x : nodes) wof[x] = 0;
+        } else {
+          const PackedLayer &pp = *layers[s.a + b - 1];
+          const auto &W = cg[b - 1][c];
+          for (size_t w = 0; w < W.size(); ++w) {
+            const int32_t g = W[w];
+            int e = 0;
+            for (int v = 0; v < pp.gg[g]; ++v) {
+              const int32_t x = pp.col[(size_t)g * pp.gmax + v];
+              nodes.push_back(x);
+              wof[x] = (int32_t)w;
+            }
+            for (int v = 0; v < pp.gg[g]; ++v) e += parP[pp.src[(size_t)g * pp.kmax + v]] == 0;
+            cap.push_back(e);
+          }
+        }
+        // read pairs of layer b (groups 2i, 2i+1 of the record, the same term)
+        std::vector<std::array<int32_t, 2>> E;
+        std::vector<int32_t> epair;                // reader pair of each edge
+        for (size_t i = 0; i + 1 < G.size(); i += 2) {
+          const int32_t ga = G[i], gb = G[i + 1];
+          const int kk = std::min(p.gk[ga], p.gk[gb]);
+          for (int t = 0; t < kk; ++t) {
+            const int32_t x = p.src[(size_t)ga * p.kmax + t], y = p.src[(size_t)gb * p.kmax + t];
+            if (wof[x] < 0 || wof[y] < 0) continue;   // (a node without a writer: free)
+            eidx[x] = eidx[y] = (int32_t)E.size();
+            E.push_back({x, y});
+            epair.push_back((int32_t)(i / 2));
+          }
+        }
+        // balance of layer b's groups (writers of boundary b+1) when in place:
+        // group 2i gets half of its first gg sources even
+        const bool bal = b + 1 < m;
+        const int npairs = (int)G.size() / 2;
+        std::vector<int32_t> half(npairs, 0);
+        for (int i = 0; i < npairs; ++i) half[i] = p.gg[G[2 * i]] / 2;
+        std::vector<int8_t> o(E.size());           // orientation: 0 = x even, 1 = y even
+        std::vector<int32_t> cw(cap.size(), 0), cr(npairs, 0);
+        auto ga_counts = [&](size_t e) {           // edge e counts for group 2i's balance
+          const int32_t ga = G[2 * epair[e]];
+          const int t = (int)(e - (size_t)(std::lower_bound(epair.begin(), epair.end(), epair[e]) - epair.begin()));
+          return t < p.gg[ga];
+        };
+        std::vector<int8_t> inbal(E.size());
+        for (size_t e = 0; e < E.size(); ++e) {
+          o[e] = (int8_t)(e & 1);
+          inbal[e] = bal && ga_counts(e);
+          cw[wof[E[e][o[e]]]]++;
+          if (inbal[e] && o[e] == 0) cr[epair[e]]++;
+        }
+        auto cost_w = [&](int w, int d) { return std::abs(cw[w] + d - cap[w]) - std::abs(cw[w] - cap[w]); };
+        auto cost_r = [&](int i, int d) { return std::abs(cr[i] + d - half[i]) - std::abs(cr[i] - half[i]); };
+        for (int it = 0; it < 60 && !E.empty(); ++it) {
+          int64_t bad = 0;
+          for (size_t w = 0; w < cap.size(); ++w) bad += std::abs(cw[w] - cap[w]);
+          if (bal)
+            for (int i = 0; i < npairs; ++i) bad += std::abs(cr[i] - half[i]);
+          if (bad == 0) break;
+          for (size_t q = 0; q < E.size(); ++q) {
+            const size_t e = rnd() % E.size();
+            const int wold = wof[E[e][o[e]]], wnew = wof[E[e][1 - o[e]]];
+            int d = wold == wnew ? 0 : cost_w(wold, -1) + cost_w(wnew, +1);
+            if (inbal[e]) d += cost_r(epair[e], o[e] == 0 ? -1 : +1);
+            if (d < 0 || (d == 0 && (rnd() & 3) == 0)) {
+              cw[wold]--;
+              cw[wnew]++;
+              if (inbal[e]) cr[epair[e]] += o[e] == 0 ? -1 : +1;
+              o[e] ^= 1;
+            }
+          }
+        }
+        // wanted parity of every node (free nodes: -1), then exact writer counts
+        std::vector<int8_t> want(nodes.size(), -1);
+        for (size_t q = 0; q < nodes.size(); ++q) {
+          const int32_t x = nodes[q];
+          const int32_t e = eidx[x];
+          if (e >= 0) want[q] = (int8_t)(E[e][o[e]] == x ? 0 : 1);
+        }
+        std::vector<std::vector<int32_t>> ev(cap.size()), od(cap.size()), fr(cap.size());
+        for (size_t q = 0; q < nodes.size(); ++q)
+          (want[q] == 0 ? ev : want[q] == 1 ? od : fr)[wof[nodes[q]]].push_back(nodes[q]);
+        for (size_t w = 0; w < cap.size(); ++w) {
+          auto &E0 = ev[w], &O0 = od[w], &F0 = fr[w];
+          while ((int)E0.size() < cap[w] && !F0.empty()) { E0.push_back(F0.back()); F0.pop_back(); }
+          while ((int)E0.size() < cap[w] && !O0.empty()) { E0.push_back(O0.back()); O0.pop_back(); }
+          while ((int)E0.size() > cap[w]) { O0.push_back(E0.back()); E0.pop_back(); }
+          for (int32_t x : F0) O0.push_back(x);
+          for (int32_t x : E0) par[x] = 0;
+          for (int32_t x : O0) par[x] = 1;
+          if (b == 0) {                            // slot order: evens at even positions
+            std::vector<int32_t> ord(nodes.size());
+            size_t ie = 0, io = 0;
+            for (size_t q = 0; q < ord.size(); ++q) ord[q] = (q & 1) ? O0[io++] : E0[ie++];
+            rows0 = ord;
+          } else {                                 // member -> source slot of matching parity
+            const PackedLayer &pp = *layers[s.a + b - 1];
+            const int32_t g = cg[b - 1][c][w];
+            size_t ie = 0, io = 0;
+            for (int v = 0; v < pp.gg[g]; ++v)
+              member_at[b - 1][(size_t)g * pp.gmax + v] =
+                  parP[pp.src[(size_t)g * pp.kmax + v]] == 0 ? E0[ie++] : O0[io++];
+          }
+        }
+        for (int32_t x : nodes) {
+          wof[x] = -1;
+          eidx[x] = -1;
+          parP[x] = par[x];                        // boundary b becomes the previous one
+        }
+      }
+    }
+  }
   out.in_rows.assign((size_t)ncomp * C * R, -1);
   out.in_count.assign((size_t)ncomp * C, 0);
   for (int c = 0; c < ncomp; ++c)
@@ -449,7 +645,7 @@ static void build_pass_impl(const std::vector<const PackedLayer *> &layers, int3
   // slot.  The chains are unchanged (same operands, same order); only the
   // shared-memory stores drop by the group size.  Measured on C4: 2021 vs 1945
   // ms/step (the 1024-row passes slow down: 3.92 vs 3.11 ms), so off by default.
-  const bool dedup_on = allow_dedup && !vt;
+  const bool dedup_on = allow_dedup && !vt && out.NB != 3;   // (pass_wide.cu has no value slots)
   // A layer after a sharing layer reads shared slots, so it cannot overwrite its
   // sources in place: it must share too (or be the last layer) -- decided from
   // the back.
@@ -517,7 +713,8 @@ static void build_pass_impl(const std::vector<const PackedLayer *> &layers, int3
         }
         code0[q] = K > 0 ? code[0] : 0;
         for (int u = 0; u < G; ++u) {
-          const int32_t j = p.col[(size_t)g * p.gmax + u];
+          const int32_t j = (!last && !member_at[b].empty()) ? member_at[b][(size_t)g * p.gmax + u]
+                                                             : p.col[(size_t)g * p.gmax + u];
           H.bias[rec * 32 + u] = p.bias[j];
           if (last)
             H.orow[rec * 32 + u] = (uint16_t)j;
@@ -592,9 +789,28 @@ static void build_pass_impl(const std::vector<const PackedLayer *> &layers, int3
     }
   }
   out.rec_bytes = off;
-  if (getenv("SDNN_PLAN_DEBUG"))
-    fprintf(stderr, "pass a=%d m=%d R=%d T=%d C=%d ncomp=%d rec=%d vt=%d/%d share=%d\n", s.a, m, R, out.T, C, ncomp,
-            off, out.layers[0].vt, m > 1 ? out.layers[1].vt : -1, (int)allow_dedup);
+  if (getenv("SDNN_PLAN_DEBUG")) {
+    // 16-position tiles: read pairs (groups 2i, 2i+1, same term) whose slots
+    // have equal parity (one shared-memory bank conflict each), per layer
+    std::string conf;
+    if (out.T == 16 && C == 1)
+      for (int b = 0; b < m; ++b) {
+        const PassHostLayer &H = out.layers[b];
+        int64_t cnt = 0, tot = 0;
+        for (size_t cb = 0; cb < (size_t)ncomp; ++cb)
+          for (int q = 0; q + 1 < H.NG; q += 2) {
+            const int kk = std::min(H.k[cb * H.NG + q], H.k[cb * H.NG + q + 1]);
+            for (int t = 0; t < kk; ++t) {
+              tot++;
+              cnt += ((H.src[(cb * H.NG + q) * 32 + t] ^ H.src[(cb * H.NG + q + 1) * 32 + t]) & 1) == 0;
+            }
+          }
+        conf += " " + std::to_string(cnt) + "/" + std::to_string(tot);
+      }
+    fprintf(stderr, "pass a=%d m=%d R=%d T=%d C=%d NB=%d ncomp=%d rec=%d vt=%d/%d share=%d parity-conflicts%s\n", s.a,
+            m, R, out.T, C, out.NB, ncomp, off, out.layers[0].vt, m > 1 ? out.layers[1].vt : -1, (int)allow_dedup,
+            conf.c_str());
+  }
   // components of <= 128 rows: two half-size tiles per CTA (double-buffered)
   // when both records fit and a kernel instance exists (SDNN_PASS_NB=1: off).
   // Measured on C4: 128-row passes 2.69 ms (T = 64 x 2) vs 2.75 ms (T = 128);
@@ -605,7 +821,7 @@ static void build_pass_impl(const std::vector<const PackedLayer *> &layers, int3
       return !(e && atoi(e) == 1);
     }();
     const int T2 = std::max(16, std::min(512, tile_floats / 2 / Rp));
-    if (nb2 && C == 1 && Rp <= 128 && ncomp >= 256 && off <= ((kPassRecMax / 2) & ~15) &&
+    if (nb2 && out.NW == 0 && C == 1 && Rp <= 128 && ncomp >= 256 && off <= ((kPassRecMax / 2) & ~15) &&
         pass_variant(T2, 1, 2)) {                 // (C2's 32-component passes: 18.8 vs 18.4 ms without)
       out.NB = 2;
       out.T = T2;

@@ -691,6 +691,7 @@ int pass_tile_floats() { return kPassTile; }
   X(64, 1, false, 2) X(128, 1, false, 2)
 
 bool pass_variant(int T, int C, int NB) {
+  if (NB == 3) return T == 32 && C == 1;         // k_pass_wide
 #define X(TT, CC, XX, NN) \
   if (T == TT && C == CC && NB == NN) return true;
   SDNN_PASS_VARIANTS(X)
@@ -698,43 +699,6 @@ bool pass_variant(int T, int C, int NB) {
   return false;
 }
 
-
-// Lane arithmetic on 4 consecutive positions.  X2: packed fp32x2 FFMA2 / FADD2
-// (sm_100; per component identical to __fmaf_rn / __fadd_rn).
-template <bool X2>
-__device__ __forceinline__ void acc4(float (&a)[4], const float4 &v, float w) {
-  if (X2) {
-    const float2 w2 = make_float2(w, w);
-    const float2 lo = __ffma2_rn(make_float2(v.x, v.y), w2, make_float2(a[0], a[1]));
-    const float2 hi = __ffma2_rn(make_float2(v.z, v.w), w2, make_float2(a[2], a[3]));
-    a[0] = lo.x;
-    a[1] = lo.y;
-    a[2] = hi.x;
-    a[3] = hi.y;
-  } else {
-    a[0] = __fmaf_rn(v.x, w, a[0]);
-    a[1] = __fmaf_rn(v.y, w, a[1]);
-    a[2] = __fmaf_rn(v.z, w, a[2]);
-    a[3] = __fmaf_rn(v.w, w, a[3]);
-  }
-}
-// y = clamp(acc + b); o |= bit pattern (y is +0 exactly when dead: z is never -0)
-template <bool X2>
-__device__ __forceinline__ float4 out4(const float (&a)[4], float b, float ymax, uint32_t &o) {
-  float4 y;
-  if (X2) {
-    const float2 b2 = make_float2(b, b);
-    const float2 lo = __fadd2_rn(make_float2(a[0], a[1]), b2);
-    const float2 hi = __fadd2_rn(make_float2(a[2], a[3]), b2);
-    y = make_float4(clampy(lo.x, ymax), clampy(lo.y, ymax), clampy(hi.x, ymax), clampy(hi.y, ymax));
-  } else {
-    y = make_float4(clampy(__fadd_rn(a[0], b), ymax), clampy(__fadd_rn(a[1], b), ymax),
-                    clampy(__fadd_rn(a[2], b), ymax), clampy(__fadd_rn(a[3], b), ymax));
-  }
-  o |= (__float_as_uint(y.x) ? 1u : 0u) | (__float_as_uint(y.y) ? 2u : 0u) |
-       (__float_as_uint(y.z) ? 4u : 0u) | (__float_as_uint(y.w) ? 8u : 0u);
-  return y;
-}
 
 template <int T, int C, bool X2, int NB>
 __global__ void __launch_bounds__(32 * kPassNW, 3)
@@ -1510,6 +1474,7 @@ static void launch_bulk(const LaunchCfg &c, const Workspace &w, const DevLayer &
 }
 
 void configure_kernels() {
+  configure_pass_wide();
 #define X(TT, RR, SS, CC)                                                                      \
   cudaFuncSetAttribute(k_layer_bulk<TT, RR, SS, CC>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                        (int)bulk_smem<TT, RR, SS>());
@@ -1653,6 +1618,14 @@ void launch_layer(const LaunchCfg &c, const Workspace &w, const DevLayer &L, int
 
 void launch_pass(const LaunchCfg &c, const Workspace &w, const DevPass &P, uint32_t *alive,
                  float ymax, cudaStream_t s) {
+  if (P.NB == 3) {
+    launch_pass_wide(c, w, P, alive, ymax, s);
+    return;
+  }
+  if (P.NW > 0) {
+    launch_pass_t32(c, w, P, alive, ymax, s);
+    return;
+  }
   // SDNN_PASS_X2=1: packed FFMA2 path for single-CTA passes too; =T: only for
   // tiles of T positions (A/B knob; the default is scalar for C = 1)
   static const int x2_c1 = [] {

@@ -1,0 +1,523 @@
+// pass_wide.cu -- fused multi-layer pass for components of 513-1024 rows with
+// 32-position tiles, one CTA per SM (position-blocked activations only).
+//
+// k_pass holds a component's rows for one batch tile in a 64 KB shared-memory
+// tile, 3 CTAs per SM.  A 1024-row component then gets 16-position tiles: 64 B
+// half-block rows, loaded as 16-byte LDGSTS chunks, two rows per 128 B bank
+// line (a quarter-warp phase of two units conflicts whenever their source rows
+// have equal parity -- 31 % of the shared-load wavefronts on C4).  Here the
+// tile keeps 32 positions (128 B rows, one bank line each: conflict-free) and
+// is split into two 64 KB halves (rows 0-511 and 512-1023 of the component,
+// each ONE contiguous run of the position-blocked buffer, one cp.async.bulk
+// each) that rotate through three 64 KB buffers:
+//
+//   item k of the CTA: half 0 (+ the record) in buffer (2k) % 3, half 1 in
+//   buffer (2k+1) % 3.  When item k's last layer has read its tile, its two
+//   buffers take half 1 of item k+1 and half 0 of item k+2 -- so half 0 of
+//   the next item streams in during this item's whole layer chain.
+//
+// 8 warps; a unit is (group, the 32 positions), 8 lanes x 4 positions, 4 units
+// per warp: one round of units covers the 32 groups of a 1024-row layer.  The
+// arithmetic is k_pass's (the canonical ascending-source fmaf chain per group,
+// bias add, clamp; A5/A6) and the record format is the same
+// (fuse.cpp build_pass, PassHost.NB = 3).  Slot s of the component lives at
+// float offset hoff[s >= split] + s * 32 of the buffer space (split = 512).
+//
+// Measured on C4 (1024-row 3-layer passes): 3.27 ms vs 3.43-3.50 ms for the
+// 16-position k_pass tiles.  Tried and slower (5.08 ms): half-warp units of
+// 2 positions per lane with layers 0..m-2 of the half-0 sub-components run
+// before half 1 is waited for (a third of the chains per lane, twice the
+// barriers; with one CTA per SM every barrier idles the SM).
+#include <algorithm>
+#include <array>
+#include <cstdio>
+#include <cstdlib>
+
+#include "sdnn_internal.h"
+#include "device_util.cuh"
+
+namespace sdnn {
+
+constexpr int kWideNW = 8;                              // warps
+constexpr int kWideHalf = 512;                          // rows per half buffer
+constexpr int kWideHalfFloats = kWideHalf * 32;         // 64 KB
+constexpr int kWideRec = (kPassRecMax + 15) & ~15;      // record buffer bytes
+constexpr size_t kWideSmem = 3 * (size_t)kWideHalfFloats * 4 + 2 * (size_t)kWideRec + 3 * 8 + kMaxPassLayers * 4;
+
+template <bool X2>
+__global__ void __launch_bounds__(32 * kWideNW, 1)
+    k_pass_wide(const __grid_constant__ DevPass P, const LayerState *__restrict__ st, float *Ya, float *Yb,
+                uint32_t *__restrict__ alive, int64_t wstride, float ymax) {
+  constexpr int NW = kWideNW, T = 32, LPU = 8, UPW = 4, EPL = 4;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float *const smf = reinterpret_cast<float *>(smem_raw);                          // [3][512][32]
+  unsigned char *const rec0 = smem_raw + 3 * (size_t)kWideHalfFloats * 4;          // [2][kWideRec]
+  uint64_t *const bar = reinterpret_cast<uint64_t *>(rec0 + 2 * (size_t)kWideRec); // [3]
+  uint32_t *const aw = reinterpret_cast<uint32_t *>(bar + 3);                       // [kMaxPassLayers]
+  const LayerState Sx = st[P.a];
+  const int width = Sx.width;
+  if (width <= 0) return;                        // uniform over the grid
+  const float *__restrict__ Yin = Sx.in ? Yb : Ya;
+  float *__restrict__ Yout = Sx.in ? Ya : Yb;
+  const int tiles = (width + T - 1) / T;
+  const int64_t items = (int64_t)P.ncomp * tiles;
+  const bool tmaj = P.order != 0;
+  auto item_comp = [&](int64_t it) -> int64_t { return tmaj ? it % P.ncomp : it / tiles; };
+  auto item_tile = [&](int64_t it) -> int { return (int)(tmaj ? it / P.ncomp : it % tiles); };
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int seg = lane / LPU, sll = lane % LPU;  // unit (lane octet) of the lane, lane in it
+  const int pa = sll * 4;                        // this lane's 4 positions in the tile
+  const int64_t R = P.yblk;                      // storage rows per position block
+  const int lgo = P.lg_out;
+  const int64_t cid = blockIdx.x, ncl = gridDim.x;
+  if (tid == 0) {
+    for (int b = 0; b < 3; ++b) mbar_init(bar + b, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int q = tid; q < kMaxPassLayers; q += blockDim.x) aw[q] = 0u;
+  __syncthreads();
+  // half h of item it into buffer j (half 0 also brings the record into rb):
+  // rows [0, split) and [split, cnt) of the component, each one contiguous run
+  auto issue_half = [&](int64_t it, int h, int j, int rb) {
+    if (tid != 0 || it >= items) return;
+    const int64_t c = item_comp(it);
+    const int tile = item_tile(it);
+    const int cnt = __ldg(P.in_count + c);
+    const int s0 = __ldg(P.split + c);
+    const int nh = h == 0 ? s0 : cnt - s0;
+    mbar_expect_tx_arrive(bar + j, (uint32_t)nh * 128u + (h ? 0u : (uint32_t)P.rec_bytes));
+    if (!h) bulk_g2s(rec0 + (size_t)rb * kWideRec, P.rec + c * P.rec_bytes, (uint32_t)P.rec_bytes, bar + j);
+    if (nh > 0) {
+      const int64_t row0 = __ldg(P.in_rows + c * P.rin) + (h ? s0 : 0);
+      bulk_g2s(smf + (size_t)j * kWideHalfFloats, Yin + ((int64_t)tile * R + row0) * 32, (uint32_t)nh * 128u,
+               bar + j);
+    }
+  };
+  issue_half(cid, 0, 0, 0);
+  issue_half(cid, 1, 1, 0);
+  issue_half(cid + ncl, 0, 2, 1);
+  uint32_t phase = 0u;                           // bit j: parity of buffer j's next completion
+  int64_t kk = 0;
+  for (int64_t it = cid; it < items; it += ncl, ++kk) {
+    const int bA = (int)((2 * kk) % 3), bB = (int)((2 * kk + 1) % 3);
+    const unsigned char *rec_s = rec0 + (size_t)(kk & 1) * kWideRec;
+    const int tile = item_tile(it);
+    const int s0 = __ldg(P.split + item_comp(it));
+    // slot s -> float offset hoff[s >= s0] + s * 32 in the buffer space
+    const int32_t hoff0 = bA * kWideHalfFloats, hoff1 = bB * kWideHalfFloats - s0 * 32;
+    mbar_wait(bar + bA, (phase >> bA) & 1u);     // half 0 and the record
+    phase ^= 1u << bA;
+    mbar_wait(bar + bB, (phase >> bB) & 1u);
+    phase ^= 1u << bB;
+    auto release_and_load = [&]() {
+      // generic-proxy tile reads/writes before the next items' TMA writes
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();
+      issue_half(it + ncl, 1, bA, 0);
+      issue_half(it + 2 * ncl, 0, bB, (int)(kk & 1));
+    };
+    bool issued = false;
+    for (int j = 0; j < P.m; ++j) {
+      const PassLayerDev PL = P.layers[j];
+      const bool last = j == P.m - 1;
+      const float wu = PL.wu;
+      const bool ubias = PL.off_bias < 0;
+      const int units = PL.NG;
+      const uint16_t *kg_s = reinterpret_cast<const uint16_t *>(rec_s + PL.off_kg);
+      const uint16_t *src_s = reinterpret_cast<const uint16_t *>(rec_s + PL.off_src);
+      const float *bias_s = reinterpret_cast<const float *>(rec_s + (ubias ? 0 : PL.off_bias));
+      const uint16_t *orow_s = reinterpret_cast<const uint16_t *>(rec_s + (last ? PL.off_orow : 0));
+      const bool early = last && units <= NW * UPW;
+      for (int u0 = 0; u0 < units; u0 += NW * UPW) {
+        const int u = u0 + warp * UPW + seg;
+        int K = 0, G = 0, gi = 0;
+        if (u < units) {
+          gi = u;
+          const uint32_t kg = kg_s[gi];
+          K = kg & 0xffu;
+          G = kg >> 8;
+        }
+        uint32_t soff[EPL];                      // float offset of the entry's slot row
+        float bia[EPL];
+        int32_t orw[EPL];
+#pragma unroll
+        for (int r = 0; r < EPL; ++r) {
+          const int e = r * LPU + sll;
+          const int32_t slot = K > 0 ? (src_s[gi * 32 + (e < K ? e : 0)] & 0x3ff) : 0;
+          soff[r] = (uint32_t)((slot < s0 ? hoff0 : hoff1) + slot * 32);
+          bia[r] = (!ubias && e < G) ? bias_s[gi * 32 + e] : 0.f;
+          orw[r] = (last && e < G) ? orow_s[gi * 32 + e] : 0;
+        }
+        const int kmax = __reduce_max_sync(FULL, K);
+        const bool fullk = __all_sync(FULL, K == kmax || K == 0);
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+        // the canonical chain: terms in ascending source order (a term past K
+        // reads source 0 with weight 0: fmaf(x, 0, acc) == acc, acc != -0)
+        if (kmax == 32 && fullk) {
+#pragma unroll
+          for (int r = 0; r < EPL; ++r)
+#pragma unroll
+            for (int l = 0; l < LPU; ++l)
+              acc4<X2>(acc, *reinterpret_cast<const float4 *>(smf + __shfl_sync(FULL, soff[r], l, LPU) + pa), wu);
+        } else {
+#pragma unroll
+          for (int r = 0; r < EPL; ++r) {
+            if (r * LPU >= kmax) break;
+#pragma unroll 4
+            for (int l = 0; l < LPU; ++l) {
+              const int t = r * LPU + l;
+              const uint32_t so = __shfl_sync(FULL, soff[r], l, LPU);
+              if (t < kmax) acc4<X2>(acc, *reinterpret_cast<const float4 *>(smf + so + pa), t < K ? wu : 0.f);
+            }
+          }
+        }
+        if (early) {
+          release_and_load();
+          issued = true;
+        }
+        const int gmax = __reduce_max_sync(FULL, G);
+        uint32_t o = 0u;
+        float4 yu = make_float4(0.f, 0.f, 0.f, 0.f);   // uniform bias: one value per group
+        if (ubias && G > 0) yu = out4<X2>(acc, PL.bu, ymax, o);
+        const int64_t opos = (int64_t)tile * T + pa;
+        float *obase = Yout + (((opos >> lgo) * R) << lgo) + (opos & ((1 << lgo) - 1));
+        const int64_t rowmul = (int64_t)1 << lgo;
+#pragma unroll
+        for (int r = 0; r < EPL; ++r) {
+          if (r * LPU >= gmax) break;
+#pragma unroll 8
+          for (int l = 0; l < LPU; ++l) {
+            const int v = r * LPU + l;           // member v (owns source slot v when in place)
+            const int32_t dst = last ? __shfl_sync(FULL, orw[r], l, LPU) : (int32_t)__shfl_sync(FULL, soff[r], l, LPU);
+            const float bv = ubias ? 0.f : __shfl_sync(FULL, bia[r], l, LPU);
+            if (v < G) {
+              const float4 y = ubias ? yu : out4<X2>(acc, bv, ymax, o);
+              if (last) *reinterpret_cast<float4 *>(obase + (int64_t)dst * rowmul) = y;
+              else *reinterpret_cast<float4 *>(smf + dst + pa) = y;
+            }
+          }
+        }
+        // liveness: word bit b = position b -> lane b / 4 of the unit, e = b % 4
+        uint32_t bal[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) bal[e] = __ballot_sync(FULL, (o >> e) & 1u);
+        if (sll == 0 && G > 0) {
+          auto spread8 = [](uint32_t x) {
+            x = (x | (x << 12)) & 0x000F000Fu;
+            x = (x | (x << 6)) & 0x03030303u;
+            return (x | (x << 3)) & 0x11111111u;
+          };
+          const int sh = seg * LPU;
+          const uint32_t word = spread8((bal[0] >> sh) & 0xffu) | (spread8((bal[1] >> sh) & 0xffu) << 1) |
+                                (spread8((bal[2] >> sh) & 0xffu) << 2) | (spread8((bal[3] >> sh) & 0xffu) << 3);
+          if (word) atomicOr(&aw[j], word);
+        }
+      }
+      __syncthreads();                           // the next layer reads slots other warps wrote
+    }
+    if (tid == 0) {
+      const int64_t base = (int64_t)tile * T;
+      for (int j = 0; j < P.m; ++j) {
+        uint32_t word = aw[j];
+        aw[j] = 0u;
+        if (base >= width) word = 0u;
+        else if (width - base < 32) word &= (1u << (width - base)) - 1u;
+        if (word) atomicOr(&alive[j * wstride + (base >> 5)], word);
+      }
+    }
+    if (!issued) release_and_load();
+    __syncthreads();                             // aw published before the next item uses it
+  }
+}
+
+static bool wide_x2() {                          // SDNN_PASS_X2=1: packed FFMA2 here too
+  static const bool v = [] {
+    const char *e = getenv("SDNN_PASS_X2");
+    return e && atoi(e) == 1;
+  }();
+  return v;
+}
+
+void configure_pass_wide() {
+  cudaFuncSetAttribute(k_pass_wide<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWideSmem);
+  cudaFuncSetAttribute(k_pass_wide<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWideSmem);
+}
+
+void launch_pass_wide(const LaunchCfg &c, const Workspace &w, const DevPass &P, uint32_t *alive, float ymax,
+                      cudaStream_t s) {
+  if (wide_x2())
+    k_pass_wide<true><<<c.sms, 32 * kWideNW, kWideSmem, s>>>(P, w.st, w.Y[0], w.Y[1], alive, w.words, ymax);
+  else
+    k_pass_wide<false><<<c.sms, 32 * kWideNW, kWideSmem, s>>>(P, w.st, w.Y[0], w.Y[1], alive, w.words, ymax);
+}
+
+// planner switch (fuse.cpp): 513-1024-row components in one CTA get this
+// kernel (SDNN_PASS_WIDE=0: 16-position k_pass tiles instead)
+bool pass_wide_enabled() {
+  static const bool v = [] {
+    const char *e = getenv("SDNN_PASS_WIDE");
+    return !(e && atoi(e) == 0);
+  }();
+  return v;
+}
+
+
+
+// ---------------------------------------------------------------------------
+// k_pass_t32<NW, S>: fused pass over components of <= 128 * NW rows with
+// 32-position tiles in CTAs of NW warps (position-blocked activations, one CTA
+// per component tile).  A tile (R rows x 128 B) is ONE contiguous run of the
+// blocked buffer: one cp.async.bulk plus the record on one mbarrier per
+// buffer; S buffers per CTA (S = 2: the next item streams in during this
+// item's layers).  The shared-memory footprint follows the pass (S x (R x
+// 128 B + record)), so small components get many small CTAs per SM -- a
+// 128-row pass runs one-warp CTAs, every warp busy -- where k_pass gives every
+// CTA a 64 KB tile and 4 warps (128-row passes: 4 groups = 2 busy warps).  The
+// arithmetic and the record are k_pass's (fuse.cpp, PassHost.NW > 0).
+// ---------------------------------------------------------------------------
+template <int NW, int S, bool X2>
+__global__ void __launch_bounds__(32 * NW)
+    k_pass_t32(const __grid_constant__ DevPass P, const LayerState *__restrict__ st, float *Ya, float *Yb,
+               uint32_t *__restrict__ alive, int64_t wstride, float ymax, uint32_t buf_bytes) {
+  constexpr int T = 32, LPU = 8, UPW = 4, EPL = 4;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  // per buffer: [tile R x 32 floats | record], buf_bytes each (128 B multiple)
+  uint64_t *const bar = reinterpret_cast<uint64_t *>(smem_raw + (size_t)S * buf_bytes);   // [S]
+  uint32_t *const aw = reinterpret_cast<uint32_t *>(bar + S);                              // [m]
+  const LayerState Sx = st[P.a];
+  const int width = Sx.width;
+  if (width <= 0) return;
+  const float *__restrict__ Yin = Sx.in ? Yb : Ya;
+  float *__restrict__ Yout = Sx.in ? Ya : Yb;
+  const int tiles = (width + T - 1) / T;
+  const int64_t items = (int64_t)P.ncomp * tiles;
+  const bool tmaj = P.order != 0;
+  auto item_comp = [&](int64_t it) -> int64_t { return tmaj ? it % P.ncomp : it / tiles; };
+  auto item_tile = [&](int64_t it) -> int { return (int)(tmaj ? it / P.ncomp : it % tiles); };
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int seg = lane / LPU, sll = lane % LPU;
+  const int pa = sll * 4;
+  const int64_t R = P.yblk;
+  const int lgo = P.lg_out;
+  const uint32_t rec_off = (uint32_t)P.R * 128u;  // record after the tile in each buffer
+  const int64_t cid = blockIdx.x, ncl = gridDim.x;
+  if (tid == 0) {
+    for (int b = 0; b < S; ++b) mbar_init(bar + b, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int q = tid; q < P.m; q += blockDim.x) aw[q] = 0u;
+  __syncthreads();
+  auto issue = [&](int64_t it, int b) {
+    if (tid != 0 || it >= items) return;
+    const int64_t c = item_comp(it);
+    const int tile = item_tile(it);
+    const int cnt = __ldg(P.in_count + c);
+    unsigned char *dst = smem_raw + (size_t)b * buf_bytes;
+    mbar_expect_tx_arrive(bar + b, (uint32_t)cnt * 128u + (uint32_t)P.rec_bytes);
+    bulk_g2s(dst + rec_off, P.rec + c * P.rec_bytes, (uint32_t)P.rec_bytes, bar + b);
+    if (cnt > 0)
+      bulk_g2s(dst, Yin + ((int64_t)tile * R + __ldg(P.in_rows + c * P.rin)) * 32, (uint32_t)cnt * 128u, bar + b);
+  };
+  for (int b = 0; b < S; ++b) issue(cid + b * ncl, b);
+  int64_t kk = 0;
+  for (int64_t it = cid; it < items; it += ncl, ++kk) {
+    const int b = S == 1 ? 0 : (int)(kk % S);
+    const uint32_t ph = (uint32_t)((kk / S) & 1);
+    float *const tile_s = reinterpret_cast<float *>(smem_raw + (size_t)b * buf_bytes);
+    const unsigned char *rec_s = smem_raw + (size_t)b * buf_bytes + rec_off;
+    const int tile = item_tile(it);
+    mbar_wait(bar + b, ph);
+    auto release_and_load = [&]() {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();
+      issue(it + S * ncl, b);
+    };
+    bool issued = false;
+    for (int j = 0; j < P.m; ++j) {
+      const PassLayerDev PL = P.layers[j];
+      const bool last = j == P.m - 1;
+      const float wu = PL.wu;
+      const bool ubias = PL.off_bias < 0;
+      const int units = PL.NG;
+      const uint16_t *kg_s = reinterpret_cast<const uint16_t *>(rec_s + PL.off_kg);
+      const uint16_t *src_s = reinterpret_cast<const uint16_t *>(rec_s + PL.off_src);
+      const float *bias_s = reinterpret_cast<const float *>(rec_s + (ubias ? 0 : PL.off_bias));
+      const uint16_t *orow_s = reinterpret_cast<const uint16_t *>(rec_s + (last ? PL.off_orow : 0));
+      const bool early = last && units <= NW * UPW;
+      for (int u0 = 0; u0 < units; u0 += NW * UPW) {
+        const int u = u0 + warp * UPW + seg;
+        int K = 0, G = 0, gi = 0;
+        if (u < units) {
+          gi = u;
+          const uint32_t kg = kg_s[gi];
+          K = kg & 0xffu;
+          G = kg >> 8;
+        }
+        uint32_t soff[EPL];
+        float bia[EPL];
+        int32_t orw[EPL];
+#pragma unroll
+        for (int r = 0; r < EPL; ++r) {
+          const int e = r * LPU + sll;
+          soff[r] = K > 0 ? (uint32_t)(src_s[gi * 32 + (e < K ? e : 0)] & 0x3ff) * 32u : 0u;
+          bia[r] = (!ubias && e < G) ? bias_s[gi * 32 + e] : 0.f;
+          orw[r] = (last && e < G) ? orow_s[gi * 32 + e] : 0;
+        }
+        const int kmax = __reduce_max_sync(FULL, K);
+        const bool fullk = __all_sync(FULL, K == kmax || K == 0);
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+        if (kmax == 32 && fullk) {
+#pragma unroll
+          for (int r = 0; r < EPL; ++r)
+#pragma unroll
+            for (int l = 0; l < LPU; ++l)
+              acc4<X2>(acc, *reinterpret_cast<const float4 *>(tile_s + __shfl_sync(FULL, soff[r], l, LPU) + pa), wu);
+        } else {
+#pragma unroll
+          for (int r = 0; r < EPL; ++r) {
+            if (r * LPU >= kmax) break;
+#pragma unroll 4
+            for (int l = 0; l < LPU; ++l) {
+              const int t = r * LPU + l;
+              const uint32_t so = __shfl_sync(FULL, soff[r], l, LPU);
+              if (t < kmax) acc4<X2>(acc, *reinterpret_cast<const float4 *>(tile_s + so + pa), t < K ? wu : 0.f);
+            }
+          }
+        }
+        if (early) {
+          release_and_load();
+          issued = true;
+        }
+        const int gmax = __reduce_max_sync(FULL, G);
+        uint32_t o = 0u;
+        float4 yu = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (ubias && G > 0) yu = out4<X2>(acc, PL.bu, ymax, o);
+        const int64_t opos = (int64_t)tile * T + pa;
+        float *obase = Yout + (((opos >> lgo) * R) << lgo) + (opos & ((1 << lgo) - 1));
+        const int64_t rowmul = (int64_t)1 << lgo;
+#pragma unroll
+        for (int r = 0; r < EPL; ++r) {
+          if (r * LPU >= gmax) break;
+#pragma unroll 8
+          for (int l = 0; l < LPU; ++l) {
+            const int v = r * LPU + l;
+            const int32_t dst = last ? __shfl_sync(FULL, orw[r], l, LPU) : (int32_t)__shfl_sync(FULL, soff[r], l, LPU);
+            const float bv = ubias ? 0.f : __shfl_sync(FULL, bia[r], l, LPU);
+            if (v < G) {
+              const float4 y = ubias ? yu : out4<X2>(acc, bv, ymax, o);
+              if (last) *reinterpret_cast<float4 *>(obase + (int64_t)dst * rowmul) = y;
+              else *reinterpret_cast<float4 *>(tile_s + dst + pa) = y;
+            }
+          }
+        }
+        uint32_t bal[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) bal[e] = __ballot_sync(FULL, (o >> e) & 1u);
+        if (sll == 0 && G > 0) {
+          auto spread8 = [](uint32_t x) {
+            x = (x | (x << 12)) & 0x000F000Fu;
+            x = (x | (x << 6)) & 0x03030303u;
+            return (x | (x << 3)) & 0x11111111u;
+          };
+          const int sh = seg * LPU;
+          const uint32_t word = spread8((bal[0] >> sh) & 0xffu) | (spread8((bal[1] >> sh) & 0xffu) << 1) |
+                                (spread8((bal[2] >> sh) & 0xffu) << 2) | (spread8((bal[3] >> sh) & 0xffu) << 3);
+          if (word) atomicOr(&aw[j], word);
+        }
+      }
+      __syncthreads();
+    }
+    if (tid == 0) {
+      const int64_t base = (int64_t)tile * T;
+      for (int j = 0; j < P.m; ++j) {
+        uint32_t word = aw[j];
+        aw[j] = 0u;
+        if (base >= width) word = 0u;
+        else if (width - base < 32) word &= (1u << (width - base)) - 1u;
+        if (word) atomicOr(&alive[j * wstride + (base >> 5)], word);
+      }
+    }
+    if (!issued) release_and_load();
+    __syncthreads();
+  }
+}
+
+// (NW, S) instances: NW = ceil(rows / 128) warps, S buffers
+#define SDNN_T32_VARIANTS(X) X(1, 1) X(1, 2) X(1, 3) X(2, 1) X(2, 2) X(2, 3) X(4, 1) X(4, 2)
+
+static uint32_t t32_buf_bytes(const DevPass &P) {
+  return (uint32_t)(((size_t)P.R * 128 + P.rec_bytes + 127) / 128 * 128);
+}
+static size_t t32_smem(const DevPass &P, int S) { return (size_t)S * t32_buf_bytes(P) + 8 * S + 4 * kMaxPassLayers; }
+
+bool pass_t32_variant(int nw, int s) {
+#define X(NN, SS) if (nw == NN && s == SS) return true;
+  SDNN_T32_VARIANTS(X)
+#undef X
+  return false;
+}
+size_t pass_t32_smem_max() { return 227 * 1024; }
+
+template <int NW, int S, bool X2>
+static void launch_t32(const LaunchCfg &c, const Workspace &w, const DevPass &P, uint32_t *alive, float ymax,
+                       cudaStream_t s) {
+  const size_t smem = t32_smem(P, S);
+  static size_t set_smem = 0;                    // (per instance: the largest size configured so far)
+  if (smem > set_smem) {
+    cudaFuncSetAttribute(k_pass_t32<NW, S, X2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    set_smem = smem;
+  }
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pass_t32<NW, S, X2>, 32 * NW, smem) != cudaSuccess ||
+      occ <= 0) {
+    cudaGetLastError();
+    occ = 1;
+  }
+  k_pass_t32<NW, S, X2><<<c.sms * occ, 32 * NW, smem, s>>>(P, w.st, w.Y[0], w.Y[1], alive, w.words, ymax,
+                                                          t32_buf_bytes(P));
+}
+
+void launch_pass_t32(const LaunchCfg &c, const Workspace &w, const DevPass &P, uint32_t *alive, float ymax,
+                     cudaStream_t s) {
+  const bool x2 = wide_x2();
+#define X(NN, SS)                                                    \
+  if (P.NW == NN && P.S == SS) {                                     \
+    if (x2) launch_t32<NN, SS, true>(c, w, P, alive, ymax, s);       \
+    else launch_t32<NN, SS, false>(c, w, P, alive, ymax, s);         \
+    return;                                                          \
+  }
+  SDNN_T32_VARIANTS(X)
+#undef X
+  fprintf(stderr, "sdnn: no k_pass_t32 instance for NW=%d S=%d\n", P.NW, P.S);
+  abort();
+}
+
+// planner switch: components of <= 512 rows in the blocked layout get
+// k_pass_t32 (SDNN_PASS_T32: 0 off, 1 up to 256 rows, 2 up to 512 rows);
+// buffers per CTA by warps (SDNN_PASS_T32_S = "s1,s2,s4" for 1 / 2 / 4 warps).
+// Measured on C4 (ms/step): k_pass everywhere 1906; t32 for <= 256 rows with
+// S = 1: 1894, S = 2: 1870; t32 up to 512 rows: S = 1 1838, S = 2 2678 (two
+// 64 KB tiles leave one CTA per SM)
+int pass_t32_mode() {
+  static const int v = [] {
+    const char *e = getenv("SDNN_PASS_T32");
+    return e ? atoi(e) : 2;
+  }();
+  return v;
+}
+int pass_t32_stages(int nw) {
+  static const std::array<int, 3> v = [] {
+    std::array<int, 3> r = {2, 2, 1};
+    if (const char *e = getenv("SDNN_PASS_T32_S")) {
+      int a = 0, b = 0, c = 0;
+      const int k = sscanf(e, "%d,%d,%d", &a, &b, &c);
+      if (k == 1) r = {a, a, a};
+      else if (k == 3) r = {a, b, c};
+      for (int &x : r) x = std::max(1, std::min(3, x));
+    }
+    return r;
+  }();
+  return v[nw <= 1 ? 0 : nw == 2 ? 1 : 2];
+}
+
+}  // namespace sdnn

@@ -145,9 +145,12 @@ struct PassHostLayer {
 struct PassHost {
   int32_t a = 0, m = 0, ncomp = 0, rin = 0, R = 0, T = 0;
   int32_t C = 1;                       // CTAs per component (cluster size; rows/records per [comp][bin])
-  int32_t NB = 1;                      // tile buffers per CTA (2: T for a half tile, double-buffered)
+  int32_t NB = 1;                      // tile buffers per CTA (2: T for a half tile, double-buffered;
+                                       // 3: pass_wide.cu, 1024 rows x 32 positions in rotating halves)
   std::vector<int32_t> in_rows;        // [ncomp][rin]  global neuron ids at boundary a
   std::vector<int32_t> in_count;       // [ncomp]
+  std::vector<int32_t> split;          // NB = 3: [ncomp] slots in half 0 (pass_wide.cu)
+  int32_t NW = 0, S = 1;               // > 0: k_pass_t32 with NW warps and S tile buffers per CTA
   std::vector<PassHostLayer> layers;   // [m]
   // per-component metadata record (one bulk copy next to the tile):
   //   for each layer j: kg[NG_j] u16 (K | G << 8) padded to 16 B, src[NG_j][32] u16
@@ -193,6 +196,8 @@ struct alignas(64) DevPass {
   int32_t pf;                          // yblk: L2-prefetch the tiles of the next pf items
   int32_t NB;                          // tile buffers per CTA (2: half-size tiles, double-buffered)
   const int32_t *in_rows, *in_count;
+  const int32_t *split;                // NB = 3: [ncomp] slots in half 0
+  int32_t NW, S;                       // NW > 0: k_pass_t32<NW, S> (pass_wide.cu)
   const unsigned char *rec;            // [ncomp][rec_bytes]
   PassLayerDev layers[kMaxPassLayers]; // by value: the kernel parameter carries them
 };
@@ -273,6 +278,21 @@ void launch_layer(const LaunchCfg &c, const Workspace &w, const DevLayer &L, int
 bool layer_tracks_saturation(const LaunchCfg &c, const DevLayer &L);
 int pass_tile_floats();        // smem floats per component tile (tile T = this / R)
 bool pass_variant(int T, int C, int NB = 1);   // a k_pass instance exists for tile T, cluster C, NB buffers
+// 513-1024-row components, 32-position tiles, one CTA per SM (pass_wide.cu;
+// PassHost.NB = 3); pass_wide_enabled(): SDNN_PASS_WIDE != 0
+bool pass_wide_enabled();
+// <= 512-row components, 32-position tiles, CTAs of NW = ceil(rows / 128)
+// warps sized by the pass (pass_wide.cu; PassHost.NW > 0); pass_t32_mode():
+// SDNN_PASS_T32 (0 off, 1 up to 256 rows, 2 up to 512 rows); buffers per CTA
+// for NW warps: pass_t32_stages(NW) (SDNN_PASS_T32_S)
+int pass_t32_mode();
+int pass_t32_stages(int nw);
+bool pass_t32_variant(int nw, int s);
+void launch_pass_t32(const LaunchCfg &c, const Workspace &w, const DevPass &P, uint32_t *alive, float ymax,
+                     cudaStream_t s);
+void configure_pass_wide();
+void launch_pass_wide(const LaunchCfg &c, const Workspace &w, const DevPass &P, uint32_t *alive, float ymax,
+                      cudaStream_t s);
 // a fused pass: reads st[P.a], liveness of layer a+j to alive + j*words
 void launch_pass(const LaunchCfg &c, const Workspace &w, const DevPass &P, uint32_t *alive,
                  float ymax, cudaStream_t s);
