@@ -150,7 +150,7 @@ def kernel_name(net, args=None):
     st = net.stats()
     if st.get("fused_layers", 0) == 0:
         return "k_layer_bulkw" if args is not None and args.net == "rw" else "k_layer_bulk"
-    return "k_pass+k_layer_bulk"
+    return "fused passes (k_pass_t32 / k_pass_wide / k_pass)"
 
 
 def make_inputs(n, B, rank):
@@ -389,7 +389,8 @@ def run_gpu(args):
                      "entry and exit), so the HBM fraction is not its bound; at C1 (1000 rows = 63 CTAs "
                      "of 16 positions for 148 SMs) it is latency/occupancy bound, see levels"
                      if st.get("resident_layers", 0) > 0 else None),
-            "levels_source": "ncu --set full, one launch per kernel (profiles/r02/r02_levels.jsonl; "
+            "levels_source": "ncu --set full, one launch per kernel (profiles/layer_traffic.json, raw CSVs "
+                             "under profiles/r02/ncu; "
                              "percentages of each unit's peak)" if levels else None}
 
     # ---- e2e through the public host-buffer call --------------------------------

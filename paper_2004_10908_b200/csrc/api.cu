@@ -561,6 +561,18 @@ sdnn_status make_plan(sdnn_net *net) {
     D.lg_in = net->step_lg[q];
     D.lg_out = net->step_lg[q + 1];
     D.pf = net->yblk ? pf : 0;
+    if (H.NB == 3) {                             // k_pass_wide: SDNN_WIDE_PF / SDNN_WIDE_ORDER knobs
+      static const int wpf = [] {
+        const char *e = getenv("SDNN_WIDE_PF");
+        return e ? atoi(e) : 0;
+      }();
+      static const int word = [] {
+        const char *e = getenv("SDNN_WIDE_ORDER");
+        return e ? atoi(e) : -1;
+      }();
+      D.pf = wpf;
+      if (word >= 0) D.order = word;
+    }
     if (!streaming) {                            // else: pointers into the slot ring
       void *p1, *p2, *p3;
       sdnn_status st;

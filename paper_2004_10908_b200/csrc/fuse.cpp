@@ -299,15 +299,17 @@ std::vector<Step> plan_steps(const std::vector<const PackedLayer *> &layers, int
 
 static void build_pass_impl(const std::vector<const PackedLayer *> &layers, int32_t n, const Step &s,
                             int tile_floats, int cta_rows, PassHost &out, bool allow_dedup,
-                            bool allow_vt = true);
+                            bool allow_vt = true, bool blocked = false, const Step *prev = nullptr);
 
 void build_pass(const std::vector<const PackedLayer *> &layers, int32_t n, const Step &s,
-                int tile_floats, int cta_rows, PassHost &out, bool share_values) {
-  build_pass_impl(layers, n, s, tile_floats, cta_rows, out, share_values);
+                int tile_floats, int cta_rows, PassHost &out, bool share_values, bool blocked,
+                const Step *prev) {
+  build_pass_impl(layers, n, s, tile_floats, cta_rows, out, share_values, true, blocked, prev);
 }
 
 static void build_pass_impl(const std::vector<const PackedLayer *> &layers, int32_t n, const Step &s,
-                            int tile_floats, int cta_rows, PassHost &out, bool allow_dedup, bool allow_vt) {
+                            int tile_floats, int cta_rows, PassHost &out, bool allow_dedup, bool allow_vt,
+                            bool blocked, const Step *prev) {
   const int m = s.m;
   UF full, sub;
   full.init((int64_t)(m + 1) * n);
@@ -347,6 +349,23 @@ static void build_pass_impl(const std::vector<const PackedLayer *> &layers, int3
     for (int32_t g = 0; g < pp.ngroups; ++g)
       for (int u = 0; u < pp.gg[g]; ++u) prev_group[pp.col[(size_t)g * pp.gmax + u]] = g;
   }
+  // writer component of each input row: the component (over the previous
+  // step's layers) whose last layer writes it.  One item of the previous pass
+  // stores all rows of its component for one tile, so rows of one writer
+  // component placed next to each other make its stores runs of consecutive
+  // storage rows (SDNN_PASS_WKEY=0: group order only)
+  std::vector<int32_t> wroot;
+  static const bool wkey_env = [] {
+    const char *e = getenv("SDNN_PASS_WKEY");
+    return !(e && atoi(e) == 0);
+  }();
+  if (wkey_env && prev && prev->m >= 1 && prev->a + prev->m == s.a) {
+    UF w;
+    w.init((int64_t)(prev->m + 1) * n);
+    for (int b = 0; b < prev->m; ++b) add_layer(w, *layers[prev->a + b], n, b);
+    wroot.assign(n, 0);
+    for (int32_t x = 0; x < n; ++x) wroot[x] = w.find((int32_t)((int64_t)prev->m * n + x));
+  }
   std::vector<std::vector<std::vector<int32_t>>> bins(ncomp);   // [comp][bin] rows
   int C = 1, R = 1;
   for (int c = 0; c < ncomp; ++c) {
@@ -372,6 +391,7 @@ static void build_pass_impl(const std::vector<const PackedLayer *> &layers, int3
         std::sort(b.begin(), b.end());
       } else {
         std::sort(b.begin(), b.end(), [&](int32_t x, int32_t y) {
+          if (!wroot.empty() && wroot[x] != wroot[y]) return wroot[x] < wroot[y];
           return prev_group[x] != prev_group[y] ? prev_group[x] < prev_group[y] : x < y;
         });
       }
@@ -405,13 +425,13 @@ static void build_pass_impl(const std::vector<const PackedLayer *> &layers, int3
   out.NB = 1;
   // 513-1024 rows in one CTA (position-blocked plans): 32-position tiles in
   // rotating halves, one CTA per SM (pass_wide.cu) instead of 16-position tiles
-  if (pass_wide_enabled() && C == 1 && Rp == 1024 && cta_rows >= 1024) {
+  if (pass_wide_enabled() && blocked && C == 1 && Rp == 1024) {
     out.T = 32;
     out.NB = 3;
   }
   // <= 512 rows (SDNN_PASS_T32=1: <= 256) in the blocked layout: CTAs of
   // ceil(rows / 128) warps with S 32-position tiles (k_pass_t32)
-  if (out.NB == 1 && C == 1 && cta_rows >= 1024 && pass_t32_mode() > 0 && Rp <= (pass_t32_mode() >= 2 ? 512 : 256)) {
+  if (out.NB == 1 && C == 1 && blocked && pass_t32_mode() > 0 && Rp <= (pass_t32_mode() >= 2 ? 512 : 256)) {
     out.T = 32;
     out.NW = Rp <= 128 ? 1 : Rp <= 256 ? 2 : 4;
     out.S = pass_t32_stages(out.NW);
@@ -645,7 +665,7 @@ static void build_pass_impl(const std::vector<const PackedLayer *> &layers, int3
   // slot.  The chains are unchanged (same operands, same order); only the
   // shared-memory stores drop by the group size.  Measured on C4: 2021 vs 1945
   // ms/step (the 1024-row passes slow down: 3.92 vs 3.11 ms), so off by default.
-  const bool dedup_on = allow_dedup && !vt && out.NB != 3;   // (pass_wide.cu has no value slots)
+  const bool dedup_on = allow_dedup && !vt && out.NB != 3 && out.NW == 0;   // (pass_wide.cu has no value slots)
   // A layer after a sharing layer reads shared slots, so it cannot overwrite its
   // sources in place: it must share too (or be the last layer) -- decided from
   // the back.
@@ -677,7 +697,7 @@ static void build_pass_impl(const std::vector<const PackedLayer *> &layers, int3
     H.dedup = dedup[b];
     if (vt && NG > 32) {                           // one round of units per layer (4 warps x 8 units),
                                                    // so the table stores follow every read of the tile
-      build_pass_impl(layers, n, s, tile_floats, cta_rows, out, allow_dedup, false);
+      build_pass_impl(layers, n, s, tile_floats, cta_rows, out, allow_dedup, false, blocked, prev);
       return;
     }
     // layer b (non-last) writes table b & 1 (lines 0.. or 256..), layer b > 0 reads table (b-1) & 1
@@ -734,7 +754,7 @@ static void build_pass_impl(const std::vector<const PackedLayer *> &layers, int3
         if (!excl) {
           while (next_free < R && live[next_free]) ++next_free;
           if (next_free >= R) {                 // no free slot left: build without sharing
-            build_pass_impl(layers, n, s, tile_floats, cta_rows, out, false, allow_vt);
+            build_pass_impl(layers, n, s, tile_floats, cta_rows, out, false, allow_vt, blocked, prev);
             return;
           }
           vcode = (code0[q] & ~0x3ff) | next_free;
@@ -867,7 +887,8 @@ std::vector<Step> plan_passes(const std::vector<const PackedLayer *> &layers, in
     for (int t = 0; t < nt && !todo.empty(); ++t)
       th.emplace_back([&] {
         for (int q = next++; q < (int)todo.size(); q = next++)
-          build_pass(layers, n, steps[todo[q]], tile_floats, cta_rows, ph[todo[q]], share_values);
+          build_pass(layers, n, steps[todo[q]], tile_floats, cta_rows, ph[todo[q]], share_values, single_passes,
+                     todo[q] > 0 ? &steps[todo[q] - 1] : nullptr);
       });
     for (auto &x : th) x.join();
     for (int i : todo) done[i] = 1;

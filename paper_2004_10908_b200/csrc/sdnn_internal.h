@@ -160,8 +160,11 @@ struct PassHost {
   std::vector<unsigned char> rec;      // [ncomp][rec_bytes]
 };
 constexpr int kPassRecMax = 10224;     // record bytes per component (3 CTAs per SM: 3 x 75 KB)
+// blocked: the plan is for position-blocked activations (pass_wide.cu kernels allowed)
+// prev: the step before s (its components order the rows of s's bins)
 void build_pass(const std::vector<const PackedLayer *> &layers, int32_t n, const Step &s,
-                int tile_floats, int cta_rows, PassHost &out, bool share_values = false);
+                int tile_floats, int cta_rows, PassHost &out, bool share_values = false, bool blocked = false,
+                const Step *prev = nullptr);
 // plan_steps, build every fused pass; a pass whose record exceeds kPassRecMax
 // drops its last layer and the rest is planned again; `built[i]` is the
 // PassHost of steps[i] (m > 1, or m == 1 with single_passes; else m == 0)
