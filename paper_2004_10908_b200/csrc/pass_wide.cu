@@ -24,10 +24,13 @@
 // float offset hoff[s >= split] + s * 32 of the buffer space (split = 512).
 //
 // Measured on C4 (1024-row 3-layer passes): 3.27 ms vs 3.43-3.50 ms for the
-// 16-position k_pass tiles.  Tried and slower (5.08 ms): half-warp units of
-// 2 positions per lane with layers 0..m-2 of the half-0 sub-components run
-// before half 1 is waited for (a third of the chains per lane, twice the
-// barriers; with one CTA per SM every barrier idles the SM).
+// 16-position k_pass tiles.  Tried and slower: half-warp units of 2
+// positions per lane with layers 0..m-2 of the half-0 sub-components run
+// before half 1 is waited for (5.08 ms: a third of the chains per lane, twice
+// the barriers; with one CTA per SM every barrier idles the SM); the
+// sub-components packed into the halves and layers 0..m-2 of each half run by
+// its own 4-warp group on a named barrier as soon as its half has landed
+// (3.52 vs 3.35 ms).
 #include <algorithm>
 #include <array>
 #include <cstdio>
@@ -42,6 +45,10 @@ namespace sdnn {
 #define SDNN_CHAIN_B 0
 #endif
 constexpr int kChainB = SDNN_CHAIN_B;                   // loads in flight per lane (chain32)
+#ifndef SDNN_CHAIN_REGS
+#define SDNN_CHAIN_REGS 1
+#endif
+constexpr bool kChainRegs = SDNN_CHAIN_REGS != 0;       // k_pass_t32: shuffle-free addresses
 constexpr int kWideNW = 8;                              // warps
 constexpr int kWideHalf = 512;                          // rows per half buffer
 constexpr int kWideHalfFloats = kWideHalf * 32;         // 64 KB
@@ -76,6 +83,30 @@ __device__ __forceinline__ void chain32(float (&acc)[4], const float *base, cons
 #pragma unroll
     for (int q = 0; q < B; ++q) acc4<X2>(acc, v[q], wu);
   }
+  }
+}
+
+// The 32-term fast path without shuffles: every lane of the unit reads the
+// group's 32 u16 slot codes itself (four 16-byte shared loads, broadcast to
+// the unit's 8 lanes) and forms each term's address with two integer ops, so
+// no term waits on a shuffle (SDNN_CHAIN_REGS=0: the shuffle version)
+template <bool X2>
+__device__ __forceinline__ void chain32_regs(float (&acc)[4], const float *base, const uint16_t *codes, int pa,
+                                             float wu) {
+  const uint4 *c4 = reinterpret_cast<const uint4 *>(codes);
+  uint32_t w[16];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint4 v = c4[q];
+    w[4 * q] = v.x;
+    w[4 * q + 1] = v.y;
+    w[4 * q + 2] = v.z;
+    w[4 * q + 3] = v.w;
+  }
+#pragma unroll
+  for (int t = 0; t < 32; ++t) {
+    const uint32_t slot = ((t & 1) ? (w[t >> 1] >> 16) : w[t >> 1]) & 0x3ffu;
+    acc4<X2>(acc, *reinterpret_cast<const float4 *>(base + slot * 32u + (uint32_t)pa), wu);
   }
 }
 
@@ -162,19 +193,21 @@ __global__ void __launch_bounds__(32 * kWideNW, 1)
       issue_half(it + 2 * ncl, 0, bB, (int)(kk & 1));
     };
     bool issued = false;
-    for (int j = 0; j < P.m; ++j) {
+    // groups [g0, g1) of layer j on nwg warps starting at warp w0 (the last
+    // layer: all groups, all warps, with the early release)
+    auto run = [&](int j, int g0, int g1, int w0, int nwg) {
       const PassLayerDev PL = P.layers[j];
       const bool last = j == P.m - 1;
       const float wu = PL.wu;
       const bool ubias = PL.off_bias < 0;
-      const int units = PL.NG;
+      const int units = g1;
       const uint16_t *kg_s = reinterpret_cast<const uint16_t *>(rec_s + PL.off_kg);
       const uint16_t *src_s = reinterpret_cast<const uint16_t *>(rec_s + PL.off_src);
       const float *bias_s = reinterpret_cast<const float *>(rec_s + (ubias ? 0 : PL.off_bias));
       const uint16_t *orow_s = reinterpret_cast<const uint16_t *>(rec_s + (last ? PL.off_orow : 0));
-      const bool early = last && units <= NW * UPW;
-      for (int u0 = 0; u0 < units; u0 += NW * UPW) {
-        const int u = u0 + warp * UPW + seg;
+      const bool early = last && g1 - g0 <= nwg * UPW;
+      for (int u0 = g0; u0 < units; u0 += nwg * UPW) {
+        const int u = u0 + (warp - w0) * UPW + seg;
         int K = 0, G = 0, gi = 0;
         if (u < units) {
           gi = u;
@@ -254,8 +287,13 @@ __global__ void __launch_bounds__(32 * kWideNW, 1)
           if (word) atomicOr(&aw[j], word);
         }
       }
+    };
+    for (int j = 0; j + 1 < P.m; ++j) {
+      run(j, 0, P.layers[j].NG, 0, NW);
       __syncthreads();                           // the next layer reads slots other warps wrote
     }
+    run(P.m - 1, 0, P.layers[P.m - 1].NG, 0, NW);
+    __syncthreads();
     if (tid == 0) {
       const int64_t base = (int64_t)tile * T;
       for (int j = 0; j < P.m; ++j) {
@@ -408,7 +446,8 @@ __global__ void __launch_bounds__(32 * NW)
         const bool fullk = __all_sync(FULL, K == kmax || K == 0);
         float acc[4] = {0.f, 0.f, 0.f, 0.f};
         if (kmax == 32 && fullk) {
-          chain32<X2, kChainB>(acc, tile_s, soff, pa, wu);
+          if (kChainRegs) chain32_regs<X2>(acc, tile_s, src_s + gi * 32, pa, wu);
+          else chain32<X2, kChainB>(acc, tile_s, soff, pa, wu);
         } else {
 #pragma unroll
           for (int r = 0; r < EPL; ++r) {
