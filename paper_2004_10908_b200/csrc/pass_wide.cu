@@ -46,7 +46,7 @@ namespace sdnn {
 #endif
 constexpr int kChainB = SDNN_CHAIN_B;                   // loads in flight per lane (chain32)
 #ifndef SDNN_CHAIN_REGS
-#define SDNN_CHAIN_REGS 1
+#define SDNN_CHAIN_REGS 0
 #endif
 constexpr bool kChainRegs = SDNN_CHAIN_REGS != 0;       // k_pass_t32: shuffle-free addresses
 constexpr int kWideNW = 8;                              // warps
@@ -89,7 +89,8 @@ __device__ __forceinline__ void chain32(float (&acc)[4], const float *base, cons
 // The 32-term fast path without shuffles: every lane of the unit reads the
 // group's 32 u16 slot codes itself (four 16-byte shared loads, broadcast to
 // the unit's 8 lanes) and forms each term's address with two integer ops, so
-// no term waits on a shuffle (SDNN_CHAIN_REGS=0: the shuffle version)
+// no term waits on a shuffle (opt-in, SDNN_CHAIN_REGS=1 at build time:
+// measured on C4 1797 vs 1760 ms/step for the shuffle version)
 template <bool X2>
 __device__ __forceinline__ void chain32_regs(float (&acc)[4], const float *base, const uint16_t *codes, int pa,
                                              float wu) {
