@@ -368,6 +368,7 @@ static void build_pass_impl(const std::vector<const PackedLayer *> &layers, int3
   }
   std::vector<std::vector<std::vector<int32_t>>> bins(ncomp);   // [comp][bin] rows
   int C = 1, R = 1;
+  if (blocked && pass_wide_mode() == 2) cta_rows = std::min(cta_rows, 512);   // 2-CTA clusters
   for (int c = 0; c < ncomp; ++c) {
     auto &v = subs[c];
     std::stable_sort(v.begin(), v.end(), [](const auto &x, const auto &y) { return x.size() > y.size(); });
@@ -436,6 +437,13 @@ static void build_pass_impl(const std::vector<const PackedLayer *> &layers, int3
     out.NW = Rp <= 128 ? 1 : Rp <= 256 ? 2 : 4;
     out.S = pass_t32_stages(out.NW);
     if (!pass_t32_variant(out.NW, out.S)) out.NW = 0;
+  }
+  // SDNN_PASS_WIDE=2: components of 513-1024 rows over 2-CTA clusters of
+  // k_pass_t32 (512 rows per CTA, binned with cta = 512 above)
+  if (out.NB == 1 && C == 2 && blocked && pass_wide_mode() == 2 && pass_t32_variant(4, 1, 2)) {
+    out.T = 32;
+    out.NW = 4;
+    out.S = 1;
   }
   if (out.NB == 3) {                              // half 0 = the first 512 slots
     out.split.assign(ncomp, 0);

@@ -333,13 +333,7 @@ void launch_pass_wide(const LaunchCfg &c, const Workspace &w, const DevPass &P, 
 
 // planner switch (fuse.cpp): 513-1024-row components in one CTA get this
 // kernel (SDNN_PASS_WIDE=0: 16-position k_pass tiles instead)
-bool pass_wide_enabled() {
-  static const bool v = [] {
-    const char *e = getenv("SDNN_PASS_WIDE");
-    return !(e && atoi(e) == 0);
-  }();
-  return v;
-}
+bool pass_wide_enabled() { return pass_wide_mode() == 1; }
 
 
 
@@ -355,7 +349,7 @@ bool pass_wide_enabled() {
 // CTA a 64 KB tile and 4 warps (128-row passes: 4 groups = 2 busy warps).  The
 // arithmetic and the record are k_pass's (fuse.cpp, PassHost.NW > 0).
 // ---------------------------------------------------------------------------
-template <int NW, int S, bool X2>
+template <int NW, int S, bool X2, int C>
 __global__ void __launch_bounds__(32 * NW)
     k_pass_t32(const __grid_constant__ DevPass P, const LayerState *__restrict__ st, float *Ya, float *Yb,
                uint32_t *__restrict__ alive, int64_t wstride, float ymax, uint32_t buf_bytes) {
@@ -380,7 +374,12 @@ __global__ void __launch_bounds__(32 * NW)
   const int64_t R = P.yblk;
   const int lgo = P.lg_out;
   const uint32_t rec_off = (uint32_t)P.R * 128u;  // record after the tile in each buffer
-  const int64_t cid = blockIdx.x, ncl = gridDim.x;
+  // C = 2: a component of up to 1024 rows over a 2-CTA cluster (each CTA
+  // holds its bin's rows); layers 0..m-2 stay in the CTA, the last reads its
+  // sources from both CTAs' tiles (DSMEM) between two cluster barriers
+  const uint32_t rank = C > 1 ? cluster_rank() : 0u;
+  const int64_t cid = C > 1 ? (int64_t)cluster_id_x() : (int64_t)blockIdx.x;
+  const int64_t ncl = C > 1 ? (int64_t)nclusters_x() : (int64_t)gridDim.x;
   if (tid == 0) {
     for (int b = 0; b < S; ++b) mbar_init(bar + b, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -389,7 +388,7 @@ __global__ void __launch_bounds__(32 * NW)
   __syncthreads();
   auto issue = [&](int64_t it, int b) {
     if (tid != 0 || it >= items) return;
-    const int64_t c = item_comp(it);
+    const int64_t c = item_comp(it) * C + rank;
     const int tile = item_tile(it);
     const int cnt = __ldg(P.in_count + c);
     unsigned char *dst = smem_raw + (size_t)b * buf_bytes;
@@ -409,7 +408,8 @@ __global__ void __launch_bounds__(32 * NW)
     mbar_wait(bar + b, ph);
     auto release_and_load = [&]() {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncthreads();
+      if (C > 1) cluster_sync();                 // the peer has read this tile too
+      else __syncthreads();
       issue(it + S * ncl, b);
     };
     bool issued = false;
@@ -424,6 +424,8 @@ __global__ void __launch_bounds__(32 * NW)
       const float *bias_s = reinterpret_cast<const float *>(rec_s + (ubias ? 0 : PL.off_bias));
       const uint16_t *orow_s = reinterpret_cast<const uint16_t *>(rec_s + (last ? PL.off_orow : 0));
       const bool early = last && units <= NW * UPW;
+      const bool remote = C > 1 && last;
+      if (remote) cluster_sync();                // every CTA's tile is at boundary m-1
       for (int u0 = 0; u0 < units; u0 += NW * UPW) {
         const int u = u0 + warp * UPW + seg;
         int K = 0, G = 0, gi = 0;
@@ -439,14 +441,27 @@ __global__ void __launch_bounds__(32 * NW)
 #pragma unroll
         for (int r = 0; r < EPL; ++r) {
           const int e = r * LPU + sll;
-          soff[r] = K > 0 ? (uint32_t)(src_s[gi * 32 + (e < K ? e : 0)] & 0x3ff) * 32u : 0u;
+          const uint32_t code = K > 0 ? src_s[gi * 32 + (e < K ? e : 0)] : 0u;
+          soff[r] = remote ? cluster_map(smem_u32(tile_s) + (code & 0x3ffu) * 128u, code >> 10)
+                           : (code & 0x3ffu) * 32u;
           bia[r] = (!ubias && e < G) ? bias_s[gi * 32 + e] : 0.f;
           orw[r] = (last && e < G) ? orow_s[gi * 32 + e] : 0;
         }
         const int kmax = __reduce_max_sync(FULL, K);
         const bool fullk = __all_sync(FULL, K == kmax || K == 0);
         float acc[4] = {0.f, 0.f, 0.f, 0.f};
-        if (kmax == 32 && fullk) {
+        if (remote) {                            // DSMEM: byte addresses in the cluster window
+#pragma unroll
+          for (int r = 0; r < EPL; ++r) {
+            if (r * LPU >= kmax) break;
+#pragma unroll
+            for (int l = 0; l < LPU; ++l) {
+              const int t = r * LPU + l;
+              const uint32_t a = __shfl_sync(FULL, soff[r], l, LPU);
+              if (t < kmax) acc4<X2>(acc, ld_cluster_f4(a + (uint32_t)(pa * 4)), t < K ? wu : 0.f);
+            }
+          }
+        } else if (kmax == 32 && fullk) {
           if (kChainRegs) chain32_regs<X2>(acc, tile_s, src_s + gi * 32, pa, wu);
           else chain32<X2, kChainB>(acc, tile_s, soff, pa, wu);
         } else {
@@ -517,55 +532,102 @@ __global__ void __launch_bounds__(32 * NW)
     if (!issued) release_and_load();
     __syncthreads();
   }
+  if (C > 1) cluster_sync();                     // no CTA exits while its peer may read its tile
 }
 
 // (NW, S) instances: NW = ceil(rows / 128) warps, S buffers
 #define SDNN_T32_VARIANTS(X) X(1, 1) X(1, 2) X(1, 3) X(2, 1) X(2, 2) X(2, 3) X(4, 1) X(4, 2)
+#define SDNN_T32C_VARIANTS(X) X(4, 1)           // 2-CTA clusters
 
 static uint32_t t32_buf_bytes(const DevPass &P) {
   return (uint32_t)(((size_t)P.R * 128 + P.rec_bytes + 127) / 128 * 128);
 }
 static size_t t32_smem(const DevPass &P, int S) { return (size_t)S * t32_buf_bytes(P) + 8 * S + 4 * kMaxPassLayers; }
 
-bool pass_t32_variant(int nw, int s) {
-#define X(NN, SS) if (nw == NN && s == SS) return true;
+bool pass_t32_variant(int nw, int s, int c) {
+#define X(NN, SS) if (c == 1 && nw == NN && s == SS) return true;
   SDNN_T32_VARIANTS(X)
+#undef X
+#define X(NN, SS) if (c == 2 && nw == NN && s == SS) return true;
+  SDNN_T32C_VARIANTS(X)
 #undef X
   return false;
 }
+// 513-1024-row components (SDNN_PASS_WIDE): 2 = 2-CTA clusters of k_pass_t32
+// (default; C4 1024-row passes 3.03 ms, 1718 ms/step), 1 = k_pass_wide (3.35
+// ms, 1750-1762 ms/step), 0 = 16-position k_pass tiles (3.45 ms)
+int pass_wide_mode() {
+  static const int v = [] {
+    const char *e = getenv("SDNN_PASS_WIDE");
+    return e ? atoi(e) : 2;
+  }();
+  return v;
+}
 size_t pass_t32_smem_max() { return 227 * 1024; }
 
-template <int NW, int S, bool X2>
+template <int NW, int S, bool X2, int C>
 static void launch_t32(const LaunchCfg &c, const Workspace &w, const DevPass &P, uint32_t *alive, float ymax,
                        cudaStream_t s) {
   const size_t smem = t32_smem(P, S);
   static size_t set_smem = 0;                    // (per instance: the largest size configured so far)
   if (smem > set_smem) {
-    cudaFuncSetAttribute(k_pass_t32<NW, S, X2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_pass_t32<NW, S, X2, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     set_smem = smem;
   }
-  int occ = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pass_t32<NW, S, X2>, 32 * NW, smem) != cudaSuccess ||
-      occ <= 0) {
-    cudaGetLastError();
-    occ = 1;
+  if (C == 1) {
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pass_t32<NW, S, X2, C>, 32 * NW, smem) !=
+            cudaSuccess ||
+        occ <= 0) {
+      cudaGetLastError();
+      occ = 1;
+    }
+    k_pass_t32<NW, S, X2, C><<<c.sms * occ, 32 * NW, smem, s>>>(P, w.st, w.Y[0], w.Y[1], alive, w.words, ymax,
+                                                               t32_buf_bytes(P));
+    return;
   }
-  k_pass_t32<NW, S, X2><<<c.sms * occ, 32 * NW, smem, s>>>(P, w.st, w.Y[0], w.Y[1], alive, w.words, ymax,
-                                                          t32_buf_bytes(P));
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = C;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cfg.blockDim = dim3(32 * NW);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.gridDim = dim3(C * c.sms);
+  int ncl = 0;
+  if (cudaOccupancyMaxActiveClusters(&ncl, k_pass_t32<NW, S, X2, C>, &cfg) != cudaSuccess || ncl <= 0) {
+    cudaGetLastError();
+    ncl = c.sms / C;
+  }
+  cfg.gridDim = dim3(C * ncl);
+  cudaLaunchKernelEx(&cfg, k_pass_t32<NW, S, X2, C>, P, (const LayerState *)w.st, w.Y[0], w.Y[1], alive,
+                     (int64_t)w.words, ymax, t32_buf_bytes(P));
 }
 
 void launch_pass_t32(const LaunchCfg &c, const Workspace &w, const DevPass &P, uint32_t *alive, float ymax,
                      cudaStream_t s) {
   const bool x2 = wide_x2();
-#define X(NN, SS)                                                    \
-  if (P.NW == NN && P.S == SS) {                                     \
-    if (x2) launch_t32<NN, SS, true>(c, w, P, alive, ymax, s);       \
-    else launch_t32<NN, SS, false>(c, w, P, alive, ymax, s);         \
-    return;                                                          \
+#define X(NN, SS)                                                      \
+  if (P.C == 1 && P.NW == NN && P.S == SS) {                           \
+    if (x2) launch_t32<NN, SS, true, 1>(c, w, P, alive, ymax, s);      \
+    else launch_t32<NN, SS, false, 1>(c, w, P, alive, ymax, s);        \
+    return;                                                            \
   }
   SDNN_T32_VARIANTS(X)
 #undef X
-  fprintf(stderr, "sdnn: no k_pass_t32 instance for NW=%d S=%d\n", P.NW, P.S);
+#define X(NN, SS)                                                      \
+  if (P.C == 2 && P.NW == NN && P.S == SS) {                           \
+    if (x2) launch_t32<NN, SS, true, 2>(c, w, P, alive, ymax, s);      \
+    else launch_t32<NN, SS, false, 2>(c, w, P, alive, ymax, s);        \
+    return;                                                            \
+  }
+  SDNN_T32C_VARIANTS(X)
+#undef X
+  fprintf(stderr, "sdnn: no k_pass_t32 instance for NW=%d S=%d C=%d\n", P.NW, P.S, P.C);
   abort();
 }
 

@@ -290,7 +290,8 @@ bool pass_wide_enabled();
 // for NW warps: pass_t32_stages(NW) (SDNN_PASS_T32_S)
 int pass_t32_mode();
 int pass_t32_stages(int nw);
-bool pass_t32_variant(int nw, int s);
+bool pass_t32_variant(int nw, int s, int c = 1);
+int pass_wide_mode();
 void launch_pass_t32(const LaunchCfg &c, const Workspace &w, const DevPass &P, uint32_t *alive, float ymax,
                      cudaStream_t s);
 void configure_pass_wide();

@@ -1,5 +1,5 @@
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-L=$GRAFT_REPO_ROOT/paper_2004_10908_b200
-timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "knob or c2 or c4 or c1" > gpurun_out/r3a_t.log 2>&1; tail -1 gpurun_out/r3a_t.log
-bash tools/gpujob.sh r3a bench:c4::regs env:SDNN_LIB=$L/libsdnn_r0.so bench:c4::shfl env:SDNN_LIB=$L/libsdnn.so bench:c4::regs2 "full:c4:k_pass_t32<.int.4:60"
+timeout 600 python tools/e2e_probe.py c2 > gpurun_out/r3d_probe_c2.log 2>&1; tail -6 gpurun_out/r3d_probe_c2.log
+SDNN_PASS_WIDE=1 timeout 600 python tools/e2e_probe.py c2 > gpurun_out/r3d_probe_c2_w1.log 2>&1; tail -6 gpurun_out/r3d_probe_c2_w1.log
+bash tools/gpujob.sh r3d bench:c2 bench:c2::rep "bench:c4:--net,rn-plain:plain" "bench:c3:--net,rn-plain:plain" "bench:c4:--net,rw:rw" "bench:c3:--net,rw:rw"
