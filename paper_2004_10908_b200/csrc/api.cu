@@ -551,6 +551,7 @@ sdnn_status make_plan(sdnn_net *net) {
     D.NB = H.NB;
     D.NW = H.NW;
     D.S = H.S;
+    D.general = H.general ? 1 : 0;
     D.rec_bytes = H.rec_bytes;
     if ((H.NB == 3 || H.NW > 0) && !net->yblk)
       return fail(SDNN_E_UNSUPPORTED, "a position-blocked pass kernel was planned for row-major activations");
@@ -591,8 +592,12 @@ sdnn_status make_plan(sdnn_net *net) {
     }
     for (int j = 0; j < H.m; ++j) {
       const PassHostLayer &HL = H.layers[j];
+      const DevLayer &DL = net->dl[H.a + j];
       D.layers[j] = PassLayerDev{HL.off_kg, HL.off_src, HL.off_bias, HL.off_orow, HL.NG, HL.wu, HL.bu,
-                                 HL.off_vs, HL.vt};
+                                 HL.off_vs, HL.vt, HL.off_gid, HL.general ? DL.val : nullptr,
+                                 DL.kmax, DL.gmax};
+      if (HL.general && (!DL.val || (reinterpret_cast<uintptr_t>(DL.val) & 15)))
+        return fail(SDNN_E_UNSUPPORTED, "per-slot weights of a fused layer are not 16-byte aligned");
     }
     net->steps[q].pass = (int32_t)net->passes.size();
     net->passes.push_back(D);

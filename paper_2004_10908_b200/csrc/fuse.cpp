@@ -46,7 +46,12 @@ struct UF {
   }
 };
 
-bool fusable(const PackedLayer &p) { return p.uniform && p.kmax <= 32 && p.gmax <= 32; }
+// general: per-slot (non-uniform) layers may be fused too (blocked plans only:
+// k_pass_gw is their only pass kernel); a lane reads 8 members' weights of a
+// term as two float4 of a 32-member row, hence gmax == 32
+bool fusable(const PackedLayer &p, bool general = false) {
+  return (p.uniform || (general && p.gmax == 32)) && p.kmax <= 32 && p.gmax <= 32;
+}
 
 // a layer whose groups can overwrite their own source slots: every source row
 // feeds at most one group, and no group has more members than sources
@@ -157,10 +162,10 @@ namespace {
 // length k <= that, the largest component (rows at the first boundary); every
 // prefix of a feasible pass is feasible
 int max_pass_len(const std::vector<const PackedLayer *> &layers, int32_t n, int a, int cap,
-                 int max_m, int cta_rows, std::vector<int> &rows_at) {
+                 int max_m, int cta_rows, std::vector<int> &rows_at, bool general) {
   const int L = (int)layers.size();
   rows_at.assign(max_m + 1, 1);
-  if (!(cap > 0 && max_m > 1 && fusable(*layers[a]))) return 1;
+  if (!(cap > 0 && max_m > 1 && fusable(*layers[a], general))) return 1;
   const int cap_cta = std::min(cap, cta_rows);
   const int max_bins = std::max(1, cap / cta_rows);
   UF full, sub;
@@ -180,7 +185,7 @@ int max_pass_len(const std::vector<const PackedLayer *> &layers, int32_t n, int 
   };
   rows_at[1] = 32;
   int m = 1;
-  while (a + m < L && m < max_m && fusable(*layers[a + m]) && inplace(*layers[a + m - 1])) {
+  while (a + m < L && m < max_m && fusable(*layers[a + m], general) && inplace(*layers[a + m - 1])) {
     add_layer(sub, *layers[a + m - 1], n, m - 1);
     add_layer(full, *layers[a + m], n, m);
     std::fill(stamp.begin(), stamp.begin() + (int64_t)(m + 1) * n, 0);
@@ -200,7 +205,7 @@ bool cost_planner() {                            // default; SDNN_PLAN=greedy fo
 }  // namespace
 
 static std::vector<Step> plan_steps_greedy(const std::vector<const PackedLayer *> &layers, int32_t n,
-                                           int cap, int max_m, int cta_rows, int a_begin) {
+                                           int cap, int max_m, int cta_rows, int a_begin, bool general) {
   std::vector<Step> steps;
   const int L = (int)layers.size();
   max_m = std::max(1, std::min(max_m, kMaxPassLayers));
@@ -211,7 +216,7 @@ static std::vector<Step> plan_steps_greedy(const std::vector<const PackedLayer *
   std::vector<int32_t> cnt, stamp, size, owner;
   for (int a = a_begin; a < L;) {
     int m = 1;
-    if (cap > 0 && max_m > 1 && fusable(*layers[a])) {
+    if (cap > 0 && max_m > 1 && fusable(*layers[a], general)) {
       const int64_t nodes = (int64_t)(max_m + 1) * n;
       full.init(nodes);
       sub.init(nodes);
@@ -220,7 +225,7 @@ static std::vector<Step> plan_steps_greedy(const std::vector<const PackedLayer *
       size.assign(nodes, 0);
       add_layer(full, *layers[a], n, 0);
       // layer a+m-1 stops being the last layer of the pass: it must allow in-place slots
-      while (a + m < L && m < max_m && fusable(*layers[a + m]) && inplace(*layers[a + m - 1])) {
+      while (a + m < L && m < max_m && fusable(*layers[a + m], general) && inplace(*layers[a + m - 1])) {
         add_layer(sub, *layers[a + m - 1], n, m - 1);
         add_layer(full, *layers[a + m], n, m);
         std::fill(stamp.begin(), stamp.end(), 0);
@@ -246,7 +251,7 @@ static std::vector<Step> plan_steps_greedy(const std::vector<const PackedLayer *
 // 2.61 ms on C4); ties go to the longer first pass.  Measured: C4 2021 vs
 // 2056 ms/step, C3 368 vs 376 ms for the greedy cover.
 static std::vector<Step> plan_steps_cost(const std::vector<const PackedLayer *> &layers, int32_t n,
-                                         int cap, int max_m, int cta_rows, int a_begin) {
+                                         int cap, int max_m, int cta_rows, int a_begin, bool general) {
   const int L = (int)layers.size();
   std::vector<int> mm(L, 1);
   std::vector<std::vector<int>> rows(L);
@@ -256,7 +261,7 @@ static std::vector<Step> plan_steps_cost(const std::vector<const PackedLayer *> 
     std::vector<std::thread> th;
     for (int t = 0; t < nt; ++t)
       th.emplace_back([&] {
-        for (int a = next++; a < L; a = next++) mm[a] = max_pass_len(layers, n, a, cap, max_m, cta_rows, rows[a]);
+        for (int a = next++; a < L; a = next++) mm[a] = max_pass_len(layers, n, a, cap, max_m, cta_rows, rows[a], general);
       });
     for (auto &x : th) x.join();
   }
@@ -289,12 +294,12 @@ static std::vector<Step> plan_steps_cost(const std::vector<const PackedLayer *> 
 }
 
 std::vector<Step> plan_steps(const std::vector<const PackedLayer *> &layers, int32_t n, int cap,
-                             int max_m, int cta_rows, int a_begin) {
+                             int max_m, int cta_rows, int a_begin, bool general) {
   if (a_begin >= (int)layers.size()) return {};
   const int mm_ = std::max(1, std::min(max_m, kMaxPassLayers));
   const int cap_ = std::min(cap, cta_rows * kMaxPassCluster);
-  return cost_planner() ? plan_steps_cost(layers, n, cap_, mm_, cta_rows, a_begin)
-                        : plan_steps_greedy(layers, n, cap, max_m, cta_rows, a_begin);
+  return cost_planner() ? plan_steps_cost(layers, n, cap_, mm_, cta_rows, a_begin, general)
+                        : plan_steps_greedy(layers, n, cap, max_m, cta_rows, a_begin, general);
 }
 
 static void build_pass_impl(const std::vector<const PackedLayer *> &layers, int32_t n, const Step &s,
@@ -368,7 +373,9 @@ static void build_pass_impl(const std::vector<const PackedLayer *> &layers, int3
   }
   std::vector<std::vector<std::vector<int32_t>>> bins(ncomp);   // [comp][bin] rows
   int C = 1, R = 1;
-  if (blocked && pass_wide_mode() == 2) cta_rows = std::min(cta_rows, 512);   // 2-CTA clusters
+  bool gen_pass = false;                          // per-slot weights somewhere in the pass
+  for (int b = 0; b < m; ++b) gen_pass = gen_pass || !layers[s.a + b]->uniform;
+  if (blocked && pass_wide_mode() == 2 && m >= 3 && !gen_pass) cta_rows = std::min(cta_rows, 512);   // 2-CTA clusters
   for (int c = 0; c < ncomp; ++c) {
     auto &v = subs[c];
     std::stable_sort(v.begin(), v.end(), [](const auto &x, const auto &y) { return x.size() > y.size(); });
@@ -438,9 +445,24 @@ static void build_pass_impl(const std::vector<const PackedLayer *> &layers, int3
     out.S = pass_t32_stages(out.NW);
     if (!pass_t32_variant(out.NW, out.S)) out.NW = 0;
   }
+  // per-slot-weight layers in the pass: only k_pass_gw runs them (blocked
+  // layout, one CTA per component of <= 512 rows); anything else is not
+  // buildable here and plan_passes falls back (shorter pass / plain layer)
+  if (gen_pass) {
+    if (!(blocked && C == 1 && Rp <= 1024)) {
+      out = PassHost();
+      return;
+    }
+    out.general = true;
+    out.T = 32;
+    out.NB = 1;
+    out.NW = Rp <= 128 ? 4 : 8;                   // warps: one group (32 rows) per warp and round
+    out.S = 1;
+    out.split.clear();
+  }
   // SDNN_PASS_WIDE=2: components of 513-1024 rows over 2-CTA clusters of
   // k_pass_t32 (512 rows per CTA, binned with cta = 512 above)
-  if (out.NB == 1 && C == 2 && blocked && pass_wide_mode() == 2 && pass_t32_variant(4, 1, 2)) {
+  if (out.NB == 1 && C == 2 && R <= 512 && blocked && pass_wide_mode() == 2 && pass_t32_variant(4, 1, 2)) {
     out.T = 32;
     out.NW = 4;
     out.S = 1;
@@ -715,6 +737,8 @@ static void build_pass_impl(const std::vector<const PackedLayer *> &layers, int3
     H.bias.assign(units * NG * 32, 0.f);
     H.k.assign(units * NG, 0);
     H.g.assign(units * NG, 0);
+    H.general = !p.uniform;
+    if (H.general) H.gid.assign(units * NG, 0);
     if (last) H.orow.assign(units * NG * 32, 0);      // u16: N <= 65536
     const int64_t in0 = (int64_t)b * n, out0 = (int64_t)(b + 1) * n;
     if (!last && dedup[b]) H.vs.assign(units * NG, 0);
@@ -731,6 +755,7 @@ static void build_pass_impl(const std::vector<const PackedLayer *> &layers, int3
         const int K = p.gk[g], G = p.gg[g];
         H.k[rec] = (uint8_t)K;
         H.g[rec] = (uint8_t)G;
+        if (!p.uniform) H.gid[rec] = (uint16_t)g;      // per-slot weights: W_l[g] (k_pass_gw)
         // keeps the ascending source order (canonical chain); non-last layers read
         // their own CTA's slots, the last layer the (bin << 10 | slot) code
         int32_t code[32];
@@ -801,6 +826,11 @@ static void build_pass_impl(const std::vector<const PackedLayer *> &layers, int3
     off += (H.NG * 2 + 15) / 16 * 16;
     H.off_src = off;
     off += H.NG * 64;
+    H.off_gid = -1;
+    if (H.general) {                              // group ids (u16) of a per-slot-weight layer
+      H.off_gid = off;
+      off += (H.NG * 2 + 15) / 16 * 16;
+    }
     H.off_vs = -1;
     if (!H.vs.empty()) {                          // shared-value slots (dedup), u16 per group
       H.off_vs = off;
@@ -868,6 +898,7 @@ static void build_pass_impl(const std::vector<const PackedLayer *> &layers, int3
       }
       std::memcpy(r + H.off_src, H.src.data() + g0 * 32, (size_t)H.NG * 64);
       if (H.off_vs >= 0) std::memcpy(r + H.off_vs, H.vs.data() + g0, (size_t)H.NG * 2);
+      if (H.off_gid >= 0) std::memcpy(r + H.off_gid, H.gid.data() + g0, (size_t)H.NG * 2);
       if (H.off_bias >= 0) std::memcpy(r + H.off_bias, H.bias.data() + g0 * 32, (size_t)H.NG * 128);
       if (H.off_orow >= 0) std::memcpy(r + H.off_orow, H.orow.data() + g0 * 32, (size_t)H.NG * 64);
     }
@@ -878,12 +909,22 @@ std::vector<Step> plan_passes(const std::vector<const PackedLayer *> &layers, in
                               int max_m, int tile_floats, int threads,
                               std::vector<PassHost> *built, int cta_rows, bool single_passes,
                               bool share_values) {
-  std::vector<Step> steps = plan_steps(layers, n, cap, max_m, cta_rows, 0);
+  // per-slot-weight layers join passes in blocked plans (k_pass_gw) only on
+  // request (SDNN_PASS_GENERAL=1): exact, but measured slower than the
+  // single-layer k_layer_bulkw steps (C4-RW 10.9 vs 4.1 s/step, C3-RW 3.17 vs
+  // 1.52 s: the weights of every term come from L2 into registers, 96-128
+  // registers per thread, two CTAs per SM)
+  static const bool gen_env = [] {
+    const char *e = getenv("SDNN_PASS_GENERAL");
+    return e && atoi(e) == 1;
+  }();
+  const bool general = single_passes && gen_env;
+  std::vector<Step> steps = plan_steps(layers, n, cap, max_m, cta_rows, 0, general);
   std::vector<PassHost> ph(steps.size());
   std::vector<char> done(steps.size(), 0);
   // single_passes: a lone fusable layer also runs as a (one-layer) pass
   auto is_pass = [&](const Step &x) {
-    return x.m > 1 || (single_passes && cap > 0 && fusable(*layers[x.a]));
+    return x.m > 1 || (single_passes && cap > 0 && fusable(*layers[x.a], general));
   };
   for (;;) {
     std::vector<int> todo;
@@ -916,7 +957,7 @@ std::vector<Step> plan_passes(const std::vector<const PackedLayer *> &layers, in
     done.resize(bad + 1);
     done[bad] = 0;
     ph[bad] = PassHost();
-    for (const Step &x : plan_steps(layers, n, cap, max_m, cta_rows, resume)) {
+    for (const Step &x : plan_steps(layers, n, cap, max_m, cta_rows, resume, general)) {
       steps.push_back(x);
       ph.emplace_back();
       done.push_back(0);

@@ -1622,6 +1622,10 @@ void launch_pass(const LaunchCfg &c, const Workspace &w, const DevPass &P, uint3
     launch_pass_wide(c, w, P, alive, ymax, s);
     return;
   }
+  if (P.general) {
+    launch_pass_gw(c, w, P, alive, ymax, s);
+    return;
+  }
   if (P.NW > 0) {
     launch_pass_t32(c, w, P, alive, ymax, s);
     return;

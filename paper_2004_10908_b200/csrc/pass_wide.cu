@@ -41,6 +41,13 @@
 
 namespace sdnn {
 
+#ifndef SDNN_T32_FETCH
+#define SDNN_T32_FETCH 0                                // k_pass_t32: next item's rows fetched an item ahead
+#endif
+#ifndef SDNN_REMOTE_FAST
+#define SDNN_REMOTE_FAST 0                              // k_pass_t32 C = 2: unconditional 32-term DSMEM chain
+#endif
+// (both measured within run-to-run noise, 1754 vs 1762-1766 ms/step on one box: off)
 #ifndef SDNN_CHAIN_B
 #define SDNN_CHAIN_B 0
 #endif
@@ -333,7 +340,7 @@ void launch_pass_wide(const LaunchCfg &c, const Workspace &w, const DevPass &P, 
 
 // planner switch (fuse.cpp): 513-1024-row components in one CTA get this
 // kernel (SDNN_PASS_WIDE=0: 16-position k_pass tiles instead)
-bool pass_wide_enabled() { return pass_wide_mode() == 1; }
+bool pass_wide_enabled() { return pass_wide_mode() >= 1; }   // (mode 2: the 2-layer passes)
 
 
 
@@ -386,18 +393,31 @@ __global__ void __launch_bounds__(32 * NW)
   }
   for (int q = tid; q < P.m; q += blockDim.x) aw[q] = 0u;
   __syncthreads();
-  auto issue = [&](int64_t it, int b) {
+  // the row count and first storage row of an item's (component, rank) come
+  // from global memory: fetched (thread 0) an item ahead of the issue, so the
+  // issue after the release does not wait on a dependent global load
+  int nx_cnt = 0;
+  int64_t nx_row = 0;
+  auto fetch = [&](int64_t it) {
+    if (tid != 0 || it >= items) return;
+    const int64_t c = item_comp(it) * C + rank;
+    nx_cnt = __ldg(P.in_count + c);
+    nx_row = __ldg(P.in_rows + c * P.rin);
+  };
+  auto issue = [&](int64_t it, int b) {          // (after fetch(it))
     if (tid != 0 || it >= items) return;
     const int64_t c = item_comp(it) * C + rank;
     const int tile = item_tile(it);
-    const int cnt = __ldg(P.in_count + c);
+    const int cnt = nx_cnt;
     unsigned char *dst = smem_raw + (size_t)b * buf_bytes;
     mbar_expect_tx_arrive(bar + b, (uint32_t)cnt * 128u + (uint32_t)P.rec_bytes);
     bulk_g2s(dst + rec_off, P.rec + c * P.rec_bytes, (uint32_t)P.rec_bytes, bar + b);
-    if (cnt > 0)
-      bulk_g2s(dst, Yin + ((int64_t)tile * R + __ldg(P.in_rows + c * P.rin)) * 32, (uint32_t)cnt * 128u, bar + b);
+    if (cnt > 0) bulk_g2s(dst, Yin + ((int64_t)tile * R + nx_row) * 32, (uint32_t)cnt * 128u, bar + b);
   };
-  for (int b = 0; b < S; ++b) issue(cid + b * ncl, b);
+  for (int b = 0; b < S; ++b) {
+    fetch(cid + b * ncl);
+    issue(cid + b * ncl, b);
+  }
   int64_t kk = 0;
   for (int64_t it = cid; it < items; it += ncl, ++kk) {
     const int b = S == 1 ? 0 : (int)(kk % S);
@@ -405,11 +425,17 @@ __global__ void __launch_bounds__(32 * NW)
     float *const tile_s = reinterpret_cast<float *>(smem_raw + (size_t)b * buf_bytes);
     const unsigned char *rec_s = smem_raw + (size_t)b * buf_bytes + rec_off;
     const int tile = item_tile(it);
+#if SDNN_T32_FETCH
+    fetch(it + S * ncl);                         // in flight while this item computes
+#endif
     mbar_wait(bar + b, ph);
     auto release_and_load = [&]() {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       if (C > 1) cluster_sync();                 // the peer has read this tile too
       else __syncthreads();
+#if !SDNN_T32_FETCH
+      fetch(it + S * ncl);
+#endif
       issue(it + S * ncl, b);
     };
     bool issued = false;
@@ -450,7 +476,13 @@ __global__ void __launch_bounds__(32 * NW)
         const int kmax = __reduce_max_sync(FULL, K);
         const bool fullk = __all_sync(FULL, K == kmax || K == 0);
         float acc[4] = {0.f, 0.f, 0.f, 0.f};
-        if (remote) {                            // DSMEM: byte addresses in the cluster window
+        if (SDNN_REMOTE_FAST && remote && kmax == 32 && fullk) {   // DSMEM: cluster-window byte addresses
+#pragma unroll
+          for (int r = 0; r < EPL; ++r)
+#pragma unroll
+            for (int l = 0; l < LPU; ++l)
+              acc4<X2>(acc, ld_cluster_f4(__shfl_sync(FULL, soff[r], l, LPU) + (uint32_t)(pa * 4)), wu);
+        } else if (remote) {
 #pragma unroll
           for (int r = 0; r < EPL; ++r) {
             if (r * LPU >= kmax) break;
@@ -535,6 +567,195 @@ __global__ void __launch_bounds__(32 * NW)
   if (C > 1) cluster_sync();                     // no CTA exits while its peer may read its tile
 }
 
+// ---------------------------------------------------------------------------
+// k_pass_gw<NW>: the fused pass for layers with per-slot weights (RW nets).
+// Structure of k_pass_t32 (one 32-position tile of the component per CTA,
+// one bulk copy + record, in-place slots, writer-ordered rows), but every
+// member has its own chain: a warp takes one group per round and computes its
+// 32 members x 32 positions as a register block -- lane = (member octet mo,
+// position quad pq): 8 members x 4 positions, 32 accumulators -- per term one
+// float4 of Y from shared memory and the 8 weights W_l[g][t][8mo..8mo+7] as
+// two float4 from L2 (the layer's weight block stays L2-resident across the
+// pass's tiles), 32 FMAs, each the canonical per-member chain (terms in
+// ascending source order, fmaf from +0, then the bias add and clamp; DESIGN
+// A5/A6).  Uniform layers of the same pass use the same loop with wu.
+// ---------------------------------------------------------------------------
+template <int NW>
+__global__ void __launch_bounds__(32 * NW)
+    k_pass_gw(const __grid_constant__ DevPass P, const LayerState *__restrict__ st, float *Ya, float *Yb,
+              uint32_t *__restrict__ alive, int64_t wstride, float ymax, uint32_t buf_bytes) {
+  constexpr int T = 32;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint64_t *const bar = reinterpret_cast<uint64_t *>(smem_raw + (size_t)buf_bytes);
+  uint32_t *const aw = reinterpret_cast<uint32_t *>(bar + 1);
+  float *const tile_s = reinterpret_cast<float *>(smem_raw);
+  const uint32_t rec_off = (uint32_t)P.R * 128u;
+  const unsigned char *rec_s = smem_raw + rec_off;
+  const LayerState Sx = st[P.a];
+  const int width = Sx.width;
+  if (width <= 0) return;
+  const float *__restrict__ Yin = Sx.in ? Yb : Ya;
+  float *__restrict__ Yout = Sx.in ? Ya : Yb;
+  const int tiles = (width + T - 1) / T;
+  const int64_t items = (int64_t)P.ncomp * tiles;
+  const bool tmaj = P.order != 0;
+  auto item_comp = [&](int64_t it) -> int64_t { return tmaj ? it % P.ncomp : it / tiles; };
+  auto item_tile = [&](int64_t it) -> int { return (int)(tmaj ? it / P.ncomp : it % tiles); };
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int mo = lane >> 3, pq = lane & 7;       // members 8 mo .. 8 mo + 7, positions 4 pq .. 4 pq + 3
+  const int pa = pq * 4;
+  const int64_t R = P.yblk;
+  const int lgo = P.lg_out;
+  const int64_t cid = blockIdx.x, ncl = gridDim.x;
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int q = tid; q < P.m; q += blockDim.x) aw[q] = 0u;
+  __syncthreads();
+  auto issue = [&](int64_t it) {
+    if (tid != 0 || it >= items) return;
+    const int64_t c = item_comp(it);
+    const int tile = item_tile(it);
+    const int cnt = __ldg(P.in_count + c);
+    mbar_expect_tx_arrive(bar, (uint32_t)cnt * 128u + (uint32_t)P.rec_bytes);
+    bulk_g2s(smem_raw + rec_off, P.rec + c * P.rec_bytes, (uint32_t)P.rec_bytes, bar);
+    if (cnt > 0)
+      bulk_g2s(tile_s, Yin + ((int64_t)tile * R + __ldg(P.in_rows + c * P.rin)) * 32, (uint32_t)cnt * 128u, bar);
+  };
+  issue(cid);
+  int64_t kk = 0;
+  for (int64_t it = cid; it < items; it += ncl, ++kk) {
+    const int tile = item_tile(it);
+    mbar_wait(bar, (uint32_t)(kk & 1));
+    for (int j = 0; j < P.m; ++j) {
+      const PassLayerDev PL = P.layers[j];
+      const bool last = j == P.m - 1;
+      const bool ubias = PL.off_bias < 0;
+      const uint16_t *kg_s = reinterpret_cast<const uint16_t *>(rec_s + PL.off_kg);
+      const uint16_t *src_s = reinterpret_cast<const uint16_t *>(rec_s + PL.off_src);
+      const float *bias_s = reinterpret_cast<const float *>(rec_s + (ubias ? 0 : PL.off_bias));
+      const uint16_t *orow_s = reinterpret_cast<const uint16_t *>(rec_s + (last ? PL.off_orow : 0));
+      const uint16_t *gid_s = reinterpret_cast<const uint16_t *>(rec_s + (PL.off_gid >= 0 ? PL.off_gid : 0));
+      for (int u = warp; u < PL.NG; u += NW) {   // warp-uniform: one group per warp
+        const uint32_t kg = kg_s[u];
+        const int K = kg & 0xffu, G = kg >> 8;
+        if (G == 0) continue;
+        const uint32_t code = lane < K ? src_s[u * 32 + lane] : 0u;   // lane t: source t's slot
+        float acc[4][8];
+#pragma unroll
+        for (int p = 0; p < 4; ++p)
+#pragma unroll
+          for (int i = 0; i < 8; ++i) acc[p][i] = 0.f;
+        if (PL.off_gid >= 0) {
+          const float *W = PL.wv + (size_t)gid_s[u] * PL.wk * PL.wg + mo * 8;
+#pragma unroll 4
+          for (int t = 0; t < K; ++t) {
+            const uint32_t slot = __shfl_sync(FULL, code, t) & 0x3ffu;
+            const float4 y = *reinterpret_cast<const float4 *>(tile_s + slot * 32u + pa);
+            const float4 w0 = __ldg(reinterpret_cast<const float4 *>(W + (size_t)t * PL.wg));
+            const float4 w1 = __ldg(reinterpret_cast<const float4 *>(W + (size_t)t * PL.wg + 4));
+            const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+            const float yv[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+            for (int p = 0; p < 4; ++p)
+#pragma unroll
+              for (int i = 0; i < 8; ++i) acc[p][i] = __fmaf_rn(yv[p], wv[i], acc[p][i]);
+          }
+        } else {                                 // a uniform layer inside a per-slot pass
+#pragma unroll 4
+          for (int t = 0; t < K; ++t) {
+            const uint32_t slot = __shfl_sync(FULL, code, t) & 0x3ffu;
+            const float4 y = *reinterpret_cast<const float4 *>(tile_s + slot * 32u + pa);
+            const float yv[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+            for (int p = 0; p < 4; ++p)
+#pragma unroll
+              for (int i = 0; i < 8; ++i) acc[p][i] = __fmaf_rn(yv[p], PL.wu, acc[p][i]);
+          }
+        }
+        __syncwarp();                            // every source read before a member overwrites one
+        const int64_t opos = (int64_t)tile * T + pa;
+        float *obase = Yout + (((opos >> lgo) * R) << lgo) + (opos & ((1 << lgo) - 1));
+        const int64_t rowmul = (int64_t)1 << lgo;
+        uint32_t ob = 0u;                        // positions of this lane alive in some member
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int mm = mo * 8 + i;
+          const uint32_t dslot = __shfl_sync(FULL, code, mm & 31) & 0x3ffu;   // in place: member mm -> slot of source mm
+          const int32_t orw = (last && mm < G) ? orow_s[u * 32 + mm] : 0;
+          if (mm < G) {
+            const float b = ubias ? PL.bu : bias_s[u * 32 + mm];
+            float4 y;
+            y.x = clampy(__fadd_rn(acc[0][i], b), ymax);
+            y.y = clampy(__fadd_rn(acc[1][i], b), ymax);
+            y.z = clampy(__fadd_rn(acc[2][i], b), ymax);
+            y.w = clampy(__fadd_rn(acc[3][i], b), ymax);
+            ob |= (__float_as_uint(y.x) ? 1u : 0u) | (__float_as_uint(y.y) ? 2u : 0u) |
+                  (__float_as_uint(y.z) ? 4u : 0u) | (__float_as_uint(y.w) ? 8u : 0u);
+            if (last) *reinterpret_cast<float4 *>(obase + (int64_t)orw * rowmul) = y;
+            else *reinterpret_cast<float4 *>(tile_s + dslot * 32u + pa) = y;
+          }
+        }
+        // liveness word of the tile: bit 4 pq + p from any member octet
+        uint32_t word = 0u;
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+          uint32_t b = __ballot_sync(FULL, (ob >> p) & 1u);
+          b = (b | (b >> 8) | (b >> 16) | (b >> 24)) & 0xffu;   // lane pq of any octet
+          b = (b | (b << 12)) & 0x000F000Fu;                    // bit k -> bit 4 k
+          b = (b | (b << 6)) & 0x03030303u;
+          b = (b | (b << 3)) & 0x11111111u;
+          word |= b << p;
+        }
+        if (lane == 0 && word) atomicOr(&aw[j], word);
+      }
+      if (last) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();                         // every read of the tile and record is done
+        issue(it + ncl);
+      } else {
+        __syncthreads();                         // the next layer reads slots other warps wrote
+      }
+    }
+    if (tid == 0) {
+      const int64_t base = (int64_t)tile * T;
+      for (int j = 0; j < P.m; ++j) {
+        uint32_t word = aw[j];
+        aw[j] = 0u;
+        if (base >= width) word = 0u;
+        else if (width - base < 32) word &= (1u << (width - base)) - 1u;
+        if (word) atomicOr(&alive[j * wstride + (base >> 5)], word);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <int NW>
+static void launch_gw(const LaunchCfg &c, const Workspace &w, const DevPass &P, uint32_t *alive, float ymax,
+                      cudaStream_t s) {
+  const uint32_t bb = (uint32_t)(((size_t)P.R * 128 + P.rec_bytes + 127) / 128 * 128);
+  const size_t smem = (size_t)bb + 8 + 4 * kMaxPassLayers;
+  static size_t set_smem = 0;
+  if (smem > set_smem) {
+    cudaFuncSetAttribute(k_pass_gw<NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    set_smem = smem;
+  }
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pass_gw<NW>, 32 * NW, smem) != cudaSuccess || occ <= 0) {
+    cudaGetLastError();
+    occ = 1;
+  }
+  k_pass_gw<NW><<<c.sms * occ, 32 * NW, smem, s>>>(P, w.st, w.Y[0], w.Y[1], alive, w.words, ymax, bb);
+}
+
+void launch_pass_gw(const LaunchCfg &c, const Workspace &w, const DevPass &P, uint32_t *alive, float ymax,
+                    cudaStream_t s) {
+  if (P.NW <= 4) launch_gw<4>(c, w, P, alive, ymax, s);
+  else launch_gw<8>(c, w, P, alive, ymax, s);
+}
+
 // (NW, S) instances: NW = ceil(rows / 128) warps, S buffers
 #define SDNN_T32_VARIANTS(X) X(1, 1) X(1, 2) X(1, 3) X(2, 1) X(2, 2) X(2, 3) X(4, 1) X(4, 2)
 #define SDNN_T32C_VARIANTS(X) X(4, 1)           // 2-CTA clusters
@@ -554,8 +775,11 @@ bool pass_t32_variant(int nw, int s, int c) {
   return false;
 }
 // 513-1024-row components (SDNN_PASS_WIDE): 2 = 2-CTA clusters of k_pass_t32
-// (default; C4 1024-row passes 3.03 ms, 1718 ms/step), 1 = k_pass_wide (3.35
-// ms, 1750-1762 ms/step), 0 = 16-position k_pass tiles (3.45 ms)
+// for passes of >= 3 layers and k_pass_wide for 2-layer passes (default; C4
+// 1024-row 3-layer passes 3.03 vs 3.35 ms; on the plain schedule, whose
+// 1024-row passes have 2 layers, half the terms of a 2-layer pass are remote:
+// C4-plain 2742 ms/step with clusters vs 2567 with k_pass_wide), 1 =
+// k_pass_wide always, 0 = 16-position k_pass tiles (3.45 ms)
 int pass_wide_mode() {
   static const int v = [] {
     const char *e = getenv("SDNN_PASS_WIDE");

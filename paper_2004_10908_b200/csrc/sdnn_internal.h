@@ -125,7 +125,7 @@ constexpr int32_t kResidentStep = -2;  // layers [a, L) in the SMEM-resident ker
 // cap / kMaxPassRows CTAs (cap <= kMaxPassRows * kMaxPassCluster); tile
 // T = 16384 / (rows per CTA rounded up to a power of two), 32 <= T <= 512
 std::vector<Step> plan_steps(const std::vector<const PackedLayer *> &layers, int32_t n, int cap,
-                             int max_m, int cta_rows, int a_begin = 0);
+                             int max_m, int cta_rows, int a_begin = 0, bool general = false);
 
 struct PassHostLayer {
   int32_t NG = 0;                      // group slots per component (max over components)
@@ -141,6 +141,9 @@ struct PassHostLayer {
   std::vector<float> bias;             // [ncomp][NG][32] bias of each member
   std::vector<uint16_t> orow;          // last layer only: [ncomp][NG][32] output rows (N <= 65536)
   std::vector<uint8_t> k, g;           // [ncomp][NG] sources / members (0 = empty slot)
+  bool general = false;                // per-slot weights (k_pass_gw): gid[ncomp][NG] = the group's
+  std::vector<uint16_t> gid;           // index in W_l (source-major [G][kmax][gmax])
+  int32_t off_gid = -1;
 };
 struct PassHost {
   int32_t a = 0, m = 0, ncomp = 0, rin = 0, R = 0, T = 0;
@@ -151,6 +154,7 @@ struct PassHost {
   std::vector<int32_t> in_count;       // [ncomp]
   std::vector<int32_t> split;          // NB = 3: [ncomp] slots in half 0 (pass_wide.cu)
   int32_t NW = 0, S = 1;               // > 0: k_pass_t32 with NW warps and S tile buffers per CTA
+  bool general = false;                // some layer has per-slot weights: k_pass_gw<NW>
   std::vector<PassHostLayer> layers;   // [m]
   // per-component metadata record (one bulk copy next to the tile):
   //   for each layer j: kg[NG_j] u16 (K | G << 8) padded to 16 B, src[NG_j][32] u16
@@ -181,6 +185,9 @@ struct PassLayerDev {
                                                  // into the slot vs[group] (u16 array at this offset)
   int32_t vt;                                    // value table: 1 = write (two copies per group line),
                                                  // 2 = read (line = code, copy = phase half)
+  int32_t off_gid;                               // >= 0: per-slot weights, u16 group ids at this offset
+  const float *wv;                               // ... of W_l = wv[gid][t][member], strides wk, wg
+  int32_t wk, wg;
 };
 struct alignas(64) DevPass {
   // T = 16 passes over position-blocked activations: one TMA tensor map per
@@ -201,6 +208,7 @@ struct alignas(64) DevPass {
   const int32_t *in_rows, *in_count;
   const int32_t *split;                // NB = 3: [ncomp] slots in half 0
   int32_t NW, S;                       // NW > 0: k_pass_t32<NW, S> (pass_wide.cu)
+  int32_t general;                     // k_pass_gw<NW> (per-slot weights)
   const unsigned char *rec;            // [ncomp][rec_bytes]
   PassLayerDev layers[kMaxPassLayers]; // by value: the kernel parameter carries them
 };
@@ -295,6 +303,8 @@ int pass_wide_mode();
 void launch_pass_t32(const LaunchCfg &c, const Workspace &w, const DevPass &P, uint32_t *alive, float ymax,
                      cudaStream_t s);
 void configure_pass_wide();
+void launch_pass_gw(const LaunchCfg &c, const Workspace &w, const DevPass &P, uint32_t *alive, float ymax,
+                    cudaStream_t s);
 void launch_pass_wide(const LaunchCfg &c, const Workspace &w, const DevPass &P, uint32_t *alive, float ymax,
                       cudaStream_t s);
 // a fused pass: reads st[P.a], liveness of layer a+j to alive + j*words

@@ -8,7 +8,7 @@
 #   tests_fast   pytest -m "gpu and not slow"
 #   smoke        __graft_entry__.smoke()
 #   bench:CFG[:ARGS]   bench.py --config CFG (ARGS: extra flags, ',' -> ' ')
-#   launches:CFG       ncu launch list (gpu__time_duration, cold, serialised) of one inference
+#   launches:CFG[:ARGS[:SUFFIX]]  ncu launch list (gpu__time_duration, cold, serialised) of one inference
 #   full:CFG:KREGEX[:SKIP]  ncu --set full of one launch of the kernels matching KREGEX
 #   env:VAR=VAL  export for the following recipes
 #   sanitize     compute-sanitizer memcheck / synccheck / racecheck on tools/sanitize_run.py
@@ -41,10 +41,11 @@ for R in "$@"; do
     bench) X=${B//,/ }; N=${TAG}_bench_${A}${C:+_$C}
            timeout 1200 python bench.py --config $A $X > gpurun_out/$N.json 2> gpurun_out/$N.err
            echo "bench $A $X: $(summ gpurun_out/$N.json)" ;;
-    launches) timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
-                --log-file gpurun_out/${TAG}_launches_$A.csv python bench.py --config $A --oneshot --steps 1 --warmup 0 \
+    launches) X=${B//,/ }; N=${TAG}_launches_$A${C:+_$C}
+              timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+                --log-file gpurun_out/$N.csv python bench.py --config $A $X --oneshot --steps 1 --warmup 0 \
                 > /dev/null 2>&1
-              python tools/ncu_summary.py launches gpurun_out/${TAG}_launches_$A.csv 2>&1 | head -12 ;;
+              python tools/ncu_summary.py launches gpurun_out/$N.csv 2>&1 | head -12 ;;
     full) timeout 1200 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
             -k "regex:$B" -s "${C:-60}" -c 1 -o gpurun_out/${TAG}_full_${A}_$(echo "$B" | tr -cd 'a-z0-9_') \
             python bench.py --config $A --oneshot --steps 1 --warmup 0 ${FULLARGS:-} > gpurun_out/${TAG}_full.log 2>&1
