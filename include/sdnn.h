@@ -108,16 +108,18 @@ typedef struct sdnn_opts {
   void *stream;     /* cudaStream_t for sdnn_infer (NULL = a stream owned by the net) */
   int32_t fuse_rows;   /* multi-layer passes ("model decomposition"):
                           consecutive uniform layers run as one pass over the
-                          connected components of their union.  All layers but the
-                          last stay inside one CTA (sub-components of <= R
-                          neurons, updated in place in a 64 KB shared-memory tile
-                          of 16384/rows batch positions; R = 1024 with
-                          position-blocked activations, see stats.path bit 2,
-                          else 512); the last layer reads across a thread-block
-                          cluster of up to fuse_rows / R CTAs (distributed shared
-                          memory), so a component has <= fuse_rows neurons
-                          (<= 4 R, larger values are clamped; <= R: single-CTA
-                          passes; 0 = off; -1 = 1024)                             */
+                          connected components of their union, so a component
+                          has <= fuse_rows neurons (0 = off; -1 = 1024).  All
+                          layers but the last stay inside one CTA (sub-components
+                          of <= R neurons updated in place in shared memory); the
+                          last layer may read across a thread-block cluster
+                          (distributed shared memory).  Position-blocked
+                          activations (stats.path bit 2): R = 1024, 32-position
+                          tiles of <= 512-row components in CTAs sized by the
+                          component, 1024-row components over 2-CTA clusters
+                          (passes of >= 3 layers) or one CTA per SM (2 layers);
+                          row-major: R = 512, up to 4 R over clusters, larger
+                          values are clamped                                      */
   int32_t fuse_layers; /* at most this many layers per pass (<= 16; -1 = 8)           */
   int32_t resident_from; /* N <= 4096: layers [resident_from, L) run in one kernel that
                           keeps each CTA's batch tile resident in shared memory

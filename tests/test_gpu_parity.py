@@ -152,6 +152,23 @@ def test_fused_passes_rn(sd, fuse_rows, fuse_layers):
         assert st["live_rows"] == prof
 
 
+@pytest.mark.parametrize("spec_fn,n,fuse_rows", [("rn", 8192, 4096), ("rn", 8192, 2048), ("rn", 8192, -1),
+                                                  ("plain", 4096, -1), ("plain", 8192, -1)])
+def test_large_caps_and_schedules(sd, spec_fn, n, fuse_rows):
+    """Component caps above one CTA at N = 8192 (the planner must fall back from
+    shapes without a kernel instance), and the plain field schedule
+    whose 1024-row passes have two layers (k_pass_wide) -- full Y_L parity."""
+    L, B = 24, 300
+    spec = g.rn_spec(n, L) if spec_fn == "rn" else g.rn_plain_spec(n, L)
+    layers = list(g.iter_layers(spec))
+    rp, idx = g.ms_inputs(n, B, seed=41)
+    cats, Y, prof = oracle.infer(n, layers, rp, idx, None, profile=True)
+    cg, Yg, st = run_gpu(sd, n, layers, rp, idx, None, fmt="ell", fuse_rows=fuse_rows)
+    assert st["fused_layers"] > 0
+    assert_parity(cg, Yg, cats, Y)
+    assert st["live_rows"] == prof
+
+
 def test_fused_t64_and_irregular_components(sd):
     """N = 512: component sizes 128 / 256 -> tiles of T = 64 / 32 positions."""
     n, L = 512, 30
