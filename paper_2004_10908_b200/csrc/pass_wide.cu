@@ -588,6 +588,9 @@ __global__ void __launch_bounds__(32 * NW)
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t *const bar = reinterpret_cast<uint64_t *>(smem_raw + (size_t)buf_bytes);
   uint32_t *const aw = reinterpret_cast<uint32_t *>(bar + 1);
+  // per warp: the current group's weight block W_l[g] (<= 32 x 32 floats),
+  // copied from L2 with 16-byte cp.async before its chain
+  float *const wsm = reinterpret_cast<float *>(smem_raw + (size_t)buf_bytes + 128) + (threadIdx.x >> 5) * 1024;
   float *const tile_s = reinterpret_cast<float *>(smem_raw);
   const uint32_t rec_off = (uint32_t)P.R * 128u;
   const unsigned char *rec_s = smem_raw + rec_off;
@@ -648,13 +651,17 @@ __global__ void __launch_bounds__(32 * NW)
 #pragma unroll
           for (int i = 0; i < 8; ++i) acc[p][i] = 0.f;
         if (PL.off_gid >= 0) {
-          const float *W = PL.wv + (size_t)gid_s[u] * PL.wk * PL.wg + mo * 8;
+          const float *Wg = PL.wv + (size_t)gid_s[u] * PL.wk * PL.wg;   // [t][32 members], wg == 32
+          for (int q = lane; q < K * 8; q += 32) cp_async16(wsm + q * 4, Wg + q * 4);
+          asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+          __syncwarp();
+          const float *W = wsm + mo * 8;
 #pragma unroll 4
           for (int t = 0; t < K; ++t) {
             const uint32_t slot = __shfl_sync(FULL, code, t) & 0x3ffu;
             const float4 y = *reinterpret_cast<const float4 *>(tile_s + slot * 32u + pa);
-            const float4 w0 = __ldg(reinterpret_cast<const float4 *>(W + (size_t)t * PL.wg));
-            const float4 w1 = __ldg(reinterpret_cast<const float4 *>(W + (size_t)t * PL.wg + 4));
+            const float4 w0 = *reinterpret_cast<const float4 *>(W + t * 32);
+            const float4 w1 = *reinterpret_cast<const float4 *>(W + t * 32 + 4);
             const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
             const float yv[4] = {y.x, y.y, y.z, y.w};
 #pragma unroll
@@ -674,7 +681,8 @@ __global__ void __launch_bounds__(32 * NW)
               for (int i = 0; i < 8; ++i) acc[p][i] = __fmaf_rn(yv[p], PL.wu, acc[p][i]);
           }
         }
-        __syncwarp();                            // every source read before a member overwrites one
+        __syncwarp();                            // every source (and weight) read before a member
+                                                 // overwrites one / the next group's weights land
         const int64_t opos = (int64_t)tile * T + pa;
         float *obase = Yout + (((opos >> lgo) * R) << lgo) + (opos & ((1 << lgo) - 1));
         const int64_t rowmul = (int64_t)1 << lgo;
@@ -736,7 +744,7 @@ template <int NW>
 static void launch_gw(const LaunchCfg &c, const Workspace &w, const DevPass &P, uint32_t *alive, float ymax,
                       cudaStream_t s) {
   const uint32_t bb = (uint32_t)(((size_t)P.R * 128 + P.rec_bytes + 127) / 128 * 128);
-  const size_t smem = (size_t)bb + 8 + 4 * kMaxPassLayers;
+  const size_t smem = (size_t)bb + 128 + (size_t)NW * 4096;   // + barrier, liveness words, weight blocks
   static size_t set_smem = 0;
   if (smem > set_smem) {
     cudaFuncSetAttribute(k_pass_gw<NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
