@@ -317,10 +317,12 @@ __global__ void __launch_bounds__(32 * kWideNW, 1)
   }
 }
 
-static bool wide_x2() {                          // SDNN_PASS_X2=1: packed FFMA2 here too
+static bool wide_x2() {                          // packed FFMA2 / FADD2 (SDNN_PASS_X2=0: scalar)
+  // measured on one box, alternating runs: C4 1748.2 / 1748.6 vs 1756.1 / 1756.6
+  // ms/step scalar, C3 329.1 vs 329.8 ms
   static const bool v = [] {
     const char *e = getenv("SDNN_PASS_X2");
-    return e && atoi(e) == 1;
+    return !(e && atoi(e) == 0);
   }();
   return v;
 }

@@ -696,7 +696,7 @@ _T16 = {"SDNN_PASS_WIDE": "0"}     # 16-position k_pass tiles for 1024-row compo
 @pytest.mark.parametrize("env,flags", [({**_T16, "SDNN_PASS_VT": "1"}, 0), ({**_T16, "SDNN_PASS_TMA16": "1"}, 0),
                                        ({**_T16, "SDNN_BLK16": "1"}, 0), (_T16, 0), (_T16, 512),
                                        ({**_T16, "SDNN_PASS_PARITY": "1"}, 0), ({"SDNN_PASS_T32": "0"}, 0),
-                                       ({"SDNN_PASS_T32": "2", "SDNN_PASS_T32_S": "2"}, 0), ({"SDNN_PASS_X2": "1"}, 0), ({"SDNN_PASS_WIDE": "1"}, 0), ({"SDNN_PASS_GENERAL": "1", "SDNN_KNOB_NET": "rw"}, 0),
+                                       ({"SDNN_PASS_T32": "2", "SDNN_PASS_T32_S": "2"}, 0), ({"SDNN_PASS_X2": "1"}, 0), ({"SDNN_PASS_X2": "0"}, 0), ({"SDNN_PASS_WIDE": "1"}, 0), ({"SDNN_PASS_GENERAL": "1", "SDNN_KNOB_NET": "rw"}, 0),
                                        ({"SDNN_KNOB_NET": "rw"}, 0),
                                        ({"SDNN_PASS_ORDER": "tile"}, 0), ({"SDNN_PASS_ORDER": "comp"}, 0),
                                        ({"SDNN_PASS_NB": "1", "SDNN_PASS_X2": "1"}, 0), ({}, 512)])
