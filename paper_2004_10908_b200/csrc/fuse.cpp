@@ -460,9 +460,11 @@ static void build_pass_impl(const std::vector<const PackedLayer *> &layers, int3
     out.S = 1;
     out.split.clear();
   }
-  // SDNN_PASS_WIDE=2: components of 513-1024 rows over 2-CTA clusters of
-  // k_pass_t32 (512 rows per CTA, binned with cta = 512 above)
-  if (out.NB == 1 && C == 2 && R <= 512 && blocked && pass_wide_mode() == 2 && pass_t32_variant(4, 1, 2)) {
+  // SDNN_PASS_WIDE=2: components of 513-1024 rows (up to 2048 with
+  // fuse_rows = 2048) over 2- (4-) CTA clusters of k_pass_t32 (512 rows per
+  // CTA, binned with cta = 512 above)
+  if (out.NB == 1 && (C == 2 || C == 4) && R <= 512 && blocked && pass_wide_mode() == 2 &&
+      pass_t32_variant(4, 1, C)) {
     out.T = 32;
     out.NW = 4;
     out.S = 1;

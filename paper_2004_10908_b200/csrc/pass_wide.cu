@@ -768,7 +768,7 @@ void launch_pass_gw(const LaunchCfg &c, const Workspace &w, const DevPass &P, ui
 
 // (NW, S) instances: NW = ceil(rows / 128) warps, S buffers
 #define SDNN_T32_VARIANTS(X) X(1, 1) X(1, 2) X(1, 3) X(2, 1) X(2, 2) X(2, 3) X(4, 1) X(4, 2)
-#define SDNN_T32C_VARIANTS(X) X(4, 1)           // 2-CTA clusters
+#define SDNN_T32C_VARIANTS(X) X(4, 1)           // clusters (2 or 4 CTAs)
 
 static uint32_t t32_buf_bytes(const DevPass &P) {
   return (uint32_t)(((size_t)P.R * 128 + P.rec_bytes + 127) / 128 * 128);
@@ -779,7 +779,7 @@ bool pass_t32_variant(int nw, int s, int c) {
 #define X(NN, SS) if (c == 1 && nw == NN && s == SS) return true;
   SDNN_T32_VARIANTS(X)
 #undef X
-#define X(NN, SS) if (c == 2 && nw == NN && s == SS) return true;
+#define X(NN, SS) if ((c == 2 || c == 4) && nw == NN && s == SS) return true;
   SDNN_T32C_VARIANTS(X)
 #undef X
   return false;
@@ -857,6 +857,11 @@ void launch_pass_t32(const LaunchCfg &c, const Workspace &w, const DevPass &P, u
   if (P.C == 2 && P.NW == NN && P.S == SS) {                           \
     if (x2) launch_t32<NN, SS, true, 2>(c, w, P, alive, ymax, s);      \
     else launch_t32<NN, SS, false, 2>(c, w, P, alive, ymax, s);        \
+    return;                                                            \
+  }                                                                    \
+  if (P.C == 4 && P.NW == NN && P.S == SS) {                           \
+    if (x2) launch_t32<NN, SS, true, 4>(c, w, P, alive, ymax, s);      \
+    else launch_t32<NN, SS, false, 4>(c, w, P, alive, ymax, s);        \
     return;                                                            \
   }
   SDNN_T32C_VARIANTS(X)
