@@ -48,6 +48,11 @@ namespace sdnn {
 #define SDNN_REMOTE_FAST 0                              // k_pass_t32 C = 2: unconditional 32-term DSMEM chain
 #endif
 // (both measured within run-to-run noise, 1754 vs 1762-1766 ms/step on one box: off)
+#ifndef SDNN_SPLIT_RELEASE
+#define SDNN_SPLIT_RELEASE 0                            // clusters: arrive before the stores, wait after
+#endif
+// (measured in alternating runs: 1772 / 1771 vs 1762 / 1760 ms/step on C4: off)
+constexpr bool kSplitRelease = SDNN_SPLIT_RELEASE != 0;
 #ifndef SDNN_CHAIN_B
 #define SDNN_CHAIN_B 0
 #endif
@@ -440,7 +445,7 @@ __global__ void __launch_bounds__(32 * NW)
 #endif
       issue(it + S * ncl, b);
     };
-    bool issued = false;
+    bool issued = false, split_pending = false;
     for (int j = 0; j < P.m; ++j) {
       const PassLayerDev PL = P.layers[j];
       const bool last = j == P.m - 1;
@@ -511,7 +516,15 @@ __global__ void __launch_bounds__(32 * NW)
           }
         }
         if (early) {
-          release_and_load();
+          if (C > 1 && kSplitRelease) {
+            // arrive now (this CTA's reads of every tile are done), wait for the
+            // peers only after the member stores below, then issue the load
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            cluster_arrive();
+            split_pending = true;
+          } else {
+            release_and_load();
+          }
           issued = true;
         }
         const int gmax = __reduce_max_sync(FULL, G);
@@ -550,6 +563,11 @@ __global__ void __launch_bounds__(32 * NW)
                                 (spread8((bal[2] >> sh) & 0xffu) << 2) | (spread8((bal[3] >> sh) & 0xffu) << 3);
           if (word) atomicOr(&aw[j], word);
         }
+      }
+      if (split_pending) {                       // (last layer, C > 1)
+        cluster_wait();
+        issue(it + S * ncl, b);
+        split_pending = false;
       }
       __syncthreads();
     }
