@@ -32,6 +32,7 @@
 // its own 4-warp group on a named barrier as soon as its half has landed
 // (3.52 vs 3.35 ms).
 #include <algorithm>
+#include <cassert>
 #include <array>
 #include <cstdio>
 #include <cstdlib>
@@ -53,6 +54,17 @@ namespace sdnn {
 #endif
 // (measured in alternating runs: 1772 / 1771 vs 1762 / 1760 ms/step on C4: off)
 constexpr bool kSplitRelease = SDNN_SPLIT_RELEASE != 0;
+// SDNN_DEBUG_CHECKS=1 (build time, tools/debug_checks.sh): device asserts on
+// every slot, storage row and row count the pass kernels use (a stand-in for
+// compute-sanitizer, which is closed on the GPU pool)
+#ifndef SDNN_DEBUG_CHECKS
+#define SDNN_DEBUG_CHECKS 0
+#endif
+#if SDNN_DEBUG_CHECKS
+#define SDNN_CHECK(c) assert(c)
+#else
+#define SDNN_CHECK(c) ((void)0)
+#endif
 #ifndef SDNN_CHAIN_B
 #define SDNN_CHAIN_B 0
 #endif
@@ -416,6 +428,7 @@ __global__ void __launch_bounds__(32 * NW)
     const int64_t c = item_comp(it) * C + rank;
     const int tile = item_tile(it);
     const int cnt = nx_cnt;
+    SDNN_CHECK(cnt >= 0 && cnt <= P.R && (cnt == 0 || (nx_row >= 0 && nx_row + cnt <= P.yblk)));
     unsigned char *dst = smem_raw + (size_t)b * buf_bytes;
     mbar_expect_tx_arrive(bar + b, (uint32_t)cnt * 128u + (uint32_t)P.rec_bytes);
     bulk_g2s(dst + rec_off, P.rec + c * P.rec_bytes, (uint32_t)P.rec_bytes, bar + b);
@@ -475,6 +488,7 @@ __global__ void __launch_bounds__(32 * NW)
         for (int r = 0; r < EPL; ++r) {
           const int e = r * LPU + sll;
           const uint32_t code = K > 0 ? src_s[gi * 32 + (e < K ? e : 0)] : 0u;
+          SDNN_CHECK((code & 0x3ffu) < (uint32_t)P.R && (code >> 10) < (uint32_t)C);
           soff[r] = remote ? cluster_map(smem_u32(tile_s) + (code & 0x3ffu) * 128u, code >> 10)
                            : (code & 0x3ffu) * 32u;
           bia[r] = (!ubias && e < G) ? bias_s[gi * 32 + e] : 0.f;
@@ -544,6 +558,7 @@ __global__ void __launch_bounds__(32 * NW)
             const float bv = ubias ? 0.f : __shfl_sync(FULL, bia[r], l, LPU);
             if (v < G) {
               const float4 y = ubias ? yu : out4<X2>(acc, bv, ymax, o);
+              SDNN_CHECK(last ? (dst >= 0 && dst < P.yblk) : (uint32_t)dst < (uint32_t)P.R * 32u);
               if (last) *reinterpret_cast<float4 *>(obase + (int64_t)dst * rowmul) = y;
               else *reinterpret_cast<float4 *>(tile_s + dst + pa) = y;
             }
