@@ -34,6 +34,7 @@
 #include <algorithm>
 #include <cassert>
 #include <array>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 
@@ -332,6 +333,15 @@ __global__ void __launch_bounds__(32 * kWideNW, 1)
     if (!issued) release_and_load();
     __syncthreads();                             // aw published before the next item uses it
   }
+}
+
+// function attributes are per device: launches track the configured shared
+// memory size per device ordinal
+constexpr int kMaxDevices = 64;
+static int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d < 0 || d >= kMaxDevices ? 0 : d;
 }
 
 static bool wide_x2() {                          // packed FFMA2 / FADD2 (SDNN_PASS_X2=0: scalar)
@@ -780,10 +790,11 @@ static void launch_gw(const LaunchCfg &c, const Workspace &w, const DevPass &P, 
                       cudaStream_t s) {
   const uint32_t bb = (uint32_t)(((size_t)P.R * 128 + P.rec_bytes + 127) / 128 * 128);
   const size_t smem = (size_t)bb + 128 + (size_t)NW * 4096;   // + barrier, liveness words, weight blocks
-  static size_t set_smem = 0;
-  if (smem > set_smem) {
+  static std::atomic<size_t> set_smem[kMaxDevices];   // per device: the largest size configured
+  const int dev = current_device();
+  if (smem > set_smem[dev].load()) {
     cudaFuncSetAttribute(k_pass_gw<NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    set_smem = smem;
+    set_smem[dev] = smem;
   }
   int occ = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pass_gw<NW>, 32 * NW, smem) != cudaSuccess || occ <= 0) {
@@ -836,10 +847,11 @@ template <int NW, int S, bool X2, int C>
 static void launch_t32(const LaunchCfg &c, const Workspace &w, const DevPass &P, uint32_t *alive, float ymax,
                        cudaStream_t s) {
   const size_t smem = t32_smem(P, S);
-  static size_t set_smem = 0;                    // (per instance: the largest size configured so far)
-  if (smem > set_smem) {
+  static std::atomic<size_t> set_smem[kMaxDevices];   // per device: the largest size configured
+  const int dev = current_device();
+  if (smem > set_smem[dev].load()) {
     cudaFuncSetAttribute(k_pass_t32<NW, S, X2, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    set_smem = smem;
+    set_smem[dev] = smem;
   }
   if (C == 1) {
     int occ = 0;

@@ -1,3 +1,3 @@
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-bash tools/gpujob.sh r3s tests smoke bench:c4
+bash tools/gpujob.sh r3t tests smoke
